@@ -1,0 +1,342 @@
+"""Generate the golden fixtures in tests/golden/*.npz from the UNMODIFIED
+reference package (/root/reference/pkg/src/graphopt, read-only).
+
+Run once in the development container (the reference does not exist on the
+GPU box; the fixtures travel instead):
+
+    python tests/golden/make_golden.py
+
+Parameters are never stored (1.2M float64 would bloat the fixtures): each
+case records (config, task sizes, init seed) and the oracle/product rebuild
+them with their restated init_all_params + randomize_zero_init; a per-tensor
+checksum pins that restatement.
+"""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(REF / "tests"))
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+
+from graphopt import tensor as T  # noqa: E402
+from graphopt.baselines import default_assignments, greedy_placement  # noqa: E402
+from graphopt.costmodel import DeviceSpec, DeviceTopology  # noqa: E402
+from graphopt.embedding import EmbedConfig, _neighbor_arrays, embed, sample_neighbors  # noqa: E402
+from graphopt.graph import OP_INDEX, node_features  # noqa: E402
+from graphopt.policy import (PolicyConfig, init_all_params, iterate_decisions,  # noqa: E402
+                             ordered_tasks, sample_actions, task_heads, trunk_forward)
+from graphopt.simulator import (ActionAssignment, FusedGraph, FusionConfig,  # noqa: E402
+                                apply_fusion, simulate, singleton_fused)
+from graphopt.training import (PPOHyper, collect_rollouts, ppo_update,  # noqa: E402
+                               task_action_sizes)
+from graphopt.workloads import WorkloadSpec, gen_workload  # noqa: E402
+
+import conftest as C  # noqa: E402  (reference test fixtures: random_graph, make_graph)
+
+OUT = Path(__file__).resolve().parent
+
+
+def graph_arrays(g, prefix, out):
+    names = {}
+    coloc = []
+    for nd in g.nodes:
+        c = nd.colocation_group
+        coloc.append(-1 if c is None else names.setdefault(c, len(names)))
+    out[prefix + "n"] = np.int64(g.num_nodes)
+    out[prefix + "op"] = np.array([OP_INDEX[nd.op_type] for nd in g.nodes], np.int64)
+    out[prefix + "flops"] = np.array([nd.flops for nd in g.nodes], np.float64)
+    out[prefix + "out_bytes"] = np.array([nd.output_bytes for nd in g.nodes], np.float64)
+    out[prefix + "coloc"] = np.array(coloc, np.int64)
+    out[prefix + "src"] = np.array([e.src for e in g.edges], np.int64)
+    out[prefix + "dst"] = np.array([e.dst for e in g.edges], np.int64)
+    out[prefix + "ebytes"] = np.array([e.bytes for e in g.edges], np.float64)
+    out[prefix + "topo"] = np.array(g.topo_order(), np.int64)
+
+
+def randomize(store, seed=1):
+    rng = np.random.default_rng(seed)
+    for name in store.names():
+        t = store[name]
+        if not np.any(t.data):
+            s = 1.0 / np.sqrt(max(1, t.data.shape[0]))
+            t.data = rng.uniform(-s, s, size=t.data.shape)
+
+
+def checksums(store):
+    names = store.names()
+    return (np.array(names), np.array([store[n].data.sum() for n in names]),
+            np.array([(store[n].data ** 2).sum() for n in names]))
+
+
+def topo_arrays(top, prefix, out):
+    d = top.num_devices
+    out[prefix + "top_peak"] = np.array([top.device(i).peak_flops for i in range(d)])
+    out[prefix + "top_mem_bw"] = np.array([top.device(i).mem_bw for i in range(d)])
+    out[prefix + "top_cap"] = np.array([top.device(i).mem_capacity for i in range(d)])
+    lb = np.zeros((d, d))
+    for i in range(d):
+        for j in range(d):
+            if i != j:
+                lb[i, j] = top.link(i, j).bandwidth
+    out[prefix + "top_link_bw"] = lb
+
+
+# ------------------------------------------------------------------------------------------
+def make_rng():
+    out = {}
+    rows = []
+    for leaves in (6, 10, 30, 100, 7501):
+        specs = [{"op": "relu", "out_bytes": 4} for _ in range(leaves + 1)]
+        g = C.make_graph(specs, [(0, i) for i in range(1, leaves + 1)])
+        for seed in (0, 1, 3, 9, 12345, 2**31 - 1):
+            for k in (1, 3, 5):
+                pick = sample_neighbors(g, 0, k, seed)
+                rows.append([leaves, seed, k] + pick + [-1] * (5 - len(pick)))
+    out["star_picks"] = np.array(rows, np.int64)
+    us = []
+    for seed in (0, 7, 2**31 - 1):
+        r = np.random.default_rng(seed).random(3000)
+        for idx in (0, 1, 2, 100, 1999, 2999):
+            us.append([seed, idx, r[idx]])
+    out["uniforms"] = np.array(us, np.float64)
+    np.savez_compressed(OUT / "golden_rng.npz", **out)
+
+
+FORWARD_CASES = [
+    # name, graph builder, ecfg, pcfg, sizes, embed seed, decision seed
+    ("tiny", lambda: C.random_graph(np.random.default_rng(0), 6, p_edge=0.4),
+     EmbedConfig(1, 8, 4), PolicyConfig(2, 8, 2, 3, 16, 4, 2),
+     {"placement": 3, "schedule_priority": 4, "fusion_priority": 4}, 0, 9),
+    ("small", lambda: C.random_graph(np.random.default_rng(5), 13, p_edge=0.3),
+     EmbedConfig(2, 8, 3), PolicyConfig(2, 8, 2, 3, 16, 4, 2), {"placement": 3}, 11, 4),
+    ("default70", lambda: C.random_graph(np.random.default_rng(1), 70, p_edge=0.1),
+     EmbedConfig(), PolicyConfig(), {"placement": 4, "schedule_priority": 8,
+                                    "fusion_priority": 8}, 3, 21),
+    ("cfg1", lambda: gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0)),
+     EmbedConfig(), PolicyConfig(), {"placement": 2}, 5, 17),
+    ("dilated", lambda: gen_workload(WorkloadSpec("dilated-stack", 2, 50, 64, seed=3)),
+     EmbedConfig(), PolicyConfig(), {"placement": 8}, 8, 33),
+]
+
+
+def make_forward():
+    out = {}
+    meta = []
+    for name, build, ecfg, pcfg, sizes, eseed, dseed in FORWARD_CASES:
+        g = build()
+        p = name + "/"
+        graph_arrays(g, p, out)
+        store = init_all_params(ecfg, pcfg, sizes, seed=0)
+        randomize(store)
+        nm, s1, s2 = checksums(store)
+        out[p + "param_names"], out[p + "param_sum"], out[p + "param_sq"] = nm, s1, s2
+        tasks = ordered_tasks(sizes)
+        feats = node_features(g, None, [a for _, a in tasks])
+        gather, seg = _neighbor_arrays(g, ecfg.gs_knn, eseed)
+        emb = embed(g, feats, store, ecfg, seed=eseed)
+        hid = trunk_forward(emb.node_embed, emb.graph_embed, store, pcfg)
+        heads = task_heads(hid, store, pcfg, tasks)
+        out[p + "feats"] = feats
+        out[p + "gather"], out[p + "seg"] = gather, seg
+        out[p + "node_embed"] = emb.node_embed.data
+        out[p + "graph_embed"] = emb.graph_embed.data
+        out[p + "hid"] = hid.data
+        for t, _a in tasks:
+            out[p + f"logits/{t}"] = heads.logits[t].data
+        out[p + "value"] = heads.value.data
+        bundle, traj = iterate_decisions(g, store, ecfg, pcfg, sizes, pcfg.iterations, dseed)
+        for it, b in enumerate(traj):
+            for t, _a in tasks:
+                out[p + f"it{it}/actions/{t}"] = b.actions[t]
+                out[p + f"it{it}/logp/{t}"] = b.log_probs[t]
+                out[p + f"it{it}/logits/{t}"] = b.logits[t]
+            out[p + f"it{it}/value"] = np.float64(b.value)
+        meta.append(dict(name=name, ecfg=ecfg.__dict__, pcfg=pcfg.__dict__, sizes=sizes,
+                         embed_seed=eseed, decision_seed=dseed))
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(OUT / "golden_forward.npz", **out)
+
+
+def rand_topology(rng, d, tight=False):
+    devs = [DeviceSpec(i, float(rng.choice([1e9, 2e9, 1e12])), float(rng.choice([1e10, 1e11])),
+                       float(rng.choice([1e3, 1e12]) if tight else 1e12)) for i in range(d)]
+    top = DeviceTopology(devs, uniform_bandwidth=float(rng.choice([1e9, 1e10])))
+    return top
+
+
+def make_des():
+    out = {}
+    rng = np.random.default_rng(2024)
+    cases = 0
+
+    def record(g, fg_map, top, placement, pri, policy, tag):
+        nonlocal cases
+        p = f"c{cases}/"
+        graph_arrays(g, p, out)
+        topo_arrays(top, p, out)
+        fg = FusedGraph(g, fg_map)
+        res = simulate(fg, ActionAssignment("placement", placement, top.num_devices),
+                       ActionAssignment("schedule_priority", pri, 8), top, policy=policy)
+        out[p + "group_map"] = np.asarray(fg_map, np.int64)
+        out[p + "placement"] = np.asarray(placement, np.int64)
+        out[p + "priorities"] = np.asarray(pri, np.int64)
+        out[p + "policy"] = np.array(policy)
+        out[p + "tag"] = np.array(tag)
+        out[p + "step_time"] = np.float64(res.step_time)
+        out[p + "valid"] = np.bool_(res.valid)
+        out[p + "violation"] = np.array(res.violation or "")
+        out[p + "busy"] = np.array(res.per_device_busy, np.float64)
+        out[p + "peak"] = np.array(res.peak_mem, np.float64)
+        cases += 1
+
+    # random small graphs, random placements / priorities, both policies
+    for _ in range(120):
+        n = int(rng.integers(1, 40))
+        g = C.random_graph(rng, n, p_edge=float(rng.choice([0.05, 0.2, 0.5])))
+        d = int(rng.integers(1, 5))
+        top = rand_topology(rng, d, tight=bool(rng.random() < 0.3))
+        placement = rng.integers(0, d, n)
+        pri = rng.integers(0, 8, n) if rng.random() < 0.7 else np.zeros(n, np.int64)
+        policy = "priority" if rng.random() < 0.7 else "fifo"
+        record(g, np.arange(n), top, placement, pri, policy, "random")
+    # colocation (hand-built) and fused groupings from the reference fusion pass
+    for _ in range(30):
+        n = int(rng.integers(2, 30))
+        g = C.random_graph(rng, n, p_edge=0.3, fusible_only=True)
+        pri_f = rng.integers(0, 8, n)
+        fg = apply_fusion(g, ActionAssignment("fusion_priority", pri_f, 8), FusionConfig())
+        top = rand_topology(rng, 3)
+        record(g, fg.group_map, top, rng.integers(0, 3, n), rng.integers(0, 8, n),
+               "priority", "fused")
+    specs = [{"op": "relu", "flops": 1e9, "out_bytes": 8, "colocate": "g"},
+             {"op": "relu", "flops": 1e9, "out_bytes": 8, "colocate": "g"},
+             {"op": "relu", "flops": 1e9, "out_bytes": 8}]
+    g = C.make_graph(specs, [(0, 2)])
+    for pl in ([0, 1, 0], [1, 1, 0], [0, 0, 0]):
+        record(g, np.arange(3), C.simple_topology(2), np.array(pl), np.zeros(3, np.int64),
+               "priority", "coloc")
+    g = C.make_graph([{"op": "relu", "out_bytes": 4}] * 3, [(0, 1), (1, 2), (0, 2)])
+    record(g, np.array([0, 1, 0]), C.simple_topology(1), np.zeros(3, np.int64),
+           np.zeros(3, np.int64), "priority", "cycle")
+    # workload-scale graphs: greedy (default pipeline) and random 4/8-way placements
+    for spec, d in ((WorkloadSpec("multi-branch-cnn", 200, 1, 64, seed=0), 4),
+                    (WorkloadSpec("attention-stack", 100, 1, 64, seed=0), 8),
+                    (WorkloadSpec("dilated-stack", 3, 60, 64, seed=1), 8)):
+        g = gen_workload(spec, node_cap=10**6)
+        from graphopt.costmodel import uniform_topology
+        top = uniform_topology(d)
+        base = default_assignments(g, top)
+        record(g, np.arange(g.num_nodes), top, base["placement"].actions,
+               np.zeros(g.num_nodes, np.int64), "priority", "greedy")
+        out[f"c{cases - 1}/greedy"] = base["placement"].actions
+        for _ in range(2):
+            record(g, np.arange(g.num_nodes), top, rng.integers(0, d, g.num_nodes),
+                   rng.integers(0, 8, g.num_nodes), "priority", "workload")
+    out["count"] = np.int64(cases)
+    np.savez_compressed(OUT / "golden_des.npz", **out)
+
+
+def make_sample():
+    out = {}
+    rng = np.random.default_rng(99)
+    k = 0
+    for a in (1, 2, 3, 4, 7, 8, 9, 16):
+        for temp in (1.0, 0.5, 0.0, 2.0):
+            n = int(rng.integers(1, 300))
+            logits = rng.normal(scale=float(rng.choice([0.1, 1.0, 5.0])), size=(n, a))
+            if a > 1 and rng.random() < 0.3:
+                logits[:, 1] = logits[:, 0]  # ties
+            seed = int(rng.integers(2**31))
+            r = np.random.default_rng(seed)
+            skip = int(rng.integers(0, 3))
+            if skip:
+                r.random(skip)  # stream offset, as later (iteration, task) draws are
+            acts, logp = sample_actions(logits, temp, r)
+            p = f"s{k}/"
+            out[p + "logits"], out[p + "temp"] = logits, np.float64(temp)
+            out[p + "seed"], out[p + "offset"] = np.int64(seed), np.int64(skip)
+            out[p + "actions"], out[p + "logp"] = np.asarray(acts, np.int64), logp
+            k += 1
+    out["count"] = np.int64(k)
+    np.savez_compressed(OUT / "golden_sample.npz", **out)
+
+
+def make_rollouts():
+    out = {}
+    g = gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))
+    from graphopt.costmodel import uniform_topology
+    top = uniform_topology(2)
+    sizes = task_action_sizes(top, ["placement"], 8)
+    ecfg, pcfg = EmbedConfig(), PolicyConfig()
+    store = init_all_params(ecfg, pcfg, sizes, seed=0)
+    randomize(store)
+    base = default_assignments(g, top)
+    from graphopt.baselines import baseline_step_time
+    bl = baseline_step_time(g, top)
+    hyper = PPOHyper(rollouts=6)
+    batch = collect_rollouts(store, [g], top, sizes, [bl], 6, seed=0, hyper=hyper,
+                             embed_cfg=ecfg, policy_cfg=pcfg, fusion_cfg=FusionConfig(),
+                             base_assignments=[base])
+    graph_arrays(g, "g/", out)
+    out["baseline"] = np.float64(bl)
+    for i, s in enumerate(batch.samples):
+        p = f"r{i}/"
+        out[p + "graph_index"] = np.int64(s.graph_index)
+        out[p + "reward"] = np.float64(s.reward)
+        out[p + "value"] = np.float64(s.value_estimate)
+        out[p + "advantage"] = np.float64(s.advantage)
+        out[p + "step_time"] = np.float64(s.step_time)
+        out[p + "valid"] = np.bool_(s.valid)
+        out[p + "actions"] = s.bundle.actions["placement"]
+        out[p + "prev_actions"] = s.bundle.prev_actions["placement"]
+        out[p + "logp"] = s.bundle.log_probs["placement"]
+        out[p + "embed_seed"] = np.int64(s.bundle.embed_seed)
+    out["count"] = np.int64(len(batch.samples))
+    np.savez_compressed(OUT / "golden_rollouts.npz", **out)
+
+
+def make_ppo():
+    out = {}
+    ecfg = EmbedConfig(1, 8, 4)
+    pcfg = PolicyConfig(1, 8, 2, 3, 16, 8, 2)
+    g = C.random_graph(np.random.default_rng(3), 12, p_edge=0.3)
+    top = C.simple_topology(2)
+    sizes = task_action_sizes(top, ["placement"], 8)
+    store = init_all_params(ecfg, pcfg, sizes, seed=0)
+    randomize(store)
+    from graphopt.baselines import baseline_step_time
+    bl = baseline_step_time(g, top)
+    hyper = PPOHyper(lr=1e-2, rollouts=4, minibatches=2, epochs=2, entropy_coef=0.01)
+    batch = collect_rollouts(store, [g], top, sizes, [bl], 4, seed=5, hyper=hyper,
+                             embed_cfg=ecfg, policy_cfg=pcfg, fusion_cfg=FusionConfig())
+    graph_arrays(g, "g/", out)
+    before = {n: store[n].data.copy() for n in store.names()}
+    stats = ppo_update(batch, store, [g], top, sizes, hyper, ecfg, pcfg, seed=7)
+    for n in store.names():
+        out["before/" + n] = before[n]
+        out["after/" + n] = store[n].data
+    for k, v in stats.items():
+        out["stats/" + k] = np.float64(v)
+    for i, s in enumerate(batch.samples):
+        p = f"r{i}/"
+        out[p + "reward"] = np.float64(s.reward)
+        out[p + "advantage"] = np.float64(s.advantage)
+        out[p + "actions"] = s.bundle.actions["placement"]
+        out[p + "prev_actions"] = s.bundle.prev_actions["placement"]
+        out[p + "logp"] = s.bundle.log_probs["placement"]
+        out[p + "embed_seed"] = np.int64(s.bundle.embed_seed)
+    np.savez_compressed(OUT / "golden_ppo.npz", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo"]
+    for w in which:
+        globals()["make_" + w]()
+        print("wrote", w)
