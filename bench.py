@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark: placements scored/sec (embed + policy + sample + simulate) on the
+80k-node Transformer-XL-shaped DAG (BASELINE.json configs[3] = SURVEY cfg4):
+attention-stack L=8000 (80,001 nodes), 8-device placement, 4096 placements per
+step sharded over the ranks, mode R (each rollout: own neighbour sample + 2
+forwards, iteration 2 conditioned on iteration 1), random-init weights.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line (rank 0).  `value` is device-timed with the graph and
+parameters resident in HBM; `e2e` is the same metric through the public API
+(collect_rollouts) with parameters uploaded from host memory and per-rollout
+results read back every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "placements scored/sec (embed+policy+sample+simulate), 80k-node DAG, 1–8 GPUs"
+UNIT = "placements/s"
+
+WORKLOADS = {
+    # name: (family, layers, steps, width, seed, devices, placements per step)
+    "cfg4": ("attention-stack", 8000, 1, 64, 0, 8, 4096),
+    "cfg2": ("multi-branch-cnn", 1857, 1, 64, 0, 4, 256),
+    "cfg1": ("attention-stack", 10, 1, 64, 0, 2, 800),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--placements", type=int, default=None,
+                    help="placements per step (default: the config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    return ap.parse_args()
+
+
+# -------------------------------------------------------------------------------------
+# synthetic workload
+
+
+def build_workload(name):
+    from paper_2010_12438_b200 import (EmbedConfig, PolicyConfig, init_all_params,
+                                       randomize_zero_init, uniform_topology)
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    fam, L, S, w, seed, d, k = WORKLOADS[name]
+    g = gen_workload(WorkloadSpec(fam, L, S, w, seed=seed), node_cap=10**6)
+    top = uniform_topology(d)
+    sizes = {"placement": d}
+    ecfg, pcfg = EmbedConfig(), PolicyConfig()
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
+    return dict(graph=g, top=top, sizes=sizes, ecfg=ecfg, pcfg=pcfg, store=store, k=k, d=d,
+                spec=(fam, L, S, w, seed))
+
+
+# -------------------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# -------------------------------------------------------------------------------------
+# CPU baseline: the oracle port, bounded sample of one placement
+
+
+def cpu_placement_sample(w, seed=123, head_rows=1024):
+    """Time one placement of the workload on the host with the float64 oracle (a
+    faithful, vectorised restatement of the reference): neighbour sampling, embed
+    and trunk in full, the N x N task-head attention on `head_rows` query rows
+    (scaled by N / head_rows), sampling, and the reference DES in full.  Returns
+    (seconds per placement, description)."""
+    import numpy as np
+
+    from oracle import des as od
+    from oracle import forward as of
+    from oracle import graph as ogm
+    from oracle import params as op
+    g = w["graph"]
+    ogr = ogm.make(g.num_nodes, g.op, g.flops, g.out_bytes, g.src, g.dst, g.ebytes)
+    n = ogr["n"]
+    ecfg, pcfg = of.EmbedCfg(), of.PolicyCfg()
+    P = op.randomize_zero_init(op.init_all_params(ecfg, pcfg, w["sizes"], 0))
+    tasks = of.ordered_tasks(w["sizes"])
+    t = {}
+    t0 = time.perf_counter()
+    feats = ogm.node_features(ogr, None, [a for _, a in tasks])
+    ne, ge = of.embed(ogr, feats, P, ecfg, seed=seed)
+    t["embed"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    hid = of.trunk_forward(ne, ge, P, pcfg)
+    t["trunk"] = time.perf_counter() - t0
+    # task head: full per-row layers, attention on a row chunk (scaled)
+    t0 = time.perf_counter()
+    p = "policy/task/placement/"
+    h = of.layer_norm(np.concatenate([np.zeros_like(hid), hid], axis=1) @ P[p + "cat_w"]
+                      + P[p + "cat_b"], P[p + "ln_g"], P[p + "ln_b"])
+    pre = "policy/task_attn/"
+    q = h @ P[pre + "q_w"] + P[pre + "q_b"]
+    k = h @ P[pre + "k_w"] + P[pre + "k_b"]
+    v = h @ P[pre + "v_w"] + P[pre + "v_b"]
+    t_rowwise = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rows = min(head_rows, n)
+    scale = 1.0 / np.sqrt(pcfg.d_head)
+    att = np.zeros((rows, pcfg.n_head * pcfg.d_head))
+    for i in range(pcfg.n_head):
+        sl = slice(i * pcfg.d_head, (i + 1) * pcfg.d_head)
+        s = (q[:rows, sl] @ k[:, sl].T) * scale
+        att[:, sl] = of.softmax(s) @ v[:, sl]
+    t_att = (time.perf_counter() - t0) * (n / rows)
+    t0 = time.perf_counter()
+    attn_full = np.resize(att, (n, att.shape[1]))
+    o = attn_full @ P[pre + "o_w"] + P[pre + "o_b"]
+    rep = of.relu(o @ P[p + "fc_w1"] + P[p + "fc_b1"]) @ P[p + "fc_w2"] + P[p + "fc_b2"]
+    logits = rep @ P[p + "out_w"] + P[p + "out_b"]
+    _value = rep.mean(axis=0, keepdims=True) @ P["policy/value_w"] + P["policy/value_b"]
+    t["heads"] = t_rowwise + t_att + (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    acts, _lp = of.sample_actions(logits, 1.0, np.random.default_rng(seed))
+    t["sample"] = time.perf_counter() - t0
+    placement = np.zeros(n, np.int64)
+    placement[ogr["topo"]] = acts
+    t0 = time.perf_counter()
+    fg = od.singleton(ogr)
+    res = od.simulate(ogr, fg, placement, np.zeros(n, np.int64), od.uniform_topology(w["d"]))
+    od.reward(res["step_time"], 1.0, res["valid"])
+    t["simulate"] = time.perf_counter() - t0
+    per_forward = t["embed"] + t["trunk"] + t["heads"] + t["sample"]
+    per_placement = 2 * per_forward + t["simulate"]
+    desc = (f"oracle (float64 numpy restatement of the reference) on 1 placement of "
+            f"{w['spec'][0]} L={w['spec'][1]} ({n} nodes): embed+trunk in full, task-head "
+            f"attention on {rows}/{n} query rows scaled x{n / rows:.1f}, DES in full; "
+            f"2 forwards per placement (mode R). stage seconds: "
+            + ", ".join(f"{k}={v:.2f}" for k, v in t.items()))
+    return per_placement, desc
+
+
+def cpu_threads():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return max((i.get("num_threads", 1) for i in info), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# -------------------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = build_workload(args.workload)
+    for _ in range(args.warmup):
+        cpu_placement_sample(w)
+    times, desc = [], ""
+    for _ in range(args.steps):
+        s, desc = cpu_placement_sample(w)
+        times.append(s)
+    per = sum(times) / len(times)
+    value = 1.0 / per
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1000.0, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, w),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, w):
+    fam, L, S, wd, seed = w["spec"]
+    return {"workload": f"{args.workload}: {fam} L={L} ({w['graph'].num_nodes} nodes, "
+                        f"{w['graph'].num_edges} edges), {w['d']}-device placement, "
+                        f"{args.placements or w['k']} placements/step sharded over ranks, "
+                        "mode R (own neighbour sample + 2 forwards per placement)",
+            "nodes": w["graph"].num_nodes, "devices": w["d"],
+            "placements_per_step": args.placements or w["k"], "iterations": 2,
+            "weights": "init_all_params(seed=0) + zero-init tensors refilled U(+-1/sqrt(fan_in))",
+            "l2": "inputs larger than L2 (per-step activations >> 126 MB); no explicit flush"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2010_12438_b200 import _lib
+    from paper_2010_12438_b200.baselines import baseline_step_time, default_assignments
+    from paper_2010_12438_b200.config import FusionConfig, PPOHyper
+    from paper_2010_12438_b200.engine import params_on_device
+    from paper_2010_12438_b200.runtime import context
+    from paper_2010_12438_b200.training import collect_rollouts
+
+    w = build_workload(args.workload)
+    K = args.placements or w["k"]
+    g, top, sizes = w["graph"], w["top"], w["sizes"]
+    base = [default_assignments(g, top)]
+    bl = [baseline_step_time(g, top)]
+    hyper = PPOHyper(rollouts=K)
+    ctx = context()
+
+    def step(s, store):
+        """One step: this rank's shard of the K placements (global rollout ids
+        [rank*K/world, (rank+1)*K/world) of the step's outer stream)."""
+        batch = collect_rollouts(store, [g], top, sizes, bl, K, 1000 + s, hyper, w["ecfg"],
+                                 w["pcfg"], FusionConfig(), base_assignments=base,
+                                 keep_logits=False, shard=(rank, world))
+        return batch
+
+    store = w["store"]
+    params_on_device(store, w["ecfg"], w["pcfg"], sizes)  # resident before timing
+    for s in range(args.warmup):
+        step(s, store)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.call("go_ctx_set_timing", ctx.handle, 1)
+    launches0 = _lib.lib().go_launch_count()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    batches = []
+    for s in range(args.steps):
+        batches.append(step(args.warmup + s, store))
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = _lib.lib().go_launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    stats = {}
+    for cls, name in ((0, "heads_attention"), (1, "trunk_attention"), (2, "segment_max"),
+                      (4, "des")):
+        import ctypes as C
+        cnt, tms, work = C.c_int64(), C.c_double(), C.c_double()
+        _lib.call("go_ctx_kernel_stats", ctx.handle, cls, C.byref(cnt), C.byref(tms),
+                  C.byref(work))
+        stats[name] = (cnt.value, tms.value, work.value)
+    _lib.call("go_ctx_set_timing", ctx.handle, 0)
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = K * args.steps / (ms / 1000.0)
+
+    # ---- e2e: public API, parameters from host memory, results read back
+    e2e_ms = []
+    for s in range(args.e2e_steps):
+        store.touch()  # host-side parameters changed -> re-upload inside the region
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        b = step(10_000 + s, store)
+        r = b.rewards.cpu().numpy()
+        _ = b.step_times.cpu().numpy(), b.valid.cpu().numpy(), b.values.cpu().numpy()
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1000.0)
+    et = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device="cuda")
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = K / (float(et.item()) / 1000.0)
+    n_local = len(r)
+    blob, _offs = params_on_device(store, w["ecfg"], w["pcfg"], sizes)
+    h2d = int(blob.numel() * 4 + 8 * n_local)
+    d2h = int(n_local * (8 + 8 + 1 + 4))
+
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    bf16 = peaks.get("bf16_tflops_sustained", 1400.0)
+    cnt, hms, hflops = stats["heads_attention"]
+    roof = None
+    if cnt:
+        ach = hflops / cnt / (hms / cnt / 1000.0) / 1e12
+        roof = {"bound": "tensor", "kernel": "heads N x N attention (attn_kernel)",
+                "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
+                "traffic": None, "launches": cnt, "avg_launch_ms": hms / cnt,
+                "algorithmic_flops_per_launch": hflops / cnt,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                "share_of_step": hms / ms}
+    cnt2, sms, sbytes = stats["segment_max"]
+    roof_agg = None
+    if cnt2:
+        ach = sbytes / cnt2 / (sms / cnt2 / 1000.0) / 1e9
+        roof_agg = {"bound": "hbm", "kernel": "GraphSAGE gather + segment max", "achieved": ach,
+                    "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                    "launches": cnt2, "avg_launch_ms": sms / cnt2,
+                    "algorithmic_bytes_per_launch": sbytes / cnt2, "share_of_step": sms / ms}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": workload_config(args, w),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": roof, "roofline_aggregation": roof_agg,
+        "kernel_ms": {k: v[1] / max(1, args.steps) for k, v in stats.items()},
+        "gpu_launches": int(launches), "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        per, desc = cpu_placement_sample(w)
+        line["cpu_baseline"] = {"value": 1.0 / per, "unit": UNIT, "cores": cpu_threads(),
+                                "kind": "port", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,405 @@
+// Exact batched discrete-event simulation (simulator.py:280-441) + reward
+// (training.py:37-44).  One thread simulates one placement; K placements run in
+// parallel.  Compiled with -fmad=false; all float64 arithmetic is explicit IEEE
+// round-to-nearest (__dadd_rn / __ddiv_rn), so makespans, busy times and memory
+// peaks are bit-identical to the reference.
+//
+// Reference semantics reproduced:
+//  * in-flight events: at most one compute per device and one transfer per link, so
+//    the event heap's (time, kind, dev|src, i|dst, seq) order reduces to
+//    (time, slot) with slot = dev for computes and D + src*D + dst for transfers;
+//    all events at the minimum time form one batch, processed in slot order;
+//    zero-duration events created by schedule() form the next batch.
+//  * ready queue per device: min-heap on (-priority, ready_time, topo_index) or
+//    (ready_time, topo_index) for FIFO (topo_index is unique).
+//  * schedule(t): links in sorted (src, dst) order pop FIFO if idle, then devices
+//    0..D-1 pop their queue if idle; busy[dev] += kernel_time.
+//  * memory: (finish, +b) and (last-consumer finish, -b) events swept in
+//    (time, kind, delta) order; processed online per time group (allocs before
+//    frees; exact sorted order when byte values are not all integral).
+#include <algorithm>
+
+#include "engine.cuh"
+
+namespace go {
+
+constexpr int DES_MAXD = 16;
+constexpr double DINF = __builtin_huge_val();
+
+struct HeapEnt {
+  double rt;
+  int32_t topo;
+  int32_t grp;
+  int32_t npri;  // -priority (0 for FIFO)
+  int32_t pad;
+};
+
+__device__ __forceinline__ bool heap_less(const HeapEnt& a, const HeapEnt& b) {
+  if (a.npri != b.npri) return a.npri < b.npri;
+  if (a.rt != b.rt) return a.rt < b.rt;
+  return a.topo < b.topo;
+}
+
+struct LinkEnt {
+  int32_t edge;
+  int32_t grp;
+};
+
+struct DesCaps {
+  int64_t cq;  // ready-heap capacity per device
+  int64_t cl;  // FIFO capacity per link
+  int64_t cm;  // exact-mode memory list capacity per device
+  int64_t per_placement_bytes(int G, int d) const {
+    int64_t b = 2 * (int64_t)G * 4;
+    b = round_up(b, 16) + (int64_t)d * cq * sizeof(HeapEnt);
+    b += (int64_t)d * d * cl * sizeof(LinkEnt);
+    b += 2 * (int64_t)d * cm * sizeof(double);
+    return round_up(b, 256);
+  }
+};
+
+enum { ST_OK = 0, ST_OVERFLOW = 1, ST_DEADLOCK = 2, ST_MEMLIST = 3 };
+
+__global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
+                           int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
+                           int d, const double* __restrict__ peakf, const double* __restrict__ mbw,
+                           const double* __restrict__ cap, const double* __restrict__ lbw,
+                           int policy, double baseline, DesCaps caps, char* __restrict__ scratch,
+                           int64_t scratch_stride, const int32_t* __restrict__ which,
+                           double* __restrict__ o_step, uint8_t* __restrict__ o_valid,
+                           int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
+                           double* __restrict__ o_peak, double* __restrict__ o_reward,
+                           int32_t* __restrict__ o_status) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= K) return;
+  const int kk = which ? which[tid] : tid;
+  const int32_t* pl = placement + (int64_t)kk * pstride;
+  const int32_t* pr = prio + (int64_t)kk * prio_stride;
+  const int G = V.G;
+  char* base = scratch + (int64_t)tid * scratch_stride;
+  int32_t* pending = reinterpret_cast<int32_t*>(base);
+  int32_t* rem = pending + G;
+  HeapEnt* heaps = reinterpret_cast<HeapEnt*>(base + round_up(2 * (int64_t)G * 4, 16));
+  LinkEnt* lq = reinterpret_cast<LinkEnt*>(heaps + (int64_t)d * caps.cq);
+  double* mlist = reinterpret_cast<double*>(lq + (int64_t)d * d * caps.cl);
+
+  auto gdev = [&](int g) { return pl[V.grp_rep[g]]; };
+
+  // colocation (simulator.py:308-315): checked on group devices, simulation continues
+  int8_t viol = 0;
+  for (int c = 0; c < V.num_coloc && !viol; ++c) {
+    int d0 = gdev(V.coloc_grp[V.coloc_off[c]]);
+    for (int64_t j = V.coloc_off[c] + 1; j < V.coloc_off[c + 1]; ++j)
+      if (gdev(V.coloc_grp[j]) != d0) {
+        viol = 1;
+        break;
+      }
+  }
+
+  double dev_t[DES_MAXD];
+  int32_t dev_g[DES_MAXD];
+  int32_t hs[DES_MAXD];
+  double busy[DES_MAXD], cur[DES_MAXD], pk[DES_MAXD], acc_a[DES_MAXD], acc_f[DES_MAXD];
+  int32_t na[DES_MAXD], nf[DES_MAXD];
+  double link_t[DES_MAXD * DES_MAXD];
+  int32_t link_g[DES_MAXD * DES_MAXD];
+  int32_t lq_h[DES_MAXD * DES_MAXD], lq_n[DES_MAXD * DES_MAXD];
+  uint64_t lmask[DES_MAXD * DES_MAXD / 64];
+  for (int i = 0; i < d; ++i) {
+    dev_t[i] = DINF;
+    dev_g[i] = -1;
+    hs[i] = 0;
+    busy[i] = 0.0;
+    cur[i] = 0.0;
+    pk[i] = 0.0;
+    acc_a[i] = 0.0;
+    acc_f[i] = 0.0;
+    na[i] = nf[i] = 0;
+  }
+  const int L = d * d;
+  for (int s = 0; s < L; ++s) {
+    link_t[s] = DINF;
+    link_g[s] = -1;
+    lq_h[s] = 0;
+    lq_n[s] = 0;
+  }
+  for (int w = 0; w < (L + 63) / 64; ++w) lmask[w] = 0;
+  uint32_t dmask = 0;  // devices with a non-empty ready heap
+  int status = ST_OK;
+
+  auto heap_push = [&](int dev, const HeapEnt& e) {
+    if (hs[dev] >= caps.cq) {
+      status = ST_OVERFLOW;
+      return;
+    }
+    HeapEnt* h = heaps + (int64_t)dev * caps.cq;
+    int p = hs[dev]++;
+    while (p > 0) {
+      int q = (p - 1) >> 1;
+      if (!heap_less(e, h[q])) break;
+      h[p] = h[q];
+      p = q;
+    }
+    h[p] = e;
+    dmask |= 1u << dev;
+  };
+  auto heap_pop = [&](int dev) {
+    HeapEnt* h = heaps + (int64_t)dev * caps.cq;
+    HeapEnt top = h[0];
+    int n = --hs[dev];
+    if (n > 0) {
+      HeapEnt last = h[n];
+      int p = 0;
+      while (true) {
+        int c = 2 * p + 1;
+        if (c >= n) break;
+        if (c + 1 < n && heap_less(h[c + 1], h[c])) ++c;
+        if (!heap_less(h[c], last)) break;
+        h[p] = h[c];
+        p = c;
+      }
+      h[p] = last;
+    } else {
+      dmask &= ~(1u << dev);
+    }
+    return top;
+  };
+  auto mark_ready = [&](int g, double t) {
+    HeapEnt e;
+    e.rt = t;
+    e.topo = V.topo_index[g];
+    e.grp = g;
+    e.npri = policy == 0 ? -pr[V.grp_rep[g]] : 0;
+    e.pad = 0;
+    heap_push(gdev(g), e);
+  };
+  auto deliver = [&](int g, double t) {
+    if (--pending[g] == 0) mark_ready(g, t);
+  };
+  const bool exact_int = V.mem_int_exact != 0;
+  auto mem_add = [&](int dev, double b, bool alloc) {
+    if (exact_int) {
+      if (alloc) acc_a[dev] = __dadd_rn(acc_a[dev], b);
+      else acc_f[dev] = __dadd_rn(acc_f[dev], b);
+      if (alloc) na[dev]++;
+      else nf[dev]++;
+      return;
+    }
+    double* lst = mlist + ((int64_t)dev * 2 + (alloc ? 0 : 1)) * caps.cm;
+    int32_t& n = alloc ? na[dev] : nf[dev];
+    if (n >= caps.cm) {
+      status = ST_MEMLIST;
+      return;
+    }
+    // keep sorted by delta ascending: allocs ascending b, frees descending b
+    int p = n++;
+    while (p > 0 && (alloc ? lst[p - 1] > b : lst[p - 1] < b)) {
+      lst[p] = lst[p - 1];
+      --p;
+    }
+    lst[p] = b;
+  };
+  auto mem_flush = [&]() {
+    for (int dev = 0; dev < d; ++dev) {
+      if (na[dev] == 0 && nf[dev] == 0) continue;
+      if (exact_int) {
+        double c = __dadd_rn(cur[dev], acc_a[dev]);
+        if (na[dev]) pk[dev] = fmax(pk[dev], c);
+        cur[dev] = __dsub_rn(c, acc_f[dev]);
+        acc_a[dev] = acc_f[dev] = 0.0;
+      } else {
+        double* la = mlist + ((int64_t)dev * 2) * caps.cm;
+        double* lf = la + caps.cm;
+        for (int i = 0; i < na[dev]; ++i) {
+          cur[dev] = __dadd_rn(cur[dev], la[i]);
+          pk[dev] = fmax(pk[dev], cur[dev]);
+        }
+        for (int i = 0; i < nf[dev]; ++i) cur[dev] = __dadd_rn(cur[dev], -lf[i]);
+      }
+      na[dev] = nf[dev] = 0;
+    }
+  };
+
+  for (int g = 0; g < G; ++g) {
+    pending[g] = V.pending0[g];
+    rem[g] = V.nsucc[g];
+  }
+  for (int g = 0; g < G && status == ST_OK; ++g)
+    if (pending[g] == 0) mark_ready(g, 0.0);
+
+  auto schedule = [&](double t) {
+    for (int w = 0; w < (L + 63) / 64; ++w) {
+      uint64_t m = lmask[w];
+      while (m) {
+        int b = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        int s = w * 64 + b;
+        if (link_t[s] != DINF) continue;
+        LinkEnt* q = lq + (int64_t)s * caps.cl;
+        LinkEnt e = q[lq_h[s]];
+        lq_h[s] = (lq_h[s] + 1) % (int32_t)caps.cl;
+        if (--lq_n[s] == 0) lmask[w] &= ~(1ull << b);
+        double dt = __ddiv_rn(V.out_bytes[e.edge], lbw[s]);
+        link_t[s] = __dadd_rn(t, dt);
+        link_g[s] = e.grp;
+      }
+    }
+    uint32_t m = dmask;
+    while (m) {
+      int dev = __ffs(m) - 1;
+      m &= m - 1;
+      if (dev_t[dev] != DINF) continue;
+      HeapEnt e = heap_pop(dev);
+      int g = e.grp;
+      double dt = fmax(__ddiv_rn(V.cost_flops[g], peakf[dev]), __ddiv_rn(V.cost_bytes[g], mbw[dev]));
+      // Python max(a, b) returns a unless b > a; fmax agrees for non-NaN inputs
+      busy[dev] = __dadd_rn(busy[dev], dt);
+      dev_t[dev] = __dadd_rn(t, dt);
+      dev_g[dev] = g;
+    }
+  };
+
+  schedule(0.0);
+  int done = 0;
+  double step = 0.0;
+  double mem_time = -1.0;
+  while (status == ST_OK) {
+    double now = DINF;
+    for (int i = 0; i < d; ++i) now = fmin(now, dev_t[i]);
+    for (int s = 0; s < L; ++s) now = fmin(now, link_t[s]);
+    if (now == DINF) break;
+    if (now != mem_time) {
+      mem_flush();
+      mem_time = now;
+    }
+    // computes (kind 0) in device order
+    for (int dev = 0; dev < d; ++dev) {
+      if (dev_t[dev] != now) continue;
+      int g = dev_g[dev];
+      dev_t[dev] = DINF;
+      dev_g[dev] = -1;
+      ++done;
+      step = now;
+      for (int64_t e = V.out_off[g]; e < V.out_off[g + 1]; ++e) {
+        int gd = V.out_grp[e];
+        int dd = gdev(gd);
+        if (dd == dev) {
+          deliver(gd, now);
+        } else {
+          int s = dev * d + dd;
+          if (lq_n[s] >= caps.cl) {
+            status = ST_OVERFLOW;
+            break;
+          }
+          LinkEnt* q = lq + (int64_t)s * caps.cl;
+          q[(lq_h[s] + lq_n[s]) % (int32_t)caps.cl] = LinkEnt{(int32_t)e, gd};
+          ++lq_n[s];
+          lmask[s >> 6] |= 1ull << (s & 63);
+        }
+      }
+      double b = V.resident[g];
+      if (b != 0.0) mem_add(dev, b, true);
+      for (int64_t j = V.pred_off[g]; j < V.pred_off[g + 1]; ++j) {
+        int p = V.pred_grp[j];
+        if (--rem[p] == 0 && V.resident[p] != 0.0) mem_add(gdev(p), V.resident[p], false);
+      }
+      if (V.nsucc[g] == 0 && b != 0.0) mem_add(dev, b, false);
+    }
+    // transfers (kind 1) in (src, dst) order
+    for (int s = 0; s < L; ++s) {
+      if (link_t[s] != now) continue;
+      int g = link_g[s];
+      link_t[s] = DINF;
+      link_g[s] = -1;
+      deliver(g, now);
+    }
+    if (status != ST_OK) break;
+    schedule(now);
+  }
+  if (status == ST_OK) {
+    mem_flush();
+    if (done != G) status = ST_DEADLOCK;
+  }
+  o_status[tid] = status;
+  if (status != ST_OK) return;
+  if (!viol)
+    for (int dev = 0; dev < d; ++dev)
+      if (pk[dev] > cap[dev]) {
+        viol = 2;
+        break;
+      }
+  o_step[kk] = step;
+  o_valid[kk] = viol == 0;
+  o_viol[kk] = viol;
+  for (int dev = 0; dev < d; ++dev) {
+    if (o_busy) o_busy[(int64_t)kk * d + dev] = busy[dev];
+    if (o_peak) o_peak[(int64_t)kk * d + dev] = pk[dev];
+  }
+  if (o_reward && baseline > 0.0)
+    o_reward[kk] = viol == 0 ? -sqrt(__ddiv_rn(step, baseline)) : -10.0;
+}
+
+int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t pstride,
+                   const int32_t* prio, int64_t prio_stride, int d, const double* peak,
+                   const double* mem_bw, const double* cap, const double* link_bw, int policy,
+                   double baseline, double* step_time, uint8_t* valid, int8_t* violation,
+                   double* busy, double* peak_mem, double* reward, go_ctx* ctx,
+                   cudaStream_t st) {
+  if (K <= 0) return GO_OK;
+  if (d > DES_MAXD) GO_THROW(GO_ERR_UNSUPPORTED, "%d devices > %d", d, DES_MAXD);
+  // topology -> device (small; part of the DES workspace head)
+  std::vector<double> topo(3 * d + d * d);
+  for (int i = 0; i < d; ++i) {
+    topo[i] = peak[i];
+    topo[d + i] = mem_bw[i];
+    topo[2 * d + i] = cap[i];
+  }
+  for (int i = 0; i < d * d; ++i) topo[3 * d + i] = link_bw[i];
+  DesCaps caps{64, 64, 64};
+  const int G = v.G;
+  auto run = [&](int count, const int32_t* which, DesCaps c) {
+    int64_t stride = c.per_placement_bytes(G, d);
+    int64_t head = round_up((int64_t)topo.size() * 8, 256) + round_up((int64_t)count * 4, 256) +
+                   round_up((int64_t)K * 4, 256);
+    char* ws = reinterpret_cast<char*>(ctx->ensure_des(head + stride * count));
+    double* dtopo = reinterpret_cast<double*>(ws);
+    int32_t* dstatus = reinterpret_cast<int32_t*>(ws + round_up((int64_t)topo.size() * 8, 256));
+    int32_t* dwhich = dstatus + round_up(count, 64);
+    CUDA_CHECK(cudaMemcpyAsync(dtopo, topo.data(), topo.size() * 8, cudaMemcpyHostToDevice, st));
+    if (which)
+      CUDA_CHECK(cudaMemcpyAsync(dwhich, which, (size_t)count * 4, cudaMemcpyHostToDevice, st));
+    const int threads = 32;
+    des_kernel<<<(unsigned)cdiv(count, threads), threads, 0, st>>>(
+        v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
+        dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
+        step_time, valid, violation, busy, peak_mem, reward, dstatus);
+    LAUNCH_CHECK();
+    std::vector<int32_t> hstat(count);
+    CUDA_CHECK(cudaMemcpyAsync(hstat.data(), dstatus, (size_t)count * 4, cudaMemcpyDeviceToHost,
+                               st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    return hstat;
+  };
+  std::vector<int32_t> stat = run(K, nullptr, caps);
+  std::vector<int32_t> redo;
+  for (int i = 0; i < K; ++i) {
+    if (stat[i] == ST_DEADLOCK) GO_THROW(GO_ERR_DEADLOCK, "simulation deadlocked");
+    if (stat[i] != ST_OK) redo.push_back(i);
+  }
+  if (!redo.empty()) {
+    // rerun overflowing placements with capacities that cannot overflow
+    DesCaps big{std::max<int64_t>(G, 1), std::max<int64_t>(v.num_edges, 1),
+                std::max<int64_t>(G, 1)};
+    for (size_t i0 = 0; i0 < redo.size(); i0 += 8) {
+      int cnt = (int)std::min<size_t>(8, redo.size() - i0);
+      std::vector<int32_t> s2 = run(cnt, redo.data() + i0, big);
+      for (int j = 0; j < cnt; ++j)
+        if (s2[j] != ST_OK)
+          GO_THROW(s2[j] == ST_DEADLOCK ? GO_ERR_DEADLOCK : GO_ERR_UNSUPPORTED,
+                   "simulation failed (status %d)", s2[j]);
+    }
+  }
+  return GO_OK;
+}
+
+}  // namespace go

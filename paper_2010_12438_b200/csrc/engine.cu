@@ -1,0 +1,655 @@
+// libgo_b200 engine: context/workspace management, the batched policy forward
+// (embed -> trunk -> heads, embedding.py:73-98 + policy.py:135-217), sampling and
+// simulation entry points of the C-ABI (include/go_b200.h).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "engine.cuh"
+
+namespace go {
+
+std::atomic<long long> g_launch_count{0};
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// ---------------------------------------------------------------------------------
+// Parameter slots (canonical order; mirrored by paper_2010_12438_b200/params.py).
+struct Slots {
+  int gs_layers, trf_layers, T;
+  int e_in_w() const { return 0; }
+  int e_in_b() const { return 1; }
+  int e_layer(int l, int w) const { return 2 + 4 * l + w; }  // agg_w, agg_b, fc_w, fc_b
+  int pbase() const { return 2 + 4 * gs_layers; }
+  int p_in_w() const { return pbase(); }
+  int p_in_b() const { return pbase() + 1; }
+  // block b in [0, trf_layers]; b == trf_layers is policy/mod/
+  int blk(int b, int w) const { return pbase() + 2 + 16 * b + w; }
+  int ta(int w) const { return pbase() + 2 + 16 * (trf_layers + 1) + w; }
+  int task(int t, int w) const { return ta(8) + 10 * t + w; }
+  int value_w() const { return ta(8) + 10 * T; }
+  int value_b() const { return value_w() + 1; }
+  int count() const { return value_b() + 1; }
+};
+enum { Q_W = 0, Q_B, K_W, K_B, V_W, V_B, O_W, O_B, LN1_G, LN1_B, FF_W1, FF_B1, FF_W2, FF_B2,
+       LN2_G, LN2_B };
+enum { CAT_W = 0, CAT_B, LN_G, LN_B, FC_W1, FC_B1, FC_W2, FC_B2, OUT_W, OUT_B };
+
+static Slots slots_of(const go_config_t& c) { return Slots{c.gs_layers, c.trf_layers, c.num_tasks}; }
+
+static void validate(const go_config_t& c) {
+  GO_CHECK(c.gs_layers >= 0 && c.gs_dim > 0 && c.gs_knn >= 1, "bad EmbedConfig");
+  GO_CHECK(c.trf_layers >= 0 && c.d_model > 0 && c.n_head > 0 && c.d_head > 0 && c.d_inner > 0 &&
+               c.segment_len > 0,
+           "bad PolicyConfig");
+  GO_CHECK(c.num_tasks >= 1 && c.num_tasks <= 3, "at least one task required");
+  for (int t = 0; t < c.num_tasks; ++t) GO_CHECK(c.task_sizes[t] >= 1, "empty action space");
+}
+
+// ---------------------------------------------------------------------------------
+// Metadata staging: host tables packed into one pinned buffer, one H2D copy.
+struct Stager {
+  std::vector<char> buf;
+  size_t add(const void* p, size_t bytes) {
+    size_t off = round_up((int64_t)buf.size(), 256);
+    buf.resize(off + bytes);
+    if (bytes) std::memcpy(buf.data() + off, p, bytes);
+    return off;
+  }
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    return add(v.data(), v.size() * sizeof(T));
+  }
+  char* upload(go_ctx* ctx, cudaStream_t st) {
+    char* dev = reinterpret_cast<char*>(ctx->ensure_small(std::max<size_t>(buf.size(), 256)));
+    char* pin = reinterpret_cast<char*>(ctx->ensure_pinned(std::max<size_t>(buf.size(), 256)));
+    std::memcpy(pin, buf.data(), buf.size());
+    CUDA_CHECK(cudaMemcpyAsync(dev, pin, buf.size(), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaEventRecord(ctx->staged, st));
+    return dev;
+  }
+};
+
+struct BatchMeta {
+  int F = 0;
+  int64_t R = 0;
+  std::vector<int64_t> row_off, gbase;
+  int64_t gtotal = 0;
+  // device
+  const int64_t* d_row_off = nullptr;
+  const int64_t* d_seeds = nullptr;
+  const int64_t* d_gbase = nullptr;
+  const GraphView* d_views = nullptr;
+  const AttnTile* d_trunk_tiles = nullptr;
+  int64_t n_trunk_tiles = 0;
+  const AttnTile* d_head_tiles = nullptr;
+  int64_t n_head_tiles = 0;
+  const int64_t* d_chunks = nullptr;
+  int64_t n_chunks = 0;
+  double trunk_pairs = 0, head_pairs = 0;  // sum of (query, key) pairs per head
+};
+
+static void build_tiles(const std::vector<int64_t>& row_off, int64_t S, bool banded,
+                        std::vector<AttnTile>& out) {
+  const int64_t QT = 64;
+  for (size_t f = 0; f + 1 < row_off.size(); ++f) {
+    int64_t f0 = row_off[f], f1 = row_off[f + 1];
+    if (!banded) {
+      for (int64_t q = f0; q < f1; q += QT) out.push_back({q, std::min(q + QT, f1), f0, f1});
+      continue;
+    }
+    for (int64_t s0 = f0; s0 < f1; s0 += S) {
+      int64_t s1 = std::min(s0 + S, f1);
+      int64_t k0 = std::max(f0, s0 - S);
+      for (int64_t q = s0; q < s1; q += QT) out.push_back({q, std::min(q + QT, s1), k0, s1});
+    }
+  }
+}
+
+static BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
+                           bool need_embed, bool need_trunk, bool need_heads, cudaStream_t st,
+                           const void* extra = nullptr, size_t extra_bytes = 0,
+                           const void** extra_dev = nullptr) {
+  BatchMeta m;
+  m.F = b.num_forwards;
+  GO_CHECK(m.F >= 1, "empty batch");
+  m.row_off.assign(m.F + 1, 0);
+  m.gbase.assign(m.F, 0);
+  std::vector<GraphView> views(m.F);
+  std::vector<int64_t> seeds(m.F, 0);
+  GO_CHECK(b.graphs || (b.row_counts && !need_embed), "graph handles required");
+  for (int f = 0; f < m.F; ++f) {
+    m.gbase[f] = m.gtotal;
+    seeds[f] = b.embed_seeds ? b.embed_seeds[f] : 0;
+    GO_CHECK(seeds[f] >= 0, "seed must be non-negative");
+    if (!b.graphs) {
+      GO_CHECK(b.row_counts[f] >= 0, "negative row count");
+      m.row_off[f + 1] = m.row_off[f] + b.row_counts[f];
+      views[f] = GraphView{};
+      views[f].n = (int32_t)b.row_counts[f];
+      continue;
+    }
+    go_graph* g = b.graphs[f];
+    GO_CHECK(g != nullptr, "null graph handle");
+    if (need_embed) g->ensure_samp(cfg.gs_knn);
+    m.row_off[f + 1] = m.row_off[f] + g->n;
+    m.gtotal += need_embed ? g->samp_total : 0;
+    views[f] = g->view();
+  }
+  m.R = m.row_off[m.F];
+  Stager s;
+  size_t o_row = s.add(m.row_off), o_seed = s.add(seeds), o_gb = s.add(m.gbase),
+         o_views = s.add(views);
+  std::vector<AttnTile> tt, ht;
+  if (need_trunk) build_tiles(m.row_off, cfg.segment_len, true, tt);
+  if (need_heads) build_tiles(m.row_off, 0, false, ht);
+  for (auto& t : tt) m.trunk_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
+  for (auto& t : ht) m.head_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
+  size_t o_tt = s.add(tt), o_ht = s.add(ht);
+  // mean chunks: [nc] r0, [nc] r1, [F] first, [F] end
+  std::vector<int64_t> c0, c1, f0(m.F), f1(m.F);
+  for (int f = 0; f < m.F; ++f) {
+    f0[f] = (int64_t)c0.size();
+    for (int64_t r = m.row_off[f]; r < m.row_off[f + 1]; r += MEAN_CHUNK) {
+      c0.push_back(r);
+      c1.push_back(std::min<int64_t>(r + MEAN_CHUNK, m.row_off[f + 1]));
+    }
+    f1[f] = (int64_t)c0.size();
+  }
+  m.n_chunks = (int64_t)c0.size();
+  std::vector<int64_t> ch;
+  ch.insert(ch.end(), c0.begin(), c0.end());
+  ch.insert(ch.end(), c1.begin(), c1.end());
+  ch.insert(ch.end(), f0.begin(), f0.end());
+  ch.insert(ch.end(), f1.begin(), f1.end());
+  size_t o_ch = s.add(ch);
+  size_t o_ex = s.add(extra, extra_bytes);
+  char* dev = s.upload(ctx, st);
+  if (extra_dev) *extra_dev = dev + o_ex;
+  m.d_row_off = reinterpret_cast<const int64_t*>(dev + o_row);
+  m.d_seeds = reinterpret_cast<const int64_t*>(dev + o_seed);
+  m.d_gbase = reinterpret_cast<const int64_t*>(dev + o_gb);
+  m.d_views = reinterpret_cast<const GraphView*>(dev + o_views);
+  m.d_trunk_tiles = reinterpret_cast<const AttnTile*>(dev + o_tt);
+  m.n_trunk_tiles = (int64_t)tt.size();
+  m.d_head_tiles = reinterpret_cast<const AttnTile*>(dev + o_ht);
+  m.n_head_tiles = (int64_t)ht.size();
+  m.d_chunks = reinterpret_cast<const int64_t*>(dev + o_ch);
+  return m;
+}
+
+// Simple bump allocator over the context workspace.
+struct Arena {
+  char* base;
+  size_t off = 0, cap;
+  template <class T>
+  T* take(int64_t count) {
+    size_t bytes = round_up(std::max<int64_t>(count, 1) * (int64_t)sizeof(T), 256);
+    GO_CHECK(off + bytes <= cap, "workspace overflow");
+    T* p = reinterpret_cast<T*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+static inline int64_t ldp(int w) { return round_up(w, 4); }
+
+static size_t forward_ws_bytes(const go_config_t& c, int64_t R, int64_t gtotal, int F,
+                               int64_t nchunks) {
+  int64_t wmax = std::max(c.gs_dim, c.d_model);
+  int64_t W = (int64_t)c.n_head * c.d_head;
+  int64_t per_row = 6 * ldp((int)wmax) + 4 * ldp((int)W) + ldp(c.d_inner);
+  size_t b = (size_t)R * per_row * 4 + (size_t)R * 8 + (size_t)gtotal * 4 +
+             (size_t)(F + 4) * (ldp(c.d_model) + ldp(c.gs_dim)) * 8 +
+             (size_t)(nchunks + 4) * wmax * 4 + 64 * 256;
+  return b + (1 << 20);
+}
+
+}  // namespace go
+
+using namespace go;
+
+// ---------------------------------------------------------------------------------
+void* go_ctx::ensure(size_t bytes) {
+  if (bytes > ws_bytes) {
+    if (ws) CUDA_CHECK(cudaFree(ws));
+    ws = nullptr;
+    size_t nb = std::max(bytes, ws_bytes + ws_bytes / 4);
+    CUDA_CHECK(cudaMalloc(&ws, nb));
+    ws_bytes = nb;
+  }
+  return ws;
+}
+void* go_ctx::ensure_small(size_t bytes) {
+  if (bytes > ws_small_bytes) {
+    if (staged) CUDA_CHECK(cudaEventSynchronize(staged));
+    if (ws_small) CUDA_CHECK(cudaFree(ws_small));
+    ws_small = nullptr;
+    size_t nb = std::max(bytes, (size_t)1 << 20);
+    CUDA_CHECK(cudaMalloc(&ws_small, nb));
+    ws_small_bytes = nb;
+  } else if (staged) {
+    // the previous call's kernels may still read the small buffer
+    CUDA_CHECK(cudaEventSynchronize(staged));
+  }
+  return ws_small;
+}
+void* go_ctx::ensure_pinned(size_t bytes) {
+  if (bytes > pinned_bytes) {
+    if (pinned) CUDA_CHECK(cudaFreeHost(pinned));
+    pinned = nullptr;
+    size_t nb = std::max(bytes, (size_t)1 << 20);
+    CUDA_CHECK(cudaMallocHost(&pinned, nb));
+    pinned_bytes = nb;
+  }
+  return pinned;
+}
+void* go_ctx::ensure_des(size_t bytes) {
+  if (bytes > des_ws_bytes) {
+    if (des_ws) CUDA_CHECK(cudaFree(des_ws));
+    des_ws = nullptr;
+    CUDA_CHECK(cudaMalloc(&des_ws, bytes));
+    des_ws_bytes = bytes;
+  }
+  return des_ws;
+}
+cudaEvent_t go_ctx::get_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+
+void go_ctx::resolve_timing() {
+  for (auto& t : timed) {
+    CUDA_CHECK(cudaEventSynchronize(t.b));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, t.a, t.b));
+    stat_ms[t.cls] += ms;
+    stat_work[t.cls] += t.work;
+    stat_count[t.cls] += 1;
+    event_pool.push_back(t.a);
+    event_pool.push_back(t.b);
+  }
+  timed.clear();
+}
+
+go_ctx::~go_ctx() {
+  for (auto& t : timed) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  if (staged) cudaEventSynchronize(staged);
+  cudaDeviceSynchronize();
+  if (ws) cudaFree(ws);
+  if (ws_small) cudaFree(ws_small);
+  if (pinned) cudaFreeHost(pinned);
+  if (des_ws) cudaFree(des_ws);
+  if (staged) cudaEventDestroy(staged);
+}
+
+// ---------------------------------------------------------------------------------
+// The forward.  Stage order and math follow the reference exactly; every dense op
+// is one launch over all rows of all forwards in the batch.
+static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
+                        const int64_t* off, const go_batch_t& b, float* node_embed,
+                        float* graph_embed, float* hid, float* logits, float* value,
+                        int32_t* status_dev, cudaStream_t st) {
+  validate(cfg);
+  const bool do_e = b.stage_mask & 1, do_t = b.stage_mask & 2, do_h = b.stage_mask & 4;
+  BatchMeta m = make_meta(ctx, cfg, b, do_e, do_t, do_h, st);
+  const int64_t R = m.R;
+  const int F = m.F;
+  Slots S = slots_of(cfg);
+  auto W_ = [&](int slot) { return P + off[slot]; };
+  const int gs = cfg.gs_dim, dm = cfg.d_model, W = cfg.n_head * cfg.d_head, di = cfg.d_inner;
+  const int64_t wmax = std::max(gs, dm);
+  const int64_t LW = ldp((int)wmax), LA = ldp(W), LI = ldp(di);
+  Arena A{reinterpret_cast<char*>(ctx->ensure(forward_ws_bytes(cfg, R, m.gtotal, F, m.n_chunks))),
+          0, ctx->ws_bytes};
+  float* X[6];
+  for (int i = 0; i < 6; ++i) X[i] = A.take<float>(R * LW);
+  float* Qb = A.take<float>(R * LA);
+  float* Kb = A.take<float>(R * LA);
+  float* Vb = A.take<float>(R * LA);
+  float* Ab = A.take<float>(R * LA);
+  float* F1 = A.take<float>(R * LI);
+  int32_t* row_fwd = A.take<int32_t>(R);
+  int32_t* gidx = A.take<int32_t>(m.gtotal);
+  float* mod = A.take<float>((int64_t)F * dm);
+  float* meanb = A.take<float>((int64_t)F * dm);
+  float* part = A.take<float>((m.n_chunks + 1) * wmax);
+  row_fwd_fill(m.d_row_off, F, R, row_fwd, st);
+
+  // ---- embed (embedding.py:73-98)
+  if (do_e) {
+    GO_CHECK(node_embed && graph_embed, "embed outputs required");
+    int32_t tcol[3] = {0, 0, 0};
+    int c = 16;
+    for (int t = 0; t < cfg.num_tasks; ++t) {
+      tcol[t] = c;
+      c += cfg.task_sizes[t];
+    }
+    neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, F, R, row_fwd, cfg.gs_knn,
+                    gidx, st);
+    float* h = cfg.gs_layers == 0 ? node_embed : X[0];
+    if (b.features)  // explicit feature matrix (embed() called with features)
+      gemm(b.features, b.feature_dim, b.feature_dim, nullptr, 0, 0, W_(S.e_in_w()), gs,
+           W_(S.e_in_b()), h, cfg.gs_layers == 0 ? gs : LW, R, gs, 0, st);
+    else
+      features_inproj(m.d_views, m.d_row_off, row_fwd, R, b.prev_actions, cfg.num_tasks, tcol,
+                      W_(S.e_in_w()), W_(S.e_in_b()), gs, h, cfg.gs_layers == 0 ? gs : LW, st);
+    int64_t ldh = LW;
+    for (int l = 0; l < cfg.gs_layers; ++l) {
+      float* t = X[1];
+      float* pooled = X[2];
+      gemm(h, ldh, gs, nullptr, 0, 0, W_(S.e_layer(l, 0)), gs, W_(S.e_layer(l, 1)), t, LW, R, gs,
+           2, st);
+      {
+        // algorithmic bytes: gathered rows + output rows (fp32) + indices (int32) +
+        // segment offsets (int64) + row->forward map (int32)
+        double bytes = (double)(m.gtotal + R) * gs * 4 + (double)m.gtotal * 4 +
+                       (double)(R + 1) * 8 + (double)R * 4;
+        KTimer kt(ctx, K_SEGMAX, st, bytes);
+        segment_max(t, LW, m.d_views, m.d_row_off, m.d_gbase, row_fwd, gidx, R, gs, pooled, LW,
+                    st);
+      }
+      bool last = l == cfg.gs_layers - 1;
+      float* hn = last ? node_embed : (h == X[0] ? X[3] : X[0]);
+      int64_t ldn = last ? gs : LW;
+      gemm(h, ldh, gs, pooled, LW, gs, W_(S.e_layer(l, 2)), gs, W_(S.e_layer(l, 3)), hn, ldn, R,
+           gs, 1, st);
+      h = hn;
+      ldh = ldn;
+    }
+    if (status_dev) check_finite(node_embed, gs, R, gs, status_dev, st);
+    mean_rows(node_embed, gs, m.d_row_off, F, m.d_chunks, m.n_chunks, gs, graph_embed, gs, part,
+              st);
+  }
+
+  // ---- trunk (policy.py:122-177), layer-major block-banded attention
+  if (do_t) {
+    GO_CHECK(node_embed && graph_embed && hid, "trunk inputs/outputs required");
+    const float* modp = b.mod_override;
+    if (!modp) {
+      int mb = cfg.trf_layers;
+      BlockW bw{W_(S.blk(mb, V_W)),  W_(S.blk(mb, V_B)),  W_(S.blk(mb, O_W)),  W_(S.blk(mb, O_B)),
+                W_(S.blk(mb, LN1_G)), W_(S.blk(mb, LN1_B)), W_(S.blk(mb, FF_W1)),
+                W_(S.blk(mb, FF_B1)), W_(S.blk(mb, FF_W2)), W_(S.blk(mb, FF_B2)),
+                W_(S.blk(mb, LN2_G)), W_(S.blk(mb, LN2_B))};
+      modulate(graph_embed, gs, F, gs, W_(S.p_in_w()), W_(S.p_in_b()), bw, dm, W, di, mod, st);
+      modp = mod;
+    }
+    float* x = cfg.trf_layers == 0 ? hid : X[0];
+    int64_t ldx = cfg.trf_layers == 0 ? dm : LW;
+    gemm(node_embed, gs, gs, nullptr, 0, 0, W_(S.p_in_w()), dm, W_(S.p_in_b()), x, ldx, R, dm, 0,
+         st);
+    for (int l = 0; l < cfg.trf_layers; ++l) {
+      float* xm = X[1];
+      mul_rowvec(x, ldx, modp, dm, row_fwd, xm, LW, R, dm, st);
+      gemm(xm, LW, dm, nullptr, 0, 0, W_(S.blk(l, Q_W)), W, W_(S.blk(l, Q_B)), Qb, LA, R, W, 0, st);
+      gemm(xm, LW, dm, nullptr, 0, 0, W_(S.blk(l, K_W)), W, W_(S.blk(l, K_B)), Kb, LA, R, W, 0, st);
+      gemm(xm, LW, dm, nullptr, 0, 0, W_(S.blk(l, V_W)), W, W_(S.blk(l, V_B)), Vb, LA, R, W, 0, st);
+      {
+        KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
+        attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
+                  LA, st);
+      }
+      float* o = X[2];
+      gemm(Ab, LA, W, nullptr, 0, 0, W_(S.blk(l, O_W)), dm, W_(S.blk(l, O_B)), o, LW, R, dm, 0, st);
+      float* h1 = X[3];
+      add_layernorm(xm, LW, o, LW, W_(S.blk(l, LN1_G)), W_(S.blk(l, LN1_B)), h1, LW, R, dm, st);
+      gemm(h1, LW, dm, nullptr, 0, 0, W_(S.blk(l, FF_W1)), di, W_(S.blk(l, FF_B1)), F1, LI, R, di, 1,
+           st);
+      float* f2 = X[4];
+      gemm(F1, LI, di, nullptr, 0, 0, W_(S.blk(l, FF_W2)), dm, W_(S.blk(l, FF_B2)), f2, LW, R, dm, 0,
+           st);
+      bool last = l == cfg.trf_layers - 1;
+      float* xn = last ? hid : (x == X[0] ? X[5] : X[0]);
+      int64_t ldn = last ? dm : LW;
+      add_layernorm(h1, LW, f2, LW, W_(S.blk(l, LN2_G)), W_(S.blk(l, LN2_B)), xn, ldn, R, dm, st);
+      x = xn;
+      ldx = ldn;
+    }
+  }
+
+  // ---- task heads (policy.py:187-217), full N x N attention per forward
+  if (do_h) {
+    GO_CHECK(hid && logits, "heads inputs/outputs required");
+    float* a_prev = nullptr;
+    int64_t ld_prev = LW;
+    float* rep_bufs[2] = {X[4], X[5]};
+    int64_t lcol = 0;
+    for (int t = 0; t < cfg.num_tasks; ++t) {
+      bool zero_in = (a_prev == nullptr) || (b.ablate_mask >> t & 1);
+      float* c = X[0];
+      if (zero_in)  // [0 | hid] @ cat_w == hid @ cat_w[d:]
+        gemm(hid, dm, dm, nullptr, 0, 0, W_(S.task(t, CAT_W)) + (int64_t)dm * dm, dm,
+             W_(S.task(t, CAT_B)), c, LW, R, dm, 0, st);
+      else
+        gemm(a_prev, ld_prev, dm, hid, dm, dm, W_(S.task(t, CAT_W)), dm, W_(S.task(t, CAT_B)), c, LW,
+             R, dm, 0, st);
+      float* hh = X[1];
+      add_layernorm(c, LW, nullptr, 0, W_(S.task(t, LN_G)), W_(S.task(t, LN_B)), hh, LW, R, dm, st);
+      gemm(hh, LW, dm, nullptr, 0, 0, W_(S.ta(Q_W)), W, W_(S.ta(Q_B)), Qb, LA, R, W, 0, st);
+      gemm(hh, LW, dm, nullptr, 0, 0, W_(S.ta(K_W)), W, W_(S.ta(K_B)), Kb, LA, R, W, 0, st);
+      gemm(hh, LW, dm, nullptr, 0, 0, W_(S.ta(V_W)), W, W_(S.ta(V_B)), Vb, LA, R, W, 0, st);
+      {
+        KTimer kt(ctx, K_HEADS_ATTN, st, 4.0 * m.head_pairs * W);
+        attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_head_tiles, m.n_head_tiles, Ab, LA,
+                  st);
+      }
+      float* o = X[2];
+      gemm(Ab, LA, W, nullptr, 0, 0, W_(S.ta(O_W)), dm, W_(S.ta(O_B)), o, LW, R, dm, 0, st);
+      gemm(o, LW, dm, nullptr, 0, 0, W_(S.task(t, FC_W1)), di, W_(S.task(t, FC_B1)), F1, LI, R, di,
+           1, st);
+      float* rep = b.reps ? b.reps + (int64_t)t * R * dm : rep_bufs[t & 1];
+      const int64_t ldr = b.reps ? dm : LW;
+      gemm(F1, LI, di, nullptr, 0, 0, W_(S.task(t, FC_W2)), dm, W_(S.task(t, FC_B2)), rep, ldr, R,
+           dm, 0, st);
+      int a = cfg.task_sizes[t];
+      gemm(rep, ldr, dm, nullptr, 0, 0, W_(S.task(t, OUT_W)), a, W_(S.task(t, OUT_B)), logits + lcol,
+           a, R, a, 0, st);
+      lcol += R * a;
+      a_prev = rep;
+      ld_prev = ldr;
+    }
+    if (value) {
+      mean_rows(a_prev, ld_prev, m.d_row_off, F, m.d_chunks, m.n_chunks, dm, meanb, dm, part, st);
+      value_head(meanb, F, dm, W_(S.value_w()), W_(S.value_b()), value, st);
+    }
+  }
+}
+
+extern "C" {
+
+const char* go_last_error(void) { return g_last_error.c_str(); }
+int go_version(void) { return 1; }
+
+long long go_launch_count(void) { return go::g_launch_count.load(); }
+
+int go_ctx_set_timing(go_ctx_t ctx, int enable) {
+  return guarded([&] {
+    ctx->resolve_timing();
+    for (int i = 0; i < K_NUM_CLASSES; ++i) {
+      ctx->stat_ms[i] = 0;
+      ctx->stat_work[i] = 0;
+      ctx->stat_count[i] = 0;
+    }
+    ctx->timing = enable != 0;
+  });
+}
+
+int go_ctx_kernel_stats(go_ctx_t ctx, int32_t cls, int64_t* count, double* total_ms,
+                        double* total_work) {
+  return guarded([&] {
+    GO_CHECK(cls >= 0 && cls < K_NUM_CLASSES, "bad kernel class");
+    ctx->resolve_timing();
+    *count = ctx->stat_count[cls];
+    *total_ms = ctx->stat_ms[cls];
+    *total_work = ctx->stat_work[cls];
+  });
+}
+
+int go_ctx_create(int device, go_ctx_t* out) {
+  return guarded([&] {
+    int n = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&n));
+    GO_CHECK(device >= 0 && device < n, "no CUDA device %d (found %d)", device, n);
+    CUDA_CHECK(cudaSetDevice(device));
+    auto* c = new go_ctx();
+    c->device = device;
+    CUDA_CHECK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
+    *out = c;
+  });
+}
+
+int go_ctx_destroy(go_ctx_t ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int go_ctx_workspace_bytes(go_ctx_t ctx, int64_t* out) {
+  return guarded([&] { *out = (int64_t)(ctx->ws_bytes + ctx->ws_small_bytes + ctx->des_ws_bytes); });
+}
+
+int go_param_count(const go_config_t* cfg, int32_t* num_slots_out) {
+  return guarded([&] {
+    validate(*cfg);
+    *num_slots_out = slots_of(*cfg).count();
+  });
+}
+
+int go_forward(go_ctx_t ctx, const go_config_t* cfg, const float* params,
+               const int64_t* param_offsets, const go_batch_t* batch, float* node_embed,
+               float* graph_embed, float* hid, float* logits, float* value, void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    run_forward(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid, logits,
+                value, nullptr, (cudaStream_t)stream);
+  });
+}
+
+// variant with a device status word (bit0: non-finite embeddings)
+int go_forward_status(go_ctx_t ctx, const go_config_t* cfg, const float* params,
+                      const int64_t* param_offsets, const go_batch_t* batch, float* node_embed,
+                      float* graph_embed, float* hid, float* logits, float* value,
+                      int32_t* status_dev, void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    run_forward(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid, logits,
+                value, status_dev, (cudaStream_t)stream);
+  });
+}
+
+int go_neighbor_arrays(go_ctx_t ctx, go_graph_t g, int64_t seed, int32_t k, int64_t* seg_off_out,
+                       int32_t* gather_dev, void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    GO_CHECK(k >= 1, "k must be >= 1");
+    GO_CHECK(seed >= 0, "seed must be non-negative");
+    g->ensure_samp(k);
+    std::vector<int64_t> so(g->n + 1, 0);
+    for (int r = 0; r < g->n; ++r)
+      so[r + 1] = so[r] + std::min<int64_t>(g->nbr_off[r + 1] - g->nbr_off[r], k);
+    std::copy(so.begin(), so.end(), seg_off_out);
+    if (!gather_dev) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    go_config_t cfg{};
+    cfg.gs_knn = k;
+    go_graph_t gs[1] = {g};
+    int64_t seeds[1] = {seed};
+    go_batch_t b{};
+    b.num_forwards = 1;
+    b.graphs = gs;
+    b.embed_seeds = seeds;
+    BatchMeta m = make_meta(ctx, cfg, b, true, false, false, st);
+    Arena A{reinterpret_cast<char*>(ctx->ensure((size_t)m.R * 4 + 4096)), 0, ctx->ws_bytes};
+    int32_t* row_fwd = A.take<int32_t>(m.R);
+    row_fwd_fill(m.d_row_off, 1, m.R, row_fwd, st);
+    neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, 1, m.R, row_fwd, k, gather_dev,
+                    st);
+  });
+}
+
+int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards, const go_graph_t* graphs,
+              const int64_t* row_counts, const uint64_t* pcg_states, const void* logits,
+              int32_t logits_f64, double temperature, int32_t* actions_out, double* logp_out,
+              void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    validate(*cfg);
+    GO_CHECK(temperature >= 0.0, "temperature must be >= 0");
+    GO_CHECK(pcg_states != nullptr, "generator states required");
+    cudaStream_t st = (cudaStream_t)stream;
+    go_batch_t b{};
+    b.num_forwards = num_forwards;
+    b.graphs = graphs;
+    b.row_counts = row_counts;
+    const void* dstate_v = nullptr;
+    BatchMeta m = make_meta(ctx, *cfg, b, false, false, false, st, pcg_states,
+                            (size_t)num_forwards * 32, &dstate_v);
+    const uint64_t* dstate = reinterpret_cast<const uint64_t*>(dstate_v);
+    Arena A{reinterpret_cast<char*>(ctx->ensure((size_t)m.R * 8 + 8192)), 0, ctx->ws_bytes};
+    int32_t* row_fwd = A.take<int32_t>(m.R);
+    int32_t* row_node = A.take<int32_t>(m.R);
+    row_fwd_fill(m.d_row_off, m.F, m.R, row_fwd, st);
+    row_node_fill(m.d_views, m.d_row_off, row_fwd, m.R, row_node, st);
+    int64_t col = 0;
+    const int T = cfg->num_tasks;
+    for (int t = 0; t < T; ++t) {
+      int a = cfg->task_sizes[t];
+      const char* lp = reinterpret_cast<const char*>(logits) + col * (logits_f64 ? 8 : 4);
+      sample_rows(lp, logits_f64, a, a, m.R, m.d_row_off, row_fwd, row_node, dstate, t,
+                  temperature, actions_out + (int64_t)t * m.R, logp_out + (int64_t)t * m.R, st);
+      col += m.R * a;
+    }
+  });
+}
+
+int go_simulate(go_ctx_t ctx, go_graph_t g, int32_t K, const int32_t* placement,
+                const int32_t* priorities, int32_t prio_per_placement, int32_t d,
+                const double* peak, const double* mem_bw, const double* cap,
+                const double* link_bw, int32_t policy, double baseline, double* step_time,
+                uint8_t* valid, int8_t* violation, double* busy, double* peak_mem, double* reward,
+                void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    GO_CHECK(policy == 0 || policy == 1, "unknown policy");
+    GO_CHECK(d >= 1, "need at least one device");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!g->acyclic) {
+      // simulator.py:317-319: cycle_after_fusion -> (0, invalid, zeros)
+      std::vector<double> z((size_t)K * d, 0.0), zk(K, 0.0), rk(K, -10.0);
+      std::vector<uint8_t> v(K, 0);
+      std::vector<int8_t> vi(K, 3);
+      CUDA_CHECK(cudaMemcpyAsync(step_time, zk.data(), K * 8, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(valid, v.data(), K, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(violation, vi.data(), K, cudaMemcpyHostToDevice, st));
+      if (busy) CUDA_CHECK(cudaMemcpyAsync(busy, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
+      if (peak_mem)
+        CUDA_CHECK(cudaMemcpyAsync(peak_mem, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
+      if (reward && baseline > 0)
+        CUDA_CHECK(cudaMemcpyAsync(reward, rk.data(), K * 8, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      return;
+    }
+    KTimer kt(ctx, K_DES, st, (double)K * g->n);
+    simulate_batch(g->des, K, placement, g->n, priorities, prio_per_placement ? g->n : 0, d, peak,
+                   mem_bw, cap, link_bw, policy, baseline, step_time, valid, violation, busy,
+                   peak_mem, reward, ctx, st);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+// Internal structures of libgo_b200: context, graph handle, kernel launchers.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+// Device view of one graph's static tables (topo-row space unless noted).
+struct GraphView {
+  int32_t n;
+  const int32_t* order;    // topo row -> node id
+  const int32_t* op_row;   // op index per topo row
+  const float* static4;    // [n][4]: log1p(flops), log1p(out_bytes), indeg, outdeg
+  const int64_t* nbr_off;  // [n+1] undirected neighbours, CSR by topo row
+  const int32_t* nbr_row;  // neighbour topo rows, sorted by neighbour node id
+  const int64_t* samp_off; // [n+1] prefix of min(deg, k) for the configured k
+};
+
+// Device DES tables of the current (fused) grouping: simulator.py:86-172.
+struct DesView {
+  int32_t n, G;
+  const int32_t* grp_rep;      // [G] lowest member node id
+  const int32_t* pending0;     // [G] #external in-edges
+  const int64_t* out_off;      // [G+1] external out edges sorted (src, dst), stable
+  const int32_t* out_grp;      // destination group per out edge
+  const double* out_bytes;     // bytes per out edge
+  const double* cost_flops;    // [G]
+  const double* cost_bytes;    // [G]
+  const int32_t* topo_index;   // [G]
+  const double* resident;      // [G]
+  const int32_t* nsucc;        // [G] distinct successor groups
+  const int64_t* pred_off;     // [G+1] distinct predecessor groups
+  const int32_t* pred_grp;
+  const int64_t* coloc_off;    // [C+1] colocation groups -> member groups
+  const int32_t* coloc_grp;
+  int32_t num_coloc;
+  int32_t mem_int_exact;       // all resident bytes integral and sum < 2**53
+  int64_t max_out_deg;
+  int64_t num_edges;            // external out edges in total
+};
+
+// Kernel classes timed with CUDA events on the launching stream (go_ctx_set_timing).
+enum KernelClass { K_HEADS_ATTN = 0, K_TRUNK_ATTN, K_SEGMAX, K_GEMM, K_DES, K_SAMPLE,
+                   K_NEIGHBOR, K_OTHER, K_NUM_CLASSES };
+
+struct TimedLaunch {
+  int cls;
+  cudaEvent_t a, b;
+  double work;  // algorithmic units (flops or bytes) of this launch, set by the caller
+};
+
+struct go_ctx {
+  int device = 0;
+  bool timing = false;
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> event_pool;
+  double stat_ms[K_NUM_CLASSES] = {0};
+  double stat_work[K_NUM_CLASSES] = {0};
+  long long stat_count[K_NUM_CLASSES] = {0};
+  cudaEvent_t get_event();
+  void resolve_timing();
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* ws_small = nullptr;  // metadata uploads (row offsets, tiles, graph views)
+  size_t ws_small_bytes = 0;
+  void* pinned = nullptr;    // pinned staging for metadata
+  size_t pinned_bytes = 0;
+  cudaEvent_t staged = nullptr;  // last metadata upload done
+  void* des_ws = nullptr;
+  size_t des_ws_bytes = 0;
+  void* ensure(size_t bytes);
+  void* ensure_small(size_t bytes);
+  void* ensure_pinned(size_t bytes);
+  void* ensure_des(size_t bytes);
+  ~go_ctx();
+};
+
+struct go_graph {
+  go_ctx* ctx = nullptr;
+  int32_t n = 0;
+  int64_t e = 0;
+  std::vector<int32_t> order, pos, op, src, dst, coloc;
+  std::vector<double> flops, out_bytes, ebytes;
+  std::vector<int64_t> nbr_off;
+  std::vector<int32_t> nbr_row;
+  // device
+  int32_t* d_order = nullptr;
+  int32_t* d_op_row = nullptr;
+  float* d_static4 = nullptr;
+  int64_t* d_nbr_off = nullptr;
+  int32_t* d_nbr_row = nullptr;
+  int64_t* d_samp_off = nullptr;
+  int32_t samp_k = -1;
+  int64_t samp_total = 0;
+  // DES
+  DesView des{};
+  std::vector<void*> des_allocs;
+  bool acyclic = true;
+  void set_fusion(const std::vector<int64_t>& label);
+  void ensure_samp(int32_t k);
+  GraphView view() const;
+  ~go_graph();
+};
+
+namespace go {
+
+// RAII: records start/stop events around the launches in its scope when timing is on.
+struct KTimer {
+  go_ctx* ctx;
+  int cls;
+  cudaStream_t st;
+  double work;
+  cudaEvent_t a = nullptr;
+  KTimer(go_ctx* c, int k, cudaStream_t s, double w) : ctx(c), cls(k), st(s), work(w) {
+    if (ctx && ctx->timing) {
+      a = ctx->get_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~KTimer() {
+    if (ctx && ctx->timing && a) {
+      cudaEvent_t b = ctx->get_event();
+      cudaEventRecord(b, st);
+      ctx->timed.push_back({cls, a, b, work});
+    }
+  }
+};
+
+// ---- kernels: dense.cu
+void gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
+          const float* W, int64_t ldw, const float* bias, float* C, int64_t ldc, int64_t M,
+          int N, int act, cudaStream_t st);
+void add_layernorm(const float* a, int64_t lda, const float* b, int64_t ldb, const float* g,
+                   const float* beta, float* out, int64_t ldo, int64_t M, int D, cudaStream_t st);
+void mul_rowvec(const float* x, int64_t ldx, const float* vec, int64_t ldv,
+                const int32_t* row_fwd, float* out, int64_t ldo, int64_t M, int D,
+                cudaStream_t st);
+constexpr int MEAN_CHUNK = 256;
+void mean_rows(const float* x, int64_t ldx, const int64_t* row_off_dev, int F,
+               const int64_t* chunk_tab, int64_t nc, int D, float* out, int64_t ldo,
+               float* part, cudaStream_t st);
+void check_finite(const float* x, int64_t ld, int64_t M, int D, int32_t* flag, cudaStream_t st);
+void row_fwd_fill(const int64_t* row_off_dev, int F, int64_t R, int32_t* row_fwd,
+                  cudaStream_t st);
+// one length-1 transformer block + 2*sigmoid per forward (policy.py:122-132)
+struct BlockW {
+  const float *v_w, *v_b, *o_w, *o_b, *ln1_g, *ln1_b, *w1, *b1, *w2, *b2, *ln2_g, *ln2_b;
+};
+void modulate(const float* graph_embed, int64_t ldg, int F, int gs_dim, const float* in_w,
+              const float* in_b, const BlockW& w, int d_model, int d_head_total, int d_inner,
+              float* mod_out, cudaStream_t st);
+void value_head(const float* mean, int F, int D, const float* w, const float* b, float* out,
+                cudaStream_t st);
+
+// ---- kernels: embed.cu
+void neighbor_sample(const GraphView* views_dev, const int64_t* row_off_dev,
+                     const int64_t* gbase_dev, const int64_t* seeds_dev, int F,
+                     int64_t total_rows, const int32_t* row_fwd, int k, int32_t* gidx,
+                     cudaStream_t st);
+void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
+                     const int32_t* row_fwd, int64_t R, const int32_t* prev_actions,
+                     int num_tasks, const int32_t* task_col, const float* in_w,
+                     const float* in_b, int D, float* h, int64_t ldh, cudaStream_t st);
+void segment_max(const float* t, int64_t ldt, const GraphView* views_dev,
+                 const int64_t* row_off_dev, const int64_t* gbase_dev, const int32_t* row_fwd,
+                 const int32_t* gidx, int64_t R, int D, float* out, int64_t ldo,
+                 cudaStream_t st);
+
+void row_node_fill(const GraphView* views_dev, const int64_t* row_off_dev,
+                   const int32_t* row_fwd, int64_t R, int32_t* row_node, cudaStream_t st);
+
+// ---- kernels: attention.cu
+struct AttnTile {
+  int64_t q0, q1, k0, k1;
+};
+void attention(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+               int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
+               int64_t ldo, cudaStream_t st);
+
+// ---- kernels: sample.cu
+void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t R,
+                 const int64_t* row_off_dev, const int32_t* row_fwd, const int32_t* order_of_row,
+                 const uint64_t* pcg_dev, int64_t task, double temperature,
+                 int32_t* actions, double* logp, cudaStream_t st);
+
+// ---- kernels: des.cu
+int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t pstride,
+                   const int32_t* prio, int64_t prio_stride, int d, const double* peak,
+                   const double* mem_bw, const double* cap, const double* link_bw, int policy,
+                   double baseline, double* step_time, uint8_t* valid, int8_t* violation,
+                   double* busy, double* peak_mem, double* reward, go_ctx* ctx,
+                   cudaStream_t st);
+
+}  // namespace go

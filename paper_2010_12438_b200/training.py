@@ -1,0 +1,336 @@
+"""Rollout collection (and the PPO update) on the B200 (mirrors training.py:1-384).
+
+collect_rollouts keeps the reference signature and per-sample fields; underneath,
+all K rollouts are decided in waves of batched forwards (iteration-major: every
+rollout's iteration-1 forward, sample, then iteration-2 ...) and all placements
+of a graph are scored by ONE batched DES launch with the reward fused in.
+Results stay on the device until a field is read.
+"""
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .baselines import default_assignments
+from .config import INVALID_REWARD, EmbedConfig, FusionConfig, PolicyConfig, PPOHyper, ordered_tasks
+from .engine import (DeviceArray, advance, check_status, forward_batch, params_on_device,
+                     pcg_words, sample_batch)
+from .graph import as_graph
+from .policy import TaskActionBundle
+from .runtime import context, torch
+from .simulator import ActionAssignment, FusedGraph, apply_fusion, simulate_many
+
+__all__ = ["Reward", "reward", "PPOHyper", "RolloutSample", "RolloutBatch", "task_action_sizes",
+           "bundle_assignments", "collect_rollouts", "run_decisions", "INVALID_REWARD"]
+
+
+@dataclass(frozen=True)
+class Reward:
+    value: float
+    source: str  # "measured" | "invalid"
+
+
+def reward(step_time: float, baseline_time: float, valid: bool) -> Reward:
+    """training.py:37-44 (the batched path computes the same value in des.cu)."""
+    if baseline_time <= 0:
+        raise ValueError("baseline_time must be positive")
+    if not valid:
+        return Reward(INVALID_REWARD, "invalid")
+    return Reward(-math.sqrt(step_time / baseline_time), "measured")
+
+
+def task_action_sizes(topology, tasks, num_levels: int) -> dict:
+    """training.py:93-98."""
+    from .costmodel import as_topology
+    d = as_topology(topology).num_devices
+    return {t: (d if t == "placement" else num_levels) for t in tasks}
+
+
+def bundle_assignments(graph, topology, bundle, task_sizes, fusion_cfg, base=None) -> dict:
+    """training.py:101-111."""
+    asg = dict(base) if base else default_assignments(graph, topology, fusion_cfg.num_levels)
+    for task, a in task_sizes.items():
+        asg[task] = ActionAssignment(task, bundle.actions[task], a)
+    return asg
+
+
+# ---------------------------------------------------------------------------------------
+# decisions
+
+def _wave_rows() -> int:
+    return int(os.environ.get("GO_WAVE_ROWS", str(1 << 21)))
+
+
+def _waves(sizes, max_rows):
+    waves, cur, rows = [], [], 0
+    for i, n in enumerate(sizes):
+        if cur and rows + n > max_rows:
+            waves.append(cur)
+            cur, rows = [], 0
+        cur.append(i)
+        rows += n
+    if cur:
+        waves.append(cur)
+    return waves
+
+
+class DecisionWave:
+    """Device results of one wave of rollouts (all tensors on device).
+    actions/prev: int32 [T, R] node-indexed per rollout span; logp f64 [T, R]."""
+
+    def __init__(self, idx, handles, row_off):
+        self.idx = idx
+        self.handles = handles
+        self.row_off = row_off
+        self.iters = []  # per iteration dict(actions, logp, value, logits)
+
+
+def decide(store, graphs, embed_cfg, cfg, task_sizes, iterations, seeds, temperature,
+           keep_logits=True, keep_trajectory=False, params=None):
+    """Batched iterate_decisions over rollouts (graphs[k], seeds[k]).  Returns a list
+    of DecisionWave covering all rollouts in order."""
+    ctx = context()
+    handles = [ctx.graph(g) for g in graphs]
+    tasks = ordered_tasks(task_sizes)
+    params = params or params_on_device(store, embed_cfg, cfg, task_sizes)
+    out_waves = []
+    statuses = []
+    for idx in _waves([h.n for h in handles], _wave_rows()):
+        hs = [handles[i] for i in idx]
+        sd = [int(seeds[i]) for i in idx]
+        rngs = [np.random.default_rng(s) for s in sd]
+        row_off = np.zeros(len(idx) + 1, np.int64)
+        row_off[1:] = np.cumsum([h.n for h in hs])
+        wave = DecisionWave(idx, hs, row_off)
+        prev = None
+        for it in range(iterations):
+            out = forward_batch(store, embed_cfg, cfg, task_sizes, hs, sd, prev_actions=prev,
+                                params=params)
+            statuses.append(out.status)
+            acts, logp = sample_batch(embed_cfg, cfg, task_sizes, hs, [pcg_words(r) for r in rngs],
+                                      out.logits_packed, temperature)
+            if temperature > 0:
+                for r, h in zip(rngs, hs):
+                    advance(r, len(tasks) * h.n)
+            rec = dict(actions=acts, logp=logp, value=out.value, prev=prev,
+                       logits=out.logits if keep_logits else None)
+            if keep_trajectory or it == iterations - 1:
+                wave.iters.append(rec)
+            prev = acts
+        out_waves.append(wave)
+    for s in statuses:
+        if int(s.item()) & 1:
+            raise FloatingPointError("non-finite node embeddings (bad init or features)")
+    return out_waves
+
+
+def _bundle(wave, rec, j, tasks, seed, temperature, order):
+    lo, hi = int(wave.row_off[j]), int(wave.row_off[j + 1])
+    acts = rec["actions"][:, lo:hi].cpu().numpy().astype(np.int64)
+    logp = rec["logp"][:, lo:hi].cpu().numpy()
+    prev = None
+    if rec["prev"] is not None:
+        pv = rec["prev"][:, lo:hi].cpu().numpy().astype(np.int64)
+        prev = {t: pv[i].copy() for i, (t, _a) in enumerate(tasks)}
+    logits = {}
+    if rec["logits"] is not None:
+        for i, (t, _a) in enumerate(tasks):
+            logits[t] = rec["logits"][i][lo:hi].cpu().numpy().astype(np.float64)
+    return TaskActionBundle(
+        tasks=[t for t, _ in tasks], logits=logits,
+        actions={t: acts[i] for i, (t, _a) in enumerate(tasks)},
+        log_probs={t: logp[i] for i, (t, _a) in enumerate(tasks)},
+        value=float(rec["value"][j].item()), prev_actions=prev, embed_seed=int(seed),
+        temperature=temperature)
+
+
+def run_decisions(store, graphs, embed_cfg, cfg, task_sizes, iterations, seeds, temperature=1.0,
+                  keep_trajectory=False):
+    """Host bundles per rollout: list (per rollout) of per-iteration bundles."""
+    tasks = ordered_tasks(task_sizes)
+    waves = decide(store, graphs, embed_cfg, cfg, task_sizes, iterations, seeds, temperature,
+                   keep_logits=True, keep_trajectory=keep_trajectory)
+    out = [None] * len(graphs)
+    for w in waves:
+        for j, k in enumerate(w.idx):
+            out[k] = [_bundle(w, rec, j, tasks, seeds[k], temperature, None) for rec in w.iters]
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# rollouts
+
+@dataclass
+class RolloutSample:
+    graph_index: int
+    bundle: object
+    reward: float
+    value_estimate: float
+    advantage: float
+    step_time: float
+    valid: bool
+
+
+class LazyBundle:
+    """TaskActionBundle view over device results; arrays are fetched on access."""
+
+    def __init__(self, batch, k):
+        self._b, self._k = batch, k
+        self._cache = None
+
+    def _get(self):
+        if self._cache is None:
+            b = self._b
+            w, j = b._loc[self._k]
+            self._cache = _bundle(b._waves[w], b._waves[w].iters[-1], j, b._tasks, b.seeds[self._k],
+                                  b.temperature, None)
+        return self._cache
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self._get(), name)
+
+
+class RolloutBatch:
+    """training.py:79-90 with device-resident per-rollout results."""
+
+    def __init__(self, samples=None):
+        self._samples = samples
+        self.rewards = None
+
+    @property
+    def samples(self) -> list:
+        if self._samples is None:
+            self._materialize()
+        return self._samples
+
+    def _materialize(self):
+        r = self.rewards.cpu().numpy()
+        st = self.step_times.cpu().numpy()
+        va = self.valid.cpu().numpy().astype(bool)
+        vals = self.values.cpu().numpy().astype(np.float64)
+        self._samples = [RolloutSample(graph_index=int(self.graph_index[k]),
+                                       bundle=LazyBundle(self, k), reward=float(r[k]),
+                                       value_estimate=float(vals[k]),
+                                       advantage=float(r[k] - vals[k]), step_time=float(st[k]),
+                                       valid=bool(va[k]))
+                         for k in range(len(r))]
+
+    @property
+    def mean_reward(self) -> float:
+        return float(np.mean([s.reward for s in self.samples]))
+
+    def any_valid(self) -> bool:
+        return any(s.valid for s in self.samples)
+
+
+def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed, hyper,
+                     embed_cfg, policy_cfg, fusion_cfg, base_assignments=None,
+                     keep_logits: bool = True, shard=None) -> RolloutBatch:
+    """training.py:114-143: `count` independent decision bundles, graphs drawn
+    uniformly by the same outer numpy stream; all scored on device.
+
+    shard=(rank, world) scores only global rollouts [rank*count/world,
+    (rank+1)*count/world) (rollouts are independent, no
+    communication while scoring); when torch.distributed is initialised the
+    per-rollout results are then all-gathered (NCCL) into batch.global_*."""
+    T = torch()
+    dev = T.device("cuda", context().device)
+    graphs = [as_graph(g) for g in graphs]
+    rng = np.random.default_rng(seed)
+    gi_all = np.empty(count, np.int64)
+    seeds_all = np.empty(count, np.int64)
+    for k in range(count):
+        gi_all[k] = int(rng.integers(len(graphs)))
+        seeds_all[k] = int(rng.integers(2**31))
+    lo, hi = 0, count
+    if shard is not None:
+        r, w = shard
+        lo, hi = r * count // w, (r + 1) * count // w
+    gi, seeds = gi_all[lo:hi], seeds_all[lo:hi]
+    count = hi - lo
+    tasks = ordered_tasks(task_sizes)
+    waves = decide(store, [graphs[i] for i in gi], embed_cfg, policy_cfg, task_sizes,
+                   policy_cfg.iterations, seeds, hyper.temperature, keep_logits=keep_logits)
+    batch = RolloutBatch()
+    batch._waves, batch._tasks, batch.seeds, batch.temperature = waves, tasks, seeds, hyper.temperature
+    batch.graph_index = gi
+    batch._loc = [None] * count
+    for w_i, w in enumerate(waves):
+        for j, k in enumerate(w.idx):
+            batch._loc[k] = (w_i, j)
+    tnames = [t for t, _ in tasks]
+    rewards = T.empty(count, dtype=T.float64, device=dev)
+    steps = T.empty(count, dtype=T.float64, device=dev)
+    valid = T.empty(count, dtype=T.uint8, device=dev)
+    values = T.empty(count, dtype=T.float32, device=dev)
+    for w in waves:
+        rec = w.iters[-1]
+        ix = T.as_tensor(np.asarray(w.idx, np.int64), device=dev)
+        values[ix] = rec["value"]
+    for g_i, g in enumerate(graphs):
+        ks = np.flatnonzero(gi == g_i)
+        if len(ks) == 0:
+            continue
+        base = (base_assignments[g_i] if base_assignments
+                else default_assignments(g, topology, fusion_cfg.num_levels))
+        n = g.num_nodes
+
+        def task_rows(task):
+            t = tnames.index(task)
+            rows = []
+            for k in ks:
+                w_i, j = batch._loc[k]
+                w = waves[w_i]
+                lo = int(w.row_off[j])
+                rows.append(w.iters[-1]["actions"][t, lo:lo + n])
+            return T.stack(rows)
+
+        pl = (task_rows("placement") if "placement" in task_sizes
+              else T.as_tensor(base["placement"].actions, device=dev).to(T.int32).expand(len(ks), n))
+        pr = (task_rows("schedule_priority") if "schedule_priority" in task_sizes
+              else T.as_tensor(base["schedule_priority"].actions, device=dev).to(T.int32))
+        ix = T.as_tensor(ks, device=dev)
+        if "fusion_priority" in task_sizes:
+            fus = task_rows("fusion_priority").cpu().numpy()
+            for r, k in enumerate(ks):
+                fg = apply_fusion(g, ActionAssignment("fusion_priority", fus[r],
+                                                      task_sizes["fusion_priority"]), fusion_cfg)
+                res = simulate_many(fg, pl[r:r + 1], pr[r] if pr.dim() == 2 else pr, topology,
+                                    baseline=baselines[g_i])
+                rewards[ix[r:r + 1]] = res.reward
+                steps[ix[r:r + 1]] = res.step_time
+                valid[ix[r:r + 1]] = res.valid
+        else:
+            fg = apply_fusion(g, base["fusion_priority"], fusion_cfg)
+            res = simulate_many(fg, pl.contiguous(), pr, topology, baseline=baselines[g_i])
+            rewards[ix] = res.reward
+            steps[ix] = res.step_time
+            valid[ix] = res.valid
+    batch.rewards, batch.step_times, batch.valid, batch.values = rewards, steps, valid, values
+    batch.shard = (lo, hi)
+    if shard is not None and shard[1] > 1:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            # the one exchange of the scoring path: per-rollout results to every rank
+            packed = T.stack([rewards, steps, valid.to(T.float64), values.to(T.float64)])
+            sizes = [(q + 1) * len(gi_all) // shard[1] - q * len(gi_all) // shard[1]
+                     for q in range(shard[1])]
+            bufs = [T.empty((4, s), dtype=T.float64, device=dev) for s in sizes]
+            if len(set(sizes)) == 1:
+                dist.all_gather(bufs, packed)
+            else:
+                mx = max(sizes)
+                pad = T.zeros((4, mx), dtype=T.float64, device=dev)
+                pad[:, :packed.shape[1]] = packed
+                tmp = [T.empty((4, mx), dtype=T.float64, device=dev) for _ in sizes]
+                dist.all_gather(tmp, pad)
+                bufs = [t[:, :s] for t, s in zip(tmp, sizes)]
+            full = T.cat(bufs, dim=1)
+            batch.global_rewards, batch.global_step_times = full[0], full[1]
+            batch.global_valid, batch.global_values = full[2] > 0.5, full[3]
+    return batch

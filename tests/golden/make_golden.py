@@ -335,8 +335,36 @@ def make_ppo():
     np.savez_compressed(OUT / "golden_ppo.npz", **out)
 
 
+WORKLOAD_SPECS = [
+    ("attention-stack", 10, 1, 64, 0), ("multi-branch-cnn", 1857, 1, 64, 0),
+    ("dilated-stack", 30, 250, 64, 0), ("dilated-stack", 10, 250, 64, 1),
+    ("dilated-stack", 5, 100, 64, 2), ("dilated-stack", 2, 50, 64, 3),
+    ("attention-stack", 8000, 1, 64, 0), ("grid-rnn", 3, 5, 16, 2),
+    ("enc-dec-rnn", 2, 4, 32, 1), ("cell-stack-cnn", 6, 1, 32, 4),
+]
+
+
+def make_workloads():
+    out = {}
+    for i, (fam, L, S, w, seed) in enumerate(WORKLOAD_SPECS):
+        g = gen_workload(WorkloadSpec(fam, L, S, w, seed=seed), node_cap=10**6)
+        tmp = {}
+        graph_arrays(g, "", tmp)
+        p = f"w{i}/"
+        out[p + "spec"] = np.array([fam, str(L), str(S), str(w), str(seed)])
+        out[p + "n"], out[p + "e"] = np.int64(g.num_nodes), np.int64(g.num_edges)
+        out[p + "op_sum"] = np.int64(tmp["op"].sum())
+        out[p + "flops"] = np.float64(tmp["flops"].sum())
+        out[p + "out_bytes"] = np.float64(tmp["out_bytes"].sum())
+        out[p + "edge_sig"] = np.int64((tmp["src"] * 1000003 + tmp["dst"]).sum() % (2**61 - 1))
+        out[p + "ebytes"] = np.float64(tmp["ebytes"].sum())
+        out[p + "topo_sig"] = np.int64((tmp["topo"] * np.arange(g.num_nodes)).sum() % (2**61 - 1))
+    out["count"] = np.int64(len(WORKLOAD_SPECS))
+    np.savez_compressed(OUT / "golden_workloads.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo"]
+    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)
