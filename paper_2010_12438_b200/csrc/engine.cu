@@ -94,6 +94,12 @@ struct BatchMeta {
   const int64_t* d_chunks = nullptr;
   int64_t n_chunks = 0;
   double trunk_pairs = 0, head_pairs = 0;  // sum of (query, key) pairs per head
+  // tensor-core heads attention tables
+  const TcWork* d_tc_works = nullptr;
+  int64_t n_tc_works = 0;
+  const int64_t* d_tile_row0 = nullptr;
+  const int32_t* d_tile_n = nullptr;
+  int64_t n_tiles = 0;
 };
 
 static void build_tiles(const std::vector<int64_t>& row_off, int64_t S, bool banded,
@@ -153,6 +159,11 @@ static BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t
   for (auto& t : tt) m.trunk_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
   for (auto& t : ht) m.head_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
   size_t o_tt = s.add(tt), o_ht = s.add(ht);
+  std::vector<TcWork> tcw;
+  std::vector<int64_t> trow0;
+  std::vector<int32_t> tn;
+  if (need_heads) tc_build_tables(m.row_off, tcw, trow0, tn);
+  size_t o_tcw = s.add(tcw), o_tr = s.add(trow0), o_tn = s.add(tn);
   // mean chunks: [nc] r0, [nc] r1, [F] first, [F] end
   std::vector<int64_t> c0, c1, f0(m.F), f1(m.F);
   for (int f = 0; f < m.F; ++f) {
@@ -182,6 +193,11 @@ static BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t
   m.d_head_tiles = reinterpret_cast<const AttnTile*>(dev + o_ht);
   m.n_head_tiles = (int64_t)ht.size();
   m.d_chunks = reinterpret_cast<const int64_t*>(dev + o_ch);
+  m.d_tc_works = reinterpret_cast<const TcWork*>(dev + o_tcw);
+  m.n_tc_works = (int64_t)tcw.size();
+  m.d_tile_row0 = reinterpret_cast<const int64_t*>(dev + o_tr);
+  m.d_tile_n = reinterpret_cast<const int32_t*>(dev + o_tn);
+  m.n_tiles = (int64_t)trow0.size();
   return m;
 }
 
@@ -206,7 +222,10 @@ static size_t forward_ws_bytes(const go_config_t& c, int64_t R, int64_t gtotal, 
   int64_t wmax = std::max(c.gs_dim, c.d_model);
   int64_t W = (int64_t)c.n_head * c.d_head;
   int64_t per_row = 6 * ldp((int)wmax) + 4 * ldp((int)W) + ldp(c.d_inner);
+  // + tensor-core attention operands: qh [H][R][16], kb/vb [H][tiles*64][16]
+  per_row += 3 * (int64_t)c.n_head * 16 + 2;
   size_t b = (size_t)R * per_row * 4 + (size_t)R * 8 + (size_t)gtotal * 4 +
+             (size_t)F * 2 * c.n_head * 64 * 16 * 4 +
              (size_t)(F + 4) * (ldp(c.d_model) + ldp(c.gs_dim)) * 8 +
              (size_t)(nchunks + 4) * wmax * 4 + 64 * 256;
   return b + (1 << 20);
@@ -428,6 +447,14 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
   // ---- task heads (policy.py:187-217), full N x N attention per forward
   if (do_h) {
     GO_CHECK(hid && logits, "heads inputs/outputs required");
+    const char* force = getenv("GO_ATTN");
+    const bool use_tc = tc_attention_supported(cfg.d_head) && !(force && !strcmp(force, "simt"));
+    float *tc_q = nullptr, *tc_k = nullptr, *tc_v = nullptr;
+    if (use_tc) {
+      tc_q = A.take<float>((int64_t)cfg.n_head * R * 16);
+      tc_k = A.take<float>((int64_t)cfg.n_head * m.n_tiles * 64 * 16);
+      tc_v = A.take<float>((int64_t)cfg.n_head * m.n_tiles * 64 * 16);
+    }
     float* a_prev = nullptr;
     int64_t ld_prev = LW;
     float* rep_bufs[2] = {X[4], X[5]};
@@ -448,8 +475,13 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
       gemm(hh, LW, dm, nullptr, 0, 0, W_(S.ta(V_W)), W, W_(S.ta(V_B)), Vb, LA, R, W, 0, st);
       {
         KTimer kt(ctx, K_HEADS_ATTN, st, 4.0 * m.head_pairs * W);
-        attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_head_tiles, m.n_head_tiles, Ab, LA,
-                  st);
+        if (use_tc)
+          attention_full_tc(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, R, m.n_tiles, m.d_tc_works,
+                            m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
+                            st);
+        else
+          attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_head_tiles, m.n_head_tiles, Ab,
+                    LA, st);
       }
       float* o = X[2];
       gemm(Ab, LA, W, nullptr, 0, 0, W_(S.ta(O_W)), dm, W_(S.ta(O_B)), o, LW, R, dm, 0, st);

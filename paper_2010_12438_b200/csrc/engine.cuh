@@ -176,6 +176,20 @@ void attention(const float* q, const float* k, const float* v, int64_t ld, int n
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
                int64_t ldo, cudaStream_t st);
 
+// ---- kernels: tc_attention.cu (tcgen05 / TMEM full attention, d_head <= 16)
+struct TcWork {
+  int32_t f, q0, n, tiles;
+  int64_t row0, tile0;
+};
+bool tc_attention_supported(int d_head);
+void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& works,
+                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n);
+void attention_full_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+                       int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
+                       int64_t num_works, const int64_t* tile_row0_dev,
+                       const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
+                       int64_t ldo, cudaStream_t st);
+
 // ---- kernels: sample.cu
 void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t R,
                  const int64_t* row_off_dev, const int32_t* row_fwd, const int32_t* order_of_row,

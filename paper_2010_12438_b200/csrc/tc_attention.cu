@@ -1,0 +1,456 @@
+// Full N x N task-head attention (policy.py:210, multi_head_attention(h, h)) on the
+// 5th-generation tensor cores: tcgen05.mma kind::tf32, accumulators in TMEM,
+// K/V tiles streamed by cp.async.bulk into shared memory, online softmax in the
+// exp2 domain by 8 softmax warps (one thread per query row).
+//
+// CTA = one head x 256 queries of one forward (two 128-row M tiles), 10 warps:
+//   warps 0-3  softmax for query tile 0 (TMEM lanes 0-127, warp w -> lanes 32w..)
+//   warps 4-7  softmax for query tile 1
+//   warp  8    producer: bulk copies of K_j / V_j (4 KB each) into an 8-stage ring
+//   warp  9    MMA issuer (one elected thread):
+//                S_j = Q K_j^T   (M=128, N=64, K=16 as 2 x K8, A/B from smem)
+//                O_j = P_j V_j   (M=128, N=16, K=64 as 8 x K8, A=P from TMEM)
+// Per key tile of 64, each query tile uses S[b] (64 TMEM cols) and O[b] (16 cols),
+// b = j & 1, so S_{j+1} is computed while the softmax works on S_j.  O_j is
+// produced per tile (not accumulated across tiles) and folded into registers by the
+// softmax threads with their own rescale, so the running-max correction never has
+// to touch TMEM.  P is truncated to tf32 before use and the row sum l is taken over
+// the same truncated values, so the normalisation is exactly consistent.
+//
+// Numerics: Q/K/V are rounded to tf32 (round-to-nearest) by the repack kernel;
+// softmax statistics and accumulation are fp32.  Error vs the float64 reference:
+// logits ~1e-5 normwise (tests/test_gpu_parity.py enforces 1e-4).
+#include "engine.cuh"
+
+namespace go {
+namespace tc {
+
+constexpr int KT = 64;             // keys per tile
+constexpr int QT = 128;            // queries per M tile
+constexpr int NQT = 2;             // M tiles per CTA
+constexpr int NS = 8;              // K/V pipeline stages
+constexpr int TILE_BYTES = KT * 16 * 4;  // 4 KB: 64 rows x 16 fp32
+constexpr int NUM_THREADS = 320;
+constexpr uint32_t TMEM_COLS = 512;
+
+struct Work {
+  int32_t f;       // forward
+  int32_t q0;      // first local query row of this CTA
+  int32_t n;       // rows of the forward
+  int32_t tiles;   // key tiles of the forward
+  int64_t row0;    // batch row of local row 0
+  int64_t tile0;   // first key tile of the forward in the blocked K/V arrays
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]
+__device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+#define TC_LD32(taddr, r)                                                                    \
+  asm volatile(                                                                              \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%" \
+      "15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"          \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),  \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),        \
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),        \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),        \
+        "=r"(r[31])                                                                          \
+      : "r"(taddr))
+#define TC_ST32(taddr, r)                                                                    \
+  asm volatile(                                                                              \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%" \
+      "14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(   \
+          taddr),                                                                            \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),      \
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),    \
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),    \
+      "r"(r[29]), "r"(r[30]), "r"(r[31]))
+#define TC_LD16(taddr, r)                                                                    \
+  asm volatile(                                                                              \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%" \
+      "15}, [%16];"                                                                          \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),  \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Shared-memory matrix descriptor, no swizzle ("interleave"), K-major canonical
+// layout: core matrices of 8 rows x 16 B stored contiguously; SBO = byte stride
+// between 8-row groups, LBO = byte stride between the two 16-B K chunks.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                 // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+// Instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, shape M x N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+struct Smem {
+  float q[NQT][QT * 16];               // A tiles, K-major canonical (16 KB)
+  float kv[NS][2][KT * 16];            // [stage][K|V] 4 KB each (64 KB)
+  uint64_t kv_full[NS], kv_empty[NS];
+  uint64_t s_full[NQT][2], p_full[NQT][2], o_full[NQT][2], o_free[NQT][2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    attn_tc_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
+                   const float* __restrict__ vb, int64_t R, int64_t Ttot,
+                   const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
+                   int d_head) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Work w = works[blockIdx.x];
+  const int head = blockIdx.y;
+  const int T = w.tiles;
+  const float* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  const float* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+
+  // ---- setup: barriers, TMEM, Q tiles
+  if (warp == 8 && lane == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int t = 0; t < NQT; ++t)
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&sm.s_full[t][b], 1);
+        mbar_init(&sm.p_full[t][b], 128);
+        mbar_init(&sm.o_full[t][b], 1);
+        mbar_init(&sm.o_free[t][b], 128);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // Q: row-major [R][16] per head -> K-major canonical [c][g][8][4]
+  for (int i = threadIdx.x; i < NQT * QT * 4; i += NUM_THREADS) {
+    int qt = i / (QT * 4), rem = i % (QT * 4);
+    int r = rem >> 2, c = rem & 3;
+    int lr = w.q0 + qt * QT + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lr < w.n)
+      v = *reinterpret_cast<const float4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 4);
+    *reinterpret_cast<float4*>(&sm.q[qt][c * (QT * 4) + (r >> 3) * 32 + (r & 7) * 4]) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 8) {
+    // ---------------- producer
+    if (lane == 0) {
+      for (int j = 0; j < T; ++j) {
+        int s = j % NS;
+        if (j >= NS) mbar_wait(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
+        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_tf32(QT, KT);
+      constexpr uint32_t ID_O = idesc_tf32(QT, 16);
+      uint32_t qaddr[NQT];
+      for (int t = 0; t < NQT; ++t) qaddr[t] = smem_u32(sm.q[t]);
+      auto issue_pv = [&](int j) {
+        int s = j % NS, b = j & 1;
+        uint32_t vaddr = smem_u32(sm.kv[s][1]);
+        for (int t = 0; t < NQT; ++t) {
+          mbar_wait(&sm.p_full[t][b], (j >> 1) & 1);
+          if (j >= 2) mbar_wait(&sm.o_free[t][b], ((j >> 1) - 1) & 1);
+          fence_after();
+          uint32_t d = tbase + 256 + t * 32 + b * 16;
+          uint32_t a = tbase + t * 128 + b * 64;
+#pragma unroll
+          for (int k = 0; k < KT / 8; ++k)  // V^T tile: K chunks of 4 keys at 256 B
+            umma_ts(d, a + k * 8, sdesc(vaddr + k * 512, 256, 128), ID_O, k > 0);
+          umma_commit(&sm.o_full[t][b]);
+        }
+        umma_commit(&sm.kv_empty[s]);
+      };
+      for (int j = 0; j < T; ++j) {
+        int s = j % NS, b = j & 1;
+        mbar_wait(&sm.kv_full[s], (j / NS) & 1);
+        fence_after();
+        uint32_t kaddr = smem_u32(sm.kv[s][0]);
+        for (int t = 0; t < NQT; ++t) {
+          uint32_t d = tbase + t * 128 + b * 64;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)  // dims 8k..8k+7: chunks 2k, 2k+1
+            umma_ss(d, sdesc(qaddr[t] + k * 4096, 2048, 128), sdesc(kaddr + k * 2048, 1024, 128),
+                    ID_S, k > 0);
+          umma_commit(&sm.s_full[t][b]);
+        }
+        if (j >= 1) issue_pv(j - 1);
+      }
+      if (T >= 1) issue_pv(T - 1);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax: one thread per query row
+    const int t = warp >> 2;
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const int lr = w.q0 + t * QT + row;
+    float m = -INFINITY, l = 0.f;
+    float oacc[16];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) oacc[d] = 0.f;
+    float mt[2] = {0.f, 0.f};
+    auto fold = [&](int j) {
+      int b = j & 1;
+      mbar_wait(&sm.o_full[t][b], (j >> 1) & 1);
+      fence_after();
+      uint32_t r[16];
+      TC_LD16(tbase + lane_off + 256 + t * 32 + b * 16, r);
+      tmem_wait_ld();
+      fence_before();
+      mbar_arrive(&sm.o_free[t][b]);
+      float sc = ex2(mt[b] - m);
+#pragma unroll
+      for (int d = 0; d < 16; ++d) oacc[d] = fmaf(sc, __uint_as_float(r[d]), oacc[d]);
+    };
+    for (int j = 0; j < T; ++j) {
+      int b = j & 1;
+      mbar_wait(&sm.s_full[t][b], (j >> 1) & 1);
+      fence_after();
+      uint32_t sr[64];
+      const uint32_t sa = tbase + lane_off + t * 128 + b * 64;
+      TC_LD32(sa, sr);
+      TC_LD32(sa + 32, (sr + 32));
+      tmem_wait_ld();
+      const int kvalid = w.n - j * KT;  // keys of this tile inside the forward
+      float tm = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        float v = (i < kvalid) ? __uint_as_float(sr[i]) : -INFINITY;
+        sr[i] = __float_as_uint(v);
+        tm = fmaxf(tm, v);
+      }
+      float mn = fmaxf(m, tm);
+      if (mn > m) {
+        float corr = ex2(m - mn);
+        l *= corr;
+#pragma unroll
+        for (int d = 0; d < 16; ++d) oacc[d] *= corr;
+        m = mn;
+      }
+      float ls = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        uint32_t pb = __float_as_uint(ex2(__uint_as_float(sr[i]) - m)) & 0xFFFFE000u;
+        ls += __uint_as_float(pb);
+        sr[i] = pb;
+      }
+      l += ls;
+      TC_ST32(sa, sr);
+      TC_ST32(sa + 32, (sr + 32));
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&sm.p_full[t][b]);
+      mt[b] = m;
+      if (j >= 1) fold(j - 1);
+    }
+    if (T >= 1) fold(T - 1);
+    if (lr < w.n) {
+      float inv = 1.f / l;
+      float* o = out + (w.row0 + lr) * ldo + head * d_head;
+      for (int d = 0; d < d_head; ++d) o[d] = oacc[d] * inv;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 9) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Repack the QKV projections [R, n_head*d_head] into the tensor-core layouts:
+//   qh [H][R][16]     row-major, scaled by log2(e)/sqrt(d_head), tf32-rounded
+//   kb [H][Ttot][..]  per 64-key tile, K-major canonical:  (c, g, r, e) at c*256 + g*32 + r*4 + e
+//   vb [H][Ttot][..]  per 64-key tile, V^T K-major:        (kc, dg, rd, e) at kc*64 + dg*32 + rd*4 + e
+// Rows past a forward's end (inside its last tile) are zero.
+__device__ __forceinline__ float tf32r(float x) {
+  uint32_t y;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
+  return __uint_as_float(y);
+}
+
+__global__ void repack_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                              const float* __restrict__ v, int64_t ld, int n_head, int d_head,
+                              const int64_t* __restrict__ tile_fwd_row0,
+                              const int32_t* __restrict__ tile_n, int64_t Ttot, int64_t R,
+                              float qscale, float* __restrict__ qh, float* __restrict__ kb,
+                              float* __restrict__ vb) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (head, tile, row)
+  int64_t total = (int64_t)n_head * Ttot * KT;
+  if (idx >= total) return;
+  int head = (int)(idx / (Ttot * KT));
+  int64_t rem = idx % (Ttot * KT);
+  int64_t tile = rem / KT;
+  int rk = (int)(rem % KT);
+  int local = (int)tile_n[2 * tile + 1] * KT + rk;  // row within the forward
+  bool valid = local < tile_n[2 * tile];
+  int64_t grow = tile_fwd_row0[tile] + local;
+  float* kt = kb + ((int64_t)head * Ttot + tile) * (KT * 16);
+  float* vt = vb + ((int64_t)head * Ttot + tile) * (KT * 16);
+  for (int d = 0; d < 16; ++d) {
+    float kv = 0.f, vv = 0.f, qv = 0.f;
+    if (valid && d < d_head) {
+      int64_t o = grow * ld + head * d_head + d;
+      kv = tf32r(k[o]);
+      vv = tf32r(v[o]);
+      qv = tf32r(q[o] * qscale);
+    }
+    kt[(d >> 2) * 256 + (rk >> 3) * 32 + (rk & 7) * 4 + (d & 3)] = kv;
+    vt[(rk >> 2) * 64 + (d >> 3) * 32 + (d & 7) * 4 + (rk & 3)] = vv;
+    if (valid) qh[((int64_t)head * R + grow) * 16 + d] = qv;
+  }
+}
+
+}  // namespace tc
+
+bool tc_attention_supported(int d_head) { return d_head <= 16; }
+
+void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& works,
+                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n) {
+  int F = (int)row_off.size() - 1;
+  int64_t tb = 0;
+  for (int f = 0; f < F; ++f) {
+    int64_t n = row_off[f + 1] - row_off[f];
+    int32_t T = (int32_t)cdiv(n, tc::KT);
+    for (int64_t q0 = 0; q0 < n; q0 += tc::NQT * tc::QT)
+      works.push_back(TcWork{f, (int32_t)q0, (int32_t)n, T, row_off[f], tb});
+    for (int32_t t = 0; t < T; ++t) {
+      tile_row0.push_back(row_off[f]);
+      tile_n.push_back((int32_t)n);
+      tile_n.push_back(t);
+    }
+    tb += T;
+  }
+}
+
+void attention_full_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+                       int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
+                       int64_t num_works, const int64_t* tile_row0_dev,
+                       const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
+                       int64_t ldo, cudaStream_t st) {
+  if (num_works <= 0) return;
+  if (d_head > 16) GO_THROW(GO_ERR_UNSUPPORTED, "tensor-core attention needs d_head <= 16");
+  static bool attr = false;
+  const size_t smem = sizeof(tc::Smem) + 1024;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    attr = true;
+  }
+  float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
+  int64_t total = (int64_t)n_head * Ttot * tc::KT;
+  tc::repack_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+      q, k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, R, qscale, qh, kb, vb);
+  LAUNCH_CHECK();
+  dim3 grid((unsigned)num_works, (unsigned)n_head);
+  tc::attn_tc_kernel<<<grid, tc::NUM_THREADS, smem, st>>>(
+      qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head);
+  LAUNCH_CHECK();
+}
+
+}  // namespace go
