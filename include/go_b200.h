@@ -180,6 +180,26 @@ int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards,
               const uint64_t* pcg_states, const void* logits, int32_t logits_f64,
               double temperature, int32_t* actions_out, double* logp_out, void* stream);
 
+/* PPO loss and parameter gradient of one minibatch (replaces training.py:146-227:
+ * _sample_loss per sample + mean + Tensor.backward).  The samples are the forwards of
+ * `batch` with their last-iteration inputs (prev_actions, embed_seeds = the bundle's
+ * embed seed).  actions: dev int32 [T][rows], the sampled actions, node-indexed per
+ * span; old_logp: dev float64 [T][rows], topo-row indexed; fparams: host [F][4] =
+ * (advantage, temperature, reward, 0).  grads: dev float32 with the parameter-blob
+ * layout, ACCUMULATED (caller zeroes per minibatch); the loss is the mean over the
+ * F samples.  stats_out: host float64 [14*F]: [F][3][4] (sum surr, sum entropy, sum
+ * ratio, clipped count) per task slot, then [F] (value - reward)^2, then [F] value. */
+int go_ppo_grad(go_ctx_t ctx, const go_config_t* cfg, const float* params,
+                const int64_t* param_offsets, const go_batch_t* batch, const int32_t* actions,
+                const double* old_logp, const double* fparams, double clip_eps,
+                double entropy_coef, double value_coef, float* grads, double* stats_out,
+                void* stream);
+
+/* Fused bias-corrected Adam over a flat float32 blob (replaces tensor.py:428-441
+ * ParamStore.adam_step; every element steps, zero gradient where none flowed). */
+int go_adam(go_ctx_t ctx, float* params, const float* grads, float* m, float* v, int64_t count,
+            int64_t step, double lr, double beta1, double beta2, double eps, void* stream);
+
 /* Batched exact discrete-event simulation (simulator.py:280-441) of K placements of
  * one graph (its current fused tables) + reward (training.py:37-44).
  *   placement  dev int32 [K][n] node-indexed device per node

@@ -20,7 +20,8 @@ EXPORTS = (
     "go_launch_count", "go_ctx_set_timing", "go_ctx_kernel_stats",
     "go_topo_order", "go_greedy_cuts", "go_apply_fusion", "go_graph_create", "go_graph_destroy", "go_graph_topo",
     "go_graph_num_neighbors", "go_graph_set_fusion", "go_param_count", "go_forward",
-    "go_forward_status", "go_neighbor_arrays", "go_sample", "go_simulate",
+    "go_forward_status", "go_neighbor_arrays", "go_sample", "go_simulate", "go_ppo_grad",
+    "go_adam",
 )
 
 
@@ -74,6 +75,9 @@ _SIGS = {
                                     P, P, P, P]),
     "go_neighbor_arrays": (C.c_int, [P, P, I64, I32, P, P, P]),
     "go_sample": (C.c_int, [P, C.POINTER(GoConfig), I32, P, P, P, P, I32, F64, P, P, P]),
+    "go_ppo_grad": (C.c_int, [P, C.POINTER(GoConfig), P, P, C.POINTER(GoBatch), P, P, P, F64, F64,
+                              F64, P, P, P]),
+    "go_adam": (C.c_int, [P, P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
     "go_simulate": (C.c_int, [P, P, I32, P, P, I32, I32, P, P, P, P, I32, F64, P, P, P, P, P,
                               P, P]),
 }

@@ -121,7 +121,8 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
                                    const int64_t* __restrict__ gbase,
                                    const int32_t* __restrict__ row_fwd,
                                    const int32_t* __restrict__ gidx, int64_t R, int D,
-                                   float* __restrict__ out, int64_t ldo) {
+                                   float* __restrict__ out, int64_t ldo,
+                                   int32_t* __restrict__ argmax) {
   int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if (r >= R) return;
@@ -129,6 +130,26 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
   const GraphView& G = views[f];
   int64_t lr = r - row_off[f];
   int64_t s0 = gbase[f] + G.samp_off[lr], s1 = gbase[f] + G.samp_off[lr + 1];
+  if (argmax) {
+    // training forward: also record the first maximal row per column (tensor.py:240-251)
+    for (int c = lane; c < D; c += 32) {
+      float m = 0.f;
+      int32_t am = -1;
+      if (s1 > s0) {
+        m = -INFINITY;
+        for (int64_t j = s0; j < s1; ++j) {
+          float v = t[(int64_t)gidx[j] * ldt + c];
+          if (v > m || am < 0) {
+            m = v;
+            am = gidx[j];
+          }
+        }
+      }
+      out[r * ldo + c] = m;
+      argmax[r * D + c] = am;
+    }
+    return;
+  }
   if ((D & 3) == 0 && (ldt & 3) == 0 && (ldo & 3) == 0) {
     int D4 = D >> 2;
     for (int c4 = lane; c4 < D4; c4 += 32) {
@@ -160,11 +181,11 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
 void segment_max(const float* t, int64_t ldt, const GraphView* views_dev,
                  const int64_t* row_off_dev, const int64_t* gbase_dev, const int32_t* row_fwd,
                  const int32_t* gidx, int64_t R, int D, float* out, int64_t ldo,
-                 cudaStream_t st) {
+                 cudaStream_t st, int32_t* argmax) {
   if (R <= 0) return;
   segment_max_kernel<<<(unsigned)cdiv(R, 8), 256, 0, st>>>(t, ldt, views_dev, row_off_dev,
                                                            gbase_dev, row_fwd, gidx, R, D, out,
-                                                           ldo);
+                                                           ldo, argmax);
   LAUNCH_CHECK();
 }
 

@@ -77,30 +77,7 @@ struct Stager {
   }
 };
 
-struct BatchMeta {
-  int F = 0;
-  int64_t R = 0;
-  std::vector<int64_t> row_off, gbase;
-  int64_t gtotal = 0;
-  // device
-  const int64_t* d_row_off = nullptr;
-  const int64_t* d_seeds = nullptr;
-  const int64_t* d_gbase = nullptr;
-  const GraphView* d_views = nullptr;
-  const AttnTile* d_trunk_tiles = nullptr;
-  int64_t n_trunk_tiles = 0;
-  const AttnTile* d_head_tiles = nullptr;
-  int64_t n_head_tiles = 0;
-  const int64_t* d_chunks = nullptr;
-  int64_t n_chunks = 0;
-  double trunk_pairs = 0, head_pairs = 0;  // sum of (query, key) pairs per head
-  // tensor-core heads attention tables
-  const TcWork* d_tc_works = nullptr;
-  int64_t n_tc_works = 0;
-  const int64_t* d_tile_row0 = nullptr;
-  const int32_t* d_tile_n = nullptr;
-  int64_t n_tiles = 0;
-};
+
 
 static void build_tiles(const std::vector<int64_t>& row_off, int64_t S, bool banded,
                         std::vector<AttnTile>& out) {
@@ -119,10 +96,9 @@ static void build_tiles(const std::vector<int64_t>& row_off, int64_t S, bool ban
   }
 }
 
-static BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
-                           bool need_embed, bool need_trunk, bool need_heads, cudaStream_t st,
-                           const void* extra = nullptr, size_t extra_bytes = 0,
-                           const void** extra_dev = nullptr) {
+BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
+                     bool need_embed, bool need_trunk, bool need_heads, cudaStream_t st,
+                     const void* extra, size_t extra_bytes, const void** extra_dev) {
   BatchMeta m;
   m.F = b.num_forwards;
   GO_CHECK(m.F >= 1, "empty batch");

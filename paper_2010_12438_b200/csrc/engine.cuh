@@ -163,7 +163,7 @@ void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
 void segment_max(const float* t, int64_t ldt, const GraphView* views_dev,
                  const int64_t* row_off_dev, const int64_t* gbase_dev, const int32_t* row_fwd,
                  const int32_t* gidx, int64_t R, int D, float* out, int64_t ldo,
-                 cudaStream_t st);
+                 cudaStream_t st, int32_t* argmax = nullptr);
 
 void row_node_fill(const GraphView* views_dev, const int64_t* row_off_dev,
                    const int32_t* row_fwd, int64_t R, int32_t* row_node, cudaStream_t st);
@@ -174,7 +174,7 @@ struct AttnTile {
 };
 void attention(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
-               int64_t ldo, cudaStream_t st);
+               int64_t ldo, cudaStream_t st, float* lse = nullptr);
 
 // ---- kernels: tc_attention.cu (tcgen05 / TMEM full attention, d_head <= 16)
 struct TcWork {
@@ -189,6 +189,35 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
                        int64_t num_works, const int64_t* tile_row0_dev,
                        const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
                        int64_t ldo, cudaStream_t st);
+
+// per-call batch metadata (engine.cu make_meta): row offsets, graph views, tiles
+struct BatchMeta {
+  int F = 0;
+  int64_t R = 0;
+  std::vector<int64_t> row_off, gbase;
+  int64_t gtotal = 0;
+  // device
+  const int64_t* d_row_off = nullptr;
+  const int64_t* d_seeds = nullptr;
+  const int64_t* d_gbase = nullptr;
+  const GraphView* d_views = nullptr;
+  const AttnTile* d_trunk_tiles = nullptr;
+  int64_t n_trunk_tiles = 0;
+  const AttnTile* d_head_tiles = nullptr;
+  int64_t n_head_tiles = 0;
+  const int64_t* d_chunks = nullptr;
+  int64_t n_chunks = 0;
+  double trunk_pairs = 0, head_pairs = 0;  // sum of (query, key) pairs per head
+  // tensor-core heads attention tables
+  const TcWork* d_tc_works = nullptr;
+  int64_t n_tc_works = 0;
+  const int64_t* d_tile_row0 = nullptr;
+  const int32_t* d_tile_n = nullptr;
+  int64_t n_tiles = 0;
+};
+BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b, bool need_embed,
+                    bool need_trunk, bool need_heads, cudaStream_t st, const void* extra = nullptr,
+                    size_t extra_bytes = 0, const void** extra_dev = nullptr);
 
 // ---- kernels: sample.cu
 void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t R,

@@ -27,10 +27,13 @@ namespace tc {
 
 constexpr int KT = 64;             // keys per tile
 constexpr int QT = 128;            // queries per M tile
-constexpr int NQT = 2;             // M tiles per CTA
+constexpr int NQT = 3;             // M tiles per CTA (12 softmax warps)
 constexpr int NS = 8;              // K/V pipeline stages
 constexpr int TILE_BYTES = KT * 16 * 4;  // 4 KB: 64 rows x 16 fp32
-constexpr int NUM_THREADS = 320;
+constexpr int PRODUCER_WARP = NQT * 4;
+constexpr int MMA_WARP = NQT * 4 + 1;
+constexpr int NUM_THREADS = (NQT * 4 + 2) * 32;
+constexpr uint32_t O_COL = NQT * 128;  // O buffers after the S buffers
 constexpr uint32_t TMEM_COLS = 512;
 
 struct Work {
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const float* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
 
   // ---- setup: barriers, TMEM, Q tiles
-  if (warp == 8 && lane == 0) {
+  if (warp == PRODUCER_WARP && lane == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 9) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
                  "r"(TMEM_COLS));
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   fence_after();
   const uint32_t tbase = sm.tmem_base;
 
-  if (warp == 8) {
+  if (warp == PRODUCER_WARP) {
     // ---------------- producer
     if (lane == 0) {
       for (int j = 0; j < T; ++j) {
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 9) {
+  } else if (warp == MMA_WARP) {
     // ---------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t ID_S = idesc_tf32(QT, KT);
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&sm.p_full[t][b], (j >> 1) & 1);
           if (j >= 2) mbar_wait(&sm.o_free[t][b], ((j >> 1) - 1) & 1);
           fence_after();
-          uint32_t d = tbase + 256 + t * 32 + b * 16;
+          uint32_t d = tbase + O_COL + t * 32 + b * 16;
           uint32_t a = tbase + t * 128 + b * 64;
 #pragma unroll
           for (int k = 0; k < KT / 8; ++k)  // V^T tile: K chunks of 4 keys at 256 B
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&sm.o_full[t][b], (j >> 1) & 1);
       fence_after();
       uint32_t r[16];
-      TC_LD16(tbase + lane_off + 256 + t * 32 + b * 16, r);
+      TC_LD16(tbase + lane_off + O_COL + t * 32 + b * 16, r);
       tmem_wait_ld();
       fence_before();
       mbar_arrive(&sm.o_free[t][b]);
@@ -315,13 +318,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       TC_LD32(sa + 32, (sr + 32));
       tmem_wait_ld();
       const int kvalid = w.n - j * KT;  // keys of this tile inside the forward
-      float tm = -INFINITY;
+      if (kvalid < KT) {
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        float v = (i < kvalid) ? __uint_as_float(sr[i]) : -INFINITY;
-        sr[i] = __float_as_uint(v);
-        tm = fmaxf(tm, v);
+        for (int i = 0; i < KT; ++i)
+          if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
       }
+      // row max with 8 independent chains (dependent FMNMX chains were the stall)
+      float mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(sr[i]);
+#pragma unroll
+      for (int i = 8; i < KT; ++i) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(sr[i]));
+      const float tm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                             fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
       float mn = fmaxf(m, tm);
       if (mn > m) {
         float corr = ex2(m - mn);
@@ -330,14 +339,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int d = 0; d < 16; ++d) oacc[d] *= corr;
         m = mn;
       }
-      float ls = 0.f;
+      float ls[8];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
+      for (int i = 0; i < 8; ++i) ls[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
         uint32_t pb = __float_as_uint(ex2(__uint_as_float(sr[i]) - m)) & 0xFFFFE000u;
-        ls += __uint_as_float(pb);
+        ls[i & 7] += __uint_as_float(pb);
         sr[i] = pb;
       }
-      l += ls;
+      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       TC_ST32(sa, sr);
       TC_ST32(sa + 32, (sr + 32));
       tmem_wait_st();
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 9) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
                  "r"(TMEM_COLS));
   }

@@ -334,3 +334,172 @@ def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed
             batch.global_rewards, batch.global_step_times = full[0], full[1]
             batch.global_valid, batch.global_values = full[2] > 0.5, full[3]
     return batch
+
+
+# ---------------------------------------------------------------------------------------
+# PPO update on device
+
+
+@dataclass
+class _DevSample:
+    handle: object
+    prev: object       # int32 [T, n] node-indexed (iteration-1 actions)
+    actions: object    # int32 [T, n] node-indexed
+    logp: object       # float64 [T, n] topo-row indexed
+    seed: int
+    temperature: float
+    reward: float
+
+
+def _device_samples(batch, graphs, tasks):
+    """Upload (once) what each sample's re-forward and loss need."""
+    T_ = torch()
+    ctx = context()
+    dev = T_.device("cuda", ctx.device)
+    out = []
+    for s in batch.samples:
+        g = as_graph(graphs[s.graph_index])
+        b = s.bundle
+        n = g.num_nodes
+        if b.prev_actions is None:
+            raise ValueError("PPO re-forward needs the bundle's previous-iteration actions")
+        prev = np.stack([np.asarray(b.prev_actions[t], np.int32) for t, _ in tasks])
+        acts = np.stack([np.asarray(b.actions[t], np.int32) for t, _ in tasks])
+        logp = np.stack([np.asarray(b.log_probs[t], np.float64) for t, _ in tasks])
+        if prev.shape != (len(tasks), n) or acts.shape != (len(tasks), n):
+            raise ValueError("bundle arrays do not match the graph")
+        out.append(_DevSample(ctx.graph(g), T_.as_tensor(prev, device=dev),
+                              T_.as_tensor(acts, device=dev), T_.as_tensor(logp, device=dev),
+                              int(b.embed_seed), float(b.temperature), float(s.reward)))
+    return out
+
+
+def ppo_grad(params, embed_cfg, policy_cfg, task_sizes, samples, advantages, hyper, grads):
+    """One minibatch: loss + gradient accumulated into `grads` (go_ppo_grad).
+    Returns (loss, host stats array [14 * F])."""
+    import ctypes as C
+
+    from . import _lib
+    from .runtime import handle_array, make_config, stream_ptr
+    T_ = torch()
+    tasks = ordered_tasks(task_sizes)
+    F = len(samples)
+    blob, offs = params
+    prev = T_.cat([s.prev for s in samples], dim=1).contiguous()
+    acts = T_.cat([s.actions for s in samples], dim=1).contiguous()
+    logp = T_.cat([s.logp for s in samples], dim=1).contiguous()
+    fparams = np.zeros((F, 4), np.float64)
+    for i, s in enumerate(samples):
+        fparams[i] = (advantages[i], s.temperature, s.reward, 0.0)
+    harr = handle_array([s.handle for s in samples])
+    seeds = (C.c_int64 * F)(*[s.seed for s in samples])
+    b = _lib.GoBatch()
+    b.num_forwards = F
+    b.graphs = C.cast(harr, C.POINTER(C.c_void_p))
+    b.embed_seeds = seeds
+    b.prev_actions = _lib.ptr(prev)
+    b.stage_mask = 7
+    cfg_c = make_config(embed_cfg, policy_cfg, task_sizes)
+    stats = np.zeros(14 * F, np.float64)
+    _lib.call("go_ppo_grad", context().handle, C.byref(cfg_c), _lib.ptr(blob), offs.ctypes.data,
+              C.byref(b), _lib.ptr(acts), _lib.ptr(logp), fparams.ctypes.data,
+              float(hyper.clip_epsilon), float(hyper.entropy_coef), float(hyper.value_coef),
+              _lib.ptr(grads), stats.ctypes.data, stream_ptr())
+    Tn = len(tasks)
+    per = stats[:12 * F].reshape(F, 3, 4)
+    verr = stats[12 * F:13 * F]
+    loss = 0.0
+    for i, s in enumerate(samples):
+        n = s.handle.n
+        pol = sum(per[i, t, 0] / n for t in range(Tn)) / Tn
+        ent = sum(per[i, t, 1] / n for t in range(Tn)) / Tn
+        loss += -(pol + hyper.entropy_coef * ent) + hyper.value_coef * verr[i]
+    return loss / F, stats
+
+
+def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, policy_cfg,
+               seed: int = 0) -> dict:
+    """training.py:196-233 on device: epochs of shuffled minibatches, one fused
+    forward+backward per minibatch (all its samples in one ragged batch), fused
+    Adam.  Mutates `store` (parameters, Adam moments, step_count) like the reference."""
+    from . import _lib
+    from .params import pack, slot_names
+    from .runtime import stream_ptr
+    if not batch.samples:
+        raise ValueError("empty rollout batch")
+    T_ = torch()
+    dev = T_.device("cuda", context().device)
+    tasks = ordered_tasks(task_sizes)
+    rng = np.random.default_rng(seed)
+    adv = np.array([s.advantage for s in batch.samples], dtype=np.float64)
+    if hyper.advantage_norm and len(adv) > 1 and adv.std() > 0:
+        adv = (adv - adv.mean()) / (adv.std() + 1e-8)
+    blob_h, offs = pack(store, embed_cfg, policy_cfg, task_sizes)
+    names = slot_names(embed_cfg, policy_cfg, task_sizes)
+    blob = T_.as_tensor(blob_h, device=dev).contiguous()
+
+    def moments(d):
+        out = np.zeros_like(blob_h)
+        for nm, o in zip(names, offs):
+            if d is not None and nm in d:
+                a = np.asarray(d[nm], np.float32).reshape(-1)
+                out[o:o + a.size] = a
+        return T_.as_tensor(out, device=dev)
+
+    m = moments(getattr(store, "_m", None))
+    v = moments(getattr(store, "_v", None))
+    grads = T_.zeros_like(blob)
+    samples = _device_samples(batch, graphs, tasks)
+    step = int(getattr(store, "step_count", 0))
+    stats = {"ratio_sum": 0.0, "clip_sum": 0.0, "node_count": 0, "entropy_sum": 0.0,
+             "entropy_count": 0, "value_loss_sum": 0.0, "value_count": 0}
+    for _epoch in range(hyper.epochs):
+        perm = rng.permutation(len(samples))
+        stats = {k: 0 if isinstance(val, int) else 0.0 for k, val in stats.items()}
+        for chunk in np.array_split(perm, min(hyper.minibatches, len(perm))):
+            if len(chunk) == 0:
+                continue
+            grads.zero_()
+            loss, st = ppo_grad((blob, offs), embed_cfg, policy_cfg, task_sizes,
+                                [samples[i] for i in chunk], adv[chunk], hyper, grads)
+            if not np.isfinite(loss):
+                raise RuntimeError(
+                    f"non-finite PPO loss (advantages {adv.min():.3g}..{adv.max():.3g})")
+            F = len(chunk)
+            per = st[:12 * F].reshape(F, 3, 4)
+            for i, k in enumerate(chunk):
+                n = samples[k].handle.n
+                for t in range(len(tasks)):
+                    stats["ratio_sum"] += float(per[i, t, 2])
+                    stats["clip_sum"] += float(per[i, t, 3])
+                    stats["node_count"] += n
+                    stats["entropy_sum"] += float(per[i, t, 1] / max(1, n))
+                    stats["entropy_count"] += 1
+                stats["value_loss_sum"] += float(st[12 * F + i])
+                stats["value_count"] += 1
+            step += 1
+            _lib.call("go_adam", context().handle, _lib.ptr(blob), _lib.ptr(grads), _lib.ptr(m),
+                      _lib.ptr(v), int(blob.numel()), step, float(hyper.lr), 0.9, 0.999, 1e-8,
+                      stream_ptr())
+    # write parameters and Adam state back into the store (float64 host master)
+    hb, hm, hv = (x.cpu().numpy().astype(np.float64) for x in (blob, m, v))
+    for nm, o in zip(names, offs):
+        if nm not in store:
+            continue
+        p = store[nm]
+        size = np.asarray(p.data).size
+        shape = np.asarray(p.data).shape
+        p.data = hb[o:o + size].reshape(shape).copy()
+        if hasattr(store, "_m"):
+            store._m[nm] = hm[o:o + size].reshape(shape).copy()
+            store._v[nm] = hv[o:o + size].reshape(shape).copy()
+    if hasattr(store, "step_count"):
+        store.step_count = step
+    if hasattr(store, "touch"):
+        store.touch()
+    return {
+        "mean_ratio": stats["ratio_sum"] / max(1, stats["node_count"]),
+        "clip_fraction": stats["clip_sum"] / max(1, stats["node_count"]),
+        "entropy": stats["entropy_sum"] / max(1, stats["entropy_count"]),
+        "value_loss": stats["value_loss_sum"] / max(1, stats["value_count"]),
+    }

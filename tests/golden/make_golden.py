@@ -363,8 +363,67 @@ def make_workloads():
     np.savez_compressed(OUT / "golden_workloads.npz", **out)
 
 
+def make_grads():
+    """Per-sample PPO loss and its full parameter gradient from the reference tape
+    (training.py:146-186 _sample_loss + tensor.py backward)."""
+    import graphopt.training as tr
+    out = {}
+    cases = [
+        ("small", EmbedConfig(1, 8, 4), PolicyConfig(1, 8, 2, 3, 16, 8, 2),
+         lambda: C.random_graph(np.random.default_rng(3), 12, p_edge=0.3), 2, np.float64),
+        ("joint", EmbedConfig(2, 8, 3), PolicyConfig(2, 8, 2, 3, 16, 4, 2),
+         lambda: C.random_graph(np.random.default_rng(8), 15, p_edge=0.3), 3, np.float64),
+        ("default", EmbedConfig(), PolicyConfig(),
+         lambda: C.random_graph(np.random.default_rng(4), 100, p_edge=0.05), 4, np.float32),
+    ]
+    for name, ecfg, pcfg, build, d, dt in cases:
+        g = build()
+        top = C.simple_topology(d)
+        tasks = ["placement"] if name != "joint" else ["placement", "schedule_priority",
+                                                      "fusion_priority"]
+        sizes = task_action_sizes(top, tasks, 8)
+        store = init_all_params(ecfg, pcfg, sizes, seed=0)
+        randomize(store)
+        from graphopt.baselines import baseline_step_time
+        bl = baseline_step_time(g, top)
+        hyper = PPOHyper(lr=1e-2, rollouts=3, minibatches=1, epochs=1, entropy_coef=0.3,
+                         temperature=0.8 if name == "joint" else 1.0)
+        batch = collect_rollouts(store, [g], top, sizes, [bl], 3, seed=11, hyper=hyper,
+                                 embed_cfg=ecfg, policy_cfg=pcfg, fusion_cfg=FusionConfig())
+        p = name + "/"
+        graph_arrays(g, p + "g/", out)
+        out[p + "meta"] = np.array(json.dumps(dict(ecfg=ecfg.__dict__, pcfg=pcfg.__dict__,
+                                                   sizes=sizes, d=d, hyper=hyper.__dict__)))
+        for i, s in enumerate(batch.samples):
+            q = p + f"s{i}/"
+            for t in tasks:
+                out[q + f"actions/{t}"] = s.bundle.actions[t]
+                out[q + f"prev/{t}"] = s.bundle.prev_actions[t]
+                out[q + f"logp/{t}"] = s.bundle.log_probs[t]
+            out[q + "embed_seed"] = np.int64(s.bundle.embed_seed)
+            out[q + "reward"] = np.float64(s.reward)
+            out[q + "temperature"] = np.float64(s.bundle.temperature)
+            adv = 0.7 - 0.9 * i
+            out[q + "adv"] = np.float64(adv)
+            store.zero_grads()
+            stats = {"ratio_sum": 0.0, "clip_sum": 0.0, "node_count": 0, "entropy_sum": 0.0,
+                     "entropy_count": 0, "value_loss_sum": 0.0, "value_count": 0}
+            loss = tr._sample_loss(s, adv, g, store, sizes, hyper, ecfg, pcfg, stats)
+            loss.backward()
+            out[q + "loss"] = np.float64(loss.data)
+            for k, v in stats.items():
+                out[q + "stats/" + k] = np.float64(v)
+            if name == "default" and i > 0:
+                continue  # keep the fixture small: one full fp32 gradient at 1.2M params
+            for n_ in store.names():
+                gr = store[n_].grad
+                out[q + "grad/" + n_] = (np.zeros_like(store[n_].data) if gr is None
+                                         else gr).astype(dt)
+    np.savez_compressed(OUT / "golden_grads.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads"]
+    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

@@ -1,0 +1,113 @@
+"""GPU parity of the PPO path: per-sample loss and full
+parameter gradient vs the reference tape (tests/golden/golden_grads.npz), and a
+whole ppo_update vs the reference (golden_ppo.npz).
+
+Tolerances: loss 1e-4 relative; gradients normwise relative (whole vector) 1e-3
+and per tensor 1e-3 of the largest tensor norm (fp32 device vs float64 tape);
+ppo_update: stats 1e-4 relative, parameters |delta| <= 2e-4 on >= 99% of
+coordinates (Adam's first steps are ~lr*sign(g), so a coordinate whose gradient is
+~0 in float64 can move differently in fp32)."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _graph(z, p):
+    from paper_2010_12438_b200.graph import Graph
+    return Graph(z[p + "op"], z[p + "flops"], z[p + "out_bytes"], z[p + "src"], z[p + "dst"],
+                 z[p + "ebytes"], z[p + "coloc"])
+
+
+@pytest.mark.parametrize("case", ["small", "joint", "default"])
+def test_sample_loss_and_gradient_parity(case):
+    from paper_2010_12438_b200 import (EmbedConfig, PolicyConfig, PPOHyper, init_all_params,
+                                       randomize_zero_init)
+    from paper_2010_12438_b200.params import pack, slot_names
+    from paper_2010_12438_b200.policy import TaskActionBundle, ordered_tasks
+    from paper_2010_12438_b200.training import RolloutBatch, RolloutSample, _device_samples, ppo_grad
+    z = golden("grads")
+    p = case + "/"
+    meta = json.loads(str(z[p + "meta"]))
+    ecfg, pcfg = EmbedConfig(**meta["ecfg"]), PolicyConfig(**meta["pcfg"])
+    sizes = meta["sizes"]
+    hyper = PPOHyper(**meta["hyper"])
+    g = _graph(z, p + "g/")
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
+    tasks = ordered_tasks(sizes)
+    blob_h, offs = pack(store, ecfg, pcfg, sizes)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    blob = torch.as_tensor(blob_h, device=dev)
+    names = slot_names(ecfg, pcfg, sizes)
+    for i in range(3):
+        q = p + f"s{i}/"
+        bundle = TaskActionBundle(
+            tasks=[t for t, _ in tasks], logits={},
+            actions={t: z[q + f"actions/{t}"] for t, _ in tasks},
+            log_probs={t: z[q + f"logp/{t}"] for t, _ in tasks}, value=0.0,
+            prev_actions={t: z[q + f"prev/{t}"] for t, _ in tasks},
+            embed_seed=int(z[q + "embed_seed"]), temperature=float(z[q + "temperature"]))
+        sample = RolloutSample(0, bundle, float(z[q + "reward"]), 0.0, 0.0, 0.0, True)
+        samples = _device_samples(RolloutBatch([sample]), [g], tasks)
+        grads = torch.zeros_like(blob)
+        loss, _st = ppo_grad((blob, offs), ecfg, pcfg, sizes, samples,
+                             np.array([float(z[q + "adv"])]), hyper, grads)
+        want = float(z[q + "loss"])
+        assert abs(loss - want) <= 1e-4 * max(1.0, abs(want)), (case, i, loss, want)
+        if q + f"grad/{names[0]}" not in z:
+            continue
+        gh = grads.cpu().numpy().astype(np.float64)
+        got_all, want_all = [], []
+        norms = {}
+        for nm, o in zip(names, offs):
+            w = np.asarray(z[q + "grad/" + nm], np.float64).reshape(-1)
+            gv = gh[o:o + w.size]
+            got_all.append(gv)
+            want_all.append(w)
+            norms[nm] = (np.linalg.norm(gv - w), np.linalg.norm(w))
+        ga, wa = np.concatenate(got_all), np.concatenate(want_all)
+        rel = np.linalg.norm(ga - wa) / np.linalg.norm(wa)
+        assert rel < 1e-3, (case, i, rel)
+        top = max(v[1] for v in norms.values())
+        bad = {k: v for k, v in norms.items() if v[0] > 1e-3 * top}
+        assert not bad, (case, i, bad)
+
+
+def test_ppo_update_matches_reference():
+    from paper_2010_12438_b200 import (EmbedConfig, PolicyConfig, PPOHyper, init_all_params,
+                                       randomize_zero_init)
+    from paper_2010_12438_b200.costmodel import uniform_topology
+    from paper_2010_12438_b200.policy import TaskActionBundle
+    from paper_2010_12438_b200.training import RolloutBatch, RolloutSample, ppo_update
+    z = golden("ppo")
+    g = _graph(z, "g/")
+    ecfg, pcfg = EmbedConfig(1, 8, 4), PolicyConfig(1, 8, 2, 3, 16, 8, 2)
+    sizes = {"placement": 2}
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
+    for n, prm in store.items():
+        assert np.array_equal(prm.data, z["before/" + n]), n
+    samples = []
+    for i in range(4):
+        q = f"r{i}/"
+        b = TaskActionBundle(["placement"], {}, {"placement": z[q + "actions"]},
+                             {"placement": z[q + "logp"]}, 0.0,
+                             {"placement": z[q + "prev_actions"]}, int(z[q + "embed_seed"]), 1.0)
+        samples.append(RolloutSample(0, b, float(z[q + "reward"]), 0.0,
+                                     float(z[q + "advantage"]), 0.0, True))
+    hyper = PPOHyper(lr=1e-2, rollouts=4, minibatches=2, epochs=2, entropy_coef=0.01)
+    stats = ppo_update(RolloutBatch(samples), store, [g], uniform_topology(2), sizes, hyper,
+                       ecfg, pcfg, seed=7)
+    for k in ("mean_ratio", "clip_fraction", "entropy", "value_loss"):
+        want = float(z["stats/" + k])
+        assert abs(stats[k] - want) <= 1e-4 * max(1.0, abs(want)), (k, stats[k], want)
+    deltas = []
+    for n, prm in store.items():
+        deltas.append(np.abs(prm.data - z["after/" + n]).reshape(-1))
+    d = np.concatenate(deltas)
+    assert (d <= 2e-4).mean() >= 0.99, (d.max(), (d <= 2e-4).mean())
+    assert store.step_count == 4
