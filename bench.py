@@ -357,7 +357,7 @@ def main():
     roof = None
     if cnt:
         ach = hflops / cnt / (hms / cnt / 1000.0) / 1e12
-        roof = {"bound": "tensor", "kernel": "heads N x N attention (attn_kernel)",
+        roof = {"bound": "tensor", "kernel": "task-head N x N attention, tcgen05 kind::tf32 + TMEM (attn_tc_fixed_kernel)",
                 "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
                 "traffic": None, "launches": cnt, "avg_launch_ms": hms / cnt,
                 "algorithmic_flops_per_launch": hflops / cnt,

@@ -426,10 +426,12 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
     const char* force = getenv("GO_ATTN");
     const bool use_tc = tc_attention_supported(cfg.d_head) && !(force && !strcmp(force, "simt"));
     float *tc_q = nullptr, *tc_k = nullptr, *tc_v = nullptr;
+    int32_t* tc_scratch = nullptr;
     if (use_tc) {
       tc_q = A.take<float>((int64_t)cfg.n_head * R * 16);
       tc_k = A.take<float>((int64_t)cfg.n_head * m.n_tiles * 64 * 16);
       tc_v = A.take<float>((int64_t)cfg.n_head * m.n_tiles * 64 * 16);
+      tc_scratch = A.take<int32_t>(1 + (int64_t)F * cfg.n_head);
     }
     float* a_prev = nullptr;
     int64_t ld_prev = LW;
@@ -454,7 +456,7 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
         if (use_tc)
           attention_full_tc(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, R, m.n_tiles, m.d_tc_works,
                             m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
-                            st);
+                            row_fwd, F, tc_scratch, st);
         else
           attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_head_tiles, m.n_head_tiles, Ab,
                     LA, st);

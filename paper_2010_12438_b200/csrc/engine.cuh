@@ -188,7 +188,8 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
                        int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
                        int64_t num_works, const int64_t* tile_row0_dev,
                        const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
-                       int64_t ldo, cudaStream_t st);
+                       int64_t ldo, const int32_t* row_fwd, int F, int32_t* scratch,
+                       cudaStream_t st);
 
 // per-call batch metadata (engine.cu make_meta): row offsets, graph views, tiles
 struct BatchMeta {

@@ -20,6 +20,8 @@
 // Numerics: Q/K/V are rounded to tf32 (round-to-nearest) by the repack kernel;
 // softmax statistics and accumulation are fp32.  Error vs the float64 reference:
 // logits ~1e-5 normwise (tests/test_gpu_parity.py enforces 1e-4).
+#include <cstring>
+
 #include "engine.cuh"
 
 namespace go {
@@ -183,7 +185,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     attn_tc_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
                    const float* __restrict__ vb, int64_t R, int64_t Ttot,
                    const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
-                   int d_head) {
+                   int d_head, const int32_t* __restrict__ flag) {
+  if (flag && !*flag) return;  // the fixed-offset kernel handled this launch
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -390,7 +393,8 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
                               const int64_t* __restrict__ tile_fwd_row0,
                               const int32_t* __restrict__ tile_n, int64_t Ttot, int64_t R,
                               float qscale, float* __restrict__ qh, float* __restrict__ kb,
-                              float* __restrict__ vb) {
+                              float* __restrict__ vb, const int32_t* __restrict__ flag) {
+  if (flag && !*flag) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (head, tile, row)
   int64_t total = (int64_t)n_head * Ttot * KT;
   if (idx >= total) return;
@@ -398,8 +402,8 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
   int64_t rem = idx % (Ttot * KT);
   int64_t tile = rem / KT;
   int rk = (int)(rem % KT);
-  int local = (int)tile_n[2 * tile + 1] * KT + rk;  // row within the forward
-  bool valid = local < tile_n[2 * tile];
+  int local = (int)tile_n[3 * tile + 1] * KT + rk;  // row within the forward
+  bool valid = local < tile_n[3 * tile];
   int64_t grow = tile_fwd_row0[tile] + local;
   float* kt = kb + ((int64_t)head * Ttot + tile) * (KT * 16);
   float* vt = vb + ((int64_t)head * Ttot + tile) * (KT * 16);
@@ -417,6 +421,234 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
   }
 }
 
+
+// ------------------------------------------------------------------------------------
+// Fixed-offset variant (d_head <= 15).  Column 15 of the padded head dimension is
+// spare, so it carries the softmax bookkeeping through the tensor core:
+//   Q[:,15] = -b_i  with b_i >= max_j s_ij (Cauchy-Schwarz: |q_i| * max_j |k_j|)
+//   K[:,15] = 1     =>  the S MMA returns s_ij - b_i <= 0 directly
+//   V[:,15] = 1     =>  the PV MMA returns l_i = sum_j p_ij in O[:,15], computed from
+//                       exactly the tf32 P the numerator used.
+// No running max, no rescale, no row sum and no per-tile O traffic: the softmax warps
+// only do tcgen05.ld S -> ex2 -> tcgen05.st P, and O accumulates across all key tiles
+// in TMEM.  Padding keys have all-zero K and V rows, so they contribute nothing.  Used
+// when every b_i <= BOUND_LIMIT (exp2 then never underflows for scores within 2 b_i
+// of the bound); otherwise the online-softmax kernel above takes the launch.
+constexpr float BOUND_LIMIT = 60.f;
+
+struct SmemF {
+  float q[NQT][QT * 16];
+  float kv[NS][2][KT * 16];
+  uint64_t kv_full[NS], kv_empty[NS];
+  uint64_t s_full[NQT][2], p_full[NQT][2], o_done[NQT];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    attn_tc_fixed_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
+                         const float* __restrict__ vb, int64_t R, int64_t Ttot,
+                         const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
+                         int d_head, const int32_t* __restrict__ flag) {
+  if (*flag) return;  // some bound exceeded BOUND_LIMIT: the online kernel runs instead
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SmemF& sm = *reinterpret_cast<SmemF*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Work w = works[blockIdx.x];
+  const int head = blockIdx.y;
+  const int T = w.tiles;
+  const float* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  const float* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  if (warp == PRODUCER_WARP && lane == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int t = 0; t < NQT; ++t) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&sm.s_full[t][b], 1);
+        mbar_init(&sm.p_full[t][b], 128);
+      }
+      mbar_init(&sm.o_done[t], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < NQT * QT * 4; i += NUM_THREADS) {
+    int qt = i / (QT * 4), rem = i % (QT * 4);
+    int r = rem >> 2, c = rem & 3;
+    int lr = w.q0 + qt * QT + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lr < w.n)
+      v = *reinterpret_cast<const float4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 4);
+    *reinterpret_cast<float4*>(&sm.q[qt][c * (QT * 4) + (r >> 3) * 32 + (r & 7) * 4]) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == PRODUCER_WARP) {
+    if (lane == 0) {
+      for (int j = 0; j < T; ++j) {
+        int s = j % NS;
+        if (j >= NS) mbar_wait(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
+        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == MMA_WARP) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_tf32(QT, KT);
+      constexpr uint32_t ID_O = idesc_tf32(QT, 16);
+      uint32_t qaddr[NQT];
+      for (int t = 0; t < NQT; ++t) qaddr[t] = smem_u32(sm.q[t]);
+      auto issue_pv = [&](int j) {
+        int s = j % NS, b = j & 1;
+        uint32_t vaddr = smem_u32(sm.kv[s][1]);
+        for (int t = 0; t < NQT; ++t) {
+          mbar_wait(&sm.p_full[t][b], (j >> 1) & 1);
+          fence_after();
+          uint32_t d = tbase + O_COL + t * 16;
+          uint32_t a = tbase + t * 128 + b * 64;
+#pragma unroll
+          for (int k = 0; k < KT / 8; ++k)
+            umma_ts(d, a + k * 8, sdesc(vaddr + k * 512, 256, 128), ID_O, (j > 0 || k > 0));
+        }
+        umma_commit(&sm.kv_empty[s]);
+      };
+      for (int j = 0; j < T; ++j) {
+        int s = j % NS, b = j & 1;
+        mbar_wait(&sm.kv_full[s], (j / NS) & 1);
+        fence_after();
+        uint32_t kaddr = smem_u32(sm.kv[s][0]);
+        for (int t = 0; t < NQT; ++t) {
+          uint32_t d = tbase + t * 128 + b * 64;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            umma_ss(d, sdesc(qaddr[t] + k * 4096, 2048, 128), sdesc(kaddr + k * 2048, 1024, 128),
+                    ID_S, k > 0);
+          umma_commit(&sm.s_full[t][b]);
+        }
+        if (j >= 1) issue_pv(j - 1);
+      }
+      if (T >= 1) issue_pv(T - 1);
+      for (int t = 0; t < NQT; ++t) umma_commit(&sm.o_done[t]);
+    }
+    __syncwarp();
+  } else {
+    const int t = warp >> 2;
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    for (int j = 0; j < T; ++j) {
+      int b = j & 1;
+      mbar_wait(&sm.s_full[t][b], (j >> 1) & 1);
+      fence_after();
+      uint32_t sr[64];
+      const uint32_t sa = tbase + lane_off + t * 128 + b * 64;
+      TC_LD32(sa, sr);
+      TC_LD32(sa + 32, (sr + 32));
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < KT; ++i) sr[i] = __float_as_uint(ex2(__uint_as_float(sr[i])));
+      TC_ST32(sa, sr);
+      TC_ST32(sa + 32, (sr + 32));
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&sm.p_full[t][b]);
+    }
+    mbar_wait(&sm.o_done[t], 0);
+    fence_after();
+    uint32_t r[16];
+    TC_LD16(tbase + lane_off + O_COL + t * 16, r);
+    tmem_wait_ld();
+    const int lr = w.q0 + t * QT + wq * 32 + lane;
+    if (lr < w.n) {
+      float inv = 1.f / __uint_as_float(r[15]);
+      float* o = out + (w.row0 + lr) * ldo + head * d_head;
+      for (int d = 0; d < d_head; ++d) o[d] = __uint_as_float(r[d]) * inv;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// K/V for the fixed variant: column 15 = 1 on valid rows; max |k| per (forward, head).
+__global__ void repack_kv_fixed_kernel(const float* __restrict__ k, const float* __restrict__ v,
+                                       int64_t ld, int n_head, int d_head,
+                                       const int64_t* __restrict__ tile_fwd_row0,
+                                       const int32_t* __restrict__ tile_n, int64_t Ttot,
+                                       float* __restrict__ kb, float* __restrict__ vb,
+                                       unsigned* __restrict__ kmax) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)n_head * Ttot * KT;
+  if (idx >= total) return;
+  int head = (int)(idx / (Ttot * KT));
+  int64_t rem = idx % (Ttot * KT);
+  int64_t tile = rem / KT;
+  int rk = (int)(rem % KT);
+  int local = (int)tile_n[3 * tile + 1] * KT + rk;
+  bool valid = local < tile_n[3 * tile];
+  int fwd = tile_n[3 * tile + 2];
+  int64_t grow = tile_fwd_row0[tile] + local;
+  float* kt = kb + ((int64_t)head * Ttot + tile) * (KT * 16);
+  float* vt = vb + ((int64_t)head * Ttot + tile) * (KT * 16);
+  float nk = 0.f;
+  for (int d = 0; d < 16; ++d) {
+    float kv = 0.f, vv = 0.f;
+    if (valid) {
+      if (d < d_head) {
+        int64_t o = grow * ld + head * d_head + d;
+        kv = tf32r(k[o]);
+        vv = tf32r(v[o]);
+        nk = fmaf(kv, kv, nk);
+      } else if (d == 15) {
+        kv = 1.f;
+        vv = 1.f;
+      }
+    }
+    kt[(d >> 2) * 256 + (rk >> 3) * 32 + (rk & 7) * 4 + (d & 3)] = kv;
+    vt[(rk >> 2) * 64 + (d >> 3) * 32 + (d & 7) * 4 + (rk & 3)] = vv;
+  }
+  if (valid) atomicMax(&kmax[fwd * n_head + head], __float_as_uint(sqrtf(nk)));
+}
+
+// Q for the fixed variant: scaled by log2(e)/sqrt(d_head), tf32-rounded, column 15 =
+// -b_i with b_i = |q_i| * max|k| * (1 + 2^-8) + 2^-8 (>= every score, after rounding).
+__global__ void repack_q_fixed_kernel(const float* __restrict__ q, int64_t ld, int n_head,
+                                      int d_head, int64_t R, const int32_t* __restrict__ row_fwd,
+                                      const unsigned* __restrict__ kmax, float qscale,
+                                      float* __restrict__ qh, int32_t* __restrict__ flag) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * n_head) return;
+  int64_t r = idx / n_head;
+  int head = (int)(idx % n_head);
+  float qv[16];
+  float nq = 0.f;
+  for (int d = 0; d < 16; ++d) {
+    float x = d < d_head ? tf32r(q[r * ld + head * d_head + d] * qscale) : 0.f;
+    qv[d] = x;
+    nq = fmaf(x, x, nq);
+  }
+  float km = __uint_as_float(kmax[row_fwd[r] * n_head + head]);
+  float bnd = sqrtf(nq) * km * (1.f + 1.f / 256.f) + 1.f / 256.f;
+  if (!(bnd <= BOUND_LIMIT)) atomicOr(flag, 1);
+  qv[15] = -bnd;
+  float* o = qh + ((int64_t)head * R + r) * 16;
+  for (int d = 0; d < 16; ++d) o[d] = qv[d];
+}
 }  // namespace tc
 
 bool tc_attention_supported(int d_head) { return d_head <= 16; }
@@ -434,6 +666,7 @@ void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& w
       tile_row0.push_back(row_off[f]);
       tile_n.push_back((int32_t)n);
       tile_n.push_back(t);
+      tile_n.push_back(f);
     }
     tb += T;
   }
@@ -443,24 +676,53 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
                        int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
                        int64_t num_works, const int64_t* tile_row0_dev,
                        const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
-                       int64_t ldo, cudaStream_t st) {
+                       int64_t ldo, const int32_t* row_fwd, int F, int32_t* scratch,
+                       cudaStream_t st) {
   if (num_works <= 0) return;
   if (d_head > 16) GO_THROW(GO_ERR_UNSUPPORTED, "tensor-core attention needs d_head <= 16");
   static bool attr = false;
   const size_t smem = sizeof(tc::Smem) + 1024;
+  const size_t smemf = sizeof(tc::SmemF) + 1024;
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_fixed_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf));
     attr = true;
   }
   float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   int64_t total = (int64_t)n_head * Ttot * tc::KT;
-  tc::repack_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
-      q, k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, R, qscale, qh, kb, vb);
-  LAUNCH_CHECK();
   dim3 grid((unsigned)num_works, (unsigned)n_head);
+  const char* force = getenv("GO_ATTN");
+  bool fixed_ok = d_head <= 15 && !(force && !strcmp(force, "online"));
+  if (fixed_ok) {
+    // scratch: [0] flag, [1..] kmax per (forward, head)
+    int32_t* flag = scratch;
+    unsigned* kmax = reinterpret_cast<unsigned*>(scratch + 1);
+    CUDA_CHECK(cudaMemsetAsync(scratch, 0, (size_t)(1 + F * n_head) * 4, st));
+    tc::repack_kv_fixed_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+        k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, kb, vb, kmax);
+    LAUNCH_CHECK();
+    tc::repack_q_fixed_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
+        q, ld, n_head, d_head, R, row_fwd, kmax, qscale, qh, flag);
+    LAUNCH_CHECK();
+    tc::attn_tc_fixed_kernel<<<grid, tc::NUM_THREADS, smemf, st>>>(
+        qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, flag);
+    LAUNCH_CHECK();
+    // fallback for bounds > BOUND_LIMIT: the online kernel re-packs and runs only if flagged
+    tc::repack_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+        q, k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, R, qscale, qh, kb, vb, flag);
+    LAUNCH_CHECK();
+    tc::attn_tc_kernel<<<grid, tc::NUM_THREADS, smem, st>>>(
+        qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, flag);
+    LAUNCH_CHECK();
+    return;
+  }
+  tc::repack_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+      q, k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, R, qscale, qh, kb, vb, nullptr);
+  LAUNCH_CHECK();
   tc::attn_tc_kernel<<<grid, tc::NUM_THREADS, smem, st>>>(
-      qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head);
+      qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, nullptr);
   LAUNCH_CHECK();
 }
 

@@ -228,6 +228,39 @@ class RolloutBatch:
         return any(s.valid for s in self.samples)
 
 
+def outer_draws(seed: int, count: int, num_graphs: int):
+    """training.py:122-126: per rollout, graph index then sample seed, from one
+    numpy stream (host; identical on every rank)."""
+    rng = np.random.default_rng(seed)
+    gi = np.empty(count, np.int64)
+    seeds = np.empty(count, np.int64)
+    for k in range(count):
+        gi[k] = int(rng.integers(num_graphs))
+        seeds[k] = int(rng.integers(2**31))
+    return gi, seeds
+
+
+def shard_bounds(count: int, rank: int, world: int):
+    """Contiguous shard of global rollout ids owned by `rank`."""
+    return rank * count // world, (rank + 1) * count // world
+
+
+def gather_results(packed, count: int, world: int):
+    """All-gather per-rollout result columns ([C, local] tensors) from every rank into
+    [C, count] in global rollout order -- the one collective of the scoring path
+    (NCCL on GPUs, gloo in the CPU tests)."""
+    import torch.distributed as dist
+    T = torch()
+    sizes = [shard_bounds(count, q, world)[1] - shard_bounds(count, q, world)[0]
+             for q in range(world)]
+    mx = max(sizes)
+    pad = T.zeros((packed.shape[0], mx), dtype=packed.dtype, device=packed.device)
+    pad[:, :packed.shape[1]] = packed
+    bufs = [T.empty_like(pad) for _ in sizes]
+    dist.all_gather(bufs, pad)
+    return T.cat([b[:, :s] for b, s in zip(bufs, sizes)], dim=1)
+
+
 def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed, hyper,
                      embed_cfg, policy_cfg, fusion_cfg, base_assignments=None,
                      keep_logits: bool = True, shard=None) -> RolloutBatch:
@@ -241,16 +274,8 @@ def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed
     T = torch()
     dev = T.device("cuda", context().device)
     graphs = [as_graph(g) for g in graphs]
-    rng = np.random.default_rng(seed)
-    gi_all = np.empty(count, np.int64)
-    seeds_all = np.empty(count, np.int64)
-    for k in range(count):
-        gi_all[k] = int(rng.integers(len(graphs)))
-        seeds_all[k] = int(rng.integers(2**31))
-    lo, hi = 0, count
-    if shard is not None:
-        r, w = shard
-        lo, hi = r * count // w, (r + 1) * count // w
+    gi_all, seeds_all = outer_draws(seed, count, len(graphs))
+    lo, hi = shard_bounds(count, *(shard or (0, 1)))
     gi, seeds = gi_all[lo:hi], seeds_all[lo:hi]
     count = hi - lo
     tasks = ordered_tasks(task_sizes)
@@ -316,21 +341,8 @@ def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed
     if shard is not None and shard[1] > 1:
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized():
-            # the one exchange of the scoring path: per-rollout results to every rank
-            packed = T.stack([rewards, steps, valid.to(T.float64), values.to(T.float64)])
-            sizes = [(q + 1) * len(gi_all) // shard[1] - q * len(gi_all) // shard[1]
-                     for q in range(shard[1])]
-            bufs = [T.empty((4, s), dtype=T.float64, device=dev) for s in sizes]
-            if len(set(sizes)) == 1:
-                dist.all_gather(bufs, packed)
-            else:
-                mx = max(sizes)
-                pad = T.zeros((4, mx), dtype=T.float64, device=dev)
-                pad[:, :packed.shape[1]] = packed
-                tmp = [T.empty((4, mx), dtype=T.float64, device=dev) for _ in sizes]
-                dist.all_gather(tmp, pad)
-                bufs = [t[:, :s] for t, s in zip(tmp, sizes)]
-            full = T.cat(bufs, dim=1)
+            full = gather_results(T.stack([rewards, steps, valid.to(T.float64),
+                                           values.to(T.float64)]), len(gi_all), shard[1])
             batch.global_rewards, batch.global_step_times = full[0], full[1]
             batch.global_valid, batch.global_values = full[2] > 0.5, full[3]
     return batch
