@@ -18,6 +18,7 @@
 //    (time, kind, delta) order; processed online per time group (allocs before
 //    frees; exact sorted order when byte values are not all integral).
 #include <algorithm>
+#include <cstring>
 
 #include "engine.cuh"
 
@@ -69,8 +70,10 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
                            double* __restrict__ o_step, uint8_t* __restrict__ o_valid,
                            int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
                            double* __restrict__ o_peak, double* __restrict__ o_reward,
-                           int32_t* __restrict__ o_status) {
-  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+                           int32_t* __restrict__ o_status, int lanes_per_placement) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gtid % lanes_per_placement) return;
+  const int tid = gtid / lanes_per_placement;
   if (tid >= K) return;
   const int kk = which ? which[tid] : tid;
   const int32_t* pl = placement + (int64_t)kk * pstride;
@@ -123,7 +126,8 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
     lq_h[s] = 0;
     lq_n[s] = 0;
   }
-  for (int w = 0; w < (L + 63) / 64; ++w) lmask[w] = 0;
+  uint64_t amask[DES_MAXD * DES_MAXD / 64];  // links with a transfer in flight
+  for (int w = 0; w < (L + 63) / 64; ++w) lmask[w] = amask[w] = 0;
   uint32_t dmask = 0;  // devices with a non-empty ready heap
   int status = ST_OK;
 
@@ -242,6 +246,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
         double dt = __ddiv_rn(V.out_bytes[e.edge], lbw[s]);
         link_t[s] = __dadd_rn(t, dt);
         link_g[s] = e.grp;
+        amask[w] |= 1ull << b;
       }
     }
     uint32_t m = dmask;
@@ -266,7 +271,9 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
   while (status == ST_OK) {
     double now = DINF;
     for (int i = 0; i < d; ++i) now = fmin(now, dev_t[i]);
-    for (int s = 0; s < L; ++s) now = fmin(now, link_t[s]);
+    for (int w = 0; w < (L + 63) / 64; ++w)
+      for (uint64_t mm = amask[w]; mm; mm &= mm - 1)
+        now = fmin(now, link_t[w * 64 + __ffsll((long long)mm) - 1]);
     if (now == DINF) break;
     if (now != mem_time) {
       mem_flush();
@@ -306,12 +313,17 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
       if (V.nsucc[g] == 0 && b != 0.0) mem_add(dev, b, false);
     }
     // transfers (kind 1) in (src, dst) order
-    for (int s = 0; s < L; ++s) {
-      if (link_t[s] != now) continue;
-      int g = link_g[s];
-      link_t[s] = DINF;
-      link_g[s] = -1;
-      deliver(g, now);
+    for (int w = 0; w < (L + 63) / 64; ++w) {
+      for (uint64_t mm = amask[w]; mm; mm &= mm - 1) {
+        const int b = __ffsll((long long)mm) - 1;
+        const int s = w * 64 + b;
+        if (link_t[s] != now) continue;
+        int g = link_g[s];
+        link_t[s] = DINF;
+        link_g[s] = -1;
+        amask[w] &= ~(1ull << b);
+        deliver(g, now);
+      }
     }
     if (status != ST_OK) break;
     schedule(now);
@@ -368,11 +380,14 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
     CUDA_CHECK(cudaMemcpyAsync(dtopo, topo.data(), topo.size() * 8, cudaMemcpyHostToDevice, st));
     if (which)
       CUDA_CHECK(cudaMemcpyAsync(dwhich, which, (size_t)count * 4, cudaMemcpyHostToDevice, st));
+    // one placement per lane (32 per warp) or one per warp (no intra-warp divergence)
+    const char* mode = getenv("GO_DES_MODE");
+    const int lanes = (mode && !strcmp(mode, "warp")) ? 32 : 1;
     const int threads = 32;
-    des_kernel<<<(unsigned)cdiv(count, threads), threads, 0, st>>>(
+    des_kernel<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
         v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
         dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
-        step_time, valid, violation, busy, peak_mem, reward, dstatus);
+        step_time, valid, violation, busy, peak_mem, reward, dstatus, lanes);
     LAUNCH_CHECK();
     std::vector<int32_t> hstat(count);
     CUDA_CHECK(cudaMemcpyAsync(hstat.data(), dstatus, (size_t)count * 4, cudaMemcpyDeviceToHost,

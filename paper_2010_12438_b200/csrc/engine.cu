@@ -483,6 +483,248 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
   }
 }
 
+// Tensor-core forward for 128-wide configs (the reference defaults): every dense layer
+// is a tcgen05 3xTF32 GEMM with its bias/activation or residual+LayerNorm fused in
+// the epilogue (tc_gemm.cu); Q/K/V are one merged GEMM; the trunk's modulation
+// x*m is fused into the previous layer's LN2 epilogue.  Same math as run_forward.
+static bool tc_forward_ok(const go_config_t& c, const go_batch_t& b) {
+  const char* f = getenv("GO_GEMM");
+  if (f && !strcmp(f, "simt")) return false;
+  return c.gs_dim == 128 && c.d_model == 128 && c.n_head * c.d_head <= 144 && !b.features;
+}
+
+static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
+                           const int64_t* off, const go_batch_t& b, float* node_embed,
+                           float* graph_embed, float* hid, float* logits, float* value,
+                           int32_t* status_dev, cudaStream_t st) {
+  validate(cfg);
+  const bool do_e = b.stage_mask & 1, do_t = b.stage_mask & 2, do_h = b.stage_mask & 4;
+  BatchMeta m = make_meta(ctx, cfg, b, do_e, do_t, do_h, st);
+  const int64_t R = m.R;
+  const int F = m.F;
+  Slots S = slots_of(cfg);
+  auto W_ = [&](int slot) { return P + off[slot]; };
+  const int gs = 128, dm = 128, H = cfg.n_head, dh = cfg.d_head, W = H * dh, di = cfg.d_inner;
+  const int64_t LW = 128, LQ = 144, LA = ldp(W), LI = ldp(di);
+  // workspace: activations + packed weights
+  const int Lg = cfg.gs_layers, Lt = cfg.trf_layers, T = cfg.num_tasks;
+  size_t pk = 0;
+  pk += (size_t)Lg * (tc_gemm_packed_floats(gs, gs) + tc_gemm_packed_floats(2 * gs, gs));
+  pk += tc_gemm_packed_floats(gs, dm);
+  pk += (size_t)(Lt + 1) * (tc_gemm_packed_floats(dm, 3 * W) + tc_gemm_packed_floats(W, dm));
+  pk += (size_t)Lt * (tc_gemm_packed_floats(dm, di) + tc_gemm_packed_floats(di, dm));
+  for (int t = 0; t < T; ++t)
+    pk += tc_gemm_packed_floats(2 * dm, dm) + tc_gemm_packed_floats(dm, dm) +
+          tc_gemm_packed_floats(dm, di) + tc_gemm_packed_floats(di, dm) +
+          tc_gemm_packed_floats(dm, cfg.task_sizes[t]);
+  size_t bytes = forward_ws_bytes(cfg, R, m.gtotal, F, m.n_chunks) + (size_t)R * (LQ + 16) * 4 +
+                 pk * 4 + (size_t)(Lt + 2) * 4 * 160 + (4u << 20);
+  Arena A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
+  float* X[6];
+  for (int i = 0; i < 6; ++i) X[i] = A.take<float>(R * LW);
+  float* QKV = A.take<float>(R * LQ);
+  float* Ab = A.take<float>(R * LA);
+  float* F1 = A.take<float>(R * LI);
+  int32_t* row_fwd = A.take<int32_t>(R);
+  int32_t* gidx = A.take<int32_t>(m.gtotal);
+  float* mod = A.take<float>((int64_t)F * dm);
+  float* meanb = A.take<float>((int64_t)F * dm);
+  float* part = A.take<float>((m.n_chunks + 1) * 128);
+  row_fwd_fill(m.d_row_off, F, R, row_fwd, st);
+  auto pack = [&](const float* w0, const float* w1, const float* w2, int Nsub, int64_t ldw, int K,
+                  int N) {
+    float* out = A.take<float>((int64_t)tc_gemm_packed_floats(K, N));
+    tc_gemm_pack(w0, w1, w2, Nsub, ldw, K, N, out, st);
+    return out;
+  };
+  auto pack1 = [&](const float* w, int K, int N) { return pack(w, nullptr, nullptr, N, N, K, N); };
+  auto qkv_bias = [&](const float* bq, const float* bk, const float* bv) {
+    float* bb = A.take<float>(160);
+    CUDA_CHECK(cudaMemcpyAsync(bb, bq, W * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(bb + W, bk, W * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(bb + 2 * W, bv, W * 4, cudaMemcpyDeviceToDevice, st));
+    return bb;
+  };
+  double gemm_flops = 0;
+  auto gf = [&](int K, int N) { gemm_flops += 2.0 * R * K * N; };
+
+  if (do_e) {
+    GO_CHECK(node_embed && graph_embed, "embed outputs required");
+    int32_t tcol[3] = {0, 0, 0};
+    int c = 16;
+    for (int t = 0; t < T; ++t) {
+      tcol[t] = c;
+      c += cfg.task_sizes[t];
+    }
+    neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, F, R, row_fwd, cfg.gs_knn,
+                    gidx, st);
+    float* h = Lg == 0 ? node_embed : X[0];
+    features_inproj(m.d_views, m.d_row_off, row_fwd, R, b.prev_actions, T, tcol, W_(S.e_in_w()),
+                    W_(S.e_in_b()), gs, h, gs, st);
+    for (int l = 0; l < Lg; ++l) {
+      float* t = X[1];
+      float* pooled = X[2];
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * gs);
+        tc_gemm(h, gs, gs, nullptr, 0, 0, pack1(W_(S.e_layer(l, 0)), gs, gs), W_(S.e_layer(l, 1)),
+                t, LW, R, gs, 2, st);
+      }
+      {
+        double bytes = (double)(m.gtotal + R) * gs * 4 + (double)m.gtotal * 4 +
+                       (double)(R + 1) * 8 + (double)R * 4;
+        KTimer kt(ctx, K_SEGMAX, st, bytes);
+        segment_max(t, LW, m.d_views, m.d_row_off, m.d_gbase, row_fwd, gidx, R, gs, pooled, LW,
+                    st);
+      }
+      bool last = l == Lg - 1;
+      float* hn = last ? node_embed : (h == X[0] ? X[3] : X[0]);
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * 2 * gs * gs);
+        tc_gemm(h, gs, gs, pooled, LW, gs, pack1(W_(S.e_layer(l, 2)), 2 * gs, gs),
+                W_(S.e_layer(l, 3)), hn, gs, R, gs, 1, st);
+      }
+      h = hn;
+    }
+    if (status_dev) check_finite(node_embed, gs, R, gs, status_dev, st);
+    mean_rows(node_embed, gs, m.d_row_off, F, m.d_chunks, m.n_chunks, gs, graph_embed, gs, part,
+              st);
+  }
+
+  if (do_t) {
+    GO_CHECK(node_embed && graph_embed && hid, "trunk inputs/outputs required");
+    const float* modp = b.mod_override;
+    if (!modp) {
+      int mb = Lt;
+      BlockW bw{W_(S.blk(mb, V_W)),  W_(S.blk(mb, V_B)),  W_(S.blk(mb, O_W)),  W_(S.blk(mb, O_B)),
+                W_(S.blk(mb, LN1_G)), W_(S.blk(mb, LN1_B)), W_(S.blk(mb, FF_W1)),
+                W_(S.blk(mb, FF_B1)), W_(S.blk(mb, FF_W2)), W_(S.blk(mb, FF_B2)),
+                W_(S.blk(mb, LN2_G)), W_(S.blk(mb, LN2_B))};
+      modulate(graph_embed, gs, F, gs, W_(S.p_in_w()), W_(S.p_in_b()), bw, dm, W, di, mod, st);
+      modp = mod;
+    }
+    float* x0 = Lt == 0 ? hid : X[0];
+    {
+      KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * dm);
+      tc_gemm(node_embed, gs, gs, nullptr, 0, 0, pack1(W_(S.p_in_w()), gs, dm), W_(S.p_in_b()), x0,
+              dm, R, dm, 0, st);
+    }
+    float* xm = X[1];
+    if (Lt > 0) mul_rowvec(x0, LW, modp, dm, row_fwd, xm, LW, R, dm, st);
+    for (int l = 0; l < Lt; ++l) {
+      const float* bq = qkv_bias(W_(S.blk(l, Q_B)), W_(S.blk(l, K_B)), W_(S.blk(l, V_B)));
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * 3 * W);
+        tc_gemm(xm, LW, dm, nullptr, 0, 0,
+                pack(W_(S.blk(l, Q_W)), W_(S.blk(l, K_W)), W_(S.blk(l, V_W)), W, W, dm, 3 * W), bq,
+                QKV, LQ, R, 3 * W, 0, st);
+      }
+      {
+        KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
+        attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab, LA,
+                  st);
+      }
+      float* h1 = X[2];
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * W * dm);
+        tc_gemm_ln(Ab, LA, W, nullptr, 0, 0, pack1(W_(S.blk(l, O_W)), W, dm), W_(S.blk(l, O_B)), xm,
+                   LW, W_(S.blk(l, LN1_G)), W_(S.blk(l, LN1_B)), h1, LW, nullptr, nullptr, nullptr,
+                   0, R, dm, st);
+      }
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * di);
+        tc_gemm(h1, LW, dm, nullptr, 0, 0, pack1(W_(S.blk(l, FF_W1)), dm, di), W_(S.blk(l, FF_B1)),
+                F1, LI, R, di, 1, st);
+      }
+      bool last = l == Lt - 1;
+      float* xm_next = (xm == X[1]) ? X[3] : X[1];
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * di * dm);
+        tc_gemm_ln(F1, LI, di, nullptr, 0, 0, pack1(W_(S.blk(l, FF_W2)), di, dm),
+                   W_(S.blk(l, FF_B2)), h1, LW, W_(S.blk(l, LN2_G)), W_(S.blk(l, LN2_B)),
+                   last ? hid : nullptr, dm, last ? nullptr : modp, row_fwd,
+                   last ? nullptr : xm_next, LW, R, dm, st);
+      }
+      xm = xm_next;
+    }
+  }
+
+  if (do_h) {
+    GO_CHECK(hid && logits, "heads inputs/outputs required");
+    const char* force = getenv("GO_ATTN");
+    const bool use_tc = tc_attention_supported(dh) && !(force && !strcmp(force, "simt"));
+    float *tc_q = nullptr, *tc_k = nullptr, *tc_v = nullptr;
+    int32_t* tc_scratch = nullptr;
+    if (use_tc) {
+      tc_q = A.take<float>((int64_t)H * R * 16);
+      tc_k = A.take<float>((int64_t)H * m.n_tiles * 64 * 16);
+      tc_v = A.take<float>((int64_t)H * m.n_tiles * 64 * 16);
+      tc_scratch = A.take<int32_t>(1 + (int64_t)F * H);
+    }
+    const float* ta_qkv = pack(W_(S.ta(Q_W)), W_(S.ta(K_W)), W_(S.ta(V_W)), W, W, dm, 3 * W);
+    const float* ta_b = qkv_bias(W_(S.ta(Q_B)), W_(S.ta(K_B)), W_(S.ta(V_B)));
+    const float* ta_o = pack1(W_(S.ta(O_W)), W, dm);
+    float* a_prev = nullptr;
+    int64_t ld_prev = LW;
+    float* rep_bufs[2] = {X[4], X[5]};
+    int64_t lcol = 0;
+    for (int t = 0; t < T; ++t) {
+      bool zero_in = (a_prev == nullptr) || (b.ablate_mask >> t & 1);
+      float* hh = X[1];
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * (zero_in ? 1 : 2) * dm * dm);
+        if (zero_in)  // [0 | hid] @ cat_w == hid @ cat_w[d:]
+          tc_gemm_ln(hid, dm, dm, nullptr, 0, 0, pack1(W_(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, dm),
+                     W_(S.task(t, CAT_B)), nullptr, 0, W_(S.task(t, LN_G)), W_(S.task(t, LN_B)), hh,
+                     LW, nullptr, nullptr, nullptr, 0, R, dm, st);
+        else
+          tc_gemm_ln(a_prev, ld_prev, dm, hid, dm, dm, pack1(W_(S.task(t, CAT_W)), 2 * dm, dm),
+                     W_(S.task(t, CAT_B)), nullptr, 0, W_(S.task(t, LN_G)), W_(S.task(t, LN_B)), hh,
+                     LW, nullptr, nullptr, nullptr, 0, R, dm, st);
+      }
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * 3 * W);
+        tc_gemm(hh, LW, dm, nullptr, 0, 0, ta_qkv, ta_b, QKV, LQ, R, 3 * W, 0, st);
+      }
+      {
+        KTimer kt(ctx, K_HEADS_ATTN, st, 4.0 * m.head_pairs * W);
+        if (use_tc)
+          attention_full_tc(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, R, m.n_tiles, m.d_tc_works,
+                            m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
+                            row_fwd, F, tc_scratch, st);
+        else
+          attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_head_tiles, m.n_head_tiles, Ab, LA,
+                    st);
+      }
+      float* o = X[2];
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * (W * dm + 2.0 * dm * di));
+        tc_gemm(Ab, LA, W, nullptr, 0, 0, ta_o, W_(S.ta(O_B)), o, LW, R, dm, 0, st);
+        tc_gemm(o, LW, dm, nullptr, 0, 0, pack1(W_(S.task(t, FC_W1)), dm, di), W_(S.task(t, FC_B1)),
+                F1, LI, R, di, 1, st);
+      }
+      float* rep = b.reps ? b.reps + (int64_t)t * R * dm : rep_bufs[t & 1];
+      const int64_t ldr = b.reps ? dm : LW;
+      int a = cfg.task_sizes[t];
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * (di * dm + dm * a));
+        tc_gemm(F1, LI, di, nullptr, 0, 0, pack1(W_(S.task(t, FC_W2)), di, dm), W_(S.task(t, FC_B2)),
+                rep, ldr, R, dm, 0, st);
+        tc_gemm(rep, ldr, dm, nullptr, 0, 0, pack1(W_(S.task(t, OUT_W)), dm, a), W_(S.task(t, OUT_B)),
+                logits + lcol, a, R, a, 0, st);
+      }
+      lcol += R * a;
+      a_prev = rep;
+      ld_prev = ldr;
+    }
+    if (value) {
+      mean_rows(a_prev, ld_prev, m.d_row_off, F, m.d_chunks, m.n_chunks, dm, meanb, dm, part, st);
+      value_head(meanb, F, dm, W_(S.value_w()), W_(S.value_b()), value, st);
+    }
+  }
+  (void)gf;
+  (void)gemm_flops;
+}
+
 extern "C" {
 
 const char* go_last_error(void) { return g_last_error.c_str(); }
@@ -546,8 +788,12 @@ int go_forward(go_ctx_t ctx, const go_config_t* cfg, const float* params,
                float* graph_embed, float* hid, float* logits, float* value, void* stream) {
   return guarded([&] {
     CUDA_CHECK(cudaSetDevice(ctx->device));
-    run_forward(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid, logits,
-                value, nullptr, (cudaStream_t)stream);
+    if (tc_forward_ok(*cfg, *batch))
+      run_forward_tc(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid,
+                     logits, value, nullptr, (cudaStream_t)stream);
+    else
+      run_forward(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid, logits,
+                  value, nullptr, (cudaStream_t)stream);
   });
 }
 
@@ -558,8 +804,12 @@ int go_forward_status(go_ctx_t ctx, const go_config_t* cfg, const float* params,
                       int32_t* status_dev, void* stream) {
   return guarded([&] {
     CUDA_CHECK(cudaSetDevice(ctx->device));
-    run_forward(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid, logits,
-                value, status_dev, (cudaStream_t)stream);
+    if (tc_forward_ok(*cfg, *batch))
+      run_forward_tc(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid,
+                     logits, value, status_dev, (cudaStream_t)stream);
+    else
+      run_forward(ctx, *cfg, params, param_offsets, *batch, node_embed, graph_embed, hid, logits,
+                  value, status_dev, (cudaStream_t)stream);
   });
 }
 

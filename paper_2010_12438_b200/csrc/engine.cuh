@@ -220,6 +220,20 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b, bo
                     bool need_trunk, bool need_heads, cudaStream_t st, const void* extra = nullptr,
                     size_t extra_bytes = 0, const void** extra_dev = nullptr);
 
+// ---- kernels: tc_gemm.cu (tcgen05 3xTF32 dense layers)
+int tc_gemm_bn(int N);
+size_t tc_gemm_packed_floats(int K, int N);
+void tc_gemm_pack(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw, int K,
+                  int N, float* out, cudaStream_t st);
+void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
+             const float* Wpk, const float* bias, float* C, int64_t ldc, int64_t M, int N,
+             int act, cudaStream_t st);
+void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
+                const float* Wpk, const float* bias, const float* resid, int64_t ldr,
+                const float* g, const float* beta, float* C, int64_t ldc, const float* rowscale,
+                const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M, int N,
+                cudaStream_t st);
+
 // ---- kernels: sample.cu
 void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t R,
                  const int64_t* row_off_dev, const int32_t* row_fwd, const int32_t* order_of_row,

@@ -110,3 +110,42 @@ def test_ragged_batch_matches_single_forwards():
         lo, hi = out.row_off[i], out.row_off[i + 1]
         assert rel_err(lg[lo:hi], one.logits[0].cpu().numpy()) < 1e-5
         assert abs(float(out.value[i]) - float(one.value[0])) < 1e-5
+
+
+def _forward_with(mode, store, ecfg, pcfg, sizes, graphs, seeds):
+    from paper_2010_12438_b200.engine import forward_batch
+    from paper_2010_12438_b200.runtime import context
+    old = os.environ.get("GO_GEMM")
+    os.environ["GO_GEMM"] = mode
+    try:
+        ctx = context()
+        out = forward_batch(store, ecfg, pcfg, sizes, [ctx.graph(g) for g in graphs], seeds)
+        return (out.node_embed.cpu().numpy(), out.logits[0].cpu().numpy(), out.value.cpu().numpy())
+    finally:
+        if old is None:
+            del os.environ["GO_GEMM"]
+        else:
+            os.environ["GO_GEMM"] = old
+
+
+def test_tc_gemm_forward_matches_simt_and_oracle():
+    """The tcgen05 3xTF32 dense layers (default 128-wide config) agree with the SIMT
+    fp32 GEMMs and with the float64 oracle on a workload graph and a ragged batch."""
+    from oracle import forward as of
+    from oracle import graph as og
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    sizes = {"placement": 8}
+    ecfg, pcfg, store = _store(sizes)
+    graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 300, 1, 64, seed=0), node_cap=10**6),
+              gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))]
+    seeds = [5, 6]
+    ne_t, lg_t, v_t = _forward_with("tc", store, ecfg, pcfg, sizes, graphs, seeds)
+    ne_s, lg_s, v_s = _forward_with("simt", store, ecfg, pcfg, sizes, graphs, seeds)
+    assert rel_err(ne_t, ne_s) < 1e-5
+    assert rel_err(lg_t, lg_s) < 1e-5
+    assert rel_err(v_t, v_s) < 1e-5
+    g = graphs[0]
+    ogr = og.make(g.num_nodes, g.op, g.flops, g.out_bytes, g.src, g.dst, g.ebytes)
+    logits, _, value = of.forward_policy(ogr, _oracle_P(store), of.EmbedCfg(), of.PolicyCfg(),
+                                         sizes, None, 5)
+    assert rel_err(lg_t[:g.num_nodes], logits["placement"]) < 1e-4
