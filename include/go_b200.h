@@ -186,14 +186,15 @@ int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards,
  * embed seed).  actions: dev int32 [T][rows], the sampled actions, node-indexed per
  * span; old_logp: dev float64 [T][rows], topo-row indexed; fparams: host [F][4] =
  * (advantage, temperature, reward, 0).  grads: dev float32 with the parameter-blob
- * layout, ACCUMULATED (caller zeroes per minibatch); the loss is the mean over the
- * F samples.  stats_out: host float64 [14*F]: [F][3][4] (sum surr, sum entropy, sum
+ * layout, ACCUMULATED (caller zeroes per minibatch); the loss is the sum over the F
+ * samples divided by loss_denominator (<= 0: F), so ranks holding parts of one
+ * minibatch produce gradients that all-reduce(sum) to the minibatch mean.  stats_out: host float64 [14*F]: [F][3][4] (sum surr, sum entropy, sum
  * ratio, clipped count) per task slot, then [F] (value - reward)^2, then [F] value. */
 int go_ppo_grad(go_ctx_t ctx, const go_config_t* cfg, const float* params,
                 const int64_t* param_offsets, const go_batch_t* batch, const int32_t* actions,
                 const double* old_logp, const double* fparams, double clip_eps,
-                double entropy_coef, double value_coef, float* grads, double* stats_out,
-                void* stream);
+                double entropy_coef, double value_coef, int32_t loss_denominator, float* grads,
+                double* stats_out, void* stream);
 
 /* Fused bias-corrected Adam over a flat float32 blob (replaces tensor.py:428-441
  * ParamStore.adam_step; every element steps, zero gradient where none flowed). */

@@ -76,7 +76,7 @@ _SIGS = {
     "go_neighbor_arrays": (C.c_int, [P, P, I64, I32, P, P, P]),
     "go_sample": (C.c_int, [P, C.POINTER(GoConfig), I32, P, P, P, P, I32, F64, P, P, P]),
     "go_ppo_grad": (C.c_int, [P, C.POINTER(GoConfig), P, P, C.POINTER(GoBatch), P, P, P, F64, F64,
-                              F64, P, P, P]),
+                              F64, I32, P, P, P]),
     "go_adam": (C.c_int, [P, P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
     "go_simulate": (C.c_int, [P, P, I32, P, P, I32, I32, P, P, P, P, I32, F64, P, P, P, P, P,
                               P, P]),

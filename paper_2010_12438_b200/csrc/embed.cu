@@ -150,7 +150,36 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
     }
     return;
   }
-  if ((D & 3) == 0 && (ldt & 3) == 0 && (ldo & 3) == 0) {
+  if (D == 128 && (ldt & 3) == 0 && (ldo & 3) == 0 && s1 - s0 <= 32) {
+    // fast path: one float4 column slice per lane; the segment's neighbour indices
+    // are loaded once (one lane each) and broadcast by shuffle, and the gathered rows
+    // are fetched 4 at a time so each lane keeps 4 independent 16-B loads in flight.
+    const int cnt = (int)(s1 - s0);
+    const int myidx = lane < cnt ? gidx[s0 + lane] : 0;
+    const float4* tb = reinterpret_cast<const float4*>(t) + lane;
+    const int64_t ld4 = ldt >> 2;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cnt > 0) {
+      m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      for (int j = 0; j < cnt; j += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int jj = j + u < cnt ? j + u : j;  // duplicate a valid row: max is idempotent
+          const int src = __shfl_sync(0xffffffffu, myidx, jj);
+          v[u] = __ldg(tb + (int64_t)src * ld4);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          m.x = fmaxf(m.x, v[u].x);
+          m.y = fmaxf(m.y, v[u].y);
+          m.z = fmaxf(m.z, v[u].z);
+          m.w = fmaxf(m.w, v[u].w);
+        }
+      }
+    }
+    reinterpret_cast<float4*>(out + r * ldo)[lane] = m;
+  } else if ((D & 3) == 0 && (ldt & 3) == 0 && (ldo & 3) == 0) {
     int D4 = D >> 2;
     for (int c4 = lane; c4 < D4; c4 += 32) {
       float4 m = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -435,6 +435,28 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
 // when every b_i <= BOUND_LIMIT (exp2 then never underflows for scores within 2 b_i
 // of the bound); otherwise the online-softmax kernel above takes the launch.
 constexpr float BOUND_LIMIT = 60.f;
+#ifndef GO_POLY_PER_8
+#define GO_POLY_PER_8 0
+#endif
+constexpr int POLY_PER_8 = GO_POLY_PER_8;  // of every 8 columns, this many use ex2_poly
+
+// 2^x for x <= 0 on the FMA/ALU pipes: x = n + f, n = rint(x) (magic-number add),
+// f in [-0.5, 0.5], 2^f by a degree-4 minimax polynomial, 2^n by exponent add.
+// Inputs below -126 return 0 (the MUFU path flushes there too).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer
+  const int n = __float_as_int(t) - 0x4B400000;
+  const float f = x - (t - 12582912.f);
+  float p = 1.3333558146e-3f;
+  p = fmaf(p, f, 9.6181291076e-3f);
+  p = fmaf(p, f, 5.5504108664e-2f);
+  p = fmaf(p, f, 2.4022650695e-1f);
+  p = fmaf(p, f, 6.9314718056e-1f);
+  p = fmaf(p, f, 1.0f);
+  const float r = __int_as_float(__float_as_int(p) + (n << 23));
+  return n < -126 ? 0.f : r;
+}
 
 struct SmemF {
   float q[NQT][QT * 16];
@@ -557,7 +579,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       TC_LD32(sa + 32, (sr + 32));
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < KT; ++i) sr[i] = __float_as_uint(ex2(__uint_as_float(sr[i])));
+      for (int i = 0; i < KT; ++i) {
+        const float x = __uint_as_float(sr[i]);
+        // FA4-style split: a fixed subset of the columns is exponentiated on the FMA
+        // pipe (degree-4 polynomial, rel. err < 4e-6, far below the tf32 rounding of
+        // P) so the MUFU and FMA pipes work in parallel.
+        sr[i] = __float_as_uint(((i & 7) < POLY_PER_8) ? ex2_poly(x) : ex2(x));
+      }
       TC_ST32(sa, sr);
       TC_ST32(sa + 32, (sr + 32));
       tmem_wait_st();

@@ -12,6 +12,7 @@
 // float4), split it into hi/lo and store both in the UMMA K-major canonical layout;
 // they are also the epilogue.  Warp 4 (one thread) streams the prepacked W_hi/W_lo
 // chunks with cp.async.bulk and issues the MMAs.  Multi-stage smem ring, mbarriers.
+#include <algorithm>
 #include <cstring>
 
 #include "engine.cuh"
@@ -130,209 +131,284 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KB per hi/lo tile
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int NS = (216 * 1024 / STAGE) < 4 ? (216 * 1024 / STAGE) : 4;
+  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // epilogue staging, 4 warps
+  // 227 KB opt-in limit minus staging and barriers; >= 2 stages or the B refill schedule
+  // (stage of chunk g-1 refilled after chunk g is issued) cannot make progress
+  static constexpr int BUDGET = 232448 - EPI_BYTES - 1536;
+  static constexpr int NS = (BUDGET / STAGE) < 4 ? (BUDGET / STAGE) : 4;
+  static_assert(NS >= 2, "tc_gemm needs at least two smem stages");
   static constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr size_t SMEM = (size_t)NS * STAGE + 1024 + 256;
+  static constexpr uint32_t TALLOC = 2 * TCOLS;  // double-buffered accumulator
+  static constexpr size_t SMEM = (size_t)NS * STAGE + EPI_BYTES + 1536;
 };
 
+constexpr int G_THREADS = 288;  // warps 0-3 load A, 4-7 epilogue, 8 = B producer + MMA issuer
+
+#define TG_ST16(taddr, r)                                                                    \
+  asm volatile(                                                                              \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%" \
+      "14,%15,%16};" ::"r"(taddr),                                                           \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),      \
+      "r"(r[15]))
+
+// Persistent, warp-specialised tile loop: CTA b processes tiles b, b + grid, ...
+// (tile t -> m tile t / nblk, n block t % nblk).  The smem ring and the two TMEM
+// accumulators carry their phases across tiles, so the loads and MMAs of tile i+1
+// overlap the epilogue of tile i.
 template <int BN, bool LN>
-__global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(Args a) {
+__global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk, int ntiles) {
   using CF = Cfg<BN>;
   constexpr int NS = CF::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stage_base = smem_raw;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NS * CF::STAGE);
-  uint64_t* a_full = bars;            // [NS] 128 arrivals
-  uint64_t* b_full = bars + NS;       // [NS] tx
-  uint64_t* done = bars + 2 * NS;     // [NS] MMA commit
-  uint64_t* acc_full = bars + 3 * NS; // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 1);
+  float* epi = reinterpret_cast<float*>(smem_raw + (size_t)NS * CF::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NS * CF::STAGE + CF::EPI_BYTES);
+  uint64_t* a_full = bars;              // [NS] 128 arrivals
+  uint64_t* b_full = bars + NS;         // [NS] tx bytes
+  uint64_t* done = bars + 2 * NS;       // [NS] MMA commit: stage free
+  uint64_t* acc_full = bars + 3 * NS;   // [2] MMA commit: accumulator ready
+  uint64_t* acc_empty = bars + 3 * NS + 2;  // [2] 128 arrivals: accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int nblk = blockIdx.y;
-  const int n0 = nblk * BN;
   auto A_hi = [&](int s) { return reinterpret_cast<float*>(stage_base + (size_t)s * CF::STAGE); };
   auto A_lo = [&](int s) { return A_hi(s) + BM * BK; };
   auto B_hi = [&](int s) { return A_hi(s) + 2 * BM * BK; };
   auto B_lo = [&](int s) { return B_hi(s) + BN * BK; };
-  const float* bsrc = a.Bpk + (size_t)nblk * a.nch * 2 * BN * BK;
+  const int nch = a.nch;
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       for (int s = 0; s < NS; ++s) {
         mbar_init(&a_full[s], 128);
         mbar_init(&b_full[s], 1);
         mbar_init(&done[s], 1);
       }
-      mbar_init(acc_full, 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&acc_full[b], 1);
+        mbar_init(&acc_empty[b], 128);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(CF::TCOLS));
+                 "r"(CF::TALLOC));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tacc = *tmem_slot;
-  const int nch = a.nch;
+  const uint32_t tbase = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
+    // ------------------------------------------------ B producer + MMA issuer
     if (lane == 0) {
       constexpr uint32_t ID = idesc_tf32(BM, BN);
-      auto load_b = [&](int c, int s) {
+      const int total = my_tiles * nch;
+      auto load_b = [&](int g) {
+        const int s = g % NS;
+        const int t = blockIdx.x + (g / nch) * gridDim.x;
+        const int c = g % nch;
+        const float* src = a.Bpk + ((size_t)(t % nblk) * nch + c) * 2 * BN * BK;
         mbar_expect_tx(&b_full[s], 2 * CF::B_BYTES);
-        bulk_g2s(B_hi(s), bsrc + (size_t)c * 2 * BN * BK, CF::B_BYTES, &b_full[s]);
-        bulk_g2s(B_lo(s), bsrc + (size_t)c * 2 * BN * BK + BN * BK, CF::B_BYTES, &b_full[s]);
+        bulk_g2s(B_hi(s), src, CF::B_BYTES, &b_full[s]);
+        bulk_g2s(B_lo(s), src + BN * BK, CF::B_BYTES, &b_full[s]);
       };
-      for (int c = 0; c < NS && c < nch; ++c) load_b(c, c);
-      for (int c = 0; c < nch; ++c) {
-        const int s = c % NS;
-        const uint32_t ph = (c / NS) & 1;
-        mbar_wait(&a_full[s], ph);
-        mbar_wait(&b_full[s], ph);
+      for (int g = 0; g < NS && g < total; ++g) load_b(g);
+      int g = 0;
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        const int ab = tl & 1;
+        if (tl >= 2) mbar_wait(&acc_empty[ab], ((tl >> 1) - 1) & 1);
         fence_after();
-        const uint32_t ah = smem_u32(A_hi(s)), al = smem_u32(A_lo(s));
-        const uint32_t bh = smem_u32(B_hi(s)), bl = smem_u32(B_lo(s));
+        const uint32_t tacc = tbase + ab * CF::TCOLS;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = g % NS;
+          const uint32_t ph = (g / NS) & 1;
+          mbar_wait(&a_full[s], ph);
+          mbar_wait(&b_full[s], ph);
+          fence_after();
+          const uint32_t ah = smem_u32(A_hi(s)), al = smem_u32(A_lo(s));
+          const uint32_t bh = smem_u32(B_hi(s)), bl = smem_u32(B_lo(s));
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
-          const uint64_t dah = sdesc(ah + k * 4096, 2048, 128);
-          const uint64_t dal = sdesc(al + k * 4096, 2048, 128);
-          const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
-          const uint64_t dbl = sdesc(bl + k * 32 * BN, 16 * BN, 128);
-          umma_ss(tacc, dah, dbh, ID, (c > 0 || k > 0));
-          umma_ss(tacc, dah, dbl, ID, 1);
-          umma_ss(tacc, dal, dbh, ID, 1);
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t dah = sdesc(ah + k * 4096, 2048, 128);
+            const uint64_t dal = sdesc(al + k * 4096, 2048, 128);
+            const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
+            const uint64_t dbl = sdesc(bl + k * 32 * BN, 16 * BN, 128);
+            umma_ss(tacc, dah, dbh, ID, (c > 0 || k > 0));
+            umma_ss(tacc, dah, dbl, ID, 1);
+            umma_ss(tacc, dal, dbh, ID, 1);
+          }
+          umma_commit(&done[s]);
+          if (g >= 1 && (g - 1) + NS < total) {
+            mbar_wait(&done[(g - 1) % NS], ((g - 1) / NS) & 1);
+            load_b(g - 1 + NS);
+          }
         }
-        umma_commit(&done[s]);
-        if (c >= 1 && (c - 1) + NS < nch) {
-          const int s1 = (c - 1) % NS;
-          mbar_wait(&done[s1], ((c - 1) / NS) & 1);
-          load_b(c - 1 + NS, s1);
-        }
+        umma_commit(&acc_full[ab]);
       }
-      umma_commit(acc_full);
     }
     __syncwarp();
-  } else {
-    // ---------------- A loader, then epilogue (thread = row)
-    // load mapping: 8 consecutive threads read one row's 128-B chunk (coalesced)
+  } else if (warp < 4) {
+    // ------------------------------------------------ A loaders: coalesced rows, hi/lo split
     const int lt = threadIdx.x;  // 0..127
     const int kc = lt & 7;
-    const int K = a.K1 + a.K2;
-    for (int c = 0; c < nch; ++c) {
-      const int s = c % NS;
-      if (c >= NS) mbar_wait(&done[s], ((c / NS) - 1) & 1);
-      float* ah = A_hi(s);
-      float* al = A_lo(s);
-      const int k0 = c * BK;
-      const bool first = k0 < a.K1;
-      const float* base = first ? a.A1 : a.A2;
-      const int64_t lda = first ? a.lda1 : a.lda2;
-      const int kk0 = first ? k0 : k0 - a.K1;
-      const int kend = first ? a.K1 : a.K2;  // chunks never straddle A1 | A2 (K1 % 32 == 0)
-      const int kl = kk0 + kc * 4;
+    int g = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int t = blockIdx.x + tl * gridDim.x;
+      const int64_t m0 = (int64_t)(t / nblk) * BM;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int s = g % NS;
+        if (g >= NS) mbar_wait(&done[s], ((g / NS) - 1) & 1);
+        float* ah = A_hi(s);
+        float* al = A_lo(s);
+        const int k0 = c * BK;
+        const bool first = k0 < a.K1;
+        const float* base = first ? a.A1 : a.A2;
+        const int64_t lda = first ? a.lda1 : a.lda2;
+        const int kend = first ? a.K1 : a.K2;
+        const int kl = (first ? k0 : k0 - a.K1) + kc * 4;
+        float4 x[BM / 16];
 #pragma unroll
-      for (int i = 0; i < BM / 16; ++i) {
-        const int rr = i * 16 + (lt >> 3);
-        const int64_t row = m0 + rr;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row < a.M) {
-          const float* src = base + row * lda;
-          if (kl + 4 <= kend) {
-            x = *reinterpret_cast<const float4*>(src + kl);
-          } else if (kl < kend) {
-            float t[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int e = 0; e < 4 && kl + e < kend; ++e) t[e] = src[kl + e];
-            x = make_float4(t[0], t[1], t[2], t[3]);
-          }
-        }
-        float4 h = make_float4(tf32rn(x.x), tf32rn(x.y), tf32rn(x.z), tf32rn(x.w));
-        float4 l = make_float4(tf32rn(x.x - h.x), tf32rn(x.y - h.y), tf32rn(x.z - h.z),
-                               tf32rn(x.w - h.w));
-        const int off = kc * 512 + (rr >> 3) * 32 + (rr & 7) * 4;
-        *reinterpret_cast<float4*>(ah + off) = h;
-        *reinterpret_cast<float4*>(al + off) = l;
-      }
-      (void)K;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&a_full[s]);
-    }
-    const int r = threadIdx.x;
-    const int64_t row = m0 + r;
-    const bool rv = row < a.M;
-    // ---------------- epilogue
-    mbar_wait(acc_full, 0);
-    fence_after();
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    if (LN) {
-      // full row in registers (BN == N == d_model <= 128)
-      float v[BN];
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t u[16];
-        TG_LD16(tacc + lane_off + c0, u);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[c0 + j] = __uint_as_float(u[j]);
-      }
-      if (rv) {
-        float s = 0.f;
-#pragma unroll
-        for (int j = 0; j < BN; ++j) {
-          v[j] += (a.bias ? a.bias[j] : 0.f) + (a.resid ? a.resid[row * a.ldr + j] : 0.f);
-          s += v[j];
-        }
-        const float mu = s / BN;
-        float q = 0.f;
-#pragma unroll
-        for (int j = 0; j < BN; ++j) q += (v[j] - mu) * (v[j] - mu);
-        const float inv = 1.f / sqrtf(q / BN + 1e-5f);
-        const float* rs = a.rowscale ? a.rowscale + (int64_t)a.row_fwd[row] * BN : nullptr;
-#pragma unroll
-        for (int j = 0; j < BN; j += 4) {
-          float4 o;
-          o.x = a.ln_g[j] * ((v[j] - mu) * inv) + a.ln_b[j];
-          o.y = a.ln_g[j + 1] * ((v[j + 1] - mu) * inv) + a.ln_b[j + 1];
-          o.z = a.ln_g[j + 2] * ((v[j + 2] - mu) * inv) + a.ln_b[j + 2];
-          o.w = a.ln_g[j + 3] * ((v[j + 3] - mu) * inv) + a.ln_b[j + 3];
-          if (a.C) *reinterpret_cast<float4*>(a.C + row * a.ldc + j) = o;
-          if (rs) {
-            float4 o2 = make_float4(o.x * rs[j], o.y * rs[j + 1], o.z * rs[j + 2], o.w * rs[j + 3]);
-            *reinterpret_cast<float4*>(a.C2 + row * a.ldc2 + j) = o2;
-          }
-        }
-      }
-    } else {
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t u[16];
-        TG_LD16(tacc + lane_off + c0, u);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (rv) {
-          float* out = a.C + row * a.ldc;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = n0 + c0 + j;
-            if (n < a.N) {
-              float x = __uint_as_float(u[j]) + (a.bias ? a.bias[n] : 0.f);
-              if (a.act == 1) x = x > 0.f ? x : 0.f;
-              else if (a.act == 2) x = 1.f / (1.f + expf(-x));
-              out[n] = x;
+        for (int i = 0; i < BM / 16; ++i) {  // issue all loads first (8 in flight)
+          const int64_t row = m0 + i * 16 + (lt >> 3);
+          x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < a.M) {
+            const float* src = base + row * lda;
+            if (kl + 4 <= kend) {
+              x[i] = *reinterpret_cast<const float4*>(src + kl);
+            } else if (kl < kend) {
+              float tt[4] = {0.f, 0.f, 0.f, 0.f};
+              for (int e = 0; e < 4 && kl + e < kend; ++e) tt[e] = src[kl + e];
+              x[i] = make_float4(tt[0], tt[1], tt[2], tt[3]);
             }
           }
         }
+#pragma unroll
+        for (int i = 0; i < BM / 16; ++i) {
+          const int rr = i * 16 + (lt >> 3);
+          float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
+          float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
+                                 tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
+          const int off = kc * 512 + (rr >> 3) * 32 + (rr & 7) * 4;
+          *reinterpret_cast<float4*>(ah + off) = h;
+          *reinterpret_cast<float4*>(al + off) = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&a_full[s]);
       }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: thread = accumulator row
+    const int ew = warp - 4;                 // TMEM lane quarter
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    float* stg = epi + ew * 32 * 33;         // [32 rows][33] staging for coalesced stores
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int t = blockIdx.x + tl * gridDim.x;
+      const int64_t m0 = (int64_t)(t / nblk) * BM;
+      const int n0 = (t % nblk) * BN;
+      const int ab = tl & 1;
+      mbar_wait(&acc_full[ab], (tl >> 1) & 1);
+      fence_after();
+      const uint32_t tacc = tbase + ab * CF::TCOLS + lane_off;
+      const int64_t row = m0 + ew * 32 + lane;
+      const bool rv = row < a.M;
+      // write a 32x32 block (rows of this warp, 32 columns from c0) to C coalesced
+      auto flush = [&](float* C, int64_t ldc, int c0) {
+        __syncwarp();
+        for (int i = 0; i < 32; ++i) {
+          const int64_t rr = m0 + ew * 32 + i;
+          const int n = n0 + c0 + lane;
+          if (rr < a.M && n < a.N && c0 + lane < BN) C[rr * ldc + n] = stg[i * 33 + lane];
+        }
+        __syncwarp();
+      };
+      if (LN) {
+        float mu = 0.f, inv = 0.f;
+        // pass 1: x = acc + bias + resid, kept in TMEM; running sum
+        float s = 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t u[16];
+          TG_LD16(tacc + c0, u);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float x = __uint_as_float(u[j]) + (a.bias ? a.bias[c0 + j] : 0.f);
+            if (a.resid && rv) x += a.resid[row * a.ldr + c0 + j];
+            s += x;
+            u[j] = __float_as_uint(x);
+          }
+          TG_ST16(tacc + c0, u);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        mu = s / BN;
+        float q = 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t u[16];
+          TG_LD16(tacc + c0, u);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float d = __uint_as_float(u[j]) - mu;
+            q += d * d;
+          }
+        }
+        inv = 1.f / sqrtf(q / BN + 1e-5f);
+        const float* rs = (a.rowscale && rv) ? a.rowscale + (int64_t)a.row_fwd[row] * BN : nullptr;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t u[32];
+          TG_LD16(tacc + c0, u);
+          TG_LD16(tacc + c0 + 16, (u + 16));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float y[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            y[j] = a.ln_g[c0 + j] * ((__uint_as_float(u[j]) - mu) * inv) + a.ln_b[c0 + j];
+          if (a.C) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = y[j];
+            flush(a.C, a.ldc, c0);
+          }
+          if (a.rowscale) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = rs ? y[j] * rs[c0 + j] : 0.f;
+            flush(a.C2, a.ldc2, c0);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t u[32];
+          TG_LD16(tacc + c0, u);
+          if (c0 + 16 < BN) TG_LD16(tacc + c0 + 16, (u + 16));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = n0 + c0 + j;
+            float x = (c0 + j < BN) ? __uint_as_float(u[j]) : 0.f;
+            if (a.bias && n < a.N) x += a.bias[n];
+            if (a.act == 1) x = x > 0.f ? x : 0.f;
+            else if (a.act == 2) x = 1.f / (1.f + expf(-x));
+            stg[lane * 33 + j] = x;
+          }
+          flush(a.C, a.ldc, c0);
+        }
+      }
+      fence_before();
+      mbar_arrive(&acc_empty[ab]);
     }
   }
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 4) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tacc),
-                 "r"(Cfg<BN>::TCOLS));
+  if (warp == 8) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(CF::TALLOC));
   }
 }
 
@@ -406,8 +482,9 @@ static void launch(const tg::Args& a, int nblk, cudaStream_t st) {
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr = true;
   }
-  dim3 grid((unsigned)cdiv(a.M, tg::BM), (unsigned)nblk);
-  tg::tc_gemm_kernel<BN, LN><<<grid, tg::THREADS, CF::SMEM, st>>>(a);
+  const int ntiles = (int)cdiv(a.M, tg::BM) * nblk;
+  const int grid = std::min(ntiles, num_sms());
+  tg::tc_gemm_kernel<BN, LN><<<grid, tg::G_THREADS, CF::SMEM, st>>>(a, nblk, ntiles);
   LAUNCH_CHECK();
 }
 

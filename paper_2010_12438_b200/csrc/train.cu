@@ -79,8 +79,9 @@ void build_q_tiles(const std::vector<int64_t>& row_off, int64_t S, bool banded,
 void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int64_t* off,
                   const go_batch_t& b, const int32_t* actions, const double* old_logp,
                   const double* fparams_host, double clip_eps, double ent_coef, double value_coef,
-                  float* G, double* stats_host, cudaStream_t st) {
+                  int32_t denom, float* G, double* stats_host, cudaStream_t st) {
   const int F = b.num_forwards;
+  const int C = denom > 0 ? denom : F;  // minibatch size the loss is averaged over
   GO_CHECK(F >= 1 && b.graphs, "ppo_grad needs graph handles");
   const int T = cfg.num_tasks;
   const int gs = cfg.gs_dim, dm = cfg.d_model, H = cfg.n_head, dh = cfg.d_head;
@@ -264,7 +265,7 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     int a = cfg.task_sizes[t];
     dlog[t] = A.take<float>(R * a);
     ppo_loss(hlog[t], a, R, actions + (int64_t)t * R, row_node, old_logp + (int64_t)t * R, row_fwd,
-             m.d_row_off, d_fp, clip_eps, ent_coef, T, F, t, dlog[t], stats, st);
+             m.d_row_off, d_fp, clip_eps, ent_coef, T, C, t, dlog[t], stats, st);
   }
   // value loss: fparams[f][2] holds the reward
   float* dvalue = A.take<float>(F);
@@ -305,7 +306,7 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     dgemm_nt(dlog[t], a, Pw(S.task(t, OUT_W)), a, drep, dm, R, dm, a, false, st);
     wgrad(hrep[t], dm, dm, nullptr, 0, 0, dlog[t], a, R, a, Gw(S.task(t, OUT_W)), Gw(S.task(t, OUT_B)), st);
     if (t == T - 1)
-      value_backward(value, meanrep, rewards, F, dm, value_coef, F, Pw(S.value_w()), dvalue,
+      value_backward(value, meanrep, rewards, F, dm, value_coef, C, Pw(S.value_w()), dvalue,
                      Gw(S.value_w()), Gw(S.value_w() + 1), stats + (int64_t)F * 12, drep, dm,
                      m.d_row_off, row_fwd, R, st);
     if (have_dprev) add_into(drep, dm, dprev, dm, R, dm, st);
@@ -437,11 +438,12 @@ extern "C" {
 int go_ppo_grad(go_ctx_t ctx, const go_config_t* cfg, const float* params,
                 const int64_t* param_offsets, const go_batch_t* batch, const int32_t* actions,
                 const double* old_logp, const double* fparams, double clip_eps, double ent_coef,
-                double value_coef, float* grads, double* stats_out, void* stream) {
+                double value_coef, int32_t loss_denominator, float* grads, double* stats_out,
+                void* stream) {
   return guarded([&] {
     CUDA_CHECK(cudaSetDevice(ctx->device));
     run_ppo_grad(ctx, *cfg, params, param_offsets, *batch, actions, old_logp, fparams, clip_eps,
-                 ent_coef, value_coef, grads, stats_out, (cudaStream_t)stream);
+                 ent_coef, value_coef, loss_denominator, grads, stats_out, (cudaStream_t)stream);
   });
 }
 

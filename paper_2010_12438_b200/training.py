@@ -386,8 +386,10 @@ def _device_samples(batch, graphs, tasks):
     return out
 
 
-def ppo_grad(params, embed_cfg, policy_cfg, task_sizes, samples, advantages, hyper, grads):
-    """One minibatch: loss + gradient accumulated into `grads` (go_ppo_grad).
+def ppo_grad(params, embed_cfg, policy_cfg, task_sizes, samples, advantages, hyper, grads,
+             denominator=None):
+    """One minibatch (or this rank's part of one): loss + gradient accumulated into
+    `grads` (go_ppo_grad), both divided by `denominator` (default: len(samples)).
     Returns (loss, host stats array [14 * F])."""
     import ctypes as C
 
@@ -416,7 +418,7 @@ def ppo_grad(params, embed_cfg, policy_cfg, task_sizes, samples, advantages, hyp
     _lib.call("go_ppo_grad", context().handle, C.byref(cfg_c), _lib.ptr(blob), offs.ctypes.data,
               C.byref(b), _lib.ptr(acts), _lib.ptr(logp), fparams.ctypes.data,
               float(hyper.clip_epsilon), float(hyper.entropy_coef), float(hyper.value_coef),
-              _lib.ptr(grads), stats.ctypes.data, stream_ptr())
+              int(denominator or F), _lib.ptr(grads), stats.ctypes.data, stream_ptr())
     Tn = len(tasks)
     per = stats[:12 * F].reshape(F, 3, 4)
     verr = stats[12 * F:13 * F]
@@ -426,7 +428,33 @@ def ppo_grad(params, embed_cfg, policy_cfg, task_sizes, samples, advantages, hyp
         pol = sum(per[i, t, 0] / n for t in range(Tn)) / Tn
         ent = sum(per[i, t, 1] / n for t in range(Tn)) / Tn
         loss += -(pol + hyper.entropy_coef * ent) + hyper.value_coef * verr[i]
-    return loss / F, stats
+    return loss / float(denominator or F), stats
+
+
+def rank_share(chunk, rank: int, world: int):
+    """Samples of a minibatch this rank evaluates (owner-computes)."""
+    return chunk[rank::world]
+
+
+def _dist_rank_world():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_rank(), dist.get_world_size()
+    except Exception:
+        pass
+    return 0, 1
+
+
+def allreduce_sum(grads, loss: float) -> float:
+    """NCCL all-reduce(sum) of the gradient blob and the scalar loss; every rank then
+    runs the identical fused Adam step, so parameters stay replicated."""
+    import torch.distributed as dist
+    T_ = torch()
+    lt = T_.tensor([loss], dtype=T_.float64, device=grads.device)
+    dist.all_reduce(grads)
+    dist.all_reduce(lt)
+    return float(lt.item())
 
 
 def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, policy_cfg,
@@ -461,6 +489,7 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
     m = moments(getattr(store, "_m", None))
     v = moments(getattr(store, "_v", None))
     grads = T_.zeros_like(blob)
+    rank, world = _dist_rank_world()
     samples = _device_samples(batch, graphs, tasks)
     step = int(getattr(store, "step_count", 0))
     stats = {"ratio_sum": 0.0, "clip_sum": 0.0, "node_count": 0, "entropy_sum": 0.0,
@@ -472,14 +501,20 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
             if len(chunk) == 0:
                 continue
             grads.zero_()
-            loss, st = ppo_grad((blob, offs), embed_cfg, policy_cfg, task_sizes,
-                                [samples[i] for i in chunk], adv[chunk], hyper, grads)
+            mine = rank_share(chunk, rank, world)
+            loss, st = (ppo_grad((blob, offs), embed_cfg, policy_cfg, task_sizes,
+                                 [samples[i] for i in mine], adv[mine], hyper, grads,
+                                 denominator=len(chunk))
+                        if len(mine) else (0.0, np.zeros(0)))
+            if world > 1:
+                # the one collective of the update: sum gradients (and the loss) over ranks
+                loss = allreduce_sum(grads, loss)
             if not np.isfinite(loss):
                 raise RuntimeError(
                     f"non-finite PPO loss (advantages {adv.min():.3g}..{adv.max():.3g})")
-            F = len(chunk)
+            F = len(mine)
             per = st[:12 * F].reshape(F, 3, 4)
-            for i, k in enumerate(chunk):
+            for i, k in enumerate(mine):
                 n = samples[k].handle.n
                 for t in range(len(tasks)):
                     stats["ratio_sum"] += float(per[i, t, 2])
@@ -493,6 +528,14 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
             _lib.call("go_adam", context().handle, _lib.ptr(blob), _lib.ptr(grads), _lib.ptr(m),
                       _lib.ptr(v), int(blob.numel()), step, float(hyper.lr), 0.9, 0.999, 1e-8,
                       stream_ptr())
+    if world > 1:
+        import torch.distributed as dist
+        T_ = torch()
+        keys = list(stats)
+        vec = T_.tensor([float(stats[k]) for k in keys], dtype=T_.float64, device=dev)
+        dist.all_reduce(vec)
+        stats = {k: (int(round(v)) if isinstance(stats[k], int) else float(v))
+                 for k, v in zip(keys, vec.tolist())}
     # write parameters and Adam state back into the store (float64 host master)
     hb, hm, hv = (x.cpu().numpy().astype(np.float64) for x in (blob, m, v))
     for nm, o in zip(names, offs):

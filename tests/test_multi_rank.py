@@ -60,3 +60,38 @@ def test_outer_draws_match_reference_stream():
     for k in range(6):
         assert gi[k] == int(rng.integers(1))
         assert seeds[k] == int(rng.integers(2**31))
+
+
+def _ppo_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_12438_b200.training import allreduce_sum, rank_share
+        chunk = np.array([7, 3, 11, 0, 5])
+        mine = rank_share(chunk, rank, world)
+        # per-sample "gradient" = sample id * ones; loss = sample id; divided by |chunk|
+        g = torch.zeros(4, dtype=torch.float32)
+        loss = 0.0
+        for k in mine:
+            g += float(k) / len(chunk)
+            loss += float(k) / len(chunk)
+        loss = allreduce_sum(g, loss)
+        out[rank] = (sorted(int(k) for k in mine), g.numpy().tolist(), loss)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ppo_minibatch_split_and_allreduce_world2():
+    """Owner-computes split of a minibatch over 2 ranks + all-reduce(sum) of the
+    partial gradients equals the single-rank minibatch mean on every rank."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ppo_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    owned = sorted(out[0][0] + out[1][0])
+    assert owned == [0, 3, 5, 7, 11]
+    want = sum([7, 3, 11, 0, 5]) / 5
+    for r in range(world):
+        assert np.allclose(out[r][1], [want] * 4)
+        assert abs(out[r][2] - want) < 1e-12
