@@ -16,13 +16,17 @@ __global__ void neighbor_sample_kernel(const GraphView* __restrict__ views,
                                        const int64_t* __restrict__ gbase,
                                        const int64_t* __restrict__ seeds,
                                        const int32_t* __restrict__ row_fwd, int64_t R, int k,
-                                       int32_t* __restrict__ gidx) {
+                                       int32_t* __restrict__ gidx, int32_t* __restrict__ segoff) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   int f = row_fwd[r];
   const GraphView& G = views[f];
   int64_t base = row_off[f];
   int64_t lr = r - base;
+  if (segoff) {  // flat segment bounds (forwards are contiguous in gidx)
+    if (r == 0) segoff[0] = 0;
+    segoff[r + 1] = (int32_t)(gbase[f] + G.samp_off[lr + 1]);
+  }
   int64_t o0 = G.nbr_off[lr], o1 = G.nbr_off[lr + 1];
   int64_t deg = o1 - o0;
   int32_t* out = gidx + gbase[f] + G.samp_off[lr];
@@ -55,12 +59,12 @@ __global__ void neighbor_sample_kernel(const GraphView* __restrict__ views,
 void neighbor_sample(const GraphView* views_dev, const int64_t* row_off_dev,
                      const int64_t* gbase_dev, const int64_t* seeds_dev, int F,
                      int64_t total_rows, const int32_t* row_fwd, int k, int32_t* gidx,
-                     cudaStream_t st) {
+                     int32_t* segoff, cudaStream_t st) {
   (void)F;
   if (total_rows <= 0) return;
   if (k > 32) GO_THROW(GO_ERR_UNSUPPORTED, "gs_knn %d > 32", k);
   neighbor_sample_kernel<<<(unsigned)cdiv(total_rows, 128), 128, 0, st>>>(
-      views_dev, row_off_dev, gbase_dev, seeds_dev, row_fwd, total_rows, k, gidx);
+      views_dev, row_off_dev, gbase_dev, seeds_dev, row_fwd, total_rows, k, gidx, segoff);
   LAUNCH_CHECK();
 }
 
@@ -113,25 +117,69 @@ void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
 
 // ---------------------------------------------------------------------------------
 // pooled[r] = max over sampled neighbours j of t[j] (tensor.py:199-263 gather_rows +
-// segment_max; empty segment -> 0).  One warp per row, float4 columns.  This is the
-// HBM-bound GraphSAGE aggregation.
+// segment_max; empty segment -> 0).  This is the HBM-bound GraphSAGE aggregation
+// (SURVEY.md §8 A6).  segoff[R+1] holds the flat segment bounds into gidx.
+//
+// D == 128 fast path: 8 lanes per row (4 rows per warp), each lane owning 4 float4
+// columns, so one load instruction of an 8-lane group reads a full 128-B line; the
+// neighbour indices are fetched once and shuffled, and 4 neighbours x 4 column
+// slices = 16 independent 16-B loads are in flight per lane.
+__global__ void segment_max128_kernel(const float* __restrict__ t, int64_t ldt,
+                                      const int32_t* __restrict__ segoff,
+                                      const int32_t* __restrict__ gidx, int64_t R,
+                                      float* __restrict__ out, int64_t ldo) {
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane & 24;
+  const int64_t r = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + (lane >> 3);
+  const bool live = r < R;
+  const int s0 = live ? segoff[r] : 0, s1 = live ? segoff[r + 1] : 0;
+  const int cnt = s1 - s0;
+  const float4* tb = reinterpret_cast<const float4*>(t) + sub;
+  const int64_t ld4 = ldt >> 2;
+  float4 m[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) m[q] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  for (int j0 = 0; __any_sync(0xffffffffu, j0 < cnt); j0 += 8) {
+    const int myidx = (j0 + sub < cnt) ? gidx[s0 + j0 + sub] : -1;
+#pragma unroll
+    for (int jb = 0; jb < 8; jb += 4) {
+      float4 v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int src = __shfl_sync(0xffffffffu, myidx, grp + jb + u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          v[u][q] = src >= 0 ? __ldg(tb + (int64_t)src * ld4 + 8 * q)
+                             : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          m[q].x = fmaxf(m[q].x, v[u][q].x);
+          m[q].y = fmaxf(m[q].y, v[u][q].y);
+          m[q].z = fmaxf(m[q].z, v[u][q].z);
+          m[q].w = fmaxf(m[q].w, v[u][q].w);
+        }
+    }
+  }
+  if (!live) return;
+  float4* o = reinterpret_cast<float4*>(out + r * ldo) + sub;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[8 * q] = cnt > 0 ? m[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// General D (and the training forward, which also records the first maximal row per
+// column, tensor.py:240-251): one warp per row.
 __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
-                                   const GraphView* __restrict__ views,
-                                   const int64_t* __restrict__ row_off,
-                                   const int64_t* __restrict__ gbase,
-                                   const int32_t* __restrict__ row_fwd,
+                                   const int32_t* __restrict__ segoff,
                                    const int32_t* __restrict__ gidx, int64_t R, int D,
                                    float* __restrict__ out, int64_t ldo,
                                    int32_t* __restrict__ argmax) {
   int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if (r >= R) return;
-  int f = row_fwd[r];
-  const GraphView& G = views[f];
-  int64_t lr = r - row_off[f];
-  int64_t s0 = gbase[f] + G.samp_off[lr], s1 = gbase[f] + G.samp_off[lr + 1];
+  const int64_t s0 = segoff[r], s1 = segoff[r + 1];
   if (argmax) {
-    // training forward: also record the first maximal row per column (tensor.py:240-251)
     for (int c = lane; c < D; c += 32) {
       float m = 0.f;
       int32_t am = -1;
@@ -150,36 +198,7 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
     }
     return;
   }
-  if (D == 128 && (ldt & 3) == 0 && (ldo & 3) == 0 && s1 - s0 <= 32) {
-    // fast path: one float4 column slice per lane; the segment's neighbour indices
-    // are loaded once (one lane each) and broadcast by shuffle, and the gathered rows
-    // are fetched 4 at a time so each lane keeps 4 independent 16-B loads in flight.
-    const int cnt = (int)(s1 - s0);
-    const int myidx = lane < cnt ? gidx[s0 + lane] : 0;
-    const float4* tb = reinterpret_cast<const float4*>(t) + lane;
-    const int64_t ld4 = ldt >> 2;
-    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (cnt > 0) {
-      m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      for (int j = 0; j < cnt; j += 4) {
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int jj = j + u < cnt ? j + u : j;  // duplicate a valid row: max is idempotent
-          const int src = __shfl_sync(0xffffffffu, myidx, jj);
-          v[u] = __ldg(tb + (int64_t)src * ld4);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          m.x = fmaxf(m.x, v[u].x);
-          m.y = fmaxf(m.y, v[u].y);
-          m.z = fmaxf(m.z, v[u].z);
-          m.w = fmaxf(m.w, v[u].w);
-        }
-      }
-    }
-    reinterpret_cast<float4*>(out + r * ldo)[lane] = m;
-  } else if ((D & 3) == 0 && (ldt & 3) == 0 && (ldo & 3) == 0) {
+  if ((D & 3) == 0 && (ldt & 3) == 0 && (ldo & 3) == 0) {
     int D4 = D >> 2;
     for (int c4 = lane; c4 < D4; c4 += 32) {
       float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -207,14 +226,18 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
   }
 }
 
-void segment_max(const float* t, int64_t ldt, const GraphView* views_dev,
-                 const int64_t* row_off_dev, const int64_t* gbase_dev, const int32_t* row_fwd,
-                 const int32_t* gidx, int64_t R, int D, float* out, int64_t ldo,
-                 cudaStream_t st, int32_t* argmax) {
+void segment_max(const float* t, int64_t ldt, const int32_t* segoff, const int32_t* gidx,
+                 int64_t R, int D, float* out, int64_t ldo, cudaStream_t st, int32_t* argmax) {
   if (R <= 0) return;
-  segment_max_kernel<<<(unsigned)cdiv(R, 8), 256, 0, st>>>(t, ldt, views_dev, row_off_dev,
-                                                           gbase_dev, row_fwd, gidx, R, D, out,
-                                                           ldo, argmax);
+  const bool aligned = ((uintptr_t)t % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                       (ldt & 3) == 0 && (ldo & 3) == 0;
+  if (!argmax && D == 128 && aligned) {
+    segment_max128_kernel<<<(unsigned)cdiv(R, 32), 256, 0, st>>>(t, ldt, segoff, gidx, R, out,
+                                                                 ldo);
+  } else {
+    segment_max_kernel<<<(unsigned)cdiv(R, 8), 256, 0, st>>>(t, ldt, segoff, gidx, R, D, out,
+                                                             ldo, argmax);
+  }
   LAUNCH_CHECK();
 }
 

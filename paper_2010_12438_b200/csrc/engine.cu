@@ -200,7 +200,7 @@ static size_t forward_ws_bytes(const go_config_t& c, int64_t R, int64_t gtotal, 
   int64_t per_row = 6 * ldp((int)wmax) + 4 * ldp((int)W) + ldp(c.d_inner);
   // + tensor-core attention operands: qh [H][R][16], kb/vb [H][tiles*64][16]
   per_row += 3 * (int64_t)c.n_head * 16 + 2;
-  size_t b = (size_t)R * per_row * 4 + (size_t)R * 8 + (size_t)gtotal * 4 +
+  size_t b = (size_t)R * per_row * 4 + (size_t)R * 12 + (size_t)gtotal * 4 + 512 +
              (size_t)F * 2 * c.n_head * 64 * 16 * 4 +
              (size_t)(F + 4) * (ldp(c.d_model) + ldp(c.gs_dim)) * 8 +
              (size_t)(nchunks + 4) * wmax * 4 + 64 * 256;
@@ -322,7 +322,9 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
   float* Ab = A.take<float>(R * LA);
   float* F1 = A.take<float>(R * LI);
   int32_t* row_fwd = A.take<int32_t>(R);
+  GO_CHECK(m.gtotal + R < ((int64_t)1 << 31), "neighbour list exceeds 2^31 entries");
   int32_t* gidx = A.take<int32_t>(m.gtotal);
+  int32_t* segoff = A.take<int32_t>(R + 1);
   float* mod = A.take<float>((int64_t)F * dm);
   float* meanb = A.take<float>((int64_t)F * dm);
   float* part = A.take<float>((m.n_chunks + 1) * wmax);
@@ -338,7 +340,7 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
       c += cfg.task_sizes[t];
     }
     neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, F, R, row_fwd, cfg.gs_knn,
-                    gidx, st);
+                    gidx, segoff, st);
     float* h = cfg.gs_layers == 0 ? node_embed : X[0];
     if (b.features)  // explicit feature matrix (embed() called with features)
       gemm(b.features, b.feature_dim, b.feature_dim, nullptr, 0, 0, W_(S.e_in_w()), gs,
@@ -358,7 +360,7 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
         double bytes = (double)(m.gtotal + R) * gs * 4 + (double)m.gtotal * 4 +
                        (double)(R + 1) * 8 + (double)R * 4;
         KTimer kt(ctx, K_SEGMAX, st, bytes);
-        segment_max(t, LW, m.d_views, m.d_row_off, m.d_gbase, row_fwd, gidx, R, gs, pooled, LW,
+        segment_max(t, LW, segoff, gidx, R, gs, pooled, LW,
                     st);
       }
       bool last = l == cfg.gs_layers - 1;
@@ -526,7 +528,9 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
   float* Ab = A.take<float>(R * LA);
   float* F1 = A.take<float>(R * LI);
   int32_t* row_fwd = A.take<int32_t>(R);
+  GO_CHECK(m.gtotal + R < ((int64_t)1 << 31), "neighbour list exceeds 2^31 entries");
   int32_t* gidx = A.take<int32_t>(m.gtotal);
+  int32_t* segoff = A.take<int32_t>(R + 1);
   float* mod = A.take<float>((int64_t)F * dm);
   float* meanb = A.take<float>((int64_t)F * dm);
   float* part = A.take<float>((m.n_chunks + 1) * 128);
@@ -557,7 +561,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       c += cfg.task_sizes[t];
     }
     neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, F, R, row_fwd, cfg.gs_knn,
-                    gidx, st);
+                    gidx, segoff, st);
     float* h = Lg == 0 ? node_embed : X[0];
     features_inproj(m.d_views, m.d_row_off, row_fwd, R, b.prev_actions, T, tcol, W_(S.e_in_w()),
                     W_(S.e_in_b()), gs, h, gs, st);
@@ -573,7 +577,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
         double bytes = (double)(m.gtotal + R) * gs * 4 + (double)m.gtotal * 4 +
                        (double)(R + 1) * 8 + (double)R * 4;
         KTimer kt(ctx, K_SEGMAX, st, bytes);
-        segment_max(t, LW, m.d_views, m.d_row_off, m.d_gbase, row_fwd, gidx, R, gs, pooled, LW,
+        segment_max(t, LW, segoff, gidx, R, gs, pooled, LW,
                     st);
       }
       bool last = l == Lg - 1;
@@ -839,7 +843,7 @@ int go_neighbor_arrays(go_ctx_t ctx, go_graph_t g, int64_t seed, int32_t k, int6
     int32_t* row_fwd = A.take<int32_t>(m.R);
     row_fwd_fill(m.d_row_off, 1, m.R, row_fwd, st);
     neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, 1, m.R, row_fwd, k, gather_dev,
-                    st);
+                    nullptr, st);
   });
 }
 

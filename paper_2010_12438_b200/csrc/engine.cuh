@@ -155,15 +155,15 @@ void value_head(const float* mean, int F, int D, const float* w, const float* b,
 void neighbor_sample(const GraphView* views_dev, const int64_t* row_off_dev,
                      const int64_t* gbase_dev, const int64_t* seeds_dev, int F,
                      int64_t total_rows, const int32_t* row_fwd, int k, int32_t* gidx,
-                     cudaStream_t st);
+                     int32_t* segoff, cudaStream_t st);
 void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
                      const int32_t* row_fwd, int64_t R, const int32_t* prev_actions,
                      int num_tasks, const int32_t* task_col, const float* in_w,
                      const float* in_b, int D, float* h, int64_t ldh, cudaStream_t st);
-void segment_max(const float* t, int64_t ldt, const GraphView* views_dev,
-                 const int64_t* row_off_dev, const int64_t* gbase_dev, const int32_t* row_fwd,
-                 const int32_t* gidx, int64_t R, int D, float* out, int64_t ldo,
-                 cudaStream_t st, int32_t* argmax = nullptr);
+// segoff[R+1]: flat segment bounds into gidx, written by neighbor_sample
+void segment_max(const float* t, int64_t ldt, const int32_t* segoff, const int32_t* gidx,
+                 int64_t R, int D, float* out, int64_t ldo, cudaStream_t st,
+                 int32_t* argmax = nullptr);
 
 void row_node_fill(const GraphView* views_dev, const int64_t* row_off_dev,
                    const int32_t* row_fwd, int64_t R, int32_t* row_node, cudaStream_t st);

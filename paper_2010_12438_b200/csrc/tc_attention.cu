@@ -20,6 +20,8 @@
 // Numerics: Q/K/V are rounded to tf32 (round-to-nearest) by the repack kernel;
 // softmax statistics and accumulation are fp32.  Error vs the float64 reference:
 // logits ~1e-5 normwise (tests/test_gpu_parity.py enforces 1e-4).
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.cuh"
@@ -435,10 +437,6 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
 // when every b_i <= BOUND_LIMIT (exp2 then never underflows for scores within 2 b_i
 // of the bound); otherwise the online-softmax kernel above takes the launch.
 constexpr float BOUND_LIMIT = 60.f;
-#ifndef GO_POLY_PER_8
-#define GO_POLY_PER_8 0
-#endif
-constexpr int POLY_PER_8 = GO_POLY_PER_8;  // of every 8 columns, this many use ex2_poly
 
 // 2^x for x <= 0 on the FMA/ALU pipes: x = n + f, n = rint(x) (magic-number add),
 // f in [-0.5, 0.5], 2^f by a degree-4 minimax polynomial, 2^n by exponent add.
@@ -458,15 +456,28 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return n < -126 ? 0.f : r;
 }
 
+// The fixed kernel runs two CTAs per SM (TMEM 2 x 256 columns) so the softmax warps
+// of two independent CTAs interleave on each SM sub-partition and keep the MUFU pipe
+// busy through each other's tcgen05.ld/st and barrier latencies.  Each 64-key K/V
+// tile is consumed as two 32-key halves (S sub-tiles of 32 TMEM columns, double
+// buffered per query tile): 3 x 2 x 32 S columns + 3 x 16 O columns = 240 <= 256.
+constexpr int HK = 32;                      // keys per softmax sub-tile
+constexpr int NSF = 6;                      // K/V ring stages per CTA
+constexpr uint32_t O_COL_F = NQT * 2 * HK;  // O accumulators after the S buffers
+constexpr uint32_t TMEM_COLS_F = 256;
+
 struct SmemF {
   float q[NQT][QT * 16];
-  float kv[NS][2][KT * 16];
-  uint64_t kv_full[NS], kv_empty[NS];
+  float kv[NSF][2][KT * 16];
+  uint64_t kv_full[NSF], kv_empty[NSF];
   uint64_t s_full[NQT][2], p_full[NQT][2], o_done[NQT];
   uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// POLY_PER_8: of every 8 score columns, this many are exponentiated by ex2_poly on
+// the FMA pipe instead of MUFU.EX2.
+template <int POLY_PER_8>
+__global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_tc_fixed_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
                          const float* __restrict__ vb, int64_t R, int64_t Ttot,
                          const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
@@ -478,10 +489,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const Work w = works[blockIdx.x];
   const int head = blockIdx.y;
   const int T = w.tiles;
+  const int U = 2 * T;  // 32-key sub-tiles
   const float* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
   const float* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
   if (warp == PRODUCER_WARP && lane == 0) {
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NSF; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
     }
@@ -497,7 +509,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
-                 "r"(TMEM_COLS));
+                 "r"(TMEM_COLS_F));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   for (int i = threadIdx.x; i < NQT * QT * 4; i += NUM_THREADS) {
@@ -518,8 +530,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == PRODUCER_WARP) {
     if (lane == 0) {
       for (int j = 0; j < T; ++j) {
-        int s = j % NS;
-        if (j >= NS) mbar_wait(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        int s = j % NSF;
+        if (j >= NSF) mbar_wait(&sm.kv_empty[s], ((j / NSF) - 1) & 1);
         mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
         bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
         bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
@@ -528,40 +540,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp == MMA_WARP) {
     if (lane == 0) {
-      constexpr uint32_t ID_S = idesc_tf32(QT, KT);
+      constexpr uint32_t ID_S = idesc_tf32(QT, HK);
       constexpr uint32_t ID_O = idesc_tf32(QT, 16);
       uint32_t qaddr[NQT];
       for (int t = 0; t < NQT; ++t) qaddr[t] = smem_u32(sm.q[t]);
-      auto issue_pv = [&](int j) {
-        int s = j % NS, b = j & 1;
-        uint32_t vaddr = smem_u32(sm.kv[s][1]);
+      // O += P_u V_u; the K/V stage is released after the second half's PV
+      auto issue_pv = [&](int u) {
+        const int j = u >> 1, h = u & 1, s = j % NSF, b = u & 1;
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]) + h * (HK * 16 * 4);
         for (int t = 0; t < NQT; ++t) {
-          mbar_wait(&sm.p_full[t][b], (j >> 1) & 1);
+          mbar_wait(&sm.p_full[t][b], (u >> 1) & 1);
           fence_after();
-          uint32_t d = tbase + O_COL + t * 16;
-          uint32_t a = tbase + t * 128 + b * 64;
+          const uint32_t d = tbase + O_COL_F + t * 16;
+          const uint32_t a = tbase + t * 2 * HK + b * HK;
 #pragma unroll
-          for (int k = 0; k < KT / 8; ++k)
-            umma_ts(d, a + k * 8, sdesc(vaddr + k * 512, 256, 128), ID_O, (j > 0 || k > 0));
+          for (int k = 0; k < HK / 8; ++k)
+            umma_ts(d, a + k * 8, sdesc(vaddr + k * 512, 256, 128), ID_O, (u > 0 || k > 0));
         }
-        umma_commit(&sm.kv_empty[s]);
+        if (h == 1) umma_commit(&sm.kv_empty[s]);
       };
-      for (int j = 0; j < T; ++j) {
-        int s = j % NS, b = j & 1;
-        mbar_wait(&sm.kv_full[s], (j / NS) & 1);
-        fence_after();
-        uint32_t kaddr = smem_u32(sm.kv[s][0]);
+      for (int u = 0; u < U; ++u) {
+        const int j = u >> 1, h = u & 1, s = j % NSF, b = u & 1;
+        if (h == 0) {
+          mbar_wait(&sm.kv_full[s], (j / NSF) & 1);
+          fence_after();
+        }
+        const uint32_t kaddr = smem_u32(sm.kv[s][0]) + h * (HK * 4 * 4);
         for (int t = 0; t < NQT; ++t) {
-          uint32_t d = tbase + t * 128 + b * 64;
+          const uint32_t d = tbase + t * 2 * HK + b * HK;
 #pragma unroll
           for (int k = 0; k < 2; ++k)
             umma_ss(d, sdesc(qaddr[t] + k * 4096, 2048, 128), sdesc(kaddr + k * 2048, 1024, 128),
                     ID_S, k > 0);
           umma_commit(&sm.s_full[t][b]);
         }
-        if (j >= 1) issue_pv(j - 1);
+        if (u >= 1) issue_pv(u - 1);
       }
-      if (T >= 1) issue_pv(T - 1);
+      if (U >= 1) issue_pv(U - 1);
       for (int t = 0; t < NQT; ++t) umma_commit(&sm.o_done[t]);
     }
     __syncwarp();
@@ -569,25 +584,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int t = warp >> 2;
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    for (int j = 0; j < T; ++j) {
-      int b = j & 1;
-      mbar_wait(&sm.s_full[t][b], (j >> 1) & 1);
+    for (int u = 0; u < U; ++u) {
+      const int b = u & 1;
+      mbar_wait(&sm.s_full[t][b], (u >> 1) & 1);
       fence_after();
-      uint32_t sr[64];
-      const uint32_t sa = tbase + lane_off + t * 128 + b * 64;
+      uint32_t sr[HK];
+      const uint32_t sa = tbase + lane_off + t * 2 * HK + b * HK;
       TC_LD32(sa, sr);
-      TC_LD32(sa + 32, (sr + 32));
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < KT; ++i) {
+      for (int i = 0; i < HK; ++i) {
         const float x = __uint_as_float(sr[i]);
         // FA4-style split: a fixed subset of the columns is exponentiated on the FMA
-        // pipe (degree-4 polynomial, rel. err < 4e-6, far below the tf32 rounding of
+        // pipe (degree-5 polynomial, rel. err < 4e-6, far below the tf32 rounding of
         // P) so the MUFU and FMA pipes work in parallel.
         sr[i] = __float_as_uint(((i & 7) < POLY_PER_8) ? ex2_poly(x) : ex2(x));
       }
       TC_ST32(sa, sr);
-      TC_ST32(sa + 32, (sr + 32));
       tmem_wait_st();
       fence_before();
       mbar_arrive(&sm.p_full[t][b]);
@@ -595,7 +608,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_wait(&sm.o_done[t], 0);
     fence_after();
     uint32_t r[16];
-    TC_LD16(tbase + lane_off + O_COL + t * 16, r);
+    TC_LD16(tbase + lane_off + O_COL_F + t * 16, r);
     tmem_wait_ld();
     const int lr = w.q0 + t * QT + wq * 32 + lane;
     if (lr < w.n) {
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   fence_after();
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
-                 "r"(TMEM_COLS));
+                 "r"(TMEM_COLS_F));
   }
 }
 
@@ -711,13 +724,21 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
   static bool attr = false;
   const size_t smem = sizeof(tc::Smem) + 1024;
   const size_t smemf = sizeof(tc::SmemF) + 1024;
+  using FixedFn = void (*)(const float*, const float*, const float*, int64_t, int64_t,
+                           const tc::Work*, float*, int64_t, int, const int32_t*);
+  static const FixedFn fixed_fns[5] = {tc::attn_tc_fixed_kernel<0>, tc::attn_tc_fixed_kernel<1>,
+                                       tc::attn_tc_fixed_kernel<2>, tc::attn_tc_fixed_kernel<3>,
+                                       tc::attn_tc_fixed_kernel<4>};
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-    CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_fixed_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf));
+    for (FixedFn fn : fixed_fns)
+      CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf));
     attr = true;
   }
+  // GO_POLY=k: k of every 8 exponentials on the FMA pipe (default 0)
+  const char* poly_env = getenv("GO_POLY");
+  const int poly = poly_env ? std::max(0, std::min(4, atoi(poly_env))) : 0;
   float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   int64_t total = (int64_t)n_head * Ttot * tc::KT;
   dim3 grid((unsigned)num_works, (unsigned)n_head);
@@ -734,7 +755,7 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
     tc::repack_q_fixed_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
         q, ld, n_head, d_head, R, row_fwd, kmax, qscale, qh, flag);
     LAUNCH_CHECK();
-    tc::attn_tc_fixed_kernel<<<grid, tc::NUM_THREADS, smemf, st>>>(
+    fixed_fns[poly]<<<grid, tc::NUM_THREADS, smemf, st>>>(
         qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, flag);
     LAUNCH_CHECK();
     // fallback for bounds > BOUND_LIMIT: the online kernel re-packs and runs only if flagged

@@ -8,10 +8,18 @@
 // row scale for the trunk's modulation), replacing the reference's affine / relu /
 // sigmoid / add / layer_norm chains (tensor.py:133-180, 330-351, 378).
 //
-// CTA: 128 rows x BN columns, 5 warps.  Warps 0-3 load the A tile (fp32 rows,
-// float4), split it into hi/lo and store both in the UMMA K-major canonical layout;
-// they are also the epilogue.  Warp 4 (one thread) streams the prepacked W_hi/W_lo
-// chunks with cp.async.bulk and issues the MMAs.  Multi-stage smem ring, mbarriers.
+// Persistent CTA per SM, 9 warps:
+//   warp 8 (one thread): TMA of the fp32 A chunk (128 rows x 32 cols, 128-B swizzle,
+//           OOB rows/cols zero-filled), cp.async.bulk of the prepacked W_hi/W_lo chunk,
+//           and the MMA issue;
+//   warps 0-3: split the landed A chunk in shared memory: hi = tf32_rn(x) in place,
+//           lo = tf32_rn(x - hi) into the twin buffer (same swizzled layout);
+//   warps 4-7: epilogue, one accumulator row per thread.
+// NS-stage smem ring + double-buffered TMEM accumulator, all handshakes on mbarriers,
+// so TMA, split, MMA and the previous tile's epilogue all overlap.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstring>
 
@@ -21,7 +29,6 @@ namespace go {
 namespace tg {
 
 constexpr int BM = 128, BK = 32;
-constexpr int THREADS = 160;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -55,6 +62,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -75,12 +90,24 @@ __device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// no-swizzle K-major canonical layout (the prepacked B tiles)
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
+  return d;
+}
+// 128-B swizzled K-major layout (TMA-written A tiles): rows of 128 B, 8-row groups
+// 1024 B apart; the K step inside the swizzle atom advances the start address.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
@@ -100,50 +127,6 @@ __device__ __forceinline__ float tf32rn(float x) {
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                \
       : "r"(taddr))
-
-struct Args {
-  const float* A1;
-  int64_t lda1;
-  int K1;
-  const float* A2;
-  int64_t lda2;
-  int K2;
-  const float* Bpk;  // [nblk][nch][2][BN*32]
-  const float* bias;
-  float* C;
-  int64_t ldc;
-  int64_t M;
-  int N;
-  int nch;
-  int act;                                   // 0 none, 1 relu, 2 sigmoid
-  const float* resid;                        // LN mode: C = LN(resid + acc + bias)
-  int64_t ldr;
-  const float* ln_g;
-  const float* ln_b;
-  const float* rowscale;                     // optional: C2 = C * rowscale[row_fwd[r]]
-  const int32_t* row_fwd;
-  float* C2;
-  int64_t ldc2;
-};
-
-template <int BN>
-struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB per hi/lo tile
-  static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // epilogue staging, 4 warps
-  // 227 KB opt-in limit minus staging and barriers; >= 2 stages or the B refill schedule
-  // (stage of chunk g-1 refilled after chunk g is issued) cannot make progress
-  static constexpr int BUDGET = 232448 - EPI_BYTES - 1536;
-  static constexpr int NS = (BUDGET / STAGE) < 4 ? (BUDGET / STAGE) : 4;
-  static_assert(NS >= 2, "tc_gemm needs at least two smem stages");
-  static constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr uint32_t TALLOC = 2 * TCOLS;  // double-buffered accumulator
-  static constexpr size_t SMEM = (size_t)NS * STAGE + EPI_BYTES + 1536;
-};
-
-constexpr int G_THREADS = 288;  // warps 0-3 load A, 4-7 epilogue, 8 = B producer + MMA issuer
-
 #define TG_ST16(taddr, r)                                                                    \
   asm volatile(                                                                              \
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%" \
@@ -152,20 +135,71 @@ constexpr int G_THREADS = 288;  // warps 0-3 load A, 4-7 epilogue, 8 = B produce
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),      \
       "r"(r[15]))
 
+struct Args {
+  int K1, K2;                                // A1 columns (multiple of 32 if A2), A2 columns
+  const float* Bpk;                          // [nblk][nch][2][BN*32]
+  const float* bias;
+  float* C;
+  int64_t ldc;
+  int64_t M;
+  int N;
+  int nch;
+  const float* resid;                        // LN mode: C = LN(resid + acc + bias)
+  int64_t ldr;
+  const float* ln_g;
+  const float* ln_b;
+  const float* rowscale;                     // optional: C2 = C * rowscale[row_fwd[r]]
+  const int32_t* row_fwd;
+  float* C2;
+  int64_t ldc2;
+  int vec;                                   // C, C2 rows 16-B aligned: float4 stores
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB per hi/lo tile
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // multiple of 1024 (BN % 4 == 0)
+  // epilogue staging (4 warps x [32][36]) + bias[256] + ln gamma/beta[128]
+  static constexpr int EPI_BYTES = 4 * 32 * 36 * 4 + 512 * 4;
+  static constexpr int ALIGN_PAD = 1024;  // the swizzled A tiles need 1024-B alignment
+  // 227 KB opt-in limit minus staging, barriers and alignment; >= 2 stages or the refill
+  // schedule (stage of chunk g-1 refilled after chunk g is issued) cannot progress
+  static constexpr int BUDGET = 232448 - EPI_BYTES - 1536 - ALIGN_PAD;
+  static constexpr int NS = (BUDGET / STAGE) < 4 ? (BUDGET / STAGE) : 4;
+  static_assert(NS >= 2, "tc_gemm needs at least two smem stages");
+  static_assert(STAGE % 1024 == 0, "stage must keep 1024-B alignment");
+  static constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr uint32_t TALLOC = 2 * TCOLS;  // double-buffered accumulator
+  static constexpr size_t SMEM = (size_t)NS * STAGE + EPI_BYTES + 1536 + ALIGN_PAD;
+};
+
+constexpr int G_THREADS = 288;  // warps 0-3 split A, 4-7 epilogue, 8 = TMA producer + MMA
+
+template <int ACT>
+__device__ __forceinline__ float activate(float x) {
+  if (ACT == 1) return x > 0.f ? x : 0.f;
+  if (ACT == 2) return __frcp_rn(1.f + __expf(-x));
+  return x;
+}
+
 // Persistent, warp-specialised tile loop: CTA b processes tiles b, b + grid, ...
 // (tile t -> m tile t / nblk, n block t % nblk).  The smem ring and the two TMEM
 // accumulators carry their phases across tiles, so the loads and MMAs of tile i+1
 // overlap the epilogue of tile i.
-template <int BN, bool LN>
-__global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk, int ntiles) {
+template <int BN, bool LN, int ACT>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA1,
+                   const __grid_constant__ CUtensorMap tmA2, Args a, int nblk, int ntiles) {
   using CF = Cfg<BN>;
   constexpr int NS = CF::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* stage_base = smem_raw;
-  float* epi = reinterpret_cast<float*>(smem_raw + (size_t)NS * CF::STAGE);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NS * CF::STAGE + CF::EPI_BYTES);
-  uint64_t* a_full = bars;              // [NS] 128 arrivals
-  uint64_t* b_full = bars + NS;         // [NS] tx bytes
+  uint8_t* stage_base =
+      smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // 1024-B aligned
+  float* epi = reinterpret_cast<float*>(stage_base + (size_t)NS * CF::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_base + (size_t)NS * CF::STAGE + CF::EPI_BYTES);
+  uint64_t* full = bars;                // [NS] tx bytes: A (TMA) + B (bulk)
+  uint64_t* a_full = bars + NS;         // [NS] 128 arrivals: A split into hi/lo
   uint64_t* done = bars + 2 * NS;       // [NS] MMA commit: stage free
   uint64_t* acc_full = bars + 3 * NS;   // [2] MMA commit: accumulator ready
   uint64_t* acc_empty = bars + 3 * NS + 2;  // [2] 128 arrivals: accumulator drained
@@ -181,8 +215,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
   if (warp == 8) {
     if (lane == 0) {
       for (int s = 0; s < NS; ++s) {
+        mbar_init(&full[s], 1);
         mbar_init(&a_full[s], 128);
-        mbar_init(&b_full[s], 1);
         mbar_init(&done[s], 1);
       }
       for (int b = 0; b < 2; ++b) {
@@ -190,6 +224,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
         mbar_init(&acc_empty[b], 128);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA1)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
     }
     __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -203,20 +239,24 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
   const uint32_t tbase = *tmem_slot;
 
   if (warp == 8) {
-    // ------------------------------------------------ B producer + MMA issuer
+    // ------------------------------------------------ TMA producer + MMA issuer
     if (lane == 0) {
       constexpr uint32_t ID = idesc_tf32(BM, BN);
       const int total = my_tiles * nch;
-      auto load_b = [&](int g) {
+      auto load = [&](int g) {
         const int s = g % NS;
         const int t = blockIdx.x + (g / nch) * gridDim.x;
         const int c = g % nch;
+        const int m0 = (t / nblk) * BM;
+        const int k0 = c * BK;
         const float* src = a.Bpk + ((size_t)(t % nblk) * nch + c) * 2 * BN * BK;
-        mbar_expect_tx(&b_full[s], 2 * CF::B_BYTES);
-        bulk_g2s(B_hi(s), src, CF::B_BYTES, &b_full[s]);
-        bulk_g2s(B_lo(s), src + BN * BK, CF::B_BYTES, &b_full[s]);
+        mbar_expect_tx(&full[s], CF::A_BYTES + 2 * CF::B_BYTES);
+        if (k0 < a.K1) tma_2d(A_hi(s), &tmA1, k0, m0, &full[s]);
+        else tma_2d(A_hi(s), &tmA2, k0 - a.K1, m0, &full[s]);
+        bulk_g2s(B_hi(s), src, CF::B_BYTES, &full[s]);
+        bulk_g2s(B_lo(s), src + BN * BK, CF::B_BYTES, &full[s]);
       };
-      for (int g = 0; g < NS && g < total; ++g) load_b(g);
+      for (int g = 0; g < NS && g < total; ++g) load(g);
       int g = 0;
       for (int tl = 0; tl < my_tiles; ++tl) {
         const int ab = tl & 1;
@@ -226,15 +266,15 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = g % NS;
           const uint32_t ph = (g / NS) & 1;
+          mbar_wait(&full[s], ph);
           mbar_wait(&a_full[s], ph);
-          mbar_wait(&b_full[s], ph);
           fence_after();
           const uint32_t ah = smem_u32(A_hi(s)), al = smem_u32(A_lo(s));
           const uint32_t bh = smem_u32(B_hi(s)), bl = smem_u32(B_lo(s));
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t dah = sdesc(ah + k * 4096, 2048, 128);
-            const uint64_t dal = sdesc(al + k * 4096, 2048, 128);
+            const uint64_t dah = sdesc_sw128(ah + k * 32);
+            const uint64_t dal = sdesc_sw128(al + k * 32);
             const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
             const uint64_t dbl = sdesc(bl + k * 32 * BN, 16 * BN, 128);
             umma_ss(tacc, dah, dbh, ID, (c > 0 || k > 0));
@@ -244,7 +284,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
           umma_commit(&done[s]);
           if (g >= 1 && (g - 1) + NS < total) {
             mbar_wait(&done[(g - 1) % NS], ((g - 1) / NS) & 1);
-            load_b(g - 1 + NS);
+            load(g - 1 + NS);
           }
         }
         umma_commit(&acc_full[ab]);
@@ -252,112 +292,151 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
     }
     __syncwarp();
   } else if (warp < 4) {
-    // ------------------------------------------------ A loaders: coalesced rows, hi/lo split
+    // ------------------------------------------------ A split: hi in place, lo in the twin
+    // (elementwise, so the lo tile inherits the TMA's swizzled layout)
     const int lt = threadIdx.x;  // 0..127
-    const int kc = lt & 7;
-    int g = 0;
-    for (int tl = 0; tl < my_tiles; ++tl) {
-      const int t = blockIdx.x + tl * gridDim.x;
-      const int64_t m0 = (int64_t)(t / nblk) * BM;
-      for (int c = 0; c < nch; ++c, ++g) {
-        const int s = g % NS;
-        if (g >= NS) mbar_wait(&done[s], ((g / NS) - 1) & 1);
-        float* ah = A_hi(s);
-        float* al = A_lo(s);
-        const int k0 = c * BK;
-        const bool first = k0 < a.K1;
-        const float* base = first ? a.A1 : a.A2;
-        const int64_t lda = first ? a.lda1 : a.lda2;
-        const int kend = first ? a.K1 : a.K2;
-        const int kl = (first ? k0 : k0 - a.K1) + kc * 4;
-        float4 x[BM / 16];
+    const int total = my_tiles * nch;
+    for (int g = 0; g < total; ++g) {
+      const int s = g % NS;
+      mbar_wait(&full[s], (g / NS) & 1);
+      float4* hp = reinterpret_cast<float4*>(A_hi(s));
+      float4* lp = reinterpret_cast<float4*>(A_lo(s));
+      float4 x[8];
 #pragma unroll
-        for (int i = 0; i < BM / 16; ++i) {  // issue all loads first (8 in flight)
-          const int64_t row = m0 + i * 16 + (lt >> 3);
-          x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row < a.M) {
-            const float* src = base + row * lda;
-            if (kl + 4 <= kend) {
-              x[i] = *reinterpret_cast<const float4*>(src + kl);
-            } else if (kl < kend) {
-              float tt[4] = {0.f, 0.f, 0.f, 0.f};
-              for (int e = 0; e < 4 && kl + e < kend; ++e) tt[e] = src[kl + e];
-              x[i] = make_float4(tt[0], tt[1], tt[2], tt[3]);
-            }
-          }
-        }
+      for (int i = 0; i < 8; ++i) x[i] = hp[i * 128 + lt];
 #pragma unroll
-        for (int i = 0; i < BM / 16; ++i) {
-          const int rr = i * 16 + (lt >> 3);
-          float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
-          float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
-                                 tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
-          const int off = kc * 512 + (rr >> 3) * 32 + (rr & 7) * 4;
-          *reinterpret_cast<float4*>(ah + off) = h;
-          *reinterpret_cast<float4*>(al + off) = l;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&a_full[s]);
+      for (int i = 0; i < 8; ++i) {
+        const float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
+        const float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
+                                     tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
+        hp[i * 128 + lt] = h;
+        lp[i * 128 + lt] = l;
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a_full[s]);
     }
   } else {
     // ------------------------------------------------ epilogue: thread = accumulator row
+    // Each thread holds one accumulator row (tcgen05.ld 32x32b); 32x32 blocks are
+    // transposed through a padded smem tile (row stride 36 floats: conflict-free
+    // STS.128 / LDS.128) so every global load/store is a float4 and each warp
+    // instruction touches 4 full 128-B lines.
     const int ew = warp - 4;                 // TMEM lane quarter
+    const int et = threadIdx.x - 128;        // 0..127
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    float* stg = epi + ew * 32 * 33;         // [32 rows][33] staging for coalesced stores
+    float* stg = epi + ew * 32 * 36;
+    float* s_bias = epi + 4 * 32 * 36;       // [256]
+    float* s_g = s_bias + 256;               // [128]
+    float* s_b = s_g + 128;                  // [128]
+    const int rq = lane >> 3, c4 = lane & 7;
+    auto epi_bar = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    auto ld4 = [](const float* p) { return *reinterpret_cast<const float4*>(p); };
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int t = blockIdx.x + tl * gridDim.x;
       const int64_t m0 = (int64_t)(t / nblk) * BM;
       const int n0 = (t % nblk) * BN;
+      const int64_t rbase = m0 + ew * 32;
       const int ab = tl & 1;
+      epi_bar();  // previous tile's parameter reads are done
+      for (int i = et; i < BN; i += 128) {
+        s_bias[i] = (a.bias && n0 + i < a.N) ? a.bias[n0 + i] : 0.f;
+        if (LN) {
+          s_g[i] = a.ln_g[i];
+          s_b[i] = a.ln_b[i];
+        }
+      }
+      epi_bar();
       mbar_wait(&acc_full[ab], (tl >> 1) & 1);
       fence_after();
       const uint32_t tacc = tbase + ab * CF::TCOLS + lane_off;
-      const int64_t row = m0 + ew * 32 + lane;
+      const int64_t row = rbase + lane;
       const bool rv = row < a.M;
-      // write a 32x32 block (rows of this warp, 32 columns from c0) to C coalesced
-      auto flush = [&](float* C, int64_t ldc, int c0) {
+      // y[32] of this thread's row (columns c0..c0+31 of the block) -> C, coalesced
+      auto store32 = [&](float* C, int64_t ldc, int c0, const float* y) {
         __syncwarp();
-        for (int i = 0; i < 32; ++i) {
-          const int64_t rr = m0 + ew * 32 + i;
-          const int n = n0 + c0 + lane;
-          if (rr < a.M && n < a.N && c0 + lane < BN) C[rr * ldc + n] = stg[i * 33 + lane];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + lane * 36 + 4 * q) =
+              make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + rq;
+          const int cl = c0 + c4 * 4;  // column within the block
+          const int64_t gr = rbase + r;
+          const int n = n0 + cl;
+          if (gr < a.M && cl < BN && n < a.N) {
+            const float4 v = ld4(stg + r * 36 + c4 * 4);
+            float* dst = C + gr * ldc + n;
+            if (a.vec && n + 4 <= a.N) {
+              *reinterpret_cast<float4*>(dst) = v;
+            } else {
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+              for (int e = 0; e < 4 && n + e < a.N; ++e) dst[e] = vv[e];
+            }
+          }
         }
-        __syncwarp();
       };
       if (LN) {
-        float mu = 0.f, inv = 0.f;
         // pass 1: x = acc + bias + resid, kept in TMEM; running sum
         float s = 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t u[16];
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t u[32];
           TG_LD16(tacc + c0, u);
+          TG_LD16(tacc + c0 + 16, (u + 16));
+          float rr[32];
+          if (a.resid) {
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = i * 4 + rq;
+              const int64_t gr = rbase + r;
+              const float4 v = gr < a.M ? __ldg(reinterpret_cast<const float4*>(
+                                              a.resid + gr * a.ldr + c0 + c4 * 4))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+              *reinterpret_cast<float4*>(stg + r * 36 + c4 * 4) = v;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 v = ld4(stg + lane * 36 + 4 * q);
+              rr[4 * q] = v.x; rr[4 * q + 1] = v.y; rr[4 * q + 2] = v.z; rr[4 * q + 3] = v.w;
+            }
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float x = __uint_as_float(u[j]) + (a.bias ? a.bias[c0 + j] : 0.f);
-            if (a.resid && rv) x += a.resid[row * a.ldr + c0 + j];
-            s += x;
-            u[j] = __float_as_uint(x);
+          for (int q = 0; q < 8; ++q) {
+            const float4 b4 = ld4(s_bias + c0 + 4 * q);
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = 4 * q + e;
+              float x = __uint_as_float(u[j]) + bb[e];
+              if (a.resid) x += rr[j];
+              s += x;
+              u[j] = __float_as_uint(x);
+            }
           }
           TG_ST16(tacc + c0, u);
+          TG_ST16(tacc + c0 + 16, (u + 16));
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        mu = s / BN;
+        const float mu = s / BN;
         float q = 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t u[16];
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t u[32];
           TG_LD16(tacc + c0, u);
+          TG_LD16(tacc + c0 + 16, (u + 16));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < 32; ++j) {
             const float d = __uint_as_float(u[j]) - mu;
             q += d * d;
           }
         }
-        inv = 1.f / sqrtf(q / BN + 1e-5f);
+        const float inv = 1.f / sqrtf(q / BN + 1e-5f);
         const float* rs = (a.rowscale && rv) ? a.rowscale + (int64_t)a.row_fwd[row] * BN : nullptr;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -367,17 +446,24 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           float y[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            y[j] = a.ln_g[c0 + j] * ((__uint_as_float(u[j]) - mu) * inv) + a.ln_b[c0 + j];
-          if (a.C) {
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 g4 = ld4(s_g + c0 + 4 * q4), b4 = ld4(s_b + c0 + 4 * q4);
+            const float gg[4] = {g4.x, g4.y, g4.z, g4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = y[j];
-            flush(a.C, a.ldc, c0);
+            for (int e = 0; e < 4; ++e) {
+              const int j = 4 * q4 + e;
+              y[j] = gg[e] * ((__uint_as_float(u[j]) - mu) * inv) + bb[e];
+            }
           }
+          if (a.C) store32(a.C, a.ldc, c0, y);
           if (a.rowscale) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = rs ? y[j] * rs[c0 + j] : 0.f;
-            flush(a.C2, a.ldc2, c0);
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 r4 = rs ? __ldg(reinterpret_cast<const float4*>(rs + c0) + q4)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+              y[4 * q4] *= r4.x; y[4 * q4 + 1] *= r4.y; y[4 * q4 + 2] *= r4.z; y[4 * q4 + 3] *= r4.w;
+            }
+            store32(a.C2, a.ldc2, c0, y);
           }
         }
       } else {
@@ -387,16 +473,18 @@ __global__ void __launch_bounds__(G_THREADS, 1) tc_gemm_kernel(Args a, int nblk,
           TG_LD16(tacc + c0, u);
           if (c0 + 16 < BN) TG_LD16(tacc + c0 + 16, (u + 16));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float y[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = n0 + c0 + j;
-            float x = (c0 + j < BN) ? __uint_as_float(u[j]) : 0.f;
-            if (a.bias && n < a.N) x += a.bias[n];
-            if (a.act == 1) x = x > 0.f ? x : 0.f;
-            else if (a.act == 2) x = 1.f / (1.f + expf(-x));
-            stg[lane * 33 + j] = x;
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 b4 = ld4(s_bias + c0 + 4 * q4);  // s_bias has 256 entries: in range
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = 4 * q4 + e;
+              y[j] = activate<ACT>(__uint_as_float(u[j]) + bb[e]);
+            }
           }
-          flush(a.C, a.ldc, c0);
+          store32(a.C, a.ldc, c0, y);
         }
       }
       fence_before();
@@ -473,20 +561,67 @@ void tc_gemm_pack(const float* W0, const float* W1, const float* W2, int Nsub, i
   LAUNCH_CHECK();
 }
 
-template <int BN, bool LN>
-static void launch(const tg::Args& a, int nblk, cudaStream_t st) {
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      GO_THROW(GO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D fp32 map over A[rows, cols] (row stride ld floats): boxes of 128 rows x 32 cols,
+// 128-B swizzle, out-of-range rows/cols read as zero.
+CUtensorMap a_map(const float* A, int64_t rows, int cols, int64_t ld) {
+  GO_CHECK((uintptr_t)A % 16 == 0 && ld % 4 == 0, "A rows must be 16-B aligned");
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)tg::BK, (cuuint32_t)tg::BM};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) GO_THROW(GO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return m;
+}
+
+template <int BN, bool LN, int ACT>
+void launch(const float* A1, int64_t lda1, const float* A2, int64_t lda2, const tg::Args& a,
+            int nblk, cudaStream_t st) {
   using CF = tg::Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, LN>,
+    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, LN, ACT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr = true;
   }
+  GO_CHECK(a.M < ((int64_t)1 << 31), "too many rows for one GEMM launch");
+  const CUtensorMap m1 = a_map(A1, a.M, a.K1, lda1);
+  const CUtensorMap m2 = A2 ? a_map(A2, a.M, a.K2, lda2) : m1;
   const int ntiles = (int)cdiv(a.M, tg::BM) * nblk;
   const int grid = std::min(ntiles, num_sms());
-  tg::tc_gemm_kernel<BN, LN><<<grid, tg::G_THREADS, CF::SMEM, st>>>(a, nblk, ntiles);
+  tg::tc_gemm_kernel<BN, LN, ACT><<<grid, tg::G_THREADS, CF::SMEM, st>>>(m1, m2, a, nblk, ntiles);
   LAUNCH_CHECK();
 }
+
+template <int BN>
+void launch_act(int act, const float* A1, int64_t lda1, const float* A2, int64_t lda2,
+                const tg::Args& a, int nblk, cudaStream_t st) {
+  switch (act) {
+    case 1: launch<BN, false, 1>(A1, lda1, A2, lda2, a, nblk, st); break;
+    case 2: launch<BN, false, 2>(A1, lda1, A2, lda2, a, nblk, st); break;
+    default: launch<BN, false, 0>(A1, lda1, A2, lda2, a, nblk, st); break;
+  }
+}
+
+}  // namespace
 
 // C = act([A1|A2] @ W + bias) with W prepacked by tc_gemm_pack(K1+K2, N).
 void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
@@ -494,22 +629,21 @@ void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda
              int act, cudaStream_t st) {
   if (M <= 0) return;
   GO_CHECK(A2 == nullptr || K1 % tg::BK == 0, "concat split must be a multiple of 32");
-  GO_CHECK(lda1 % 4 == 0 && (A2 == nullptr || lda2 % 4 == 0), "A rows must be 16-B aligned");
   tg::Args a{};
-  a.A1 = A1; a.lda1 = lda1; a.K1 = K1; a.A2 = A2; a.lda2 = lda2; a.K2 = A2 ? K2 : 0;
+  a.K1 = K1; a.K2 = A2 ? K2 : 0;
   a.Bpk = Wpk; a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
   a.nch = (int)cdiv(K1 + a.K2, tg::BK);
-  a.act = act;
+  a.vec = ((uintptr_t)C % 16 == 0) && ldc % 4 == 0;
   int BN = tc_gemm_bn(N);
   int nblk = (int)cdiv(N, BN);
   switch (BN) {
-    case 16: launch<16, false>(a, nblk, st); break;
-    case 32: launch<32, false>(a, nblk, st); break;
-    case 48: launch<48, false>(a, nblk, st); break;
-    case 64: launch<64, false>(a, nblk, st); break;
-    case 128: launch<128, false>(a, nblk, st); break;
-    case 144: launch<144, false>(a, nblk, st); break;
-    default: launch<256, false>(a, nblk, st); break;
+    case 16: launch_act<16>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    case 32: launch_act<32>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    case 48: launch_act<48>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    case 64: launch_act<64>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    case 128: launch_act<128>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    case 144: launch_act<144>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    default: launch_act<256>(act, A1, lda1, A2, lda2, a, nblk, st); break;
   }
 }
 
@@ -523,12 +657,16 @@ void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t 
   GO_CHECK(N == 128, "fused LayerNorm epilogue needs N == 128");
   GO_CHECK(A2 == nullptr || K1 % tg::BK == 0, "concat split must be a multiple of 32");
   tg::Args a{};
-  a.A1 = A1; a.lda1 = lda1; a.K1 = K1; a.A2 = A2; a.lda2 = lda2; a.K2 = A2 ? K2 : 0;
+  a.K1 = K1; a.K2 = A2 ? K2 : 0;
   a.Bpk = Wpk; a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
   a.nch = (int)cdiv(K1 + a.K2, tg::BK);
   a.resid = resid; a.ldr = ldr; a.ln_g = g; a.ln_b = beta;
   a.rowscale = rowscale; a.row_fwd = row_fwd; a.C2 = C2; a.ldc2 = ldc2;
-  launch<128, true>(a, 1, st);
+  GO_CHECK(resid == nullptr || ((uintptr_t)resid % 16 == 0 && ldr % 4 == 0),
+           "LayerNorm residual rows must be 16-B aligned");
+  a.vec = (C == nullptr || ((uintptr_t)C % 16 == 0 && ldc % 4 == 0)) &&
+          (C2 == nullptr || ((uintptr_t)C2 % 16 == 0 && ldc2 % 4 == 0));
+  launch<128, true, 0>(A1, lda1, A2, lda2, a, 1, st);
 }
 
 }  // namespace go

@@ -133,7 +133,9 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   Arena2 A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   int32_t* row_fwd = A.take<int32_t>(R);
   int32_t* row_node = A.take<int32_t>(R);
+  GO_CHECK(m.gtotal + R < ((int64_t)1 << 31), "neighbour list exceeds 2^31 entries");
   int32_t* gidx = A.take<int32_t>(m.gtotal);
+  int32_t* segoff = A.take<int32_t>(R + 1);
   row_fwd_fill(m.d_row_off, F, R, row_fwd, st);
   row_node_fill(m.d_views, m.d_row_off, row_fwd, R, row_node, st);
 
@@ -157,13 +159,13 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     }
   }
   const int Fdim = 16 + [&] { int s = 0; for (int t = 0; t < T; ++t) s += cfg.task_sizes[t]; return s; }();
-  neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, F, R, row_fwd, cfg.gs_knn, gidx, st);
+  neighbor_sample(m.d_views, m.d_row_off, m.d_gbase, m.d_seeds, F, R, row_fwd, cfg.gs_knn, gidx, segoff, st);
   features_inproj(m.d_views, m.d_row_off, row_fwd, R, b.prev_actions, T, tcol, Pw(S.e_in_w()),
                   Pw(S.e_in_b()), gs, eh[0], gs, st);
   for (int l = 0; l < Lg; ++l) {
     gemm(eh[l], gs, gs, nullptr, 0, 0, Pw(S.e_layer(l, 0)), gs, Pw(S.e_layer(l, 1)), et[l], gs, R,
          gs, 2, st);
-    segment_max(et[l], gs, m.d_views, m.d_row_off, m.d_gbase, row_fwd, gidx, R, gs, ep[l], gs, st,
+    segment_max(et[l], gs, segoff, gidx, R, gs, ep[l], gs, st,
                 ea[l]);
     gemm(eh[l], gs, gs, ep[l], gs, gs, Pw(S.e_layer(l, 2)), gs, Pw(S.e_layer(l, 3)), eh[l + 1], gs,
          R, gs, 1, st);

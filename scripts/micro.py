@@ -2,7 +2,8 @@
 """Micro-benchmarks on one GPU (development aid, not the headline bench):
   des      : batched DES throughput on the cfg4 graph, per launch mode
   forward  : one wave of cfg4 forwards, per-kernel-class CUDA-event times
-Usage: python scripts/micro.py des|forward [K]"""
+  poly     : forward with GO_POLY = 0..4 (exp2 split between MUFU and FMA)
+Usage: python scripts/micro.py des|forward|poly [K]"""
 import ctypes as C
 import os
 import sys
@@ -41,7 +42,7 @@ def des(K):
               f"step[0]={float(r.step_time[0]):.6g}", flush=True)
 
 
-def forward(F):
+def forward(F, modes=("tc", "simt"), env=None):
     from paper_2010_12438_b200 import EmbedConfig, PolicyConfig, init_all_params, randomize_zero_init
     from paper_2010_12438_b200 import _lib
     from paper_2010_12438_b200.engine import forward_batch
@@ -53,8 +54,11 @@ def forward(F):
     ctx = context()
     hs = [ctx.graph(g)] * F
     names = ["heads_attn", "trunk_attn", "segmax", "gemm", "des", "sample", "neighbor", "other"]
-    for mode in ("tc", "simt"):
+    runs = [(m, None) for m in modes] if env is None else [(modes[0], e) for e in env]
+    for mode, ev in runs:
         os.environ["GO_GEMM"] = mode
+        if ev:
+            os.environ[ev[0]] = ev[1]
         forward_batch(store, ecfg, pcfg, sizes, hs, list(range(F)))
         torch.cuda.synchronize()
         _lib.call("go_ctx_set_timing", ctx.handle, 1)
@@ -70,7 +74,7 @@ def forward(F):
                 rate = work.value / (ms.value / 1e3)
                 parts.append(f"{nm}={ms.value:.1f}ms({rate/1e12:.1f}T/s)")
         _lib.call("go_ctx_set_timing", ctx.handle, 0)
-        print(f"forward GEMM={mode} F={F}: {dt*1e3:.1f} ms total ({dt*1e3/F:.2f} ms/forward) "
+        print(f"forward GEMM={mode} {ev or ''} F={F}: {dt*1e3:.1f} ms total ({dt*1e3/F:.2f} ms/forward) "
               + " ".join(parts), flush=True)
         lg = out.logits[0].float()
         print("  logits checksum", float(lg.sum()), float(lg.abs().max()), flush=True)
@@ -81,5 +85,7 @@ if __name__ == "__main__":
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     if what == "des":
         des(n or 512)
+    elif what == "poly":
+        forward(n or 8, env=[("GO_POLY", str(k)) for k in (0, 1, 2, 3, 4, 0)])
     else:
         forward(n or 8)
