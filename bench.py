@@ -123,6 +123,34 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------------------------------
+# roofline denominators and profiler evidence
+
+N_HEAD, HEAD_W = 3, 45  # PolicyConfig defaults: 3 heads x 15
+
+
+def mufu_peak():
+    """MUFU ex2 throughput measured live by scripts/mufu_peak (built by build()); the
+    recorded B200 measurement if the probe is missing."""
+    probe = ROOT / "scripts" / "mufu_peak"
+    if probe.exists():
+        try:
+            out = subprocess.run([str(probe)], capture_output=True, text=True, timeout=60)
+            d = json.loads(out.stdout.strip().splitlines()[-1])
+            return {"gops": float(d["ex2_gops"]), "source": "measured live (scripts/mufu_peak)"}
+        except Exception:
+            pass
+    d = json.loads((ROOT / "profiles" / "r1_mufu_peak.json").read_text())
+    return {"gops": float(d["ex2_gops"]), "source": "profiles/r1_mufu_peak.json"}
+
+
+def ncu_traffic():
+    try:
+        return json.loads((ROOT / "profiles" / "r1_ncu_summary.json").read_text())["traffic"]
+    except Exception:
+        return {}
+
+
+# -------------------------------------------------------------------------------------
 # CPU baseline: the oracle port, bounded sample of one placement
 
 
@@ -353,22 +381,35 @@ def main():
         pass
     hbm = peaks.get("hbm_gbs", 6650.0)
     bf16 = peaks.get("bf16_tflops_sustained", 1400.0)
+    mufu = mufu_peak()
+    ncu = ncu_traffic()
     cnt, hms, hflops = stats["heads_attention"]
     roof = None
     if cnt:
         ach = hflops / cnt / (hms / cnt / 1000.0) / 1e12
-        roof = {"bound": "tensor", "kernel": "task-head N x N attention, tcgen05 kind::tf32 + TMEM (attn_tc_fixed_kernel)",
+        # exps: one per (query, key, head); flops counted as 4 * pairs * W
+        exps = hflops / 4.0 / HEAD_W * N_HEAD
+        exp_rate = exps / (hms / 1000.0) / 1e9
+        roof = {"bound": "tensor", "binding_unit": "MUFU ex2 (softmax exponentials)",
+                "kernel": "task-head N x N attention, tcgen05 kind::tf32 + TMEM (attn_tc_fixed_kernel)",
                 "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
-                "traffic": None, "launches": cnt, "avg_launch_ms": hms / cnt,
+                "traffic": ncu.get("attn_tc_fixed_bytes_per_forward"),
+                "traffic_note": "dram read+write per forward (one launch = one wave of forwards), "
+                                "ncu --set full, profiles/r1_ncu_summary.json",
+                "launches": cnt, "avg_launch_ms": hms / cnt,
                 "algorithmic_flops_per_launch": hflops / cnt,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if peaks
+                                else "fallback 1400 TF/s"),
+                "exp": {"achieved_gexp_s": exp_rate, "peak_gexp_s": mufu["gops"],
+                        "frac": exp_rate / mufu["gops"], "peak_source": mufu["source"]},
                 "share_of_step": hms / ms}
     cnt2, sms, sbytes = stats["segment_max"]
     roof_agg = None
     if cnt2:
         ach = sbytes / cnt2 / (sms / cnt2 / 1000.0) / 1e9
         roof_agg = {"bound": "hbm", "kernel": "GraphSAGE gather + segment max", "achieved": ach,
-                    "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                    "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": ncu.get("segment_max_bytes_per_launch_F1"),
                     "launches": cnt2, "avg_launch_ms": sms / cnt2,
                     "algorithmic_bytes_per_launch": sbytes / cnt2, "share_of_step": sms / ms}
     line = {

@@ -60,9 +60,26 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")
+    _build_probe(force)
     if verbose:
         print("built", LIB)
     return LIB
+
+
+PROBE_SRC = PKG.parent / "scripts" / "mufu_peak.cu"
+PROBE = PKG.parent / "scripts" / "mufu_peak"
+
+
+def _build_probe(force: bool) -> None:
+    """The MUFU/FMA throughput probe bench.py uses as the exp2 roofline denominator."""
+    if not PROBE_SRC.exists():
+        return
+    if not force and PROBE.exists() and PROBE.stat().st_mtime >= PROBE_SRC.stat().st_mtime:
+        return
+    cmd = [NVCC, *ARCH, "-O3", "-o", str(PROBE), str(PROBE_SRC)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {PROBE_SRC.name}:\n{res.stderr}")
 
 
 if __name__ == "__main__":

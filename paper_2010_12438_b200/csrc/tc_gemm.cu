@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.cuh"
@@ -532,12 +533,15 @@ __global__ void pack_b_kernel(const float* __restrict__ W0, const float* __restr
 }  // namespace tg
 
 int tc_gemm_bn(int N) {
+  // GO_GEMM_BN256=0 caps the block width at 144 (deeper smem ring, more A re-reads)
+  const char* e = getenv("GO_GEMM_BN256");
+  const bool allow256 = !(e && e[0] == '0');
   if (N <= 16) return 16;
   if (N <= 32) return 32;
   if (N <= 48) return 48;
   if (N <= 64) return 64;
   if (N <= 128) return 128;
-  if (N <= 144) return 144;
+  if (N <= 144 || !allow256) return N <= 144 ? 144 : 128;
   return 256;
 }
 

@@ -85,6 +85,8 @@ if __name__ == "__main__":
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     if what == "des":
         des(n or 512)
+    elif what == "bn":
+        forward(n or 8, env=[("GO_GEMM_BN256", "1"), ("GO_GEMM_BN256", "0"), ("GO_GEMM_BN256", "1")])
     elif what == "poly":
         forward(n or 8, env=[("GO_POLY", str(k)) for k in (0, 1, 2, 3, 4, 0)])
     else:
