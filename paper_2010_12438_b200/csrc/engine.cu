@@ -134,7 +134,9 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   if (need_heads) build_tiles(m.row_off, 0, false, ht);
   for (auto& t : tt) m.trunk_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
   for (auto& t : ht) m.head_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
-  size_t o_tt = s.add(tt), o_ht = s.add(ht);
+  std::vector<TrunkTile> ttc;
+  if (need_trunk) m.trunk_tc_ok = trunk_tc_build_tiles(m.row_off, cfg.segment_len, ttc);
+  size_t o_tt = s.add(tt), o_ht = s.add(ht), o_ttc = s.add(ttc);
   std::vector<TcWork> tcw;
   std::vector<int64_t> trow0;
   std::vector<int32_t> tn;
@@ -166,6 +168,8 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   m.d_views = reinterpret_cast<const GraphView*>(dev + o_views);
   m.d_trunk_tiles = reinterpret_cast<const AttnTile*>(dev + o_tt);
   m.n_trunk_tiles = (int64_t)tt.size();
+  m.d_trunk_tc = reinterpret_cast<const TrunkTile*>(dev + o_ttc);
+  m.n_trunk_tc = (int64_t)ttc.size();
   m.d_head_tiles = reinterpret_cast<const AttnTile*>(dev + o_ht);
   m.n_head_tiles = (int64_t)ht.size();
   m.d_chunks = reinterpret_cast<const int64_t*>(dev + o_ch);
@@ -607,6 +611,10 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       modp = mod;
     }
     float* x0 = Lt == 0 ? hid : X[0];
+    // GO_TRUNK=tc selects the tcgen05 segmented attention (measured 0.66 ms/forward vs
+    // 0.41 ms for the SIMT banded kernel at cfg4, so SIMT stays the default)
+    const char* trunk_env = getenv("GO_TRUNK");
+    const bool trunk_tc = m.trunk_tc_ok && dh <= 15 && trunk_env && !strcmp(trunk_env, "tc");
     {
       KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * dm);
       tc_gemm(node_embed, gs, gs, nullptr, 0, 0, pack1(W_(S.p_in_w()), gs, dm), W_(S.p_in_b()), x0,
@@ -624,8 +632,12 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       }
       {
         KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
-        attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab, LA,
-                  st);
+        if (trunk_tc)
+          trunk_attention_tc(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, cfg.segment_len,
+                             m.d_trunk_tc, m.n_trunk_tc, Ab, LA, st);
+        else
+          attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
+                    LA, st);
       }
       float* h1 = X[2];
       {

@@ -137,6 +137,13 @@ __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t b, uint
       "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),    \
       "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),    \
       "r"(r[29]), "r"(r[30]), "r"(r[31]))
+#define TC_ST16(taddr, r)                                                                    \
+  asm volatile(                                                                              \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%" \
+      "14,%15,%16};" ::"r"(taddr),                                                           \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),      \
+      "r"(r[15]))
 #define TC_LD16(taddr, r)                                                                    \
   asm volatile(                                                                              \
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%" \
@@ -475,8 +482,9 @@ struct SmemF {
 };
 
 // POLY_PER_8: of every 8 score columns, this many are exponentiated by ex2_poly on
-// the FMA pipe instead of MUFU.EX2.
-template <int POLY_PER_8>
+// the FMA pipe instead of MUFU.EX2.  PIPE: software-pipelined softmax loop (16-column
+// chunks; the next chunk's tcgen05.ld is in flight while this chunk's ex2s issue).
+template <int POLY_PER_8, bool PIPE>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_tc_fixed_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
                          const float* __restrict__ vb, int64_t R, int64_t Ttot,
@@ -595,26 +603,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     const int t = warp >> 2;
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    for (int u = 0; u < U; ++u) {
-      const int b = u & 1;
-      mbar_wait(&sm.s_full[t][b], (u >> 1) & 1);
-      fence_after();
-      uint32_t sr[HK];
-      const uint32_t sa = tbase + lane_off + t * 2 * HK + b * HK;
-      TC_LD32(sa, sr);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < HK; ++i) {
-        const float x = __uint_as_float(sr[i]);
-        // FA4-style split: a fixed subset of the columns is exponentiated on the FMA
-        // pipe (degree-5 polynomial, rel. err < 4e-6, far below the tf32 rounding of
-        // P) so the MUFU and FMA pipes work in parallel.
-        sr[i] = __float_as_uint(((i & 7) < POLY_PER_8) ? ex2_poly(x) : ex2(x));
+    if (PIPE) {
+      // chunk c = 2u + h: columns [16h, 16h + 16) of sub-tile u.  The tcgen05.ld of
+      // chunk c + 1 is issued before chunk c's ex2s, so the MUFU queue never waits on
+      // a TMEM load; P(u) is released after its second chunk's tcgen05.st lands.
+      const uint32_t base = tbase + lane_off + t * 2 * HK;
+      auto caddr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 16; };
+      uint32_t ra[16], rb[16];
+      if (U > 0) {
+        mbar_wait(&sm.s_full[t][0], 0);
+        fence_after();
+        TC_LD16(caddr(0), ra);
+        tmem_wait_ld();
       }
-      TC_ST32(sa, sr);
-      tmem_wait_st();
-      fence_before();
-      mbar_arrive(&sm.p_full[t][b]);
+      for (int u = 0; u < U; ++u) {
+        const int c = 2 * u;
+        TC_LD16(caddr(c + 1), rb);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ra[i] = __float_as_uint(ex2(__uint_as_float(ra[i])));
+        TC_ST16(caddr(c), ra);
+        tmem_wait_ld();
+        const bool more = u + 1 < U;
+        if (more) {
+          mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
+          fence_after();
+          TC_LD16(caddr(c + 2), ra);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) rb[i] = __float_as_uint(ex2(__uint_as_float(rb[i])));
+        TC_ST16(caddr(c + 1), rb);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&sm.p_full[t][u & 1]);
+        if (more) tmem_wait_ld();
+      }
+    } else {
+      for (int u = 0; u < U; ++u) {
+        const int b = u & 1;
+        mbar_wait(&sm.s_full[t][b], (u >> 1) & 1);
+        fence_after();
+        uint32_t sr[HK];
+        const uint32_t sa = tbase + lane_off + t * 2 * HK + b * HK;
+        TC_LD32(sa, sr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < HK; ++i) {
+          const float x = __uint_as_float(sr[i]);
+          // FA4-style split: a fixed subset of the columns is exponentiated on the FMA
+          // pipe (degree-5 polynomial, rel. err < 4e-6, far below the tf32 rounding of
+          // P) so the MUFU and FMA pipes work in parallel.
+          sr[i] = __float_as_uint(((i & 7) < POLY_PER_8) ? ex2_poly(x) : ex2(x));
+        }
+        TC_ST32(sa, sr);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&sm.p_full[t][b]);
+      }
     }
     mbar_wait(&sm.o_done[t], 0);
     fence_after();
@@ -737,9 +781,10 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
   const size_t smemf = sizeof(tc::SmemF) + 1024;
   using FixedFn = void (*)(const float*, const float*, const float*, int64_t, int64_t,
                            const tc::Work*, float*, int64_t, int, const int32_t*);
-  static const FixedFn fixed_fns[5] = {tc::attn_tc_fixed_kernel<0>, tc::attn_tc_fixed_kernel<1>,
-                                       tc::attn_tc_fixed_kernel<2>, tc::attn_tc_fixed_kernel<3>,
-                                       tc::attn_tc_fixed_kernel<4>};
+  static const FixedFn fixed_fns[6] = {
+      tc::attn_tc_fixed_kernel<0, true>,  tc::attn_tc_fixed_kernel<1, false>,
+      tc::attn_tc_fixed_kernel<2, false>, tc::attn_tc_fixed_kernel<3, false>,
+      tc::attn_tc_fixed_kernel<4, false>, tc::attn_tc_fixed_kernel<0, false>};
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
@@ -747,9 +792,10 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
       CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf));
     attr = true;
   }
-  // GO_POLY=k: k of every 8 exponentials on the FMA pipe (default 0)
+  // GO_POLY=k (1..4): k of every 8 exponentials on the FMA pipe; GO_POLY=5: the
+  // unpipelined pure-MUFU loop; default 0: pipelined pure-MUFU loop
   const char* poly_env = getenv("GO_POLY");
-  const int poly = poly_env ? std::max(0, std::min(4, atoi(poly_env))) : 0;
+  const int poly = poly_env ? std::max(0, std::min(5, atoi(poly_env))) : 0;
   float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   int64_t total = (int64_t)n_head * Ttot * tc::KT;
   dim3 grid((unsigned)num_works, (unsigned)n_head);
