@@ -176,6 +176,16 @@ void attention(const float* q, const float* k, const float* v, int64_t ld, int n
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
                int64_t ldo, cudaStream_t st, float* lse = nullptr);
 
+// ---- kernels: tc_attention16.cu (fp16 operands, fixed-offset softmax; flags the launch
+// over to the tf32 / online kernels when a bound exceeds the fp16-exact range)
+struct TcWork;
+void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+                      int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
+                      int64_t num_works, const int64_t* tile_row0_dev, const int32_t* tile_n_dev,
+                      void* qh, void* kb, void* vb, float* out, int64_t ldo,
+                      const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
+                      cudaStream_t st);
+
 // ---- kernels: tc_trunk.cu (tcgen05 / TMEM segmented trunk attention, d_head <= 15)
 constexpr int TRUNK_TC_MAX_KEYS = 240;
 struct TrunkTile {

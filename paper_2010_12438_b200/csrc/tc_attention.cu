@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const float* __restrict__ vb, int64_t R, int64_t Ttot,
                    const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
                    int d_head, const int32_t* __restrict__ flag) {
-  if (flag && !*flag) return;  // the fixed-offset kernel handled this launch
+  if (flag && !(*flag & 1)) return;  // no bound above BOUND_LIMIT: another kernel ran
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -403,7 +403,7 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
                               const int32_t* __restrict__ tile_n, int64_t Ttot, int64_t R,
                               float qscale, float* __restrict__ qh, float* __restrict__ kb,
                               float* __restrict__ vb, const int32_t* __restrict__ flag) {
-  if (flag && !*flag) return;
+  if (flag && !(*flag & 1)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (head, tile, row)
   int64_t total = (int64_t)n_head * Ttot * KT;
   if (idx >= total) return;
@@ -489,8 +489,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_tc_fixed_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
                          const float* __restrict__ vb, int64_t R, int64_t Ttot,
                          const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
-                         int d_head, const int32_t* __restrict__ flag) {
-  if (*flag) return;  // some bound exceeded BOUND_LIMIT: the online kernel runs instead
+                         int d_head, const int32_t* __restrict__ flag, int want) {
+  if (*flag != want) return;  // another variant takes this launch
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SmemF& sm = *reinterpret_cast<SmemF*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -687,7 +687,9 @@ __global__ void repack_kv_fixed_kernel(const float* __restrict__ k, const float*
                                        const int64_t* __restrict__ tile_fwd_row0,
                                        const int32_t* __restrict__ tile_n, int64_t Ttot,
                                        float* __restrict__ kb, float* __restrict__ vb,
-                                       unsigned* __restrict__ kmax) {
+                                       unsigned* __restrict__ kmax,
+                                       const int32_t* __restrict__ flag, int want) {
+  if (*flag != want) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)n_head * Ttot * KT;
   if (idx >= total) return;
@@ -726,7 +728,9 @@ __global__ void repack_kv_fixed_kernel(const float* __restrict__ k, const float*
 __global__ void repack_q_fixed_kernel(const float* __restrict__ q, int64_t ld, int n_head,
                                       int d_head, int64_t R, const int32_t* __restrict__ row_fwd,
                                       const unsigned* __restrict__ kmax, float qscale,
-                                      float* __restrict__ qh, int32_t* __restrict__ flag) {
+                                      float* __restrict__ qh, int32_t* __restrict__ flag,
+                                      int want) {
+  if (*flag != want) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * n_head) return;
   int64_t r = idx / n_head;
@@ -780,7 +784,7 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
   const size_t smem = sizeof(tc::Smem) + 1024;
   const size_t smemf = sizeof(tc::SmemF) + 1024;
   using FixedFn = void (*)(const float*, const float*, const float*, int64_t, int64_t,
-                           const tc::Work*, float*, int64_t, int, const int32_t*);
+                           const tc::Work*, float*, int64_t, int, const int32_t*, int);
   static const FixedFn fixed_fns[6] = {
       tc::attn_tc_fixed_kernel<0, true>,  tc::attn_tc_fixed_kernel<1, false>,
       tc::attn_tc_fixed_kernel<2, false>, tc::attn_tc_fixed_kernel<3, false>,
@@ -793,27 +797,37 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
     attr = true;
   }
   // GO_POLY=k (1..4): k of every 8 exponentials on the FMA pipe; GO_POLY=5: the
-  // unpipelined pure-MUFU loop; default 0: pipelined pure-MUFU loop
+  // unpipelined pure-MUFU loop; default 0: pipelined pure-MUFU loop (tf32 variant)
   const char* poly_env = getenv("GO_POLY");
   const int poly = poly_env ? std::max(0, std::min(5, atoi(poly_env))) : 0;
+  const char* force = getenv("GO_ATTN");
+  // GO_ATTN=tf32 skips the fp16 variant, GO_ATTN=online forces the online kernel
+  const bool use16 = d_head <= 15 && !(force && (!strcmp(force, "tf32") || !strcmp(force, "online")));
   float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   int64_t total = (int64_t)n_head * Ttot * tc::KT;
   dim3 grid((unsigned)num_works, (unsigned)n_head);
-  const char* force = getenv("GO_ATTN");
   bool fixed_ok = d_head <= 15 && !(force && !strcmp(force, "online"));
   if (fixed_ok) {
     // scratch: [0] flag, [1..] kmax per (forward, head)
     int32_t* flag = scratch;
     unsigned* kmax = reinterpret_cast<unsigned*>(scratch + 1);
     CUDA_CHECK(cudaMemsetAsync(scratch, 0, (size_t)(1 + F * n_head) * 4, st));
+    // flag after the fp16 repack: 0 -> fp16 kernel, 2 -> tf32 kernel, odd -> online
+    int want = 0;
+    if (use16) {
+      attention_f16_tc(q, k, v, ld, n_head, d_head, R, Ttot, works_dev, num_works, tile_row0_dev,
+                       tile_n_dev, qh, kb, vb, out, ldo, row_fwd, kmax, flag, qscale, st);
+      want = 2;
+    }
     tc::repack_kv_fixed_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
-        k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, kb, vb, kmax);
+        k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, kb, vb, kmax, flag, want);
     LAUNCH_CHECK();
     tc::repack_q_fixed_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
-        q, ld, n_head, d_head, R, row_fwd, kmax, qscale, qh, flag);
+        q, ld, n_head, d_head, R, row_fwd, kmax, qscale, qh, flag, want);
     LAUNCH_CHECK();
     fixed_fns[poly]<<<grid, tc::NUM_THREADS, smemf, st>>>(
-        qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, flag);
+        qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, flag,
+        want);
     LAUNCH_CHECK();
     // fallback for bounds > BOUND_LIMIT: the online kernel re-packs and runs only if flagged
     tc::repack_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(

@@ -1,0 +1,352 @@
+// Task-head N x N attention, fp16 tensor-core variant (policy.py:210).
+//
+// Same structure and fixed-offset trick as attn_tc_fixed_kernel (tc_attention.cu), with
+// the two MMAs in kind::f16 (fp16 operands, fp32 accumulation), because at these shapes
+// the tensor pipe, not the MUFU, binds the tf32 kernel: a tcgen05.mma with M=128 and
+// N <= 64 costs ~45.5 cycles regardless of N (scripts/umma_probe.cu), and kind::f16 does
+// K=16 per instruction against kind::tf32's K=8, halving the instruction count:
+//   S = Q K^T    M=128, N=32, K=16: 1 instruction per query tile and 32-key sub-tile
+//   O += P V     M=128, N=16, K=16 (A = P packed fp16x2 in TMEM): 2 instructions
+//
+// Precision.  fp16 carries the same 10 explicit mantissa bits as tf32 (Q, K, V and P are
+// rounded to nearest), so products match the tf32 kernel's.  The range is handled by the
+// offset: Q[:,15] = 15 - b_i against K[:,15] = 1 gives S' = s - b_i + 15 <= 15, so
+// P' = 2^S' <= 2^15 never overflows fp16, and as long as b_i <= F16_LIMIT = 14 every
+// score satisfies S' >= 15 - 2 b_i >= -13, i.e. every P' is a normal fp16 (no subnormal
+// precision loss).  The 2^15 scale cancels in O / O[:,15].  Rows with a larger bound (or
+// |k|, |v| beyond fp16 range) flag the launch over to the tf32 kernel (bound <= 60) or
+// the online-softmax kernel (> 60).
+#include <algorithm>
+#include <cmath>
+#include <cuda_fp16.h>
+
+#include "engine.cuh"
+#include "tcgen05.cuh"
+
+namespace go {
+namespace t16 {
+
+using namespace ptx;
+
+constexpr int KT = 64;   // keys per K/V tile (the tile tables are shared with the tf32 path)
+constexpr int QT = 128;  // queries per M tile
+constexpr int NQT = 3;   // M tiles per CTA
+constexpr int HK = 32;   // keys per softmax sub-tile
+constexpr int NS = 8;    // K/V ring stages
+constexpr int TILE_BYTES = KT * 16 * 2;
+constexpr int PRODUCER_WARP = NQT * 4;
+constexpr int MMA_WARP = NQT * 4 + 1;
+constexpr int NUM_THREADS = (NQT * 4 + 2) * 32;
+constexpr uint32_t O_COL = NQT * 2 * HK;
+constexpr uint32_t TMEM_COLS = 256;
+constexpr float F16_LIMIT = 14.f;
+constexpr float BOUND_LIMIT = 60.f;
+constexpr float RANGE_LIMIT = 60000.f;  // |k|, |v| that still round to a finite fp16
+
+struct Smem {
+  uint16_t q[NQT][QT * 16];
+  uint16_t kv[NS][2][KT * 16];
+  uint64_t kv_full[NS], kv_empty[NS];
+  uint64_t s_full[NQT][2], p_full[NQT][2], o_done[NQT];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 2)
+    attn_f16_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
+                    const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
+                    const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
+                    int d_head, const int32_t* __restrict__ flag) {
+  if (*flag) return;  // some row needs the tf32 or the online kernel
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TcWork w = works[blockIdx.x];
+  const int head = blockIdx.y;
+  const int T = w.tiles;
+  const int U = 2 * T;
+  const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  if (warp == PRODUCER_WARP && lane == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int t = 0; t < NQT; ++t) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&sm.s_full[t][b], 1);
+        mbar_init(&sm.p_full[t][b], 128);
+      }
+      mbar_init(&sm.o_done[t], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // Q: per query tile, K-major canonical (two 8-half K chunks of 8-row core matrices)
+  for (int i = threadIdx.x; i < NQT * QT * 2; i += NUM_THREADS) {
+    const int qt = i / (QT * 2), rem = i % (QT * 2);
+    const int r = rem >> 1, c = rem & 1;
+    const int lr = w.q0 + qt * QT + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (lr < w.n)
+      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
+    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
+  }
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == PRODUCER_WARP) {
+    if (lane == 0) {
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        if (j >= NS) mbar_wait(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
+        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == MMA_WARP) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_f16(QT, HK);
+      constexpr uint32_t ID_O = idesc_f16(QT, 16);
+      uint32_t qaddr[NQT];
+      for (int t = 0; t < NQT; ++t) qaddr[t] = smem_u32(sm.q[t]);
+      auto wait_kv = [&](int u) {
+        if ((u & 1) == 0) {
+          const int j = u >> 1;
+          mbar_wait(&sm.kv_full[j % NS], (j / NS) & 1);
+          fence_after();
+        }
+      };
+      // S(u, t): keys [32h, 32h + 32) of tile j = u / 2 (K chunk stride 1 KB, 8-key
+      // groups 128 B apart, so the second half starts 4 groups = 512 B in)
+      auto issue_s = [&](int u, int t) {
+        const int j = u >> 1, h = u & 1, s = j % NS, b = u & 1;
+        const uint32_t kaddr = smem_u32(sm.kv[s][0]) + h * 512;
+        umma_ss_f16(tbase + t * 2 * HK + b * HK, sdesc(qaddr[t], QT * 16, 128),
+                    sdesc(kaddr, KT * 16, 128), ID_S, 0);
+        umma_commit(&sm.s_full[t][b]);
+      };
+      for (int u = 0; u < 2 && u < U; ++u) {
+        wait_kv(u);
+        for (int t = 0; t < NQT; ++t) issue_s(u, t);
+      }
+      for (int u = 0; u < U; ++u) {
+        const int j = u >> 1, h = u & 1, s = j % NS, b = u & 1;
+        const bool more = u + 2 < U;
+        if (more) wait_kv(u + 2);
+        // V^T: 8-key chunks of 256 B (16 d rows x 16 B); second half 4 chunks in
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]) + h * 1024;
+        for (int t = 0; t < NQT; ++t) {
+          mbar_wait(&sm.p_full[t][b], (u >> 1) & 1);
+          fence_after();
+          const uint32_t d = tbase + O_COL + t * 16;
+          const uint32_t a = tbase + t * 2 * HK + b * HK;  // P: 16 packed columns
+#pragma unroll
+          for (int kk = 0; kk < HK / 16; ++kk)
+            umma_ts_f16(d, a + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (u > 0 || kk > 0));
+          if (more) issue_s(u + 2, t);
+        }
+        if (h == 1) umma_commit(&sm.kv_empty[s]);
+      }
+      for (int t = 0; t < NQT; ++t) umma_commit(&sm.o_done[t]);
+    }
+    __syncwarp();
+  } else {
+    // softmax: thread = query row; 16-column chunks, the next chunk's tcgen05.ld in
+    // flight while this chunk's ex2s issue; P (fp16x2) overwrites the consumed S columns
+    const int t = warp >> 2;
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t base = tbase + lane_off + t * 2 * HK;
+    auto s_addr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 16; };
+    auto p_addr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 8; };
+    auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        pk[i] = pack_f16x2(ex2f(__uint_as_float(r[2 * i])), ex2f(__uint_as_float(r[2 * i + 1])));
+    };
+    uint32_t ra[16], rb[16], pk[8];
+    if (U > 0) {
+      mbar_wait(&sm.s_full[t][0], 0);
+      fence_after();
+      PTX_LD16(s_addr(0), ra);
+      tmem_wait_ld();
+    }
+    for (int u = 0; u < U; ++u) {
+      const int c = 2 * u;
+      PTX_LD16(s_addr(c + 1), rb);
+      softmax16(ra, pk);
+      PTX_ST8(p_addr(c), pk);
+      tmem_wait_ld();
+      const bool more = u + 1 < U;
+      if (more) {
+        mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
+        fence_after();
+        PTX_LD16(s_addr(c + 2), ra);
+      }
+      softmax16(rb, pk);
+      PTX_ST8(p_addr(c + 1), pk);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&sm.p_full[t][u & 1]);
+      if (more) tmem_wait_ld();
+    }
+    mbar_wait(&sm.o_done[t], 0);
+    fence_after();
+    uint32_t r[16];
+    PTX_LD16(tbase + lane_off + O_COL + t * 16, r);
+    tmem_wait_ld();
+    const int lr = w.q0 + t * QT + wq * 32 + lane;
+    if (lr < w.n) {
+      const float inv = 1.f / __uint_as_float(r[15]);
+      float* o = out + (w.row0 + lr) * ldo + head * d_head;
+      for (int d = 0; d < d_head; ++d) o[d] = __uint_as_float(r[d]) * inv;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// K and V^T tiles in fp16: K[:,15] = V[:,15] = 1 on valid keys, zero rows past the end;
+// max |k| (of the rounded values) per (forward, head); flags |k|, |v| out of fp16 range.
+__global__ void repack_kv16_kernel(const float* __restrict__ k, const float* __restrict__ v,
+                                   int64_t ld, int n_head, int d_head,
+                                   const int64_t* __restrict__ tile_fwd_row0,
+                                   const int32_t* __restrict__ tile_n, int64_t Ttot,
+                                   __half* __restrict__ kb, __half* __restrict__ vb,
+                                   unsigned* __restrict__ kmax, int32_t* __restrict__ flag) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)n_head * Ttot * KT;
+  if (idx >= total) return;
+  const int head = (int)(idx / (Ttot * KT));
+  const int64_t rem = idx % (Ttot * KT);
+  const int64_t tile = rem / KT;
+  const int rk = (int)(rem % KT);
+  const int local = tile_n[3 * tile + 1] * KT + rk;
+  const bool valid = local < tile_n[3 * tile];
+  const int fwd = tile_n[3 * tile + 2];
+  const int64_t grow = tile_fwd_row0[tile] + local;
+  __half* kt = kb + ((int64_t)head * Ttot + tile) * (KT * 16);
+  __half* vt = vb + ((int64_t)head * Ttot + tile) * (KT * 16);
+  float nk = 0.f;
+  bool big = false;
+  for (int d = 0; d < 16; ++d) {
+    float kv = 0.f, vv = 0.f;
+    if (valid) {
+      if (d < d_head) {
+        const int64_t o = grow * ld + head * d_head + d;
+        kv = k[o];
+        vv = v[o];
+        big |= !(fabsf(kv) <= RANGE_LIMIT) || !(fabsf(vv) <= RANGE_LIMIT);
+        kv = __half2float(__float2half_rn(kv));
+        nk = fmaf(kv, kv, nk);
+      } else if (d == 15) {
+        kv = 1.f;
+        vv = 1.f;
+      }
+    }
+    kt[(d >> 3) * (KT * 8) + (rk >> 3) * 64 + (rk & 7) * 8 + (d & 7)] = __float2half_rn(kv);
+    vt[(rk >> 3) * 128 + (d >> 3) * 64 + (d & 7) * 8 + (rk & 7)] = __float2half_rn(vv);
+  }
+  if (valid) atomicMax(&kmax[fwd * n_head + head], __float_as_uint(sqrtf(nk)));
+  if (big) atomicOr(flag, 2);
+}
+
+// Q in fp16, scaled by log2(e)/sqrt(d_head); column 15 = 15 - b_i.  Flags: 1 = some
+// bound > BOUND_LIMIT (online kernel), 2 = some bound > F16_LIMIT (tf32 kernel).
+__global__ void repack_q16_kernel(const float* __restrict__ q, int64_t ld, int n_head, int d_head,
+                                  int64_t R, const int32_t* __restrict__ row_fwd,
+                                  const unsigned* __restrict__ kmax, float qscale,
+                                  __half* __restrict__ qh, int32_t* __restrict__ flag) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * n_head) return;
+  const int64_t r = idx / n_head;
+  const int head = (int)(idx % n_head);
+  __align__(16) __half qv[16];
+  float nq = 0.f;
+  bool big = false;
+  for (int d = 0; d < 16; ++d) {
+    float x = 0.f;
+    if (d < d_head) {
+      x = q[r * ld + head * d_head + d] * qscale;
+      big |= !(fabsf(x) <= RANGE_LIMIT);
+    }
+    qv[d] = __float2half_rn(x);
+    x = __half2float(qv[d]);
+    nq = fmaf(x, x, nq);
+  }
+  const float km = __uint_as_float(kmax[row_fwd[r] * n_head + head]);
+  const float bnd = sqrtf(nq) * km * (1.f + 1.f / 256.f) + 1.f / 256.f;
+  if (!(bnd <= BOUND_LIMIT)) atomicOr(flag, 1);
+  else if (bnd > F16_LIMIT || big) atomicOr(flag, 2);
+  qv[15] = __float2half_rn(15.f - bnd);
+  uint4* o = reinterpret_cast<uint4*>(qh + ((int64_t)head * R + r) * 16);
+  o[0] = reinterpret_cast<const uint4*>(qv)[0];
+  o[1] = reinterpret_cast<const uint4*>(qv)[1];
+}
+
+}  // namespace t16
+
+void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+                      int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
+                      int64_t num_works, const int64_t* tile_row0_dev, const int32_t* tile_n_dev,
+                      void* qh, void* kb, void* vb, float* out, int64_t ldo,
+                      const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
+                      cudaStream_t st) {
+  static bool attr = false;
+  const size_t smem = sizeof(t16::Smem) + 1024;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(t16::attn_f16_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t total = (int64_t)n_head * Ttot * t16::KT;
+  t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+      k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, static_cast<__half*>(kb),
+      static_cast<__half*>(vb), kmax, flag);
+  LAUNCH_CHECK();
+  t16::repack_q16_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
+      q, ld, n_head, d_head, R, row_fwd, kmax, qscale, static_cast<__half*>(qh), flag);
+  LAUNCH_CHECK();
+  dim3 grid((unsigned)num_works, (unsigned)n_head);
+  t16::attn_f16_kernel<<<grid, t16::NUM_THREADS, smem, st>>>(
+      static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
+      static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
+  LAUNCH_CHECK();
+}
+
+}  // namespace go

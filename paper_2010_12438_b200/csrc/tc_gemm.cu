@@ -156,11 +156,13 @@ struct Args {
   int vec;                                   // C, C2 rows 16-B aligned: float4 stores
 };
 
-template <int BN>
+// MH = number of 128-row M halves per tile (2: each W chunk in shared memory feeds two
+// accumulators, halving the weight bytes pulled from L2 per output row).
+template <int BN, int MH>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KB per hi/lo tile
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // multiple of 1024 (BN % 4 == 0)
+  static constexpr int STAGE = MH * 2 * A_BYTES + 2 * B_BYTES;  // multiple of 1024
   // epilogue staging (4 warps x [32][36]) + bias[256] + ln gamma/beta[128]
   static constexpr int EPI_BYTES = 4 * 32 * 36 * 4 + 512 * 4;
   static constexpr int ALIGN_PAD = 1024;  // the swizzled A tiles need 1024-B alignment
@@ -171,7 +173,9 @@ struct Cfg {
   static_assert(NS >= 2, "tc_gemm needs at least two smem stages");
   static_assert(STAGE % 1024 == 0, "stage must keep 1024-B alignment");
   static constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr uint32_t TALLOC = 2 * TCOLS;  // double-buffered accumulator
+  static constexpr uint32_t ACOLS = MH * TCOLS;   // one accumulator set (all halves)
+  static constexpr uint32_t TALLOC = 2 * ACOLS;   // double-buffered
+  static_assert(TALLOC <= 512, "accumulators exceed TMEM");
   static constexpr size_t SMEM = (size_t)NS * STAGE + EPI_BYTES + 1536 + ALIGN_PAD;
 };
 
@@ -188,11 +192,12 @@ __device__ __forceinline__ float activate(float x) {
 // (tile t -> m tile t / nblk, n block t % nblk).  The smem ring and the two TMEM
 // accumulators carry their phases across tiles, so the loads and MMAs of tile i+1
 // overlap the epilogue of tile i.
-template <int BN, bool LN, int ACT>
+template <int BN, int MH, bool LN, int ACT>
 __global__ void __launch_bounds__(G_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmA2, Args a, int nblk, int ntiles) {
-  using CF = Cfg<BN>;
+  using CF = Cfg<BN, MH>;
+  constexpr int TM = BM * MH;  // rows per tile
   constexpr int NS = CF::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stage_base =
@@ -206,9 +211,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   uint64_t* acc_empty = bars + 3 * NS + 2;  // [2] 128 arrivals: accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto A_hi = [&](int s) { return reinterpret_cast<float*>(stage_base + (size_t)s * CF::STAGE); };
-  auto A_lo = [&](int s) { return A_hi(s) + BM * BK; };
-  auto B_hi = [&](int s) { return A_hi(s) + 2 * BM * BK; };
+  auto A_hi = [&](int s, int h) {
+    return reinterpret_cast<float*>(stage_base + (size_t)s * CF::STAGE + (size_t)h * 2 * CF::A_BYTES);
+  };
+  auto A_lo = [&](int s, int h) { return A_hi(s, h) + BM * BK; };
+  auto B_hi = [&](int s) { return A_hi(s, MH); };
   auto B_lo = [&](int s) { return B_hi(s) + BN * BK; };
   const int nch = a.nch;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -248,12 +255,14 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         const int s = g % NS;
         const int t = blockIdx.x + (g / nch) * gridDim.x;
         const int c = g % nch;
-        const int m0 = (t / nblk) * BM;
+        const int m0 = (t / nblk) * TM;
         const int k0 = c * BK;
         const float* src = a.Bpk + ((size_t)(t % nblk) * nch + c) * 2 * BN * BK;
-        mbar_expect_tx(&full[s], CF::A_BYTES + 2 * CF::B_BYTES);
-        if (k0 < a.K1) tma_2d(A_hi(s), &tmA1, k0, m0, &full[s]);
-        else tma_2d(A_hi(s), &tmA2, k0 - a.K1, m0, &full[s]);
+        mbar_expect_tx(&full[s], MH * CF::A_BYTES + 2 * CF::B_BYTES);
+        for (int h = 0; h < MH; ++h) {
+          if (k0 < a.K1) tma_2d(A_hi(s, h), &tmA1, k0, m0 + h * BM, &full[s]);
+          else tma_2d(A_hi(s, h), &tmA2, k0 - a.K1, m0 + h * BM, &full[s]);
+        }
         bulk_g2s(B_hi(s), src, CF::B_BYTES, &full[s]);
         bulk_g2s(B_lo(s), src + BN * BK, CF::B_BYTES, &full[s]);
       };
@@ -263,24 +272,27 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         const int ab = tl & 1;
         if (tl >= 2) mbar_wait(&acc_empty[ab], ((tl >> 1) - 1) & 1);
         fence_after();
-        const uint32_t tacc = tbase + ab * CF::TCOLS;
+        const uint32_t tacc = tbase + ab * CF::ACOLS;
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = g % NS;
           const uint32_t ph = (g / NS) & 1;
           mbar_wait(&full[s], ph);
           mbar_wait(&a_full[s], ph);
           fence_after();
-          const uint32_t ah = smem_u32(A_hi(s)), al = smem_u32(A_lo(s));
           const uint32_t bh = smem_u32(B_hi(s)), bl = smem_u32(B_lo(s));
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t dah = sdesc_sw128(ah + k * 32);
-            const uint64_t dal = sdesc_sw128(al + k * 32);
             const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
             const uint64_t dbl = sdesc(bl + k * 32 * BN, 16 * BN, 128);
-            umma_ss(tacc, dah, dbh, ID, (c > 0 || k > 0));
-            umma_ss(tacc, dah, dbl, ID, 1);
-            umma_ss(tacc, dal, dbh, ID, 1);
+#pragma unroll
+            for (int h = 0; h < MH; ++h) {
+              const uint64_t dah = sdesc_sw128(smem_u32(A_hi(s, h)) + k * 32);
+              const uint64_t dal = sdesc_sw128(smem_u32(A_lo(s, h)) + k * 32);
+              const uint32_t th = tacc + h * CF::TCOLS;
+              umma_ss(th, dah, dbh, ID, (c > 0 || k > 0));
+              umma_ss(th, dah, dbl, ID, 1);
+              umma_ss(th, dal, dbh, ID, 1);
+            }
           }
           umma_commit(&done[s]);
           if (g >= 1 && (g - 1) + NS < total) {
@@ -300,18 +312,21 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     for (int g = 0; g < total; ++g) {
       const int s = g % NS;
       mbar_wait(&full[s], (g / NS) & 1);
-      float4* hp = reinterpret_cast<float4*>(A_hi(s));
-      float4* lp = reinterpret_cast<float4*>(A_lo(s));
-      float4 x[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = hp[i * 128 + lt];
+      for (int hh = 0; hh < MH; ++hh) {
+        float4* hp = reinterpret_cast<float4*>(A_hi(s, hh));
+        float4* lp = reinterpret_cast<float4*>(A_lo(s, hh));
+        float4 x[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
-        const float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
-                                     tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
-        hp[i * 128 + lt] = h;
-        lp[i * 128 + lt] = l;
+        for (int i = 0; i < 8; ++i) x[i] = hp[i * 128 + lt];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
+          const float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
+                                       tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
+          hp[i * 128 + lt] = h;
+          lp[i * 128 + lt] = l;
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&a_full[s]);
@@ -334,9 +349,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     auto ld4 = [](const float* p) { return *reinterpret_cast<const float4*>(p); };
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int t = blockIdx.x + tl * gridDim.x;
-      const int64_t m0 = (int64_t)(t / nblk) * BM;
+      const int64_t m0 = (int64_t)(t / nblk) * TM;
       const int n0 = (t % nblk) * BN;
-      const int64_t rbase = m0 + ew * 32;
       const int ab = tl & 1;
       epi_bar();  // previous tile's parameter reads are done
       for (int i = et; i < BN; i += 128) {
@@ -349,7 +363,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       epi_bar();
       mbar_wait(&acc_full[ab], (tl >> 1) & 1);
       fence_after();
-      const uint32_t tacc = tbase + ab * CF::TCOLS + lane_off;
+#pragma unroll 1
+      for (int mh = 0; mh < MH; ++mh) {
+      const int64_t rbase = m0 + mh * BM + ew * 32;
+      const uint32_t tacc = tbase + ab * CF::ACOLS + mh * CF::TCOLS + lane_off;
       const int64_t row = rbase + lane;
       const bool rv = row < a.M;
       // y[32] of this thread's row (columns c0..c0+31 of the block) -> C, coalesced
@@ -488,6 +505,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           store32(a.C, a.ldc, c0, y);
         }
       }
+      }  // M halves
       fence_before();
       mbar_arrive(&acc_empty[ab]);
     }
@@ -596,32 +614,51 @@ CUtensorMap a_map(const float* A, int64_t rows, int cols, int64_t ld) {
   return m;
 }
 
-template <int BN, bool LN, int ACT>
+template <int BN, int MH, bool LN, int ACT>
 void launch(const float* A1, int64_t lda1, const float* A2, int64_t lda2, const tg::Args& a,
             int nblk, cudaStream_t st) {
-  using CF = tg::Cfg<BN>;
+  using CF = tg::Cfg<BN, MH>;
   static bool attr = false;
   if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, LN, ACT>,
+    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, MH, LN, ACT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr = true;
   }
   GO_CHECK(a.M < ((int64_t)1 << 31), "too many rows for one GEMM launch");
   const CUtensorMap m1 = a_map(A1, a.M, a.K1, lda1);
   const CUtensorMap m2 = A2 ? a_map(A2, a.M, a.K2, lda2) : m1;
-  const int ntiles = (int)cdiv(a.M, tg::BM) * nblk;
+  const int ntiles = (int)cdiv(a.M, tg::BM * MH) * nblk;
   const int grid = std::min(ntiles, num_sms());
-  tg::tc_gemm_kernel<BN, LN, ACT><<<grid, tg::G_THREADS, CF::SMEM, st>>>(m1, m2, a, nblk, ntiles);
+  tg::tc_gemm_kernel<BN, MH, LN, ACT><<<grid, tg::G_THREADS, CF::SMEM, st>>>(m1, m2, a, nblk,
+                                                                           ntiles);
   LAUNCH_CHECK();
+}
+
+// GO_GEMM_MH=2: two 128-row accumulators per tile sharing each W chunk (half the weight
+// traffic from L2, but only a 2-stage ring: measured 13.7-13.8 ms vs 12.4 ms per 8 cfg4
+// forwards for the default single accumulator)
+static bool two_halves() {
+  const char* e = getenv("GO_GEMM_MH");
+  return e && e[0] == '2';
 }
 
 template <int BN>
 void launch_act(int act, const float* A1, int64_t lda1, const float* A2, int64_t lda2,
                 const tg::Args& a, int nblk, cudaStream_t st) {
+  constexpr bool can2 = BN <= 128;
+  if (can2 && two_halves()) {
+    constexpr int MH = can2 ? 2 : 1;
+    switch (act) {
+      case 1: launch<BN, MH, false, 1>(A1, lda1, A2, lda2, a, nblk, st); break;
+      case 2: launch<BN, MH, false, 2>(A1, lda1, A2, lda2, a, nblk, st); break;
+      default: launch<BN, MH, false, 0>(A1, lda1, A2, lda2, a, nblk, st); break;
+    }
+    return;
+  }
   switch (act) {
-    case 1: launch<BN, false, 1>(A1, lda1, A2, lda2, a, nblk, st); break;
-    case 2: launch<BN, false, 2>(A1, lda1, A2, lda2, a, nblk, st); break;
-    default: launch<BN, false, 0>(A1, lda1, A2, lda2, a, nblk, st); break;
+    case 1: launch<BN, 1, false, 1>(A1, lda1, A2, lda2, a, nblk, st); break;
+    case 2: launch<BN, 1, false, 2>(A1, lda1, A2, lda2, a, nblk, st); break;
+    default: launch<BN, 1, false, 0>(A1, lda1, A2, lda2, a, nblk, st); break;
   }
 }
 
@@ -670,7 +707,8 @@ void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t 
            "LayerNorm residual rows must be 16-B aligned");
   a.vec = (C == nullptr || ((uintptr_t)C % 16 == 0 && ldc % 4 == 0)) &&
           (C2 == nullptr || ((uintptr_t)C2 % 16 == 0 && ldc2 % 4 == 0));
-  launch<128, true, 0>(A1, lda1, A2, lda2, a, 1, st);
+  if (two_halves()) launch<128, 2, true, 0>(A1, lda1, A2, lda2, a, 1, st);
+  else launch<128, 1, true, 0>(A1, lda1, A2, lda2, a, 1, st);
 }
 
 }  // namespace go

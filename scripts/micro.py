@@ -85,6 +85,11 @@ if __name__ == "__main__":
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     if what == "des":
         des(n or 512)
+    elif what == "attn":
+        forward(n or 8, env=[("GO_ATTN", "f16"), ("GO_ATTN", "tf32"), ("GO_ATTN", "f16")])
+    elif what == "mh":
+        forward(n or 8, env=[("GO_GEMM_MH", "2"), ("GO_GEMM_MH", "1"), ("GO_GEMM_MH", "2"),
+                             ("GO_GEMM_BN256", "0")])
     elif what == "bn":
         forward(n or 8, env=[("GO_GEMM_BN256", "1"), ("GO_GEMM_BN256", "0"), ("GO_GEMM_BN256", "1")])
     elif what == "poly":
