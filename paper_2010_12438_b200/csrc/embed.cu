@@ -124,6 +124,10 @@ void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
 // columns, so one load instruction of an 8-lane group reads a full 128-B line; the
 // neighbour indices are fetched once and shuffled, and 4 neighbours x 4 column
 // slices = 16 independent 16-B loads are in flight per lane.
+// SIGMOID: the gathered rows are pre-activations and the output is sigmoid(max) --
+// equal to max(sigmoid) because sigmoid is monotone (embedding.py:90-91), but applied
+// to N pooled rows here instead of inside the producing GEMM's epilogue.
+template <bool SIGMOID>
 __global__ void segment_max128_kernel(const float* __restrict__ t, int64_t ldt,
                                       const int32_t* __restrict__ segoff,
                                       const int32_t* __restrict__ gidx, int64_t R,
@@ -163,6 +167,11 @@ __global__ void segment_max128_kernel(const float* __restrict__ t, int64_t ldt,
     }
   }
   if (!live) return;
+  if (SIGMOID) {
+    auto sg = [](float x) { return 1.f / (1.f + expf(-x)); };
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m[q] = make_float4(sg(m[q].x), sg(m[q].y), sg(m[q].z), sg(m[q].w));
+  }
   float4* o = reinterpret_cast<float4*>(out + r * ldo) + sub;
 #pragma unroll
   for (int q = 0; q < 4; ++q) o[8 * q] = cnt > 0 ? m[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -227,13 +236,18 @@ __global__ void segment_max_kernel(const float* __restrict__ t, int64_t ldt,
 }
 
 void segment_max(const float* t, int64_t ldt, const int32_t* segoff, const int32_t* gidx,
-                 int64_t R, int D, float* out, int64_t ldo, cudaStream_t st, int32_t* argmax) {
+                 int64_t R, int D, float* out, int64_t ldo, cudaStream_t st, int32_t* argmax,
+                 bool sigmoid_of_max) {
   if (R <= 0) return;
   const bool aligned = ((uintptr_t)t % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                        (ldt & 3) == 0 && (ldo & 3) == 0;
-  if (!argmax && D == 128 && aligned) {
-    segment_max128_kernel<<<(unsigned)cdiv(R, 32), 256, 0, st>>>(t, ldt, segoff, gidx, R, out,
-                                                                 ldo);
+  if (sigmoid_of_max) {
+    GO_CHECK(!argmax && D == 128 && aligned, "sigmoid-of-max needs the D=128 fast path");
+    segment_max128_kernel<true><<<(unsigned)cdiv(R, 32), 256, 0, st>>>(t, ldt, segoff, gidx, R,
+                                                                       out, ldo);
+  } else if (!argmax && D == 128 && aligned) {
+    segment_max128_kernel<false><<<(unsigned)cdiv(R, 32), 256, 0, st>>>(t, ldt, segoff, gidx, R,
+                                                                        out, ldo);
   } else {
     segment_max_kernel<<<(unsigned)cdiv(R, 8), 256, 0, st>>>(t, ldt, segoff, gidx, R, D, out,
                                                              ldo, argmax);

@@ -524,7 +524,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
           tc_gemm_packed_floats(dm, di) + tc_gemm_packed_floats(di, dm) +
           tc_gemm_packed_floats(dm, cfg.task_sizes[t]);
   size_t bytes = forward_ws_bytes(cfg, R, m.gtotal, F, m.n_chunks) + (size_t)R * (LQ + 16) * 4 +
-                 pk * 4 + (size_t)(Lt + 2) * 4 * 160 + (4u << 20);
+                 pk * 6 + (size_t)(Lt + 2) * 4 * 160 + (4u << 20);
   Arena A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   float* X[6];
   for (int i = 0; i < 6; ++i) X[i] = A.take<float>(R * LW);
@@ -539,11 +539,24 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
   float* meanb = A.take<float>((int64_t)F * dm);
   float* part = A.take<float>((m.n_chunks + 1) * 128);
   row_fwd_fill(m.d_row_off, F, R, row_fwd, st);
+  // every packed weight gets tf32 and fp16 copies and its own fp16 range flag
+  constexpr int MAX_PACKS = 96;
+  int32_t* ovf_flags = A.take<int32_t>(MAX_PACKS);
+  CUDA_CHECK(cudaMemsetAsync(ovf_flags, 0, MAX_PACKS * sizeof(int32_t), st));
+  int n_packs = 0;
   auto pack = [&](const float* w0, const float* w1, const float* w2, int Nsub, int64_t ldw, int K,
                   int N) {
-    float* out = A.take<float>((int64_t)tc_gemm_packed_floats(K, N));
+    GO_CHECK(n_packs < MAX_PACKS, "too many packed weights");
+    const int64_t nf = (int64_t)tc_gemm_packed_floats(K, N);
+    float* out = A.take<float>(nf);
+    void* out16 = A.take<float>((nf + 1) / 2);
     tc_gemm_pack(w0, w1, w2, Nsub, ldw, K, N, out, st);
-    return out;
+    tc_gemm_pack16(w0, w1, w2, Nsub, ldw, K, N, out16, st);
+    TcW w;
+    w.w32 = out;
+    w.w16 = out16;
+    w.ovf = ovf_flags + n_packs++;
+    return w;
   };
   auto pack1 = [&](const float* w, int K, int N) { return pack(w, nullptr, nullptr, N, N, K, N); };
   auto qkv_bias = [&](const float* bq, const float* bk, const float* bv) {
@@ -574,15 +587,15 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       float* pooled = X[2];
       {
         KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * gs);
+        // pre-activations: the sigmoid is applied to the pooled max instead (monotone)
         tc_gemm(h, gs, gs, nullptr, 0, 0, pack1(W_(S.e_layer(l, 0)), gs, gs), W_(S.e_layer(l, 1)),
-                t, LW, R, gs, 2, st);
+                t, LW, R, gs, 0, st);
       }
       {
         double bytes = (double)(m.gtotal + R) * gs * 4 + (double)m.gtotal * 4 +
                        (double)(R + 1) * 8 + (double)R * 4;
         KTimer kt(ctx, K_SEGMAX, st, bytes);
-        segment_max(t, LW, segoff, gidx, R, gs, pooled, LW,
-                    st);
+        segment_max(t, LW, segoff, gidx, R, gs, pooled, LW, st, nullptr, true);
       }
       bool last = l == Lg - 1;
       float* hn = last ? node_embed : (h == X[0] ? X[3] : X[0]);
@@ -676,9 +689,9 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       tc_v = A.take<float>((int64_t)H * m.n_tiles * 64 * 16);
       tc_scratch = A.take<int32_t>(1 + (int64_t)F * H);
     }
-    const float* ta_qkv = pack(W_(S.ta(Q_W)), W_(S.ta(K_W)), W_(S.ta(V_W)), W, W, dm, 3 * W);
+    const TcW ta_qkv = pack(W_(S.ta(Q_W)), W_(S.ta(K_W)), W_(S.ta(V_W)), W, W, dm, 3 * W);
     const float* ta_b = qkv_bias(W_(S.ta(Q_B)), W_(S.ta(K_B)), W_(S.ta(V_B)));
-    const float* ta_o = pack1(W_(S.ta(O_W)), W, dm);
+    const TcW ta_o = pack1(W_(S.ta(O_W)), W, dm);
     float* a_prev = nullptr;
     int64_t ld_prev = LW;
     float* rep_bufs[2] = {X[4], X[5]};

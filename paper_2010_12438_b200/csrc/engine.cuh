@@ -161,9 +161,10 @@ void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
                      int num_tasks, const int32_t* task_col, const float* in_w,
                      const float* in_b, int D, float* h, int64_t ldh, cudaStream_t st);
 // segoff[R+1]: flat segment bounds into gidx, written by neighbor_sample
+// sigmoid_of_max: t holds pre-activations; out = sigmoid(max) (= max of sigmoid)
 void segment_max(const float* t, int64_t ldt, const int32_t* segoff, const int32_t* gidx,
                  int64_t R, int D, float* out, int64_t ldo, cudaStream_t st,
-                 int32_t* argmax = nullptr);
+                 int32_t* argmax = nullptr, bool sigmoid_of_max = false);
 
 void row_node_fill(const GraphView* views_dev, const int64_t* row_off_dev,
                    const int32_t* row_fwd, int64_t R, int32_t* row_node, cudaStream_t st);
@@ -248,16 +249,25 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b, bo
                     bool need_trunk, bool need_heads, cudaStream_t st, const void* extra = nullptr,
                     size_t extra_bytes = 0, const void** extra_dev = nullptr);
 
-// ---- kernels: tc_gemm.cu (tcgen05 3xTF32 dense layers)
+// ---- kernels: tc_gemm.cu (tcgen05 3-pass split-precision dense layers)
+// Prepacked weight: tf32 hi/lo (w32) and fp16 hi/lo of W * 2^8 (w16, optional) plus the
+// fp16 pass's range flag (ovf, zero-initialised; optional).
+struct TcW {
+  const float* w32 = nullptr;
+  const void* w16 = nullptr;
+  int32_t* ovf = nullptr;
+};
 int tc_gemm_bn(int N);
 size_t tc_gemm_packed_floats(int K, int N);
 void tc_gemm_pack(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw, int K,
                   int N, float* out, cudaStream_t st);
+void tc_gemm_pack16(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw,
+                    int K, int N, void* out, cudaStream_t st);
 void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
-             const float* Wpk, const float* bias, float* C, int64_t ldc, int64_t M, int N,
-             int act, cudaStream_t st);
+             const TcW& W, const float* bias, float* C, int64_t ldc, int64_t M, int N, int act,
+             cudaStream_t st);
 void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
-                const float* Wpk, const float* bias, const float* resid, int64_t ldr,
+                const TcW& W, const float* bias, const float* resid, int64_t ldr,
                 const float* g, const float* beta, float* C, int64_t ldc, const float* rowscale,
                 const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M, int N,
                 cudaStream_t st);

@@ -243,46 +243,75 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 // K and V^T tiles in fp16: K[:,15] = V[:,15] = 1 on valid keys, zero rows past the end;
 // max |k| (of the rounded values) per (forward, head); flags |k|, |v| out of fp16 range.
+// One thread per (head, tile, 8-key group, 8-wide d half): the group is one column of
+// core matrices in both layouts, so every store is a 16-B vector (one per key for K, one
+// per d for V^T); the two d halves of a key sit in adjacent lanes and combine |k|^2.
 __global__ void repack_kv16_kernel(const float* __restrict__ k, const float* __restrict__ v,
                                    int64_t ld, int n_head, int d_head,
                                    const int64_t* __restrict__ tile_fwd_row0,
                                    const int32_t* __restrict__ tile_n, int64_t Ttot,
                                    __half* __restrict__ kb, __half* __restrict__ vb,
                                    unsigned* __restrict__ kmax, int32_t* __restrict__ flag) {
+  constexpr int G = KT / 8;  // 8-key groups per tile
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)n_head * Ttot * KT;
-  if (idx >= total) return;
-  const int head = (int)(idx / (Ttot * KT));
-  const int64_t rem = idx % (Ttot * KT);
-  const int64_t tile = rem / KT;
-  const int rk = (int)(rem % KT);
-  const int local = tile_n[3 * tile + 1] * KT + rk;
-  const bool valid = local < tile_n[3 * tile];
-  const int fwd = tile_n[3 * tile + 2];
-  const int64_t grow = tile_fwd_row0[tile] + local;
+  const int64_t total = (int64_t)n_head * Ttot * G * 2;
+  const bool live = idx < total;
+  const int64_t id = live ? idx : total - 1;
+  const int dh = (int)(id & 1);  // d in [8 dh, 8 dh + 8)
+  const int64_t gi = id >> 1;
+  const int head = (int)(gi / (Ttot * G));
+  const int64_t rem = gi % (Ttot * G);
+  const int64_t tile = rem / G;
+  const int g = (int)(rem % G);
+  const int n = tile_n[3 * tile], fwd = tile_n[3 * tile + 2];
+  const int local0 = tile_n[3 * tile + 1] * KT + g * 8;
+  const int64_t grow0 = tile_fwd_row0[tile] + local0;
   __half* kt = kb + ((int64_t)head * Ttot + tile) * (KT * 16);
   __half* vt = vb + ((int64_t)head * Ttot + tile) * (KT * 16);
-  float nk = 0.f;
+  __align__(16) __half vv[8][8];  // [d - 8 dh][key]
+  float nkmax = 0.f;
   bool big = false;
-  for (int d = 0; d < 16; ++d) {
-    float kv = 0.f, vv = 0.f;
-    if (valid) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const bool valid = local0 + e < n;
+    __align__(16) __half kr[8];
+    float nk = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int d = dh * 8 + i;
+      float kv = 0.f, vx = 0.f;
+      if (valid) {
+        if (d < d_head) {
+          const int64_t o = (grow0 + e) * ld + head * d_head + d;
+          kv = k[o];
+          vx = v[o];
+          big |= !(fabsf(kv) <= RANGE_LIMIT) || !(fabsf(vx) <= RANGE_LIMIT);
+        } else if (d == 15) {
+          kv = 1.f;
+          vx = 1.f;
+        }
+      }
+      kr[i] = __float2half_rn(kv);
+      vv[i][e] = __float2half_rn(vx);
       if (d < d_head) {
-        const int64_t o = grow * ld + head * d_head + d;
-        kv = k[o];
-        vv = v[o];
-        big |= !(fabsf(kv) <= RANGE_LIMIT) || !(fabsf(vv) <= RANGE_LIMIT);
-        kv = __half2float(__float2half_rn(kv));
-        nk = fmaf(kv, kv, nk);
-      } else if (d == 15) {
-        kv = 1.f;
-        vv = 1.f;
+        const float kk = __half2float(kr[i]);
+        nk = fmaf(kk, kk, nk);
       }
     }
-    kt[(d >> 3) * (KT * 8) + (rk >> 3) * 64 + (rk & 7) * 8 + (d & 7)] = __float2half_rn(kv);
-    vt[(rk >> 3) * 128 + (d >> 3) * 64 + (d & 7) * 8 + (rk & 7)] = __float2half_rn(vv);
+    nk += __shfl_xor_sync(0xffffffffu, nk, 1);
+    nkmax = fmaxf(nkmax, nk);
+    // K: element (key, d) at (d>>3)*(KT*8) + (key>>3)*64 + (key&7)*8 + (d&7)
+    if (live)
+      *reinterpret_cast<uint4*>(kt + dh * (KT * 8) + g * 64 + e * 8) =
+          *reinterpret_cast<const uint4*>(kr);
   }
-  if (valid) atomicMax(&kmax[fwd * n_head + head], __float_as_uint(sqrtf(nk)));
+  if (!live) return;
+  // V^T: element (key, d) at (key>>3)*128 + (d>>3)*64 + (d&7)*8 + (key&7)
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    *reinterpret_cast<uint4*>(vt + g * 128 + dh * 64 + i * 8) =
+        *reinterpret_cast<const uint4*>(vv[i]);
+  if (dh == 0 && local0 < n) atomicMax(&kmax[fwd * n_head + head], __float_as_uint(sqrtf(nkmax)));
   if (big) atomicOr(flag, 2);
 }
 
@@ -334,7 +363,7 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t total = (int64_t)n_head * Ttot * t16::KT;
+  const int64_t total = (int64_t)n_head * Ttot * (t16::KT / 8) * 2;
   t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
       k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, static_cast<__half*>(kb),
       static_cast<__half*>(vb), kmax, flag);

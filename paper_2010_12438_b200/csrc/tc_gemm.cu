@@ -18,6 +18,7 @@
 // NS-stage smem ring + double-buffered TMEM accumulator, all handshakes on mbarriers,
 // so TMA, split, MMA and the previous tile's epilogue all overlap.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -91,6 +92,17 @@ __device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+__device__ __forceinline__ void umma_ss_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 // no-swizzle K-major canonical layout (the prepacked B tiles)
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -154,22 +166,33 @@ struct Args {
   float* C2;
   int64_t ldc2;
   int vec;                                   // C, C2 rows 16-B aligned: float4 stores
+  int32_t* ovf;                              // fp16 path: set if some |A| leaves fp16 range
+  const int32_t* gate;                       // tf32 re-run: run only if *gate != 0
 };
+
+// fp16 path: W is prepacked as W * 2^W16_SHIFT so W_lo stays a normal fp16; the
+// epilogue scales the accumulator back by 2^-W16_SHIFT (exact).
+constexpr int W16_SHIFT = 8;
+constexpr float A16_LIMIT = 32768.f;  // |A| above this re-runs the GEMM in tf32
 
 // MH = number of 128-row M halves per tile (2: each W chunk in shared memory feeds two
 // accumulators, halving the weight bytes pulled from L2 per output row).
-template <int BN, int MH>
+// H: fp16 operands (kind::f16, K=16 per MMA).  The A slot then holds the raw fp32 TMA
+// chunk, which the split warps overwrite with its fp16 hi (first 8 KB) and lo halves.
+template <int BN, int MH, bool H = false>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB per hi/lo tile
-  static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE = MH * 2 * A_BYTES + 2 * B_BYTES;  // multiple of 1024
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB: one fp32 (or tf32 hi / lo) tile
+  static constexpr int A_SLOT = H ? A_BYTES : 2 * A_BYTES;
+  static constexpr int B_BYTES = BN * BK * (H ? 2 : 4);  // one of W_hi / W_lo
+  static constexpr int STAGE = MH * A_SLOT + 2 * B_BYTES;  // multiple of 1024
   // epilogue staging (4 warps x [32][36]) + bias[256] + ln gamma/beta[128]
   static constexpr int EPI_BYTES = 4 * 32 * 36 * 4 + 512 * 4;
   static constexpr int ALIGN_PAD = 1024;  // the swizzled A tiles need 1024-B alignment
   // 227 KB opt-in limit minus staging, barriers and alignment; >= 2 stages or the refill
   // schedule (stage of chunk g-1 refilled after chunk g is issued) cannot progress
   static constexpr int BUDGET = 232448 - EPI_BYTES - 1536 - ALIGN_PAD;
-  static constexpr int NS = (BUDGET / STAGE) < 4 ? (BUDGET / STAGE) : 4;
+  static constexpr int NSMAX = H ? 6 : 4;
+  static constexpr int NS = (BUDGET / STAGE) < NSMAX ? (BUDGET / STAGE) : NSMAX;
   static_assert(NS >= 2, "tc_gemm needs at least two smem stages");
   static_assert(STAGE % 1024 == 0, "stage must keep 1024-B alignment");
   static constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
@@ -192,11 +215,13 @@ __device__ __forceinline__ float activate(float x) {
 // (tile t -> m tile t / nblk, n block t % nblk).  The smem ring and the two TMEM
 // accumulators carry their phases across tiles, so the loads and MMAs of tile i+1
 // overlap the epilogue of tile i.
-template <int BN, int MH, bool LN, int ACT>
+template <int BN, int MH, bool LN, int ACT, bool H>
 __global__ void __launch_bounds__(G_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmA2, Args a, int nblk, int ntiles) {
-  using CF = Cfg<BN, MH>;
+  static_assert(!H || MH == 1, "fp16 path uses one accumulator per tile");
+  using CF = Cfg<BN, MH, H>;
+  if (a.gate && *a.gate == 0) return;  // tf32 re-run not needed
   constexpr int TM = BM * MH;  // rows per tile
   constexpr int NS = CF::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -212,11 +237,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto A_hi = [&](int s, int h) {
-    return reinterpret_cast<float*>(stage_base + (size_t)s * CF::STAGE + (size_t)h * 2 * CF::A_BYTES);
+    return reinterpret_cast<float*>(stage_base + (size_t)s * CF::STAGE + (size_t)h * CF::A_SLOT);
   };
-  auto A_lo = [&](int s, int h) { return A_hi(s, h) + BM * BK; };
-  auto B_hi = [&](int s) { return A_hi(s, MH); };
-  auto B_lo = [&](int s) { return B_hi(s) + BN * BK; };
+  auto A_lo = [&](int s, int h) { return A_hi(s, h) + BM * BK; };  // tf32 path only
+  auto B_hi = [&](int s) {
+    return reinterpret_cast<uint8_t*>(stage_base + (size_t)s * CF::STAGE + (size_t)MH * CF::A_SLOT);
+  };
+  auto B_lo = [&](int s) { return B_hi(s) + CF::B_BYTES; };
   const int nch = a.nch;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -249,7 +276,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   if (warp == 8) {
     // ------------------------------------------------ TMA producer + MMA issuer
     if (lane == 0) {
-      constexpr uint32_t ID = idesc_tf32(BM, BN);
+      constexpr uint32_t ID = H ? idesc_f16(BM, BN) : idesc_tf32(BM, BN);
       const int total = my_tiles * nch;
       auto load = [&](int g) {
         const int s = g % NS;
@@ -257,14 +284,15 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         const int c = g % nch;
         const int m0 = (t / nblk) * TM;
         const int k0 = c * BK;
-        const float* src = a.Bpk + ((size_t)(t % nblk) * nch + c) * 2 * BN * BK;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.Bpk) +
+                             ((size_t)(t % nblk) * nch + c) * 2 * CF::B_BYTES;
         mbar_expect_tx(&full[s], MH * CF::A_BYTES + 2 * CF::B_BYTES);
         for (int h = 0; h < MH; ++h) {
           if (k0 < a.K1) tma_2d(A_hi(s, h), &tmA1, k0, m0 + h * BM, &full[s]);
           else tma_2d(A_hi(s, h), &tmA2, k0 - a.K1, m0 + h * BM, &full[s]);
         }
         bulk_g2s(B_hi(s), src, CF::B_BYTES, &full[s]);
-        bulk_g2s(B_lo(s), src + BN * BK, CF::B_BYTES, &full[s]);
+        bulk_g2s(B_lo(s), src + CF::B_BYTES, CF::B_BYTES, &full[s]);
       };
       for (int g = 0; g < NS && g < total; ++g) load(g);
       int g = 0;
@@ -280,6 +308,20 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           mbar_wait(&a_full[s], ph);
           fence_after();
           const uint32_t bh = smem_u32(B_hi(s)), bl = smem_u32(B_lo(s));
+          if constexpr (H) {
+            // fp16 hi at +0, lo at +8 KB; 8-half K chunks 2 KB apart (A) / BN*16 B (B)
+            const uint32_t a16 = smem_u32(A_hi(s, 0));
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t dah = sdesc(a16 + kk * 4096, 2048, 128);
+              const uint64_t dal = sdesc(a16 + 8192 + kk * 4096, 2048, 128);
+              const uint64_t dbh = sdesc(bh + kk * 2 * BN * 16, BN * 16, 128);
+              const uint64_t dbl = sdesc(bl + kk * 2 * BN * 16, BN * 16, 128);
+              umma_ss_f16(tacc, dah, dbh, ID, (c > 0 || kk > 0));
+              umma_ss_f16(tacc, dah, dbl, ID, 1);
+              umma_ss_f16(tacc, dal, dbh, ID, 1);
+            }
+          } else {
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
@@ -293,6 +335,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
               umma_ss(th, dah, dbl, ID, 1);
               umma_ss(th, dal, dbh, ID, 1);
             }
+          }
           }
           umma_commit(&done[s]);
           if (g >= 1 && (g - 1) + NS < total) {
@@ -312,6 +355,39 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     for (int g = 0; g < total; ++g) {
       const int s = g % NS;
       mbar_wait(&full[s], (g / NS) & 1);
+      if constexpr (H) {
+        // thread = one A row: read its 128-B swizzled fp32 row, then (after all rows are
+        // in registers) write fp16 hi / lo in the no-swizzle K-major canonical layout
+        const float4* rp = reinterpret_cast<const float4*>(A_hi(s, 0)) + lt * 8;
+        float4 x[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = rp[c ^ (lt & 7)];
+        bool big = false;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          big |= !(fabsf(x[c].x) <= A16_LIMIT) || !(fabsf(x[c].y) <= A16_LIMIT) ||
+                 !(fabsf(x[c].z) <= A16_LIMIT) || !(fabsf(x[c].w) <= A16_LIMIT);
+        if (big) atomicOr(a.ovf, 1);
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // raw reads done before overwrite
+        __half* a16 = reinterpret_cast<__half*>(A_hi(s, 0));
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          const float v[8] = {x[2 * kc].x,     x[2 * kc].y,     x[2 * kc].z,     x[2 * kc].w,
+                              x[2 * kc + 1].x, x[2 * kc + 1].y, x[2 * kc + 1].z, x[2 * kc + 1].w};
+          __align__(16) __half hi[8], lo[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            hi[e] = __float2half_rn(v[e]);
+            lo[e] = __float2half_rn(v[e] - __half2float(hi[e]));
+          }
+          const int off = kc * (BM * 8) + lt * 8;  // (r>>3)*64 + (r&7)*8 == r*8
+          *reinterpret_cast<uint4*>(a16 + off) = *reinterpret_cast<const uint4*>(hi);
+          *reinterpret_cast<uint4*>(a16 + 4096 + off) = *reinterpret_cast<const uint4*>(lo);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&a_full[s]);
+        continue;
+      }
 #pragma unroll
       for (int hh = 0; hh < MH; ++hh) {
         float4* hp = reinterpret_cast<float4*>(A_hi(s, hh));
@@ -337,6 +413,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     // transposed through a padded smem tile (row stride 36 floats: conflict-free
     // STS.128 / LDS.128) so every global load/store is a float4 and each warp
     // instruction touches 4 full 128-B lines.
+    constexpr float ASCALE = H ? 1.f / (1 << W16_SHIFT) : 1.f;  // undo the W prescale
     const int ew = warp - 4;                 // TMEM lane quarter
     const int et = threadIdx.x - 128;        // 0..127
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
@@ -430,7 +507,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int j = 4 * q + e;
-              float x = __uint_as_float(u[j]) + bb[e];
+              float x = __uint_as_float(u[j]) * ASCALE + bb[e];
               if (a.resid) x += rr[j];
               s += x;
               u[j] = __float_as_uint(x);
@@ -499,7 +576,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int j = 4 * q4 + e;
-              y[j] = activate<ACT>(__uint_as_float(u[j]) + bb[e]);
+              y[j] = activate<ACT>(__uint_as_float(u[j]) * ASCALE + bb[e]);
             }
           }
           store32(a.C, a.ldc, c0, y);
@@ -548,6 +625,35 @@ __global__ void pack_b_kernel(const float* __restrict__ W0, const float* __restr
   dst[BN * BK + off] = l;
 }
 
+// fp16 twin of pack_b_kernel: W * 2^W16_SHIFT split into fp16 hi / lo, element (n, k)
+// of a block at (k/8)*(BN*8) + (n/8)*64 + (n%8)*8 + k%8 (no-swizzle K-major, 8 halfs/16 B).
+__global__ void pack_b16_kernel(const float* __restrict__ W0, const float* __restrict__ W1,
+                                const float* __restrict__ W2, int Nsub, int64_t ldw, int K,
+                                int N, int BN, int nch, int nblk, __half* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)nblk * nch * BN * BK;
+  if (i >= total) return;
+  int64_t per_blk = (int64_t)nch * BN * BK;
+  int b = (int)(i / per_blk);
+  int64_t rem = i % per_blk;
+  int c = (int)(rem / (BN * BK));
+  int e = (int)(rem % (BN * BK));
+  int n_l = e / BK, k_l = e % BK;
+  int n = b * BN + n_l, k = c * BK + k_l;
+  float w = 0.f;
+  if (n < N && k < K) {
+    const int part = n / Nsub, nn = n % Nsub;
+    const float* W = part == 0 ? W0 : (part == 1 ? W1 : W2);
+    w = W[(int64_t)k * ldw + nn] * (float)(1 << W16_SHIFT);
+  }
+  const __half h = __float2half_rn(w);
+  const __half l = __float2half_rn(w - __half2float(h));
+  int off = (k_l >> 3) * (BN * 8) + (n_l >> 3) * 64 + (n_l & 7) * 8 + (k_l & 7);
+  __half* dst = out + ((int64_t)b * nch + c) * 2 * BN * BK;
+  dst[off] = h;
+  dst[BN * BK + off] = l;
+}
+
 }  // namespace tg
 
 int tc_gemm_bn(int N) {
@@ -568,6 +674,18 @@ size_t tc_gemm_packed_floats(int K, int N) {
   int nblk = (int)cdiv(N, BN);
   int nch = (int)cdiv(K, tg::BK);
   return (size_t)nblk * nch * 2 * BN * tg::BK;
+}
+
+// fp16 twin (W scaled by 2^W16_SHIFT): same element count, 2 bytes each.
+void tc_gemm_pack16(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw,
+                    int K, int N, void* out, cudaStream_t st) {
+  int BN = tc_gemm_bn(N);
+  int nblk = (int)cdiv(N, BN);
+  int nch = (int)cdiv(K, tg::BK);
+  int64_t total = (int64_t)nblk * nch * BN * tg::BK;
+  tg::pack_b16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+      W0, W1 ? W1 : W0, W2 ? W2 : W0, Nsub, ldw, K, N, BN, nch, nblk, static_cast<__half*>(out));
+  LAUNCH_CHECK();
 }
 
 // Pack W = [W0 | W1 | W2] (each [K, Nsub] row-major with ldw; N = parts * Nsub).
@@ -614,51 +732,66 @@ CUtensorMap a_map(const float* A, int64_t rows, int cols, int64_t ld) {
   return m;
 }
 
-template <int BN, int MH, bool LN, int ACT>
-void launch(const float* A1, int64_t lda1, const float* A2, int64_t lda2, const tg::Args& a,
-            int nblk, cudaStream_t st) {
-  using CF = tg::Cfg<BN, MH>;
+template <int BN, int MH, bool LN, int ACT, bool H>
+void launch(const CUtensorMap& m1, const CUtensorMap& m2, const tg::Args& a, int nblk,
+            cudaStream_t st) {
+  using CF = tg::Cfg<BN, MH, H>;
   static bool attr = false;
   if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, MH, LN, ACT>,
+    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, MH, LN, ACT, H>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr = true;
   }
-  GO_CHECK(a.M < ((int64_t)1 << 31), "too many rows for one GEMM launch");
-  const CUtensorMap m1 = a_map(A1, a.M, a.K1, lda1);
-  const CUtensorMap m2 = A2 ? a_map(A2, a.M, a.K2, lda2) : m1;
   const int ntiles = (int)cdiv(a.M, tg::BM * MH) * nblk;
   const int grid = std::min(ntiles, num_sms());
-  tg::tc_gemm_kernel<BN, MH, LN, ACT><<<grid, tg::G_THREADS, CF::SMEM, st>>>(m1, m2, a, nblk,
-                                                                           ntiles);
+  tg::tc_gemm_kernel<BN, MH, LN, ACT, H><<<grid, tg::G_THREADS, CF::SMEM, st>>>(m1, m2, a, nblk,
+                                                                              ntiles);
   LAUNCH_CHECK();
 }
 
 // GO_GEMM_MH=2: two 128-row accumulators per tile sharing each W chunk (half the weight
 // traffic from L2, but only a 2-stage ring: measured 13.7-13.8 ms vs 12.4 ms per 8 cfg4
-// forwards for the default single accumulator)
+// forwards for the default single accumulator; tf32 path only)
 static bool two_halves() {
   const char* e = getenv("GO_GEMM_MH");
   return e && e[0] == '2';
 }
+// GO_GEMM_F16=0 keeps the tf32 operands
+static bool use_f16() {
+  const char* e = getenv("GO_GEMM_F16");
+  return !(e && e[0] == '0');
+}
+
+// fp16-operand GEMM, then the tf32 GEMM gated on the fp16 pass's range flag (a no-op
+// launch unless some |A| left the fp16 range); or the tf32 GEMM alone.
+template <int BN, bool LN, int ACT>
+void launch_all(const float* A1, int64_t lda1, const float* A2, int64_t lda2, tg::Args a,
+                const TcW& W, int nblk, cudaStream_t st) {
+  GO_CHECK(a.M < ((int64_t)1 << 31), "too many rows for one GEMM launch");
+  const CUtensorMap m1 = a_map(A1, a.M, a.K1, lda1);
+  const CUtensorMap m2 = A2 ? a_map(A2, a.M, a.K2, lda2) : m1;
+  constexpr bool can2 = BN <= 128;
+  const bool f16 = W.w16 && W.ovf && use_f16();
+  if (f16) {
+    tg::Args a16 = a;
+    a16.Bpk = static_cast<const float*>(W.w16);
+    a16.ovf = W.ovf;
+    a16.gate = nullptr;
+    launch<BN, 1, LN, ACT, true>(m1, m2, a16, nblk, st);
+    a.gate = W.ovf;
+  }
+  a.Bpk = W.w32;
+  if (can2 && !f16 && two_halves()) launch<BN, can2 ? 2 : 1, LN, ACT, false>(m1, m2, a, nblk, st);
+  else launch<BN, 1, LN, ACT, false>(m1, m2, a, nblk, st);
+}
 
 template <int BN>
 void launch_act(int act, const float* A1, int64_t lda1, const float* A2, int64_t lda2,
-                const tg::Args& a, int nblk, cudaStream_t st) {
-  constexpr bool can2 = BN <= 128;
-  if (can2 && two_halves()) {
-    constexpr int MH = can2 ? 2 : 1;
-    switch (act) {
-      case 1: launch<BN, MH, false, 1>(A1, lda1, A2, lda2, a, nblk, st); break;
-      case 2: launch<BN, MH, false, 2>(A1, lda1, A2, lda2, a, nblk, st); break;
-      default: launch<BN, MH, false, 0>(A1, lda1, A2, lda2, a, nblk, st); break;
-    }
-    return;
-  }
+                const tg::Args& a, const TcW& W, int nblk, cudaStream_t st) {
   switch (act) {
-    case 1: launch<BN, 1, false, 1>(A1, lda1, A2, lda2, a, nblk, st); break;
-    case 2: launch<BN, 1, false, 2>(A1, lda1, A2, lda2, a, nblk, st); break;
-    default: launch<BN, 1, false, 0>(A1, lda1, A2, lda2, a, nblk, st); break;
+    case 1: launch_all<BN, false, 1>(A1, lda1, A2, lda2, a, W, nblk, st); break;
+    case 2: launch_all<BN, false, 2>(A1, lda1, A2, lda2, a, W, nblk, st); break;
+    default: launch_all<BN, false, 0>(A1, lda1, A2, lda2, a, W, nblk, st); break;
   }
 }
 
@@ -666,31 +799,31 @@ void launch_act(int act, const float* A1, int64_t lda1, const float* A2, int64_t
 
 // C = act([A1|A2] @ W + bias) with W prepacked by tc_gemm_pack(K1+K2, N).
 void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
-             const float* Wpk, const float* bias, float* C, int64_t ldc, int64_t M, int N,
+             const TcW& Wpk, const float* bias, float* C, int64_t ldc, int64_t M, int N,
              int act, cudaStream_t st) {
   if (M <= 0) return;
   GO_CHECK(A2 == nullptr || K1 % tg::BK == 0, "concat split must be a multiple of 32");
   tg::Args a{};
   a.K1 = K1; a.K2 = A2 ? K2 : 0;
-  a.Bpk = Wpk; a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
+  a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
   a.nch = (int)cdiv(K1 + a.K2, tg::BK);
   a.vec = ((uintptr_t)C % 16 == 0) && ldc % 4 == 0;
   int BN = tc_gemm_bn(N);
   int nblk = (int)cdiv(N, BN);
   switch (BN) {
-    case 16: launch_act<16>(act, A1, lda1, A2, lda2, a, nblk, st); break;
-    case 32: launch_act<32>(act, A1, lda1, A2, lda2, a, nblk, st); break;
-    case 48: launch_act<48>(act, A1, lda1, A2, lda2, a, nblk, st); break;
-    case 64: launch_act<64>(act, A1, lda1, A2, lda2, a, nblk, st); break;
-    case 128: launch_act<128>(act, A1, lda1, A2, lda2, a, nblk, st); break;
-    case 144: launch_act<144>(act, A1, lda1, A2, lda2, a, nblk, st); break;
-    default: launch_act<256>(act, A1, lda1, A2, lda2, a, nblk, st); break;
+    case 16: launch_act<16>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+    case 32: launch_act<32>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+    case 48: launch_act<48>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+    case 64: launch_act<64>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+    case 128: launch_act<128>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+    case 144: launch_act<144>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+    default: launch_act<256>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
   }
 }
 
 // C = LN(resid + [A1|A2] @ W + bias) * g + b  (N == 128); optional C2 = C * rowscale[f].
 void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
-                const float* Wpk, const float* bias, const float* resid, int64_t ldr,
+                const TcW& Wpk, const float* bias, const float* resid, int64_t ldr,
                 const float* g, const float* beta, float* C, int64_t ldc, const float* rowscale,
                 const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M, int N,
                 cudaStream_t st) {
@@ -699,7 +832,7 @@ void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t 
   GO_CHECK(A2 == nullptr || K1 % tg::BK == 0, "concat split must be a multiple of 32");
   tg::Args a{};
   a.K1 = K1; a.K2 = A2 ? K2 : 0;
-  a.Bpk = Wpk; a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
+  a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
   a.nch = (int)cdiv(K1 + a.K2, tg::BK);
   a.resid = resid; a.ldr = ldr; a.ln_g = g; a.ln_b = beta;
   a.rowscale = rowscale; a.row_fwd = row_fwd; a.C2 = C2; a.ldc2 = ldc2;
@@ -707,8 +840,7 @@ void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t 
            "LayerNorm residual rows must be 16-B aligned");
   a.vec = (C == nullptr || ((uintptr_t)C % 16 == 0 && ldc % 4 == 0)) &&
           (C2 == nullptr || ((uintptr_t)C2 % 16 == 0 && ldc2 % 4 == 0));
-  if (two_halves()) launch<128, 2, true, 0>(A1, lda1, A2, lda2, a, 1, st);
-  else launch<128, 1, true, 0>(A1, lda1, A2, lda2, a, 1, st);
+  launch_all<128, true, 0>(A1, lda1, A2, lda2, a, Wpk, 1, st);
 }
 
 }  // namespace go

@@ -52,10 +52,12 @@ def _heads_with(mode, hid, store, pcfg, tasks):
             os.environ["GO_ATTN"] = old
 
 
-@pytest.mark.parametrize("mode", ["tc", "online"])
+@pytest.mark.parametrize("mode", ["tc", "tf32", "online"])
 def test_tc_vs_simt_full_size_80k(mode):
-    """tc = fixed-offset tcgen05 kernel (default), online = online-softmax tcgen05
-    kernel (taken when a score bound is too large), simt = fp32 CUDA-core kernel."""
+    """tc = fixed-offset tcgen05 kernel with fp16 operands (default), tf32 = the same
+    kernel in kind::tf32 (taken when a score bound exceeds the fp16-exact range),
+    online = online-softmax tcgen05 kernel (taken when a bound is too large for a fixed
+    offset), simt = fp32 CUDA-core kernel."""
     from paper_2010_12438_b200.policy import ordered_tasks
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes)
@@ -87,6 +89,25 @@ def test_large_scores_take_online_kernel():
     out = task_heads(hid, store, pcfg, tasks)
     lg, _, _ = of.task_heads(hid, _oracle_P(store), of.PolicyCfg(), tasks)
     assert rel_err(out.logits["placement"].data, lg["placement"]) < 2e-3
+
+
+def test_medium_scores_take_tf32_kernel():
+    """Weights scaled so the score bounds land between the fp16 limit (14) and the
+    fixed-offset limit (60): the launch must flag over to the tf32 fixed-offset kernel
+    and still match the oracle (tolerance scaled with the ~9x larger scores)."""
+    from oracle import forward as of
+    from paper_2010_12438_b200.policy import ordered_tasks, task_heads
+    sizes = {"placement": 4}
+    ecfg, pcfg, store = _store(sizes)
+    for nm in ("policy/task_attn/q_w", "policy/task_attn/k_w"):
+        store[nm].data = store[nm].data * 3.0
+    store.touch()
+    rng = np.random.default_rng(4)
+    hid = rng.normal(size=(900, pcfg.d_model))
+    tasks = ordered_tasks(sizes)
+    out = task_heads(hid, store, pcfg, tasks)
+    lg, _, _ = of.task_heads(hid, _oracle_P(store), of.PolicyCfg(), tasks)
+    assert rel_err(out.logits["placement"].data, lg["placement"]) < 5e-4
 
 
 def test_ragged_batch_matches_single_forwards():
