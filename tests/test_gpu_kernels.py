@@ -210,3 +210,27 @@ def test_trunk_tc_matches_simt(seg):
     # single-pass tf32 Q.K^T and P.V (as in the task-head kernel): ~4e-5 normwise
     assert rel_err(h_tc, h_s) < 1e-4
     assert rel_err(lg_tc, lg_s) < 1e-4
+
+
+def test_fp16_gemm_matches_tf32_and_reruns_out_of_range():
+    """The fp16-operand GEMMs (default) agree with the tf32-operand GEMMs
+    (GO_GEMM_F16=0); with embedding weights scaled so activations exceed the fp16
+    range, the fp16 pass flags itself and the tf32 re-run produces the same result."""
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    sizes = {"placement": 8}
+    ecfg, pcfg, store = _store(sizes)
+    graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 200, 1, 64, seed=4), node_cap=10**6)]
+    seeds = [9]
+    for scale in (1.0, 3e4):
+        if scale != 1.0:
+            store["embed/in_w"].data = store["embed/in_w"].data * scale
+            store.touch()
+        h16, lg16 = _forward_env("GO_GEMM_F16", None, store, ecfg, pcfg, sizes, graphs, seeds)
+        h32, lg32 = _forward_env("GO_GEMM_F16", "0", store, ecfg, pcfg, sizes, graphs, seeds)
+        assert np.isfinite(lg16).all()
+        # at 3e4 the embedding is ~1e5 in magnitude and the trunk's LayerNorms amplify the
+        # (equal-size, differently rounded) 3-pass errors of both paths; without the
+        # re-run the fp16 pass would overflow to inf
+        tol = 1e-5 if scale == 1.0 else 1e-4
+        assert rel_err(h16, h32) < tol, scale
+        assert rel_err(lg16, lg32) < tol, scale
