@@ -18,7 +18,9 @@ __global__ void __launch_bounds__(ATT_Q) attn_kernel(const float* __restrict__ q
                                                      int d_head, const AttnTile* __restrict__ tiles,
                                                      float* __restrict__ out, int64_t ldo,
                                                      float scale_log2,
-                                                     float* __restrict__ lse, int n_head) {
+                                                     float* __restrict__ lse, int n_head,
+                                                     const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ __align__(16) float Ks[ATT_KC][DH];
   __shared__ __align__(16) float Vs[ATT_KC][DH];
   const AttnTile tl = tiles[blockIdx.x];
@@ -78,13 +80,13 @@ __global__ void __launch_bounds__(ATT_Q) attn_kernel(const float* __restrict__ q
 
 void attention(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
-               int64_t ldo, cudaStream_t st, float* lse) {
+               int64_t ldo, cudaStream_t st, float* lse, const int32_t* gate) {
   if (num_tiles <= 0) return;
   float scale_log2 = (float)(1.4426950408889634 / sqrt((double)d_head));
   dim3 grid((unsigned)num_tiles, (unsigned)n_head);
 #define GO_ATT(DHV)                                                                          \
   attn_kernel<DHV><<<grid, ATT_Q, 0, st>>>(q, k, v, ld, d_head, tiles_dev, out, ldo,           \
-                                           scale_log2, lse, n_head)
+                                           scale_log2, lse, n_head, gate)
   if (d_head <= 4) GO_ATT(4);
   else if (d_head <= 8) GO_ATT(8);
   else if (d_head <= 16) GO_ATT(16);

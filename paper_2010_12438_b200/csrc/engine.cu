@@ -624,10 +624,15 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       modp = mod;
     }
     float* x0 = Lt == 0 ? hid : X[0];
-    // GO_TRUNK=tc selects the tcgen05 segmented attention (measured 0.66 ms/forward vs
-    // 0.41 ms for the SIMT banded kernel at cfg4, so SIMT stays the default)
+    // GO_TRUNK=tc: tcgen05 segmented attention (fp16 operands; the SIMT kernel re-runs a
+    // layer whose operands left the fp16 range).  Measured 0.61-0.66 ms/forward at cfg4
+    // against 0.41 ms for the SIMT banded kernel (2 CTAs/SM by TMEM, latency-bound
+    // staging), so SIMT stays the default.
     const char* trunk_env = getenv("GO_TRUNK");
-    const bool trunk_tc = m.trunk_tc_ok && dh <= 15 && trunk_env && !strcmp(trunk_env, "tc");
+    const bool trunk_tc = m.trunk_tc_ok && trunk_tc_supported(H, dh) && trunk_env &&
+                          !strcmp(trunk_env, "tc");
+    int32_t* trunk_flags = A.take<int32_t>(Lt + 1);
+    if (trunk_tc) CUDA_CHECK(cudaMemsetAsync(trunk_flags, 0, (Lt + 1) * sizeof(int32_t), st));
     {
       KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * dm);
       tc_gemm(node_embed, gs, gs, nullptr, 0, 0, pack1(W_(S.p_in_w()), gs, dm), W_(S.p_in_b()), x0,
@@ -645,12 +650,15 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       }
       {
         KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
-        if (trunk_tc)
-          trunk_attention_tc(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, cfg.segment_len,
-                             m.d_trunk_tc, m.n_trunk_tc, Ab, LA, st);
-        else
+        if (trunk_tc) {
+          trunk_attention_tc(QKV, LQ, H, dh, cfg.segment_len, m.d_trunk_tc, m.n_trunk_tc, Ab, LA,
+                             trunk_flags + l, st);
+          attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
+                    LA, st, nullptr, trunk_flags + l);
+        } else {
           attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
                     LA, st);
+        }
       }
       float* h1 = X[2];
       {

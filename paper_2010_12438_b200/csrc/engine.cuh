@@ -173,9 +173,11 @@ void row_node_fill(const GraphView* views_dev, const int64_t* row_off_dev,
 struct AttnTile {
   int64_t q0, q1, k0, k1;
 };
+// gate (optional): run only if *gate != 0 (the re-run behind the tensor-core trunk kernel)
 void attention(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
-               int64_t ldo, cudaStream_t st, float* lse = nullptr);
+               int64_t ldo, cudaStream_t st, float* lse = nullptr,
+               const int32_t* gate = nullptr);
 
 // ---- kernels: tc_attention16.cu (fp16 operands, fixed-offset softmax; flags the launch
 // over to the tf32 / online kernels when a bound exceeds the fp16-exact range)
@@ -188,7 +190,7 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                       cudaStream_t st);
 
 // ---- kernels: tc_trunk.cu (tcgen05 / TMEM segmented trunk attention, d_head <= 15)
-constexpr int TRUNK_TC_MAX_KEYS = 240;
+constexpr int TRUNK_TC_MAX_KEYS = 192;
 struct TrunkTile {
   int64_t q0, k0, f0, f1;  // first query row, first key row, forward rows [f0, f1)
   int32_t nq, nk;
@@ -197,9 +199,12 @@ struct TrunkTile {
 // window exceeds TRUNK_TC_MAX_KEYS (segment_len too large for the TMEM budget)
 bool trunk_tc_build_tiles(const std::vector<int64_t>& row_off, int64_t S,
                           std::vector<TrunkTile>& out);
-void trunk_attention_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
-                        int d_head, int S, const TrunkTile* tiles_dev, int64_t num_tiles,
-                        float* out, int64_t ldo, cudaStream_t st);
+bool trunk_tc_supported(int n_head, int d_head);
+// qkv rows hold [Q | K | V] (each n_head * d_head wide); flag (zeroed) is set if some
+// operand left the fp16 range -- the caller then re-runs attention() gated on it
+void trunk_attention_tc(const float* qkv, int64_t ld, int n_head, int d_head, int S,
+                        const TrunkTile* tiles_dev, int64_t num_tiles, float* out, int64_t ldo,
+                        int32_t* flag, cudaStream_t st);
 
 // ---- kernels: tc_attention.cu (tcgen05 / TMEM full attention, d_head <= 16)
 struct TcWork {
