@@ -391,9 +391,9 @@ def main():
         exps = hflops / 4.0 / HEAD_W * N_HEAD
         exp_rate = exps / (hms / 1000.0) / 1e9
         roof = {"bound": "tensor", "binding_unit": "MUFU ex2 (softmax exponentials)",
-                "kernel": "task-head N x N attention, tcgen05 kind::tf32 + TMEM (attn_tc_fixed_kernel)",
+                "kernel": "task-head N x N attention, tcgen05 kind::f16 + TMEM, fixed-offset softmax (attn_f16_kernel)",
                 "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
-                "traffic": ncu.get("attn_tc_fixed_bytes_per_forward"),
+                "traffic": ncu.get("heads_attention_bytes_per_forward"),
                 "traffic_note": "dram read+write per forward (one launch = one wave of forwards), "
                                 "ncu --set full, profiles/r1_ncu_summary.json",
                 "launches": cnt, "avg_launch_ms": hms / cnt,

@@ -169,33 +169,83 @@ void fuse_groups(int32_t n, int64_t e, const int32_t* src, const int32_t* dst,
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return pri[a] != pri[b] ? pri[a] > pri[b] : a < b; });
   std::vector<char> visited(n, 0);
-  std::vector<int32_t> stack;
-  std::vector<int32_t> seen_mark(n, -1);
+  // Exact, windowed cycle check.  The group graph stays a DAG, and the two candidate
+  // groups are joined by an edge a -> b, so b ~> a is impossible and only a path
+  // a ~> b through a third group can close a cycle (the reference's two DFS runs
+  // return the same answer).  A topological order of the *group* graph is maintained
+  // (pos / at): every group on such a path lies strictly between pos[a] and pos[b], so
+  // the search is confined to that window instead of all of a's descendants.  After a
+  // merge the window is re-laid out as [groups not reachable from a] [a+b] [groups
+  // reachable from a], which is again a valid order.  Cost per attempt: O(window).
+  const std::vector<int32_t> topo = topo_order(n, e, src, dst);
+  std::vector<int32_t> pos(n), at(n);
+  for (int i = 0; i < n; ++i) {
+    at[i] = topo[i];
+    pos[topo[i]] = i;
+  }
+  std::vector<int32_t> stack, nonf, fw;
+  std::vector<int32_t> mark(n, -1);
   int stamp = 0;
-  auto cycle = [&](int a, int b) {
-    for (int pass = 0; pass < 2; ++pass) {
-      int x = pass ? b : a, y = pass ? a : b;
-      ++stamp;
-      stack.clear();
-      for (int s : succ[x])
-        if (s != y && seen_mark[s] != stamp) {
-          seen_mark[s] = stamp;
-          stack.push_back(s);
-        }
-      while (!stack.empty()) {
-        int s = stack.back();
-        stack.pop_back();
-        if (s == y) return true;
-        for (int t : succ[s]) {
-          if (t == y) return true;
-          if (seen_mark[t] != stamp) {
-            seen_mark[t] = stamp;
-            stack.push_back(t);
-          }
+  auto third_path = [&](int x, int y) {  // edge x -> y exists
+    const int lim = pos[y];
+    ++stamp;
+    stack.clear();
+    for (int s : succ[x])
+      if (s != y && pos[s] < lim && mark[s] != stamp) {
+        mark[s] = stamp;
+        stack.push_back(s);
+      }
+    while (!stack.empty()) {
+      const int s = stack.back();
+      stack.pop_back();
+      for (int t : succ[s]) {
+        if (t == y) return true;
+        if (pos[t] < lim && mark[t] != stamp) {
+          mark[t] = stamp;
+          stack.push_back(t);
         }
       }
     }
     return false;
+  };
+  // re-lay the window [pos[x], pos[y]] after x and y merged into `root`
+  auto relayout = [&](int x, int y, int root) {
+    const int px = pos[x], py = pos[y];
+    ++stamp;
+    stack.clear();
+    for (int s : succ[x])
+      if (s != y && pos[s] < py && mark[s] != stamp) {
+        mark[s] = stamp;
+        stack.push_back(s);
+      }
+    while (!stack.empty()) {
+      const int s = stack.back();
+      stack.pop_back();
+      for (int t : succ[s])
+        if (pos[t] < py && mark[t] != stamp) {
+          mark[t] = stamp;
+          stack.push_back(t);
+        }
+    }
+    nonf.clear();
+    fw.clear();
+    for (int p = px + 1; p < py; ++p) {
+      const int g = at[p];
+      if (g < 0) continue;
+      (mark[g] == stamp ? fw : nonf).push_back(g);
+    }
+    int p = px;
+    for (int g : nonf) {
+      at[p] = g;
+      pos[g] = p++;
+    }
+    at[p] = root;
+    pos[root] = p++;
+    for (int g : fw) {
+      at[p] = g;
+      pos[g] = p++;
+    }
+    for (; p <= py; ++p) at[p] = -1;
   };
   for (int v : order) {
     if (pri[v] > 0 && fusible_op[op[v]]) {
@@ -206,29 +256,38 @@ void fuse_groups(int32_t n, int64_t e, const int32_t* src, const int32_t* dst,
       }
       if (best >= 0) {
         int rv = find(v), ru = find(best);
-        if (rv != ru && size[rv] + size[ru] <= max_group && !cycle(rv, ru)) {
-          if (size[rv] < size[ru]) std::swap(rv, ru);
-          parent[ru] = rv;
-          size[rv] += size[ru];
-          std::set<int32_t> ns, np;
-          for (int s : succ[rv]) ns.insert(s);
-          for (int s : succ[ru]) ns.insert(s);
-          for (int s : pred[rv]) np.insert(s);
-          for (int s : pred[ru]) np.insert(s);
-          ns.erase(rv);
-          ns.erase(ru);
-          np.erase(rv);
-          np.erase(ru);
-          for (int s : succ[ru]) pred[s].erase(ru);
-          for (int s : pred[ru]) succ[s].erase(ru);
-          for (int s : succ[rv]) pred[s].erase(rv);
-          for (int s : pred[rv]) succ[s].erase(rv);
-          succ[rv] = ns;
-          pred[rv] = np;
-          for (int s : ns) pred[s].insert(rv);
-          for (int s : np) succ[s].insert(rv);
-          succ[ru].clear();
-          pred[ru].clear();
+        if (rv != ru && size[rv] + size[ru] <= max_group) {
+          // orient the joining edge (original neighbours: one direction exists)
+          const bool fwd_edge = succ[rv].count(ru) > 0;
+          const int x = fwd_edge ? rv : ru, y = fwd_edge ? ru : rv;
+          if (!third_path(x, y)) {
+            // the group-graph edits must see the pre-merge adjacency: relayout first
+            if (size[rv] < size[ru]) std::swap(rv, ru);
+            parent[ru] = rv;
+            size[rv] += size[ru];
+            // relayout uses succ[x] before the fold (reachability from x within the
+            // window is unchanged by the fold: it only renames x, y to rv)
+            relayout(x, y, rv);
+            std::set<int32_t> ns, np;
+            for (int s : succ[rv]) ns.insert(s);
+            for (int s : succ[ru]) ns.insert(s);
+            for (int s : pred[rv]) np.insert(s);
+            for (int s : pred[ru]) np.insert(s);
+            ns.erase(rv);
+            ns.erase(ru);
+            np.erase(rv);
+            np.erase(ru);
+            for (int s : succ[ru]) pred[s].erase(ru);
+            for (int s : pred[ru]) succ[s].erase(ru);
+            for (int s : succ[rv]) pred[s].erase(rv);
+            for (int s : pred[rv]) succ[s].erase(rv);
+            succ[rv] = ns;
+            pred[rv] = np;
+            for (int s : ns) pred[s].insert(rv);
+            for (int s : np) succ[s].insert(rv);
+            succ[ru].clear();
+            pred[ru].clear();
+          }
         }
       }
     }

@@ -77,8 +77,9 @@ def main():
         short = name.split("::")[-1].split("<")[0]
         b = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in ks) / len(ks)
         traffic.setdefault(f"{short}_bytes_per_launch_F1", b)
-    if "attn_tc_fixed_kernel_bytes_per_launch_F1" in traffic:
-        traffic["attn_tc_fixed_bytes_per_forward"] = traffic["attn_tc_fixed_kernel_bytes_per_launch_F1"]
+    for k in ("attn_f16_kernel_bytes_per_launch_F1", "attn_tc_fixed_kernel_bytes_per_launch_F1"):
+        if k in traffic:
+            traffic.setdefault("heads_attention_bytes_per_forward", traffic[k])
     if "segment_max128_kernel_bytes_per_launch_F1" in traffic:
         traffic["segment_max_bytes_per_launch_F1"] = traffic["segment_max128_kernel_bytes_per_launch_F1"]
     res = {"report": rep, "kernels": kernels, "traffic": traffic}

@@ -128,3 +128,50 @@ def test_workloads_match_reference():
         assert sig == int(z[p + "edge_sig"])
         topo = g.topo_order().astype(np.int64)
         assert (topo * np.arange(g.num_nodes)).sum() % (2**61 - 1) == int(z[p + "topo_sig"])
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_fusion_pass_vs_oracle_permuted_ids(seed):
+    """Node ids in random (non-topological) order, multi-edges, long-range edges and
+    up to 300 nodes: the windowed cycle check (group-graph topological order) must make
+    exactly the reference's merge decisions."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(2, 300))
+    perm = rng.permutation(n)
+    fus = [2, 3, 4, 5, 6, 7]
+    op = rng.choice(fus + [0, 1], size=n, p=[0.14] * 6 + [0.08, 0.08])
+    src, dst = [], []
+    dens = float(rng.choice([0.01, 0.03, 0.08]))
+    for i in range(n):
+        for j in range(i + 1, min(n, i + 1 + int(rng.integers(1, 40)))):
+            if rng.random() < dens * 8:
+                src.append(perm[i])
+                dst.append(perm[j])
+                if rng.random() < 0.05:  # multi-edge
+                    src.append(perm[i])
+                    dst.append(perm[j])
+        if i + 50 < n and rng.random() < 0.05:  # long-range edge
+            j = int(rng.integers(i + 50, n))
+            src.append(perm[i])
+            dst.append(perm[j])
+    g = dict(n=n, op=op, src=np.array(src, np.int64), dst=np.array(dst, np.int64))
+    for k in range(3):
+        pri = rng.integers(0, 8, n)
+        mg = int(rng.choice([2, 4, 8]))
+        want = od.apply_fusion(g, pri, max_group=mg)
+        got = fuse_groups(Graph(op, np.zeros(n), np.zeros(n), src, dst, np.zeros(len(src))),
+                          pri, mg)
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("spec", [("attention-stack", 30, 1, 64, 0), ("dilated-stack", 5, 60, 64, 2),
+                                  ("multi-branch-cnn", 80, 1, 64, 1)])
+def test_fusion_pass_vs_oracle_workloads(spec):
+    g = gen_workload(WorkloadSpec(*spec), node_cap=10**6)
+    og_ = dict(n=g.num_nodes, op=np.asarray(g.op), src=np.asarray(g.src), dst=np.asarray(g.dst))
+    rng = np.random.default_rng(7)
+    for k in range(4):
+        pri = rng.integers(0, 8, g.num_nodes)
+        want = od.apply_fusion(og_, pri, max_group=8)
+        got = fuse_groups(g, pri, 8)
+        assert np.array_equal(got, want)
