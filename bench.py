@@ -154,7 +154,7 @@ def ncu_traffic():
 # CPU baseline: the oracle port, bounded sample of one placement
 
 
-def cpu_placement_sample(w, seed=123, head_rows=1024):
+def cpu_placement_sample(w, seed=123, head_rows=128):
     """Time one placement of the workload on the host with the float64 oracle (a
     faithful, vectorised restatement of the reference): neighbour sampling, embed
     and trunk in full, the N x N task-head attention on `head_rows` query rows

@@ -18,6 +18,7 @@
 // the online-softmax kernel (> 60).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "engine.cuh"
@@ -35,13 +36,18 @@ constexpr int HK = 32;   // keys per softmax sub-tile
 constexpr int NS = 8;    // K/V ring stages
 constexpr int TILE_BYTES = KT * 16 * 2;
 constexpr int PRODUCER_WARP = NQT * 4;
-constexpr int MMA_WARP = NQT * 4 + 1;
-constexpr int NUM_THREADS = (NQT * 4 + 2) * 32;
+// one MMA-issuing warp per query tile: a tile's PV / next-S issue never waits behind
+// another tile's softmax (a single in-order issuer left the softmax warps spinning on
+// s_full for a third of their samples, ncu source page)
+constexpr int MMA_WARP0 = NQT * 4 + 1;
+constexpr int NUM_THREADS = (NQT * 5 + 1) * 32;
 constexpr uint32_t O_COL = NQT * 2 * HK;
 constexpr uint32_t TMEM_COLS = 256;
 constexpr float F16_LIMIT = 14.f;
 constexpr float BOUND_LIMIT = 60.f;
-constexpr float RANGE_LIMIT = 60000.f;  // |k|, |v| that still round to a finite fp16
+constexpr float RANGE_LIMIT = 60000.f;
+constexpr int DEFAULT_POLY_PAIRS = 4;
+constexpr int DEFAULT_S64 = 1;  // |k|, |v| that still round to a finite fp16
 
 struct Smem {
   uint16_t q[NQT][QT * 16];
@@ -71,6 +77,13 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   return r;
 }
 
+// NP of every 8 exponential pairs go to the FMA-pipe polynomial (exp2_poly_f16x2), the
+// rest to MUFU.EX2: the MUFU (16 ex2/clk/SM) binds the all-MUFU kernel while the FMA
+// pipe idles, so splitting the work raises the exp rate (scripts/exp_probe.cu).
+// S64: one N=64 S MMA per 64-key tile into a single TMEM buffer per query tile (5 MMAs
+// per tile instead of 6; the next S waits for this tile's PV), instead of two N=32
+// halves double-buffered.  Same TMEM footprint (64 S columns + 16 O columns per tile).
+template <int NP, bool S64>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_f16_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
                     const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
@@ -89,7 +102,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   if (warp == PRODUCER_WARP && lane == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm.kv_full[s], 1);
-      mbar_init(&sm.kv_empty[s], 1);
+      mbar_init(&sm.kv_empty[s], NQT);
     }
     for (int t = 0; t < NQT; ++t) {
       for (int b = 0; b < 2; ++b) {
@@ -100,7 +113,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA_WARP) {
+  if (warp == MMA_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
                  "r"(TMEM_COLS));
@@ -133,12 +146,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       }
     }
     __syncwarp();
-  } else if (warp == MMA_WARP) {
+  } else if (warp >= MMA_WARP0 && S64) {
     if (lane == 0) {
+      const int t = warp - MMA_WARP0;
+      constexpr uint32_t ID_S = idesc_f16(QT, KT);
+      constexpr uint32_t ID_O = idesc_f16(QT, 16);
+      const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
+      const uint32_t sd = tbase + t * 2 * HK;  // 64 S columns; P packed into the first 32
+      auto issue_s = [&](int j) {
+        const int s = j % NS;
+        mbar_wait(&sm.kv_full[s], (j / NS) & 1);
+        fence_after();
+        umma_ss_f16(sd, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
+        umma_commit(&sm.s_full[t][0]);
+      };
+      if (T > 0) issue_s(0);
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
+        mbar_wait(&sm.p_full[t][0], j & 1);
+        fence_after();
+        const uint32_t d = tbase + O_COL + t * 16;
+#pragma unroll
+        for (int kk = 0; kk < KT / 16; ++kk)
+          umma_ts_f16(d, sd + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
+        if (j + 1 < T) issue_s(j + 1);  // in-order after the PV that reads P
+        umma_commit(&sm.kv_empty[s]);
+      }
+      umma_commit(&sm.o_done[t]);
+    }
+    __syncwarp();
+  } else if (warp >= MMA_WARP0) {
+    if (lane == 0) {
+      const int t = warp - MMA_WARP0;
       constexpr uint32_t ID_S = idesc_f16(QT, HK);
       constexpr uint32_t ID_O = idesc_f16(QT, 16);
-      uint32_t qaddr[NQT];
-      for (int t = 0; t < NQT; ++t) qaddr[t] = smem_u32(sm.q[t]);
+      const uint32_t qaddr = smem_u32(sm.q[t]);
       auto wait_kv = [&](int u) {
         if ((u & 1) == 0) {
           const int j = u >> 1;
@@ -146,38 +189,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           fence_after();
         }
       };
-      // S(u, t): keys [32h, 32h + 32) of tile j = u / 2 (K chunk stride 1 KB, 8-key
+      // S(u): keys [32h, 32h + 32) of tile j = u / 2 (K chunk stride 1 KB, 8-key
       // groups 128 B apart, so the second half starts 4 groups = 512 B in)
-      auto issue_s = [&](int u, int t) {
+      auto issue_s = [&](int u) {
         const int j = u >> 1, h = u & 1, s = j % NS, b = u & 1;
         const uint32_t kaddr = smem_u32(sm.kv[s][0]) + h * 512;
-        umma_ss_f16(tbase + t * 2 * HK + b * HK, sdesc(qaddr[t], QT * 16, 128),
+        umma_ss_f16(tbase + t * 2 * HK + b * HK, sdesc(qaddr, QT * 16, 128),
                     sdesc(kaddr, KT * 16, 128), ID_S, 0);
         umma_commit(&sm.s_full[t][b]);
       };
       for (int u = 0; u < 2 && u < U; ++u) {
         wait_kv(u);
-        for (int t = 0; t < NQT; ++t) issue_s(u, t);
+        issue_s(u);
       }
       for (int u = 0; u < U; ++u) {
         const int j = u >> 1, h = u & 1, s = j % NS, b = u & 1;
         const bool more = u + 2 < U;
-        if (more) wait_kv(u + 2);
         // V^T: 8-key chunks of 256 B (16 d rows x 16 B); second half 4 chunks in
         const uint32_t vaddr = smem_u32(sm.kv[s][1]) + h * 1024;
-        for (int t = 0; t < NQT; ++t) {
-          mbar_wait(&sm.p_full[t][b], (u >> 1) & 1);
-          fence_after();
-          const uint32_t d = tbase + O_COL + t * 16;
-          const uint32_t a = tbase + t * 2 * HK + b * HK;  // P: 16 packed columns
+        mbar_wait(&sm.p_full[t][b], (u >> 1) & 1);
+        fence_after();
+        const uint32_t d = tbase + O_COL + t * 16;
+        const uint32_t a = tbase + t * 2 * HK + b * HK;  // P: 16 packed columns
 #pragma unroll
-          for (int kk = 0; kk < HK / 16; ++kk)
-            umma_ts_f16(d, a + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (u > 0 || kk > 0));
-          if (more) issue_s(u + 2, t);
+        for (int kk = 0; kk < HK / 16; ++kk)
+          umma_ts_f16(d, a + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (u > 0 || kk > 0));
+        if (more) {
+          wait_kv(u + 2);
+          issue_s(u + 2);
         }
         if (h == 1) umma_commit(&sm.kv_empty[s]);
       }
-      for (int t = 0; t < NQT; ++t) umma_commit(&sm.o_done[t]);
+      umma_commit(&sm.o_done[t]);
     }
     __syncwarp();
   } else {
@@ -191,34 +234,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     auto p_addr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 8; };
     auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        pk[i] = pack_f16x2(ex2f(__uint_as_float(r[2 * i])), ex2f(__uint_as_float(r[2 * i + 1])));
+      for (int i = 0; i < 8; ++i) {
+        // interleave: polynomial pairs at odd positions first, so MUFU and FMA work mix
+        const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
+        const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+        pk[i] = poly ? exp2_poly_f16x2(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
+      }
     };
     uint32_t ra[16], rb[16], pk[8];
-    if (U > 0) {
-      mbar_wait(&sm.s_full[t][0], 0);
-      fence_after();
-      PTX_LD16(s_addr(0), ra);
-      tmem_wait_ld();
-    }
-    for (int u = 0; u < U; ++u) {
-      const int c = 2 * u;
-      PTX_LD16(s_addr(c + 1), rb);
-      softmax16(ra, pk);
-      PTX_ST8(p_addr(c), pk);
-      tmem_wait_ld();
-      const bool more = u + 1 < U;
-      if (more) {
-        mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
+    if constexpr (S64) {
+      // 64 S columns in 4 chunks of 16; chunk c's P (8 packed columns) lands on
+      // columns [8c, 8c + 8), all inside chunks already consumed
+      for (int j = 0; j < T; ++j) {
+        mbar_wait(&sm.s_full[t][0], j & 1);
         fence_after();
-        PTX_LD16(s_addr(c + 2), ra);
+        PTX_LD16(base, ra);
+        tmem_wait_ld();
+        PTX_LD16(base + 16, rb);
+        softmax16(ra, pk);
+        PTX_ST8(base, pk);
+        tmem_wait_ld();
+        PTX_LD16(base + 32, ra);
+        softmax16(rb, pk);
+        PTX_ST8(base + 8, pk);
+        tmem_wait_ld();
+        PTX_LD16(base + 48, rb);
+        softmax16(ra, pk);
+        PTX_ST8(base + 16, pk);
+        tmem_wait_ld();
+        softmax16(rb, pk);
+        PTX_ST8(base + 24, pk);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&sm.p_full[t][0]);
       }
-      softmax16(rb, pk);
-      PTX_ST8(p_addr(c + 1), pk);
-      tmem_wait_st();
-      fence_before();
-      mbar_arrive(&sm.p_full[t][u & 1]);
-      if (more) tmem_wait_ld();
+    } else {
+    uint32_t ra[16], rb[16], pk[8];
+      if (U > 0) {
+        mbar_wait(&sm.s_full[t][0], 0);
+        fence_after();
+        PTX_LD16(s_addr(0), ra);
+        tmem_wait_ld();
+      }
+      for (int u = 0; u < U; ++u) {
+        const int c = 2 * u;
+        PTX_LD16(s_addr(c + 1), rb);
+        softmax16(ra, pk);
+        PTX_ST8(p_addr(c), pk);
+        tmem_wait_ld();
+        const bool more = u + 1 < U;
+        if (more) {
+          mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
+          fence_after();
+          PTX_LD16(s_addr(c + 2), ra);
+        }
+        softmax16(rb, pk);
+        PTX_ST8(p_addr(c + 1), pk);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&sm.p_full[t][u & 1]);
+        if (more) tmem_wait_ld();
+      }
     }
     mbar_wait(&sm.o_done[t], 0);
     fence_after();
@@ -235,7 +311,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == MMA_WARP) {
+  if (warp == MMA_WARP0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
                  "r"(TMEM_COLS));
   }
@@ -356,12 +432,25 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                       void* qh, void* kb, void* vb, float* out, int64_t ldo,
                       const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
                       cudaStream_t st) {
-  static bool attr = false;
+  using Fn = void (*)(const uint16_t*, const uint16_t*, const uint16_t*, int64_t, int64_t,
+                     const TcWork*, float*, int64_t, int, const int32_t*);
+  static const Fn kernels[2][5] = {
+      {t16::attn_f16_kernel<0, false>, t16::attn_f16_kernel<1, false>,
+       t16::attn_f16_kernel<2, false>, t16::attn_f16_kernel<3, false>,
+       t16::attn_f16_kernel<4, false>},
+      {t16::attn_f16_kernel<0, true>, t16::attn_f16_kernel<1, true>,
+       t16::attn_f16_kernel<2, true>, t16::attn_f16_kernel<3, true>,
+       t16::attn_f16_kernel<4, true>}};
+  static int np = -1, s64 = 0;
   const size_t smem = sizeof(t16::Smem) + 1024;
-  if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(t16::attn_f16_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  if (np < 0) {
+    const char* e = getenv("GO_POLY16");
+    np = e ? std::min(4, std::max(0, atoi(e))) : t16::DEFAULT_POLY_PAIRS;
+    const char* e64 = getenv("GO_S64");
+    s64 = e64 ? (atoi(e64) != 0) : t16::DEFAULT_S64;
+    for (auto& row : kernels)
+      for (Fn f : row)
+        CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   const int64_t total = (int64_t)n_head * Ttot * (t16::KT / 8) * 2;
   t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
@@ -372,7 +461,7 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       q, ld, n_head, d_head, R, row_fwd, kmax, qscale, static_cast<__half*>(qh), flag);
   LAUNCH_CHECK();
   dim3 grid((unsigned)num_works, (unsigned)n_head);
-  t16::attn_f16_kernel<<<grid, t16::NUM_THREADS, smem, st>>>(
+  kernels[s64][np]<<<grid, t16::NUM_THREADS, smem, st>>>(
       static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
       static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
   LAUNCH_CHECK();

@@ -78,6 +78,8 @@ def forward(F, modes=("tc", "simt"), env=None):
               + " ".join(parts), flush=True)
         lg = out.logits[0].float()
         print("  logits checksum", float(lg.sum()), float(lg.abs().max()), flush=True)
+        if os.environ.get("GO_SAVE_LOGITS"):
+            torch.save(out.logits[0].float().cpu(), os.environ["GO_SAVE_LOGITS"])
 
 
 if __name__ == "__main__":
@@ -94,5 +96,7 @@ if __name__ == "__main__":
         forward(n or 8, env=[("GO_GEMM_BN256", "1"), ("GO_GEMM_BN256", "0"), ("GO_GEMM_BN256", "1")])
     elif what == "poly":
         forward(n or 8, env=[("GO_POLY", str(k)) for k in (0, 5, 1, 0)])
+    elif what == "tc":
+        forward(n or 8, modes=("tc",))
     else:
         forward(n or 8)
