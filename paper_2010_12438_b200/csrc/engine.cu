@@ -137,11 +137,11 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   std::vector<TrunkTile> ttc;
   if (need_trunk) m.trunk_tc_ok = trunk_tc_build_tiles(m.row_off, cfg.segment_len, ttc);
   size_t o_tt = s.add(tt), o_ht = s.add(ht), o_ttc = s.add(ttc);
-  std::vector<TcWork> tcw;
+  std::vector<TcWork> tcw, tcw2;
   std::vector<int64_t> trow0;
   std::vector<int32_t> tn;
-  if (need_heads) tc_build_tables(m.row_off, tcw, trow0, tn);
-  size_t o_tcw = s.add(tcw), o_tr = s.add(trow0), o_tn = s.add(tn);
+  if (need_heads) tc_build_tables(m.row_off, tcw, trow0, tn, tcw2);
+  size_t o_tcw = s.add(tcw), o_tr = s.add(trow0), o_tn = s.add(tn), o_tcw2 = s.add(tcw2);
   // mean chunks: [nc] r0, [nc] r1, [F] first, [F] end
   std::vector<int64_t> c0, c1, f0(m.F), f1(m.F);
   for (int f = 0; f < m.F; ++f) {
@@ -175,6 +175,8 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   m.d_chunks = reinterpret_cast<const int64_t*>(dev + o_ch);
   m.d_tc_works = reinterpret_cast<const TcWork*>(dev + o_tcw);
   m.n_tc_works = (int64_t)tcw.size();
+  m.d_tc_works2 = reinterpret_cast<const TcWork*>(dev + o_tcw2);
+  m.n_tc_works2 = (int64_t)tcw2.size();
   m.d_tile_row0 = reinterpret_cast<const int64_t*>(dev + o_tr);
   m.d_tile_n = reinterpret_cast<const int32_t*>(dev + o_tn);
   m.n_tiles = (int64_t)trow0.size();
@@ -462,7 +464,7 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
         if (use_tc)
           attention_full_tc(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, R, m.n_tiles, m.d_tc_works,
                             m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
-                            row_fwd, F, tc_scratch, st);
+                            row_fwd, F, tc_scratch, m.d_tc_works2, m.n_tc_works2, st);
         else
           attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_head_tiles, m.n_head_tiles, Ab,
                     LA, st);
@@ -727,7 +729,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
         if (use_tc)
           attention_full_tc(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, R, m.n_tiles, m.d_tc_works,
                             m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
-                            row_fwd, F, tc_scratch, st);
+                            row_fwd, F, tc_scratch, m.d_tc_works2, m.n_tc_works2, st);
         else
           attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_head_tiles, m.n_head_tiles, Ab, LA,
                     st);

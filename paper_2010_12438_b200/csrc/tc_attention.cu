@@ -754,7 +754,8 @@ __global__ void repack_q_fixed_kernel(const float* __restrict__ q, int64_t ld, i
 bool tc_attention_supported(int d_head) { return d_head <= 16; }
 
 void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& works,
-                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n) {
+                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n,
+                     std::vector<TcWork>& works2) {
   int F = (int)row_off.size() - 1;
   int64_t tb = 0;
   for (int f = 0; f < F; ++f) {
@@ -762,6 +763,8 @@ void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& w
     int32_t T = (int32_t)cdiv(n, tc::KT);
     for (int64_t q0 = 0; q0 < n; q0 += tc::NQT * tc::QT)
       works.push_back(TcWork{f, (int32_t)q0, (int32_t)n, T, row_off[f], tb});
+    for (int64_t q0 = 0; q0 < n; q0 += 2 * tc::QT)
+      works2.push_back(TcWork{f, (int32_t)q0, (int32_t)n, T, row_off[f], tb});
     for (int32_t t = 0; t < T; ++t) {
       tile_row0.push_back(row_off[f]);
       tile_n.push_back((int32_t)n);
@@ -777,7 +780,7 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
                        int64_t num_works, const int64_t* tile_row0_dev,
                        const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
                        int64_t ldo, const int32_t* row_fwd, int F, int32_t* scratch,
-                       cudaStream_t st) {
+                       const TcWork* works2_dev, int64_t num_works2, cudaStream_t st) {
   if (num_works <= 0) return;
   if (d_head > 16) GO_THROW(GO_ERR_UNSUPPORTED, "tensor-core attention needs d_head <= 16");
   static bool attr = false;
@@ -816,7 +819,8 @@ void attention_full_tc(const float* q, const float* k, const float* v, int64_t l
     int want = 0;
     if (use16) {
       attention_f16_tc(q, k, v, ld, n_head, d_head, R, Ttot, works_dev, num_works, tile_row0_dev,
-                       tile_n_dev, qh, kb, vb, out, ldo, row_fwd, kmax, flag, qscale, st);
+                       tile_n_dev, qh, kb, vb, out, ldo, row_fwd, kmax, flag, qscale,
+                       works2_dev, num_works2, st);
       want = 2;
     }
     tc::repack_kv_fixed_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_fp16.h>
 
 #include "engine.cuh"
@@ -47,7 +48,9 @@ constexpr float F16_LIMIT = 14.f;
 constexpr float BOUND_LIMIT = 60.f;
 constexpr float RANGE_LIMIT = 60000.f;
 constexpr int DEFAULT_POLY_PAIRS = 4;
-constexpr int DEFAULT_S64 = 1;  // |k|, |v| that still round to a finite fp16
+constexpr int DEFAULT_S64 = 1;
+constexpr int DEFAULT_ALT = 0;
+constexpr int DEFAULT_LP = 1;  // |k|, |v| that still round to a finite fp16
 
 struct Smem {
   uint16_t q[NQT][QT * 16];
@@ -83,7 +86,7 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
 // S64: one N=64 S MMA per 64-key tile into a single TMEM buffer per query tile (5 MMAs
 // per tile instead of 6; the next S waits for this tile's PV), instead of two N=32
 // halves double-buffered.  Same TMEM footprint (64 S columns + 16 O columns per tile).
-template <int NP, bool S64>
+template <int NP, bool S64, bool LP = false>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_f16_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
                     const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     if (lane == 0) {
       for (int j = 0; j < T; ++j) {
         const int s = j % NS;
-        if (j >= NS) mbar_wait(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        if (j >= NS) mbar_wait_sleep(&sm.kv_empty[s], ((j / NS) - 1) & 1);
         mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
         bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
         bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       const uint32_t sd = tbase + t * 2 * HK;  // 64 S columns; P packed into the first 32
       auto issue_s = [&](int j) {
         const int s = j % NS;
-        mbar_wait(&sm.kv_full[s], (j / NS) & 1);
+        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
         fence_after();
         umma_ss_f16(sd, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
         umma_commit(&sm.s_full[t][0]);
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       for (int j = 0; j < T; ++j) {
         const int s = j % NS;
         const uint32_t vaddr = smem_u32(sm.kv[s][1]);
-        mbar_wait(&sm.p_full[t][0], j & 1);
+        mbar_wait_sleep(&sm.p_full[t][0], j & 1);
         fence_after();
         const uint32_t d = tbase + O_COL + t * 16;
 #pragma unroll
@@ -238,7 +241,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         // interleave: polynomial pairs at odd positions first, so MUFU and FMA work mix
         const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
         const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-        pk[i] = poly ? exp2_poly_f16x2(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
+        pk[i] = poly ? (LP ? exp2_poly_f16x2_lp(x0, x1) : exp2_poly_f16x2(x0, x1))
+                     : pack_f16x2(ex2f(x0), ex2f(x1));
       }
     };
     uint32_t ra[16], rb[16], pk[8];
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       // 64 S columns in 4 chunks of 16; chunk c's P (8 packed columns) lands on
       // columns [8c, 8c + 8), all inside chunks already consumed
       for (int j = 0; j < T; ++j) {
-        mbar_wait(&sm.s_full[t][0], j & 1);
+        mbar_wait_sleep(&sm.s_full[t][0], j & 1);
         fence_after();
         PTX_LD16(base, ra);
         tmem_wait_ld();
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         if (more) tmem_wait_ld();
       }
     }
-    mbar_wait(&sm.o_done[t], 0);
+    mbar_wait_sleep(&sm.o_done[t], 0);
     fence_after();
     uint32_t r[16];
     PTX_LD16(tbase + lane_off + O_COL + t * 16, r);
@@ -314,6 +318,189 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   if (warp == MMA_WARP0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
                  "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Alternating-window variant (GO_ATTN16=alt): S(j+1) is issued BEFORE PV(j), so a query
+// tile's softmax waits only for one N=64 S MMA, not for the 4 PV MMAs in front of it.
+// Per query tile 96 S/P columns + 16 O columns:
+//   even j: S in [0, 64), P packed into [0, 32)   (chunks read in ascending order)
+//   odd  j: S in [32, 96), P packed into [64, 96) (chunks read in descending order, so
+//           every P chunk lands on S columns already consumed)
+// S(j+1) never touches P(j); it overwrites P(j-1), whose PV was issued before it by the
+// same thread (tcgen05 MMAs from one thread execute in order).  2 query tiles per CTA
+// (256 queries, 224 TMEM columns) and 2 CTAs per SM.
+namespace alt {
+constexpr int NQ = 2;
+constexpr int SOFT_WARPS = NQ * 4;
+constexpr int PRODUCER = SOFT_WARPS;
+constexpr int MMA0 = SOFT_WARPS + 1;
+constexpr int THREADS = (SOFT_WARPS + 1 + NQ) * 32;
+constexpr uint32_t REGION = 96;
+constexpr uint32_t O_COL = NQ * REGION;
+constexpr uint32_t TMEM_COLS = 256;
+constexpr int QPW = NQ * QT;  // queries per work item
+struct Smem {
+  uint16_t q[NQ][QT * 16];
+  uint16_t kv[NS][2][KT * 16];
+  uint64_t kv_full[NS], kv_empty[NS];
+  uint64_t s_full[NQ], p_full[NQ], o_done[NQ];
+  uint32_t tmem_base;
+};
+}  // namespace alt
+
+template <int NP>
+__global__ void __launch_bounds__(alt::THREADS, 2)
+    attn_f16_alt_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
+                        const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
+                        const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
+                        int d_head, const int32_t* __restrict__ flag) {
+  using namespace alt;
+  if (*flag) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  alt::Smem& sm = *reinterpret_cast<alt::Smem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TcWork w = works[blockIdx.x];
+  const int head = blockIdx.y;
+  const int T = w.tiles;
+  const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  if (warp == PRODUCER && lane == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], NQ);
+    }
+    for (int t = 0; t < NQ; ++t) {
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.o_done[t], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(alt::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < NQ * QT * 2; i += THREADS) {
+    const int qt = i / (QT * 2), rem = i % (QT * 2);
+    const int r = rem >> 1, c = rem & 1;
+    const int lr = w.q0 + qt * QT + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (lr < w.n)
+      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
+    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
+  }
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == PRODUCER) {
+    if (lane == 0) {
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        if (j >= NS) mbar_wait_sleep(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
+        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= MMA0) {
+    if (lane == 0) {
+      const int t = warp - MMA0;
+      constexpr uint32_t ID_S = idesc_f16(QT, KT);
+      constexpr uint32_t ID_O = idesc_f16(QT, 16);
+      const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
+      const uint32_t reg = tbase + t * REGION;
+      const uint32_t d = tbase + alt::O_COL + t * 16;
+      auto issue_s = [&](int j) {
+        const int s = j % NS;
+        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
+        fence_after();
+        umma_ss_f16(reg + (j & 1) * 32, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
+        umma_commit(&sm.s_full[t]);
+      };
+      if (T > 0) issue_s(0);
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        mbar_wait_sleep(&sm.p_full[t], j & 1);
+        fence_after();
+        if (j + 1 < T) issue_s(j + 1);
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
+        const uint32_t pa = reg + (j & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < KT / 16; ++kk)
+          umma_ts_f16(d, pa + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
+        umma_commit(&sm.kv_empty[s]);
+      }
+      umma_commit(&sm.o_done[t]);
+    }
+    __syncwarp();
+  } else {
+    const int t = warp >> 2;
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t reg = tbase + lane_off + t * REGION;
+    auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
+        const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+        pk[i] = poly ? exp2_poly_f16x2(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
+      }
+    };
+    uint32_t ra[16], rb[16], pk[8];
+    for (int j = 0; j < T; ++j) {
+      const bool odd = j & 1;
+      const uint32_t win = reg + (odd ? 32 : 0);
+      const uint32_t pb = reg + (odd ? 64 : 0);
+      // chunk order: ascending for even j, descending for odd j
+      const int c0 = odd ? 3 : 0, dc = odd ? -1 : 1;
+      mbar_wait_sleep(&sm.s_full[t], j & 1);
+      fence_after();
+      PTX_LD16(win + 16 * c0, ra);
+      tmem_wait_ld();
+      PTX_LD16(win + 16 * (c0 + dc), rb);
+      softmax16(ra, pk);
+      PTX_ST8(pb + 8 * c0, pk);
+      tmem_wait_ld();
+      PTX_LD16(win + 16 * (c0 + 2 * dc), ra);
+      softmax16(rb, pk);
+      PTX_ST8(pb + 8 * (c0 + dc), pk);
+      tmem_wait_ld();
+      PTX_LD16(win + 16 * (c0 + 3 * dc), rb);
+      softmax16(ra, pk);
+      PTX_ST8(pb + 8 * (c0 + 2 * dc), pk);
+      tmem_wait_ld();
+      softmax16(rb, pk);
+      PTX_ST8(pb + 8 * (c0 + 3 * dc), pk);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&sm.p_full[t]);
+    }
+    mbar_wait_sleep(&sm.o_done[t], 0);
+    fence_after();
+    uint32_t r[16];
+    PTX_LD16(tbase + lane_off + alt::O_COL + t * 16, r);
+    tmem_wait_ld();
+    const int lr = w.q0 + t * QT + wq * 32 + lane;
+    if (lr < w.n) {
+      const float inv = 1.f / __uint_as_float(r[15]);
+      float* o = out + (w.row0 + lr) * ldo + head * d_head;
+      for (int dd = 0; dd < d_head; ++dd) o[dd] = __uint_as_float(r[dd]) * inv;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == MMA0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(alt::TMEM_COLS));
   }
 }
 
@@ -431,7 +618,7 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                       int64_t num_works, const int64_t* tile_row0_dev, const int32_t* tile_n_dev,
                       void* qh, void* kb, void* vb, float* out, int64_t ldo,
                       const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
-                      cudaStream_t st) {
+                      const TcWork* works2_dev, int64_t num_works2, cudaStream_t st) {
   using Fn = void (*)(const uint16_t*, const uint16_t*, const uint16_t*, int64_t, int64_t,
                      const TcWork*, float*, int64_t, int, const int32_t*);
   static const Fn kernels[2][5] = {
@@ -441,16 +628,33 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       {t16::attn_f16_kernel<0, true>, t16::attn_f16_kernel<1, true>,
        t16::attn_f16_kernel<2, true>, t16::attn_f16_kernel<3, true>,
        t16::attn_f16_kernel<4, true>}};
-  static int np = -1, s64 = 0;
+  static const Fn alt_kernels[5] = {
+      t16::attn_f16_alt_kernel<0>, t16::attn_f16_alt_kernel<1>, t16::attn_f16_alt_kernel<2>,
+      t16::attn_f16_alt_kernel<3>, t16::attn_f16_alt_kernel<4>};
+  static const Fn lp_kernels[7] = {
+      t16::attn_f16_kernel<0, true, true>, t16::attn_f16_kernel<1, true, true>,
+      t16::attn_f16_kernel<2, true, true>, t16::attn_f16_kernel<3, true, true>,
+      t16::attn_f16_kernel<4, true, true>, t16::attn_f16_kernel<5, true, true>,
+      t16::attn_f16_kernel<6, true, true>};
+  static int np = -1, s64 = 0, use_alt = 0, lp = 0;
   const size_t smem = sizeof(t16::Smem) + 1024;
+  const size_t smem_alt = sizeof(t16::alt::Smem) + 1024;
   if (np < 0) {
     const char* e = getenv("GO_POLY16");
-    np = e ? std::min(4, std::max(0, atoi(e))) : t16::DEFAULT_POLY_PAIRS;
+    np = e ? std::min(6, std::max(0, atoi(e))) : t16::DEFAULT_POLY_PAIRS;
     const char* e64 = getenv("GO_S64");
     s64 = e64 ? (atoi(e64) != 0) : t16::DEFAULT_S64;
+    const char* ea = getenv("GO_ATTN16");
+    use_alt = ea ? !strcmp(ea, "alt") : t16::DEFAULT_ALT;
     for (auto& row : kernels)
       for (Fn f : row)
         CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const char* elp = getenv("GO_POLYLP");
+    lp = elp ? (atoi(elp) != 0) : t16::DEFAULT_LP;
+    for (Fn f : lp_kernels)
+      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (Fn f : alt_kernels)
+      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_alt));
   }
   const int64_t total = (int64_t)n_head * Ttot * (t16::KT / 8) * 2;
   t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
@@ -460,8 +664,16 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
   t16::repack_q16_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
       q, ld, n_head, d_head, R, row_fwd, kmax, qscale, static_cast<__half*>(qh), flag);
   LAUNCH_CHECK();
+  if (use_alt && works2_dev && num_works2 > 0) {
+    dim3 grid2((unsigned)num_works2, (unsigned)n_head);
+    alt_kernels[std::min(np, 4)]<<<grid2, t16::alt::THREADS, smem_alt, st>>>(
+        static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
+        static_cast<const uint16_t*>(vb), R, Ttot, works2_dev, out, ldo, d_head, flag);
+    LAUNCH_CHECK();
+    return;
+  }
   dim3 grid((unsigned)num_works, (unsigned)n_head);
-  kernels[s64][np]<<<grid, t16::NUM_THREADS, smem, st>>>(
+  (lp && s64 ? lp_kernels[np] : kernels[s64][std::min(np, 4)])<<<grid, t16::NUM_THREADS, smem, st>>>(
       static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
       static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
   LAUNCH_CHECK();
