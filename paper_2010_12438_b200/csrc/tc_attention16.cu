@@ -86,6 +86,8 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
 // S64: one N=64 S MMA per 64-key tile into a single TMEM buffer per query tile (5 MMAs
 // per tile instead of 6; the next S waits for this tile's PV), instead of two N=32
 // halves double-buffered.  Same TMEM footprint (64 S columns + 16 O columns per tile).
+__device__ int g_attn_debug = 0;
+
 template <int NP, bool S64, bool LP = false>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_f16_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
@@ -170,9 +172,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         mbar_wait_sleep(&sm.p_full[t][0], j & 1);
         fence_after();
         const uint32_t d = tbase + O_COL + t * 16;
+        if (g_attn_debug != 3) {
 #pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk)
-          umma_ts_f16(d, sd + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
+          for (int kk = 0; kk < KT / 16; ++kk)
+            umma_ts_f16(d, sd + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
+        }
         if (j + 1 < T) issue_s(j + 1);  // in-order after the PV that reads P
         umma_commit(&sm.kv_empty[s]);
       }
@@ -249,29 +253,49 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     if constexpr (S64) {
       // 64 S columns in 4 chunks of 16; chunk c's P (8 packed columns) lands on
       // columns [8c, 8c + 8), all inside chunks already consumed
+      const int dbg = g_attn_debug;  // timing experiments only (GO_ATTN_DEBUG)
+      if (dbg == 1 || dbg == 2) {
+        for (int j = 0; j < T; ++j) {
+          mbar_wait_sleep(&sm.s_full[t][0], j & 1);
+          fence_after();
+          if (dbg == 1) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              PTX_LD16(base + 16 * c, ra);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk[i] = ra[2 * i] ^ ra[2 * i + 1];
+              PTX_ST8(base + 8 * c, pk);
+            }
+            tmem_wait_st();
+          }
+          fence_before();
+          mbar_arrive(&sm.p_full[t][0]);
+        }
+      } else
       for (int j = 0; j < T; ++j) {
-        mbar_wait_sleep(&sm.s_full[t][0], j & 1);
-        fence_after();
-        PTX_LD16(base, ra);
-        tmem_wait_ld();
-        PTX_LD16(base + 16, rb);
-        softmax16(ra, pk);
-        PTX_ST8(base, pk);
-        tmem_wait_ld();
-        PTX_LD16(base + 32, ra);
-        softmax16(rb, pk);
-        PTX_ST8(base + 8, pk);
-        tmem_wait_ld();
-        PTX_LD16(base + 48, rb);
-        softmax16(ra, pk);
-        PTX_ST8(base + 16, pk);
-        tmem_wait_ld();
-        softmax16(rb, pk);
-        PTX_ST8(base + 24, pk);
-        tmem_wait_st();
-        fence_before();
-        mbar_arrive(&sm.p_full[t][0]);
-      }
+          mbar_wait_sleep(&sm.s_full[t][0], j & 1);
+          fence_after();
+          PTX_LD16(base, ra);
+          tmem_wait_ld();
+          PTX_LD16(base + 16, rb);
+          softmax16(ra, pk);
+          PTX_ST8(base, pk);
+          tmem_wait_ld();
+          PTX_LD16(base + 32, ra);
+          softmax16(rb, pk);
+          PTX_ST8(base + 8, pk);
+          tmem_wait_ld();
+          PTX_LD16(base + 48, rb);
+          softmax16(ra, pk);
+          PTX_ST8(base + 16, pk);
+          tmem_wait_ld();
+          softmax16(rb, pk);
+          PTX_ST8(base + 24, pk);
+          tmem_wait_st();
+          fence_before();
+          mbar_arrive(&sm.p_full[t][0]);
+        }
     } else {
     uint32_t ra[16], rb[16], pk[8];
       if (U > 0) {
@@ -322,51 +346,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 }
 
 // ---------------------------------------------------------------------------------------
-// Alternating-window variant (GO_ATTN16=alt): S(j+1) is issued BEFORE PV(j), so a query
-// tile's softmax waits only for one N=64 S MMA, not for the 4 PV MMAs in front of it.
-// Per query tile 96 S/P columns + 16 O columns:
-//   even j: S in [0, 64), P packed into [0, 32)   (chunks read in ascending order)
-//   odd  j: S in [32, 96), P packed into [64, 96) (chunks read in descending order, so
+// Alternating-window variant (GO_ATTN16=alt): S(u+1) is issued BEFORE PV(u), so a query
+// tile's softmax waits only for one S MMA, not for the PV MMAs in front of it.  With KS
+// keys per step, per query tile 1.5 KS S/P columns + 16 O columns:
+//   even u: S in [0, KS),      P packed into [0, KS/2)    (chunks read ascending)
+//   odd  u: S in [KS/2, 3KS/2), P packed into [KS, 3KS/2) (chunks read descending, so
 //           every P chunk lands on S columns already consumed)
-// S(j+1) never touches P(j); it overwrites P(j-1), whose PV was issued before it by the
-// same thread (tcgen05 MMAs from one thread execute in order).  2 query tiles per CTA
-// (256 queries, 224 TMEM columns) and 2 CTAs per SM.
-namespace alt {
-constexpr int NQ = 2;
-constexpr int SOFT_WARPS = NQ * 4;
-constexpr int PRODUCER = SOFT_WARPS;
-constexpr int MMA0 = SOFT_WARPS + 1;
-constexpr int THREADS = (SOFT_WARPS + 1 + NQ) * 32;
-constexpr uint32_t REGION = 96;
-constexpr uint32_t O_COL = NQ * REGION;
-constexpr uint32_t TMEM_COLS = 256;
-constexpr int QPW = NQ * QT;  // queries per work item
-struct Smem {
-  uint16_t q[NQ][QT * 16];
-  uint16_t kv[NS][2][KT * 16];
-  uint64_t kv_full[NS], kv_empty[NS];
-  uint64_t s_full[NQ], p_full[NQ], o_done[NQ];
-  uint32_t tmem_base;
+// S(u+1) never touches P(u); it overwrites P(u-1), whose PV was issued before it by the
+// same thread (tcgen05 MMAs from one thread execute in order).
+//   <NQ=2, KS=64>: 256 queries per CTA, 224 TMEM columns (works2 table)
+//   <NQ=3, KS=32>: 384 queries per CTA, 192 TMEM columns (works table)
+template <int NQ, int KS>
+struct AltCfg {
+  static constexpr int SOFT_WARPS = NQ * 4;
+  static constexpr int PRODUCER = SOFT_WARPS;
+  static constexpr int MMA0 = SOFT_WARPS + 1;
+  static constexpr int THREADS = (SOFT_WARPS + 1 + NQ) * 32;
+  static constexpr uint32_t REGION = KS + KS / 2;
+  static constexpr uint32_t O_COL = NQ * REGION;
+  static constexpr uint32_t TMEM_COLS = 256;
+  static constexpr int STEPS = KT / KS;  // S steps per K/V tile
+  static_assert(O_COL + NQ * 16 <= TMEM_COLS, "TMEM budget");
+  struct Smem {
+    uint16_t q[NQ][QT * 16];
+    uint16_t kv[NS][2][KT * 16];
+    uint64_t kv_full[NS], kv_empty[NS];
+    uint64_t s_full[NQ], p_full[NQ], o_done[NQ];
+    uint32_t tmem_base;
+  };
 };
-}  // namespace alt
 
-template <int NP>
-__global__ void __launch_bounds__(alt::THREADS, 2)
+template <int NP, bool LP, int NQ, int KS>
+__global__ void __launch_bounds__(AltCfg<NQ, KS>::THREADS, 2)
     attn_f16_alt_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
                         const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
                         const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
                         int d_head, const int32_t* __restrict__ flag) {
-  using namespace alt;
+  using C = AltCfg<NQ, KS>;
+  constexpr int NCH = KS / 16;  // 16-column chunks per step
   if (*flag) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  alt::Smem& sm = *reinterpret_cast<alt::Smem*>(smem_raw);
+  typename C::Smem& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TcWork w = works[blockIdx.x];
   const int head = blockIdx.y;
   const int T = w.tiles;
+  const int U = T * C::STEPS;
   const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
   const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
-  if (warp == PRODUCER && lane == 0) {
+  if (warp == C::PRODUCER && lane == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], NQ);
@@ -378,13 +406,13 @@ __global__ void __launch_bounds__(alt::THREADS, 2)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA0) {
+  if (warp == C::MMA0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
-                 "r"(alt::TMEM_COLS));
+                 "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = threadIdx.x; i < NQ * QT * 2; i += THREADS) {
+  for (int i = threadIdx.x; i < NQ * QT * 2; i += C::THREADS) {
     const int qt = i / (QT * 2), rem = i % (QT * 2);
     const int r = rem >> 1, c = rem & 1;
     const int lr = w.q0 + qt * QT + r;
@@ -399,7 +427,7 @@ __global__ void __launch_bounds__(alt::THREADS, 2)
   fence_after();
   const uint32_t tbase = sm.tmem_base;
 
-  if (warp == PRODUCER) {
+  if (warp == C::PRODUCER) {
     if (lane == 0) {
       for (int j = 0; j < T; ++j) {
         const int s = j % NS;
@@ -410,33 +438,38 @@ __global__ void __launch_bounds__(alt::THREADS, 2)
       }
     }
     __syncwarp();
-  } else if (warp >= MMA0) {
+  } else if (warp >= C::MMA0) {
     if (lane == 0) {
-      const int t = warp - MMA0;
-      constexpr uint32_t ID_S = idesc_f16(QT, KT);
+      const int t = warp - C::MMA0;
+      constexpr uint32_t ID_S = idesc_f16(QT, KS);
       constexpr uint32_t ID_O = idesc_f16(QT, 16);
       const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
-      const uint32_t reg = tbase + t * REGION;
-      const uint32_t d = tbase + alt::O_COL + t * 16;
-      auto issue_s = [&](int j) {
-        const int s = j % NS;
-        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
-        fence_after();
-        umma_ss_f16(reg + (j & 1) * 32, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
+      const uint32_t reg = tbase + t * C::REGION;
+      const uint32_t d = tbase + C::O_COL + t * 16;
+      // step u: K/V tile j = u / STEPS, key half h = u % STEPS (8-key groups are 128 B
+      // apart in K, 256 B in V^T)
+      auto issue_s = [&](int u) {
+        const int j = u / C::STEPS, h = u % C::STEPS, s = j % NS;
+        if (h == 0) {
+          mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
+          fence_after();
+        }
+        umma_ss_f16(reg + (u & 1) * (KS / 2), qd,
+                    sdesc(smem_u32(sm.kv[s][0]) + h * (KS / 8) * 128, KT * 16, 128), ID_S, 0);
         umma_commit(&sm.s_full[t]);
       };
-      if (T > 0) issue_s(0);
-      for (int j = 0; j < T; ++j) {
-        const int s = j % NS;
-        mbar_wait_sleep(&sm.p_full[t], j & 1);
+      if (U > 0) issue_s(0);
+      for (int u = 0; u < U; ++u) {
+        const int j = u / C::STEPS, h = u % C::STEPS, s = j % NS;
+        mbar_wait_sleep(&sm.p_full[t], u & 1);
         fence_after();
-        if (j + 1 < T) issue_s(j + 1);
-        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
-        const uint32_t pa = reg + (j & 1) * 64;
+        if (u + 1 < U) issue_s(u + 1);
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]) + h * (KS / 8) * 256;
+        const uint32_t pa = reg + (u & 1) * KS;
 #pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk)
-          umma_ts_f16(d, pa + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
-        umma_commit(&sm.kv_empty[s]);
+        for (int kk = 0; kk < KS / 16; ++kk)
+          umma_ts_f16(d, pa + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (u > 0 || kk > 0));
+        if (h == C::STEPS - 1) umma_commit(&sm.kv_empty[s]);
       }
       umma_commit(&sm.o_done[t]);
     }
@@ -445,40 +478,38 @@ __global__ void __launch_bounds__(alt::THREADS, 2)
     const int t = warp >> 2;
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t reg = tbase + lane_off + t * REGION;
+    const uint32_t reg = tbase + lane_off + t * C::REGION;
     auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
         const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-        pk[i] = poly ? exp2_poly_f16x2(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
+        pk[i] = poly ? (LP ? exp2_poly_f16x2_lp(x0, x1) : exp2_poly_f16x2(x0, x1))
+                     : pack_f16x2(ex2f(x0), ex2f(x1));
       }
     };
     uint32_t ra[16], rb[16], pk[8];
-    for (int j = 0; j < T; ++j) {
-      const bool odd = j & 1;
-      const uint32_t win = reg + (odd ? 32 : 0);
-      const uint32_t pb = reg + (odd ? 64 : 0);
-      // chunk order: ascending for even j, descending for odd j
-      const int c0 = odd ? 3 : 0, dc = odd ? -1 : 1;
-      mbar_wait_sleep(&sm.s_full[t], j & 1);
+    for (int u = 0; u < U; ++u) {
+      const bool odd = u & 1;
+      const uint32_t win = reg + (odd ? KS / 2 : 0);
+      const uint32_t pb = reg + (odd ? KS : 0);
+      const int c0 = odd ? NCH - 1 : 0, dc = odd ? -1 : 1;
+      mbar_wait_sleep(&sm.s_full[t], u & 1);
       fence_after();
       PTX_LD16(win + 16 * c0, ra);
       tmem_wait_ld();
-      PTX_LD16(win + 16 * (c0 + dc), rb);
-      softmax16(ra, pk);
-      PTX_ST8(pb + 8 * c0, pk);
-      tmem_wait_ld();
-      PTX_LD16(win + 16 * (c0 + 2 * dc), ra);
-      softmax16(rb, pk);
-      PTX_ST8(pb + 8 * (c0 + dc), pk);
-      tmem_wait_ld();
-      PTX_LD16(win + 16 * (c0 + 3 * dc), rb);
-      softmax16(ra, pk);
-      PTX_ST8(pb + 8 * (c0 + 2 * dc), pk);
-      tmem_wait_ld();
-      softmax16(rb, pk);
-      PTX_ST8(pb + 8 * (c0 + 3 * dc), pk);
+#pragma unroll
+      for (int i = 0; i < NCH; i += 2) {
+        const int ca = c0 + i * dc, cb = ca + dc;
+        PTX_LD16(win + 16 * cb, rb);
+        softmax16(ra, pk);
+        PTX_ST8(pb + 8 * ca, pk);
+        tmem_wait_ld();
+        if (i + 2 < NCH) PTX_LD16(win + 16 * (cb + dc), ra);
+        softmax16(rb, pk);
+        PTX_ST8(pb + 8 * cb, pk);
+        if (i + 2 < NCH) tmem_wait_ld();
+      }
       tmem_wait_st();
       fence_before();
       mbar_arrive(&sm.p_full[t]);
@@ -486,7 +517,7 @@ __global__ void __launch_bounds__(alt::THREADS, 2)
     mbar_wait_sleep(&sm.o_done[t], 0);
     fence_after();
     uint32_t r[16];
-    PTX_LD16(tbase + lane_off + alt::O_COL + t * 16, r);
+    PTX_LD16(tbase + lane_off + C::O_COL + t * 16, r);
     tmem_wait_ld();
     const int lr = w.q0 + t * QT + wq * 32 + lane;
     if (lr < w.n) {
@@ -498,9 +529,9 @@ __global__ void __launch_bounds__(alt::THREADS, 2)
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == MMA0) {
+  if (warp == C::MMA0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
-                 "r"(alt::TMEM_COLS));
+                 "r"(C::TMEM_COLS));
   }
 }
 
@@ -628,9 +659,17 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       {t16::attn_f16_kernel<0, true>, t16::attn_f16_kernel<1, true>,
        t16::attn_f16_kernel<2, true>, t16::attn_f16_kernel<3, true>,
        t16::attn_f16_kernel<4, true>}};
-  static const Fn alt_kernels[5] = {
-      t16::attn_f16_alt_kernel<0>, t16::attn_f16_alt_kernel<1>, t16::attn_f16_alt_kernel<2>,
-      t16::attn_f16_alt_kernel<3>, t16::attn_f16_alt_kernel<4>};
+  // GO_ATTN16=alt (2 tiles x 64-key steps) / alt32 (3 tiles x 32-key steps)
+  static const Fn alt64[7] = {
+      t16::attn_f16_alt_kernel<0, true, 2, 64>, t16::attn_f16_alt_kernel<1, true, 2, 64>,
+      t16::attn_f16_alt_kernel<2, true, 2, 64>, t16::attn_f16_alt_kernel<3, true, 2, 64>,
+      t16::attn_f16_alt_kernel<4, true, 2, 64>, t16::attn_f16_alt_kernel<5, true, 2, 64>,
+      t16::attn_f16_alt_kernel<6, true, 2, 64>};
+  static const Fn alt32[7] = {
+      t16::attn_f16_alt_kernel<0, true, 3, 32>, t16::attn_f16_alt_kernel<1, true, 3, 32>,
+      t16::attn_f16_alt_kernel<2, true, 3, 32>, t16::attn_f16_alt_kernel<3, true, 3, 32>,
+      t16::attn_f16_alt_kernel<4, true, 3, 32>, t16::attn_f16_alt_kernel<5, true, 3, 32>,
+      t16::attn_f16_alt_kernel<6, true, 3, 32>};
   static const Fn lp_kernels[7] = {
       t16::attn_f16_kernel<0, true, true>, t16::attn_f16_kernel<1, true, true>,
       t16::attn_f16_kernel<2, true, true>, t16::attn_f16_kernel<3, true, true>,
@@ -638,23 +677,31 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       t16::attn_f16_kernel<6, true, true>};
   static int np = -1, s64 = 0, use_alt = 0, lp = 0;
   const size_t smem = sizeof(t16::Smem) + 1024;
-  const size_t smem_alt = sizeof(t16::alt::Smem) + 1024;
+  const size_t smem64 = sizeof(t16::AltCfg<2, 64>::Smem) + 1024;
+  const size_t smem32 = sizeof(t16::AltCfg<3, 32>::Smem) + 1024;
   if (np < 0) {
     const char* e = getenv("GO_POLY16");
     np = e ? std::min(6, std::max(0, atoi(e))) : t16::DEFAULT_POLY_PAIRS;
     const char* e64 = getenv("GO_S64");
     s64 = e64 ? (atoi(e64) != 0) : t16::DEFAULT_S64;
     const char* ea = getenv("GO_ATTN16");
-    use_alt = ea ? !strcmp(ea, "alt") : t16::DEFAULT_ALT;
+    use_alt = ea ? (!strcmp(ea, "alt") ? 1 : !strcmp(ea, "alt32") ? 2 : 0) : t16::DEFAULT_ALT;
     for (auto& row : kernels)
       for (Fn f : row)
         CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const char* edbg = getenv("GO_ATTN_DEBUG");
+    if (edbg) {
+      const int v = atoi(edbg);
+      CUDA_CHECK(cudaMemcpyToSymbol(t16::g_attn_debug, &v, sizeof(int)));
+    }
     const char* elp = getenv("GO_POLYLP");
     lp = elp ? (atoi(elp) != 0) : t16::DEFAULT_LP;
     for (Fn f : lp_kernels)
       CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (Fn f : alt_kernels)
-      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_alt));
+    for (Fn f : alt64)
+      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
+    for (Fn f : alt32)
+      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32));
   }
   const int64_t total = (int64_t)n_head * Ttot * (t16::KT / 8) * 2;
   t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
@@ -664,11 +711,19 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
   t16::repack_q16_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
       q, ld, n_head, d_head, R, row_fwd, kmax, qscale, static_cast<__half*>(qh), flag);
   LAUNCH_CHECK();
-  if (use_alt && works2_dev && num_works2 > 0) {
+  if (use_alt == 1 && works2_dev && num_works2 > 0) {
     dim3 grid2((unsigned)num_works2, (unsigned)n_head);
-    alt_kernels[std::min(np, 4)]<<<grid2, t16::alt::THREADS, smem_alt, st>>>(
+    alt64[np]<<<grid2, t16::AltCfg<2, 64>::THREADS, smem64, st>>>(
         static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
         static_cast<const uint16_t*>(vb), R, Ttot, works2_dev, out, ldo, d_head, flag);
+    LAUNCH_CHECK();
+    return;
+  }
+  if (use_alt == 2) {
+    dim3 grid3((unsigned)num_works, (unsigned)n_head);
+    alt32[np]<<<grid3, t16::AltCfg<3, 32>::THREADS, smem32, st>>>(
+        static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
+        static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
     LAUNCH_CHECK();
     return;
   }
