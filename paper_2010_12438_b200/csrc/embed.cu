@@ -73,6 +73,9 @@ void neighbor_sample(const GraphView* views_dev, const int64_t* row_off_dev,
 // The feature row is sparse: one-hot op (12), log1p(flops), log1p(bytes), in/out
 // degree, and one prev-action one-hot per task; the affine is a sum of <= 5+T
 // weight rows.  task_col[t] = feature column of task t's action block.
+// One warp per feature row: the row's metadata (forward, op, the 4 static features, the
+// previous actions) is loaded once per warp and each lane produces 4 output columns as
+// a float4 (D % 4 == 0, D <= 128 * k handled by the column loop); W rows are L1-resident.
 __global__ void features_inproj_kernel(const GraphView* __restrict__ views,
                                        const int64_t* __restrict__ row_off,
                                        const int32_t* __restrict__ row_fwd, int64_t R,
@@ -80,6 +83,55 @@ __global__ void features_inproj_kernel(const GraphView* __restrict__ views,
                                        int tc0, int tc1, int tc2,
                                        const float* __restrict__ W, const float* __restrict__ b,
                                        int D, float* __restrict__ h, int64_t ldh) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= R) return;
+  const int f = row_fwd[r];
+  const GraphView& G = views[f];
+  const int64_t lr = r - row_off[f];
+  const float4 s4 = *reinterpret_cast<const float4*>(G.static4 + lr * 4);
+  const int op = G.op_row[lr];
+  int arow[3] = {0, 0, 0};
+  const int TP = prev ? T : 0;  // no previous actions on the first iteration
+  if (prev) {
+    const int node = G.order[lr];
+    const int tcs[3] = {tc0, tc1, tc2};
+    for (int t = 0; t < T; ++t) arow[t] = tcs[t] + prev[(int64_t)t * R + row_off[f] + node];
+  }
+  const int D4 = D >> 2;
+  const float4* W4 = reinterpret_cast<const float4*>(W);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float4* h4 = reinterpret_cast<float4*>(h + r * ldh);
+  for (int c = lane; c < D4; c += 32) {
+    float4 acc = W4[(int64_t)op * D4 + c];
+    const float4 w12 = W4[(int64_t)12 * D4 + c], w13 = W4[(int64_t)13 * D4 + c];
+    const float4 w14 = W4[(int64_t)14 * D4 + c], w15 = W4[(int64_t)15 * D4 + c];
+    acc.x = fmaf(s4.x, w12.x, acc.x); acc.y = fmaf(s4.x, w12.y, acc.y);
+    acc.z = fmaf(s4.x, w12.z, acc.z); acc.w = fmaf(s4.x, w12.w, acc.w);
+    acc.x = fmaf(s4.y, w13.x, acc.x); acc.y = fmaf(s4.y, w13.y, acc.y);
+    acc.z = fmaf(s4.y, w13.z, acc.z); acc.w = fmaf(s4.y, w13.w, acc.w);
+    acc.x = fmaf(s4.z, w14.x, acc.x); acc.y = fmaf(s4.z, w14.y, acc.y);
+    acc.z = fmaf(s4.z, w14.z, acc.z); acc.w = fmaf(s4.z, w14.w, acc.w);
+    acc.x = fmaf(s4.w, w15.x, acc.x); acc.y = fmaf(s4.w, w15.y, acc.y);
+    acc.z = fmaf(s4.w, w15.z, acc.z); acc.w = fmaf(s4.w, w15.w, acc.w);
+    for (int t = 0; t < TP; ++t) {
+      const float4 wa = W4[(int64_t)arow[t] * D4 + c];
+      acc.x += wa.x; acc.y += wa.y; acc.z += wa.z; acc.w += wa.w;
+    }
+    const float4 bb = b4[c];
+    h4[c] = make_float4(acc.x + bb.x, acc.y + bb.y, acc.z + bb.z, acc.w + bb.w);
+  }
+}
+
+// Scalar form (one thread per output element) for widths that are not multiples of 4.
+__global__ void features_inproj_scalar_kernel(const GraphView* __restrict__ views,
+                                              const int64_t* __restrict__ row_off,
+                                              const int32_t* __restrict__ row_fwd, int64_t R,
+                                              const int32_t* __restrict__ prev, int T,
+                                              int tc0, int tc1, int tc2,
+                                              const float* __restrict__ W,
+                                              const float* __restrict__ b, int D,
+                                              float* __restrict__ h, int64_t ldh) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= R * D) return;
   int64_t r = i / D;
@@ -109,7 +161,16 @@ void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
                      int num_tasks, const int32_t* task_col, const float* in_w,
                      const float* in_b, int D, float* h, int64_t ldh, cudaStream_t st) {
   if (R <= 0) return;
-  features_inproj_kernel<<<(unsigned)cdiv(R * D, 256), 256, 0, st>>>(
+  const bool vec = D % 4 == 0 && ldh % 4 == 0 && ((uintptr_t)in_w & 15) == 0 &&
+                   ((uintptr_t)in_b & 15) == 0 && ((uintptr_t)h & 15) == 0;
+  if (!vec) {
+    features_inproj_scalar_kernel<<<(unsigned)cdiv(R * D, 256), 256, 0, st>>>(
+        views_dev, row_off_dev, row_fwd, R, prev_actions, num_tasks, task_col[0], task_col[1],
+        task_col[2], in_w, in_b, D, h, ldh);
+    LAUNCH_CHECK();
+    return;
+  }
+  features_inproj_kernel<<<(unsigned)cdiv(R, 8), 256, 0, st>>>(
       views_dev, row_off_dev, row_fwd, R, prev_actions, num_tasks, task_col[0], task_col[1],
       task_col[2], in_w, in_b, D, h, ldh);
   LAUNCH_CHECK();
