@@ -384,6 +384,8 @@ def main():
     mufu = mufu_peak()
     ncu = ncu_traffic()
     cnt, hms, hflops = stats["heads_attention"]
+    n_fwd = K * args.steps * 2 // max(1, world)  # forwards this rank ran in the timed region
+    fwd_per_launch = n_fwd / cnt if cnt else 0.0
     roof = None
     if cnt:
         ach = hflops / cnt / (hms / cnt / 1000.0) / 1e12
@@ -393,9 +395,11 @@ def main():
         roof = {"bound": "tensor", "binding_unit": "MUFU ex2 (softmax exponentials)",
                 "kernel": "task-head N x N attention, tcgen05 kind::f16 + TMEM, fixed-offset softmax (attn_f16_kernel)",
                 "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
-                "traffic": ncu.get("heads_attention_bytes_per_forward"),
-                "traffic_note": "dram read+write per forward (one launch = one wave of forwards), "
-                                "ncu --set full, profiles/r1_ncu_summary.json",
+                "traffic": (ncu["heads_attention_bytes_per_forward"] * fwd_per_launch
+                            if "heads_attention_bytes_per_forward" in ncu else None),
+                "traffic_note": "dram read+write per launch (one launch = one wave of "
+                                f"{fwd_per_launch:.1f} forwards) = per-forward bytes of the ncu "
+                                "--set full capture (profiles/r1_ncu_summary.json) x forwards per launch",
                 "launches": cnt, "avg_launch_ms": hms / cnt,
                 "algorithmic_flops_per_launch": hflops / cnt,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if peaks
@@ -409,7 +413,8 @@ def main():
         ach = sbytes / cnt2 / (sms / cnt2 / 1000.0) / 1e9
         roof_agg = {"bound": "hbm", "kernel": "GraphSAGE gather + segment max", "achieved": ach,
                     "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": ncu.get("segment_max_bytes_per_launch_F1"),
+                    "traffic": (ncu["segment_max_bytes_per_forward_per_layer"] * n_fwd * w["ecfg"].gs_layers / cnt2
+                                if "segment_max_bytes_per_forward_per_layer" in ncu else None),
                     "launches": cnt2, "avg_launch_ms": sms / cnt2,
                     "algorithmic_bytes_per_launch": sbytes / cnt2, "share_of_step": sms / ms}
     line = {
