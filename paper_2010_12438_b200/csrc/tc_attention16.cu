@@ -80,6 +80,13 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   return r;
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // NP of every 8 exponential pairs go to the FMA-pipe polynomial (exp2_poly_f16x2), the
 // rest to MUFU.EX2: the MUFU (16 ex2/clk/SM) binds the all-MUFU kernel while the FMA
 // pipe idles, so splitting the work raises the exp rate (scripts/exp_probe.cu).
@@ -342,6 +349,191 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   if (warp == MMA_WARP0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
                  "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Double-buffered variant (GO_ATTN16=db): one CTA per SM owning all 512 TMEM columns,
+// 3 query tiles x (2 x 64 S columns) + 3 x 16 O columns.  S(j+2) is computed into the
+// buffer of step j right after PV(j), while the softmax warps work on step j+1, so the
+// softmax warps never wait for an S MMA in steady state (fewer warps per SM, though).
+// SPLIT = 2: two softmax warps per (tile, TMEM lane quarter), each owning 32 of the 64
+// columns of a step, so the SM keeps 24 softmax warps (6 per SMSP) with no S waits.
+template <int SPLIT>
+struct DbCfg {
+  static constexpr int SOFT = NQT * 4 * SPLIT;
+  static constexpr int PRODUCER = SOFT;
+  static constexpr int MMA0 = SOFT + 1;
+  static constexpr int THREADS = (SOFT + 1 + NQT) * 32;
+};
+template <int NP, int SPLIT>
+__global__ void __launch_bounds__(DbCfg<SPLIT>::THREADS, 1)
+    attn_f16_db_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
+                       const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
+                       const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
+                       int d_head, const int32_t* __restrict__ flag) {
+  constexpr uint32_t DB_COLS = 512;
+  constexpr uint32_t DB_O = NQT * 128;
+  using C = DbCfg<SPLIT>;
+  constexpr int PRODUCER_WARP = C::PRODUCER, MMA_WARP0 = C::MMA0, NUM_THREADS = C::THREADS;
+  if (*flag) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TcWork w = works[blockIdx.x];
+  const int head = blockIdx.y;
+  const int T = w.tiles;
+  const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
+  if (warp == PRODUCER_WARP && lane == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], NQT);
+    }
+    for (int t = 0; t < NQT; ++t) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&sm.s_full[t][b], 1);
+        mbar_init(&sm.p_full[t][b], 128 * SPLIT);
+      }
+      mbar_init(&sm.o_done[t], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(DB_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < NQT * QT * 2; i += NUM_THREADS) {
+    const int qt = i / (QT * 2), rem = i % (QT * 2);
+    const int r = rem >> 1, c = rem & 1;
+    const int lr = w.q0 + qt * QT + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (lr < w.n)
+      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
+    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
+  }
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == PRODUCER_WARP) {
+    if (lane == 0) {
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        if (j >= NS) mbar_wait_sleep(&sm.kv_empty[s], ((j / NS) - 1) & 1);
+        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
+        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= MMA_WARP0) {
+    if (lane == 0) {
+      const int t = warp - MMA_WARP0;
+      constexpr uint32_t ID_S = idesc_f16(QT, KT);
+      constexpr uint32_t ID_O = idesc_f16(QT, 16);
+      const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
+      const uint32_t reg = tbase + t * 128;
+      const uint32_t d = tbase + DB_O + t * 16;
+      auto issue_s = [&](int j) {
+        const int s = j % NS;
+        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
+        fence_after();
+        umma_ss_f16(reg + (j & 1) * 64, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
+        umma_commit(&sm.s_full[t][j & 1]);
+      };
+      for (int j = 0; j < 2 && j < T; ++j) issue_s(j);
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        mbar_wait_sleep(&sm.p_full[t][j & 1], (j >> 1) & 1);
+        fence_after();
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
+        const uint32_t pa = reg + (j & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < KT / 16; ++kk)
+          umma_ts_f16(d, pa + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
+        if (j + 2 < T) issue_s(j + 2);  // same buffer, in-order after the PV reading P(j)
+        umma_commit(&sm.kv_empty[s]);
+      }
+      umma_commit(&sm.o_done[t]);
+    }
+    __syncwarp();
+  } else {
+    const int t = warp / (4 * SPLIT);
+    const int wq = warp & 3;
+    const int half = SPLIT == 2 ? (warp >> 2) & 1 : 0;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
+        const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+        pk[i] = poly ? exp2_poly_f16x2_lp(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
+      }
+    };
+    uint32_t ra[16], rb[16], pk[8];
+    for (int j = 0; j < T; ++j) {
+      const uint32_t base = tbase + lane_off + t * 128 + (j & 1) * 64;
+      mbar_wait_sleep(&sm.s_full[t][j & 1], (j >> 1) & 1);
+      fence_after();
+      if constexpr (SPLIT == 2) {
+        // chunks 2*half, 2*half + 1; P of chunk c lands on columns [8c, 8c + 8), which
+        // for half 1 (c = 2, 3 -> columns 16..31) lie in half 0's S chunk 1: wait for
+        // half 0 to have read it (it reads both its chunks before its first P store)
+        const uint32_t sb = base + 32 * half;
+        PTX_LD16(sb, ra);
+        PTX_LD16(sb + 16, rb);
+        tmem_wait_ld();
+        if (half == 1) named_bar_sync(1 + t * 4 + wq, 64);
+        else named_bar_arrive(1 + t * 4 + wq, 64);
+        softmax16(ra, pk);
+        PTX_ST8(base + 16 * half, pk);
+        softmax16(rb, pk);
+        PTX_ST8(base + 16 * half + 8, pk);
+      } else {
+        PTX_LD16(base, ra);
+        tmem_wait_ld();
+        PTX_LD16(base + 16, rb);
+        softmax16(ra, pk);
+        PTX_ST8(base, pk);
+        tmem_wait_ld();
+        PTX_LD16(base + 32, ra);
+        softmax16(rb, pk);
+        PTX_ST8(base + 8, pk);
+        tmem_wait_ld();
+        PTX_LD16(base + 48, rb);
+        softmax16(ra, pk);
+        PTX_ST8(base + 16, pk);
+        tmem_wait_ld();
+        softmax16(rb, pk);
+        PTX_ST8(base + 24, pk);
+      }
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&sm.p_full[t][j & 1]);
+    }
+    mbar_wait_sleep(&sm.o_done[t], 0);
+    fence_after();
+    uint32_t r[16];
+    PTX_LD16(tbase + lane_off + DB_O + t * 16, r);
+    tmem_wait_ld();
+    const int lr = w.q0 + t * QT + wq * 32 + lane;
+    if (lr < w.n && half == 0) {
+      const float inv = 1.f / __uint_as_float(r[15]);
+      float* o = out + (w.row0 + lr) * ldo + head * d_head;
+      for (int dd = 0; dd < d_head; ++dd) o[dd] = __uint_as_float(r[dd]) * inv;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == MMA_WARP0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(DB_COLS));
   }
 }
 
@@ -675,6 +867,13 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       t16::attn_f16_kernel<2, true, true>, t16::attn_f16_kernel<3, true, true>,
       t16::attn_f16_kernel<4, true, true>, t16::attn_f16_kernel<5, true, true>,
       t16::attn_f16_kernel<6, true, true>};
+  static const Fn dbk[2][7] = {
+      {t16::attn_f16_db_kernel<0, 1>, t16::attn_f16_db_kernel<1, 1>, t16::attn_f16_db_kernel<2, 1>,
+       t16::attn_f16_db_kernel<3, 1>, t16::attn_f16_db_kernel<4, 1>, t16::attn_f16_db_kernel<5, 1>,
+       t16::attn_f16_db_kernel<6, 1>},
+      {t16::attn_f16_db_kernel<0, 2>, t16::attn_f16_db_kernel<1, 2>, t16::attn_f16_db_kernel<2, 2>,
+       t16::attn_f16_db_kernel<3, 2>, t16::attn_f16_db_kernel<4, 2>, t16::attn_f16_db_kernel<5, 2>,
+       t16::attn_f16_db_kernel<6, 2>}};
   static int np = -1, s64 = 0, use_alt = 0, lp = 0;
   const size_t smem = sizeof(t16::Smem) + 1024;
   const size_t smem64 = sizeof(t16::AltCfg<2, 64>::Smem) + 1024;
@@ -685,7 +884,11 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
     const char* e64 = getenv("GO_S64");
     s64 = e64 ? (atoi(e64) != 0) : t16::DEFAULT_S64;
     const char* ea = getenv("GO_ATTN16");
-    use_alt = ea ? (!strcmp(ea, "alt") ? 1 : !strcmp(ea, "alt32") ? 2 : 0) : t16::DEFAULT_ALT;
+    use_alt = ea ? (!strcmp(ea, "alt") ? 1 : !strcmp(ea, "alt32") ? 2 : !strcmp(ea, "db") ? 3 : !strcmp(ea, "db2") ? 4 : 0)
+                 : t16::DEFAULT_ALT;
+    for (auto& row : dbk)
+      for (Fn f : row)
+        CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (auto& row : kernels)
       for (Fn f : row)
         CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -716,6 +919,15 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
     alt64[np]<<<grid2, t16::AltCfg<2, 64>::THREADS, smem64, st>>>(
         static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
         static_cast<const uint16_t*>(vb), R, Ttot, works2_dev, out, ldo, d_head, flag);
+    LAUNCH_CHECK();
+    return;
+  }
+  if (use_alt == 3 || use_alt == 4) {
+    dim3 grid4((unsigned)num_works, (unsigned)n_head);
+    const int sp = use_alt == 4;
+    dbk[sp][np]<<<grid4, sp ? t16::DbCfg<2>::THREADS : t16::DbCfg<1>::THREADS, smem, st>>>(
+        static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
+        static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
     LAUNCH_CHECK();
     return;
   }
