@@ -553,11 +553,11 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
     float* out = A.take<float>(nf);
     void* out16 = A.take<float>((nf + 1) / 2);
     tc_gemm_pack(w0, w1, w2, Nsub, ldw, K, N, out, st);
-    tc_gemm_pack16(w0, w1, w2, Nsub, ldw, K, N, out16, st);
     TcW w;
     w.w32 = out;
     w.w16 = out16;
     w.ovf = ovf_flags + n_packs++;
+    tc_gemm_pack16(w0, w1, w2, Nsub, ldw, K, N, out16, st, w.ovf);
     return w;
   };
   auto pack1 = [&](const float* w, int K, int N) { return pack(w, nullptr, nullptr, N, N, K, N); };
@@ -630,9 +630,13 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
     // layer whose operands left the fp16 range).  Measured 0.61-0.66 ms/forward at cfg4
     // against 0.41 ms for the SIMT banded kernel (2 CTAs/SM by TMEM, latency-bound
     // staging), so SIMT stays the default.
+    // Default: warp-level MMA banded attention (trunk_mma.cu), with the SIMT kernel
+    // re-running a layer whose operands left the fp16 range; GO_TRUNK=simt forces SIMT.
     const char* trunk_env = getenv("GO_TRUNK");
     const bool trunk_tc = m.trunk_tc_ok && trunk_tc_supported(H, dh) && trunk_env &&
                           !strcmp(trunk_env, "tc");
+    const bool trunk_mma = !trunk_tc && trunk_mma_supported(dh) &&
+                           !(trunk_env && !strcmp(trunk_env, "simt"));
     int32_t* trunk_flags = A.take<int32_t>(Lt + 1);
     if (trunk_tc) CUDA_CHECK(cudaMemsetAsync(trunk_flags, 0, (Lt + 1) * sizeof(int32_t), st));
     {
@@ -655,6 +659,11 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
         if (trunk_tc) {
           trunk_attention_tc(QKV, LQ, H, dh, cfg.segment_len, m.d_trunk_tc, m.n_trunk_tc, Ab, LA,
                              trunk_flags + l, st);
+          attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
+                    LA, st, nullptr, trunk_flags + l);
+        } else if (trunk_mma) {
+          trunk_attention_mma(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles,
+                              m.n_trunk_tiles, Ab, LA, trunk_flags + l, st);
           attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
                     LA, st, nullptr, trunk_flags + l);
         } else {

@@ -206,6 +206,14 @@ void trunk_attention_tc(const float* qkv, int64_t ld, int n_head, int d_head, in
                         const TrunkTile* tiles_dev, int64_t num_tiles, float* out, int64_t ldo,
                         int32_t* flag, cudaStream_t st);
 
+// ---- kernels: trunk_mma.cu (banded trunk attention on mma.sync m16n8k16, d_head <= 16);
+// *flag (zeroed here) is set if some operand left the fp16 range -- the caller then
+// re-runs attention() gated on it
+bool trunk_mma_supported(int d_head);
+void trunk_attention_mma(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+                         int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
+                         int64_t ldo, int32_t* flag, cudaStream_t st);
+
 // ---- kernels: tc_attention.cu (tcgen05 / TMEM full attention, d_head <= 16)
 struct TcWork {
   int32_t f, q0, n, tiles;
@@ -272,7 +280,8 @@ size_t tc_gemm_packed_floats(int K, int N);
 void tc_gemm_pack(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw, int K,
                   int N, float* out, cudaStream_t st);
 void tc_gemm_pack16(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw,
-                    int K, int N, void* out, cudaStream_t st);
+                    int K, int N, void* out, cudaStream_t st,
+                    int32_t* ovf = nullptr);
 void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
              const TcW& W, const float* bias, float* C, int64_t ldc, int64_t M, int N, int act,
              cudaStream_t st);

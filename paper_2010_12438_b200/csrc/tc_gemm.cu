@@ -629,7 +629,8 @@ __global__ void pack_b_kernel(const float* __restrict__ W0, const float* __restr
 // of a block at (k/8)*(BN*8) + (n/8)*64 + (n%8)*8 + k%8 (no-swizzle K-major, 8 halfs/16 B).
 __global__ void pack_b16_kernel(const float* __restrict__ W0, const float* __restrict__ W1,
                                 const float* __restrict__ W2, int Nsub, int64_t ldw, int K,
-                                int N, int BN, int nch, int nblk, __half* __restrict__ out) {
+                                int N, int BN, int nch, int nblk, __half* __restrict__ out,
+                                int32_t* __restrict__ ovf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)nblk * nch * BN * BK;
   if (i >= total) return;
@@ -645,6 +646,8 @@ __global__ void pack_b16_kernel(const float* __restrict__ W0, const float* __res
     const int part = n / Nsub, nn = n % Nsub;
     const float* W = part == 0 ? W0 : (part == 1 ? W1 : W2);
     w = W[(int64_t)k * ldw + nn] * (float)(1 << W16_SHIFT);
+    // a weight beyond the fp16 range routes this GEMM to its tf32 re-run
+    if (ovf && !(fabsf(w) <= 65504.f)) atomicOr(ovf, 1);
   }
   const __half h = __float2half_rn(w);
   const __half l = __float2half_rn(w - __half2float(h));
@@ -678,13 +681,14 @@ size_t tc_gemm_packed_floats(int K, int N) {
 
 // fp16 twin (W scaled by 2^W16_SHIFT): same element count, 2 bytes each.
 void tc_gemm_pack16(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw,
-                    int K, int N, void* out, cudaStream_t st) {
+                    int K, int N, void* out, cudaStream_t st, int32_t* ovf) {
   int BN = tc_gemm_bn(N);
   int nblk = (int)cdiv(N, BN);
   int nch = (int)cdiv(K, tg::BK);
   int64_t total = (int64_t)nblk * nch * BN * tg::BK;
   tg::pack_b16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
-      W0, W1 ? W1 : W0, W2 ? W2 : W0, Nsub, ldw, K, N, BN, nch, nblk, static_cast<__half*>(out));
+      W0, W1 ? W1 : W0, W2 ? W2 : W0, Nsub, ldw, K, N, BN, nch, nblk, static_cast<__half*>(out),
+      ovf);
   LAUNCH_CHECK();
 }
 

@@ -1,0 +1,212 @@
+// Segmented (block-banded) trunk attention on warp-level tensor-core MMAs
+// (policy.py:157-177: the queries of segment s attend to the keys of segments s-1 and s
+// of the same forward; multi_head_attention / scaled_dot_attention, tensor.py:382-388).
+//
+// The trunk's attention is tiny per query (<= 2S = 128 keys, d_head = 15), so it is
+// bound by moving Q/K/V once and by the per-key instruction count, not by tensor math.
+// The SIMT kernel (attention.cu) spends 32 FFMA + 8 LDS per (query, key); here a warp
+// handles 16 queries with mma.sync.m16n8k16 (fp16 operands, fp32 accumulation):
+//   S  = Q K^T   8 MMAs per 64-key chunk (n-tiles of 8 keys, K = 16 = padded d_head)
+//   O += P V     8 MMAs per 64-key chunk (4 k-steps of 16 keys x 2 n-tiles of 8 dims)
+// with the S accumulator fragments reused directly as the A fragments of P (the
+// m16n8k16 C layout equals the A layout), exact online softmax (running max) per row.
+// CTA = one 64-query tile of the banded tile list x one head, 4 warps; key chunks of 64
+// staged in shared memory as fp16 (K row-major, V transposed), rows padded so the
+// fragment loads are bank-conflict free.
+//
+// Precision: Q (pre-scaled by log2(e)/sqrt(d)), K, V and P rounded to fp16 (10-bit
+// mantissa, the same as the head attention's operands); operands beyond the fp16 range
+// set *flag and the caller re-runs the SIMT kernel gated on it.
+#include <cmath>
+#include <cuda_fp16.h>
+
+#include "engine.cuh"
+
+namespace go {
+namespace tm {
+
+constexpr int QT = 64;      // queries per CTA
+constexpr int KC = 64;      // keys per chunk
+constexpr int KS = 24;      // Ks row stride (halves): 48 B, conflict-free fragment loads
+constexpr int VS = KC + 8;  // Vt row stride (halves): 144 B
+constexpr float RANGE = 60000.f;
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(128) trunk_mma_kernel(
+    const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    int64_t ld, int d_head, const AttnTile* __restrict__ tiles, float* __restrict__ out,
+    int64_t ldo, float qscale, int32_t* __restrict__ flag) {
+  __shared__ __align__(16) __half Ks[KC * KS];
+  __shared__ __align__(16) __half Vt[16 * VS];
+  const AttnTile tl = tiles[blockIdx.x];
+  const int head = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int64_t col0 = (int64_t)head * d_head;
+  bool big = false;
+
+  // A fragments of this warp's 16 queries (rows g and g + 8, dims 2tq.. and 2tq+8..)
+  uint32_t qa[4];
+  {
+    const int64_t r0 = tl.q0 + warp * 16 + g, r1 = r0 + 8;
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t r = (i & 1) ? r1 : r0;  // order: (r0,d0) (r1,d0) (r0,d8) (r1,d8) pairs
+      const int d = 2 * tq + ((i >> 2) ? 8 : 0) + ((i >> 1) & 1);
+      float val = 0.f;
+      if (r < tl.q1 && d < d_head) val = q[r * ld + col0 + d] * qscale;
+      big |= !(fabsf(val) <= RANGE);
+      x[i] = val;
+    }
+    // x[0]=(r0,2tq) x[1]=(r1,2tq) x[2]=(r0,2tq+1) x[3]=(r1,2tq+1) x[4..7] same at +8
+    qa[0] = pack2(x[0], x[2]);
+    qa[1] = pack2(x[1], x[3]);
+    qa[2] = pack2(x[4], x[6]);
+    qa[3] = pack2(x[5], x[7]);
+  }
+  float o[2][4];
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[n][e] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int64_t kc = tl.k0; kc < tl.k1; kc += KC) {
+    const int64_t rem = tl.k1 - kc;
+    const int nk = rem < KC ? (int)rem : KC;
+    __syncthreads();
+    {
+      // stage: thread = (key, 8-dim half); K row-major [key][d], V transposed [d][key]
+      const int key = tid >> 1, d0 = (tid & 1) * 8;
+      __align__(16) __half kr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int d = d0 + i;
+        float kv = 0.f, vv = 0.f;
+        if (key < nk && d < d_head) {
+          kv = k[(kc + key) * ld + col0 + d];
+          vv = v[(kc + key) * ld + col0 + d];
+          big |= !(fabsf(kv) <= RANGE) || !(fabsf(vv) <= RANGE);
+        }
+        kr[i] = __float2half_rn(kv);
+        Vt[d * VS + key] = __float2half_rn(vv);
+      }
+      *reinterpret_cast<uint4*>(&Ks[key * KS + d0]) = *reinterpret_cast<const uint4*>(kr);
+    }
+    __syncthreads();
+    // S = Q K^T: 8 n-tiles of 8 keys
+    float s[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+      const __half* kp = &Ks[(8 * n + g) * KS + 2 * tq];
+      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kp);
+      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kp + 8);
+      mma16816(s[n], qa, b0, b1);
+    }
+    // online softmax over the chunk (rows g: s[.][0..1], g + 8: s[.][2..3])
+    float c0 = -INFINITY, c1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int key = 8 * n + 2 * tq;
+      if (key >= nk) s[n][0] = s[n][2] = -INFINITY;
+      if (key + 1 >= nk) s[n][1] = s[n][3] = -INFINITY;
+      c0 = fmaxf(c0, fmaxf(s[n][0], s[n][1]));
+      c1 = fmaxf(c1, fmaxf(s[n][2], s[n][3]));
+    }
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 1));
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 2));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 1));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 2));
+    const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+    const float f0 = ex2(m0 - n0), f1 = ex2(m1 - n1);  // 0 on the first chunk
+    m0 = n0;
+    m1 = n1;
+    l0 *= f0;
+    l1 *= f1;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      o[n][0] *= f0;
+      o[n][1] *= f0;
+      o[n][2] *= f1;
+      o[n][3] *= f1;
+    }
+    uint32_t pa[8][2];  // P as fp16 pairs: [n-tile][row g | row g+8]
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float p0 = ex2(s[n][0] - m0), p1 = ex2(s[n][1] - m0);
+      const float p2 = ex2(s[n][2] - m1), p3 = ex2(s[n][3] - m1);
+      l0 += p0 + p1;
+      l1 += p2 + p3;
+      pa[n][0] = pack2(p0, p1);
+      pa[n][1] = pack2(p2, p3);
+    }
+    // O += P V: k-steps of 16 keys (n-tiles 2kk, 2kk+1), n-tiles of 8 dims
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        const __half* vp = &Vt[(8 * n + g) * VS + 16 * kk + 2 * tq];
+        mma16816(o[n], a, *reinterpret_cast<const uint32_t*>(vp),
+                 *reinterpret_cast<const uint32_t*>(vp + 8));
+      }
+    }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  const int64_t r0 = tl.q0 + warp * 16 + g, r1 = r0 + 8;
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+    const int d = 8 * n + 2 * tq;
+    if (r0 < tl.q1) {
+      if (d < d_head) out[r0 * ldo + col0 + d] = o[n][0] * i0;
+      if (d + 1 < d_head) out[r0 * ldo + col0 + d + 1] = o[n][1] * i0;
+    }
+    if (r1 < tl.q1) {
+      if (d < d_head) out[r1 * ldo + col0 + d] = o[n][2] * i1;
+      if (d + 1 < d_head) out[r1 * ldo + col0 + d + 1] = o[n][3] * i1;
+    }
+  }
+  if (big) atomicOr(flag, 1);
+}
+
+}  // namespace tm
+
+bool trunk_mma_supported(int d_head) { return d_head >= 1 && d_head <= 16; }
+
+void trunk_attention_mma(const float* q, const float* k, const float* v, int64_t ld, int n_head,
+                         int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
+                         int64_t ldo, int32_t* flag, cudaStream_t st) {
+  if (num_tiles <= 0) return;
+  GO_CHECK(d_head <= 16, "trunk_attention_mma needs d_head <= 16");
+  CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
+  const float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
+  dim3 grid((unsigned)num_tiles, (unsigned)n_head);
+  tm::trunk_mma_kernel<<<grid, 128, 0, st>>>(q, k, v, ld, d_head, tiles_dev, out, ldo, qscale,
+                                             flag);
+  LAUNCH_CHECK();
+}
+
+}  // namespace go

@@ -160,8 +160,17 @@ def test_tc_gemm_forward_matches_simt_and_oracle():
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 300, 1, 64, seed=0), node_cap=10**6),
               gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))]
     seeds = [5, 6]
-    ne_t, lg_t, v_t = _forward_with("tc", store, ecfg, pcfg, sizes, graphs, seeds)
-    ne_s, lg_s, v_s = _forward_with("simt", store, ecfg, pcfg, sizes, graphs, seeds)
+    # same trunk attention kernel in both modes (the default mma trunk runs fp16 operands)
+    old_trunk = os.environ.get("GO_TRUNK")
+    os.environ["GO_TRUNK"] = "simt"
+    try:
+        ne_t, lg_t, v_t = _forward_with("tc", store, ecfg, pcfg, sizes, graphs, seeds)
+        ne_s, lg_s, v_s = _forward_with("simt", store, ecfg, pcfg, sizes, graphs, seeds)
+    finally:
+        if old_trunk is None:
+            os.environ.pop("GO_TRUNK", None)
+        else:
+            os.environ["GO_TRUNK"] = old_trunk
     assert rel_err(ne_t, ne_s) < 1e-5
     assert rel_err(lg_t, lg_s) < 1e-5
     assert rel_err(v_t, v_s) < 1e-5
@@ -207,10 +216,47 @@ def test_trunk_tc_matches_simt(seg):
               gen_workload(WorkloadSpec("dilated-stack", 5, 40, 64, seed=2), node_cap=10**6)]
     seeds = [3, 4, 5]
     h_tc, lg_tc = _forward_env("GO_TRUNK", "tc", store, ecfg, pcfg, sizes, graphs, seeds)
-    h_s, lg_s = _forward_env("GO_TRUNK", None, store, ecfg, pcfg, sizes, graphs, seeds)
+    h_s, lg_s = _forward_env("GO_TRUNK", "simt", store, ecfg, pcfg, sizes, graphs, seeds)
     # single-pass fp16 (tf32-equivalent) Q.K^T and P.V: ~4e-5 normwise
     assert rel_err(h_tc, h_s) < 1e-4
     assert rel_err(lg_tc, lg_s) < 1e-4
+
+
+@pytest.mark.parametrize("seg", [64, 32, 16, 48, 100, 200])
+def test_trunk_mma_matches_simt(seg):
+    """The default banded trunk attention on mma.sync (trunk_mma.cu: 64-query tiles,
+    64-key chunks with an online max, fp16 operands) agrees with the fp32 SIMT kernel
+    (GO_TRUNK=simt) on a ragged batch; segment lengths that are not multiples of the
+    64-query tile and windows wider than one key chunk (200 -> 400 keys) included."""
+    from paper_2010_12438_b200 import EmbedConfig, PolicyConfig
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    sizes = {"placement": 8}
+    ecfg, pcfg, store = _store(sizes, EmbedConfig(), PolicyConfig(segment_len=seg))
+    graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 60, 1, 64, seed=1), node_cap=10**6),
+              gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0)),
+              gen_workload(WorkloadSpec("dilated-stack", 5, 40, 64, seed=2), node_cap=10**6)]
+    seeds = [3, 4, 5]
+    h_m, lg_m = _forward_env("GO_TRUNK", None, store, ecfg, pcfg, sizes, graphs, seeds)
+    h_s, lg_s = _forward_env("GO_TRUNK", "simt", store, ecfg, pcfg, sizes, graphs, seeds)
+    assert rel_err(h_m, h_s) < 1e-4
+    assert rel_err(lg_m, lg_s) < 1e-4
+
+
+def test_trunk_mma_out_of_range_reruns_simt():
+    """Q/K/V beyond the fp16 range flag the layer and the SIMT kernel re-runs it: the
+    forward stays finite and equal to the SIMT-only forward up to the fp16 rounding of
+    the other (in-range) layers; without the re-run layer 0 would be inf / NaN."""
+    sizes = {"placement": 4}
+    ecfg, pcfg, store = _store(sizes)
+    # |q| ~ 1e5 > the fp16 range: softmax becomes a near-argmax, outputs stay moderate
+    store["policy/block0/attn_q_w"].data = store["policy/block0/attn_q_w"].data * 3e5
+    store.touch()
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    graphs = [gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))]
+    h_m, lg_m = _forward_env("GO_TRUNK", None, store, ecfg, pcfg, sizes, graphs, [7])
+    h_s, lg_s = _forward_env("GO_TRUNK", "simt", store, ecfg, pcfg, sizes, graphs, [7])
+    assert np.isfinite(h_s).all() and np.isfinite(h_m).all()
+    assert rel_err(h_m, h_s) < 1e-4
 
 
 def test_fp16_gemm_matches_tf32_and_reruns_out_of_range():
@@ -222,16 +268,28 @@ def test_fp16_gemm_matches_tf32_and_reruns_out_of_range():
     ecfg, pcfg, store = _store(sizes)
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 200, 1, 64, seed=4), node_cap=10**6)]
     seeds = [9]
-    for scale in (1.0, 3e4):
-        if scale != 1.0:
-            store["embed/in_w"].data = store["embed/in_w"].data * scale
-            store.touch()
-        h16, lg16 = _forward_env("GO_GEMM_F16", None, store, ecfg, pcfg, sizes, graphs, seeds)
-        h32, lg32 = _forward_env("GO_GEMM_F16", "0", store, ecfg, pcfg, sizes, graphs, seeds)
-        assert np.isfinite(lg16).all()
-        # at 3e4 the embedding is ~1e5 in magnitude and the trunk's LayerNorms amplify the
-        # (equal-size, differently rounded) 3-pass errors of both paths; without the
-        # re-run the fp16 pass would overflow to inf
-        tol = 1e-5 if scale == 1.0 else 1e-4
-        assert rel_err(h16, h32) < tol, scale
-        assert rel_err(lg16, lg32) < tol, scale
+    old_trunk = os.environ.get("GO_TRUNK")
+    os.environ["GO_TRUNK"] = "simt"  # compare the GEMMs alone (the mma trunk is fp16)
+    try:
+        for scale in (1.0, 3e4):
+            _fp16_gemm_case(store, ecfg, pcfg, sizes, graphs, seeds, scale)
+    finally:
+        if old_trunk is None:
+            os.environ.pop("GO_TRUNK", None)
+        else:
+            os.environ["GO_TRUNK"] = old_trunk
+
+
+def _fp16_gemm_case(store, ecfg, pcfg, sizes, graphs, seeds, scale):
+    if scale != 1.0:
+        store["embed/in_w"].data = store["embed/in_w"].data * scale
+        store.touch()
+    h16, lg16 = _forward_env("GO_GEMM_F16", None, store, ecfg, pcfg, sizes, graphs, seeds)
+    h32, lg32 = _forward_env("GO_GEMM_F16", "0", store, ecfg, pcfg, sizes, graphs, seeds)
+    assert np.isfinite(lg16).all()
+    # at 3e4 the embedding is ~1e5 in magnitude and the trunk's LayerNorms amplify the
+    # (equal-size, differently rounded) 3-pass errors of both paths; without the
+    # re-run the fp16 pass would overflow to inf
+    tol = 1e-5 if scale == 1.0 else 1e-4
+    assert rel_err(h16, h32) < tol, scale
+    assert rel_err(lg16, lg32) < tol, scale
