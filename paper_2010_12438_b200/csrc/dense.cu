@@ -198,14 +198,21 @@ void row_fwd_fill(const int64_t* row_off_dev, int F, int64_t R, int32_t* row_fwd
 __global__ void mean_partial_kernel(const float* __restrict__ x, int64_t ldx,
                                     const int64_t* __restrict__ chunk_row0,
                                     const int64_t* __restrict__ chunk_row1, int D,
-                                    float* __restrict__ part) {
+                                    float* __restrict__ part, int32_t* __restrict__ flag) {
   int64_t c = blockIdx.x;
   int64_t r0 = chunk_row0[c], r1 = chunk_row1[c];
+  bool bad = false;
   for (int col = threadIdx.x; col < D; col += blockDim.x) {
     float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) s += x[r * ldx + col];
+    for (int64_t r = r0; r < r1; ++r) {
+      const float v = x[r * ldx + col];
+      bad |= !isfinite(v);
+      s += v;
+    }
     part[c * D + col] = s;
   }
+  // fused non-finite check of the rows being averaged (embedding.py:96-97)
+  if (flag && bad) atomicOr(flag, 1);
 }
 
 __global__ void mean_final_kernel(const float* __restrict__ part,
@@ -224,11 +231,11 @@ __global__ void mean_final_kernel(const float* __restrict__ part,
 
 void mean_rows(const float* x, int64_t ldx, const int64_t* row_off_dev, int F,
                const int64_t* chunk_tab, int64_t nc, int D, float* out, int64_t ldo,
-               float* part, cudaStream_t st) {
+               float* part, cudaStream_t st, int32_t* finite_flag) {
   // chunk_tab (device): [nc] chunk row0, [nc] chunk row1, [F] first chunk, [F] end chunk
   if (nc > 0)
     mean_partial_kernel<<<(unsigned)nc, 128, 0, st>>>(x, ldx, chunk_tab, chunk_tab + nc, D,
-                                                      part);
+                                                      part, finite_flag);
   mean_final_kernel<<<F, 128, 0, st>>>(part, chunk_tab + 2 * nc, chunk_tab + 2 * nc + F,
                                        row_off_dev, D, out, ldo);
   if (nc > 0) g_launch_count++;

@@ -377,9 +377,9 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
       h = hn;
       ldh = ldn;
     }
-    if (status_dev) check_finite(node_embed, gs, R, gs, status_dev, st);
+    // non-finite check fused into the mean's pass over node_embed
     mean_rows(node_embed, gs, m.d_row_off, F, m.d_chunks, m.n_chunks, gs, graph_embed, gs, part,
-              st);
+              st, status_dev);
   }
 
   // ---- trunk (policy.py:122-177), layer-major block-banded attention
@@ -608,9 +608,9 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       }
       h = hn;
     }
-    if (status_dev) check_finite(node_embed, gs, R, gs, status_dev, st);
+    // non-finite check fused into the mean's pass over node_embed
     mean_rows(node_embed, gs, m.d_row_off, F, m.d_chunks, m.n_chunks, gs, graph_embed, gs, part,
-              st);
+              st, status_dev);
   }
 
   if (do_t) {
@@ -641,11 +641,14 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
     if (trunk_tc) CUDA_CHECK(cudaMemsetAsync(trunk_flags, 0, (Lt + 1) * sizeof(int32_t), st));
     {
       KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * dm);
-      tc_gemm(node_embed, gs, gs, nullptr, 0, 0, pack1(W_(S.p_in_w()), gs, dm), W_(S.p_in_b()), x0,
-              dm, R, dm, 0, st);
+      if (Lt > 0)  // xm = (node_embed @ in_w + b) * m(forward), modulation in the epilogue
+        tc_gemm_scaled(node_embed, gs, gs, pack1(W_(S.p_in_w()), gs, dm), W_(S.p_in_b()),
+                       nullptr, 0, modp, row_fwd, X[1], LW, R, dm, 0, st);
+      else
+        tc_gemm(node_embed, gs, gs, nullptr, 0, 0, pack1(W_(S.p_in_w()), gs, dm),
+                W_(S.p_in_b()), x0, dm, R, dm, 0, st);
     }
     float* xm = X[1];
-    if (Lt > 0) mul_rowvec(x0, LW, modp, dm, row_fwd, xm, LW, R, dm, st);
     for (int l = 0; l < Lt; ++l) {
       const float* bq = qkv_bias(W_(S.blk(l, Q_B)), W_(S.blk(l, K_B)), W_(S.blk(l, V_B)));
       {

@@ -137,7 +137,8 @@ void mul_rowvec(const float* x, int64_t ldx, const float* vec, int64_t ldv,
 constexpr int MEAN_CHUNK = 256;
 void mean_rows(const float* x, int64_t ldx, const int64_t* row_off_dev, int F,
                const int64_t* chunk_tab, int64_t nc, int D, float* out, int64_t ldo,
-               float* part, cudaStream_t st);
+               float* part, cudaStream_t st,
+               int32_t* finite_flag = nullptr);
 void check_finite(const float* x, int64_t ld, int64_t M, int D, int32_t* flag, cudaStream_t st);
 void row_fwd_fill(const int64_t* row_off_dev, int F, int64_t R, int32_t* row_fwd,
                   cudaStream_t st);
@@ -285,6 +286,10 @@ void tc_gemm_pack16(const float* W0, const float* W1, const float* W2, int Nsub,
 void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
              const TcW& W, const float* bias, float* C, int64_t ldc, int64_t M, int N, int act,
              cudaStream_t st);
+// C2 = act(A1 @ W + bias) * rowscale[row_fwd[r]] (rowscale: [F, N]); C (unscaled) optional
+void tc_gemm_scaled(const float* A1, int64_t lda1, int K1, const TcW& Wpk, const float* bias,
+                    float* C, int64_t ldc, const float* rowscale, const int32_t* row_fwd,
+                    float* C2, int64_t ldc2, int64_t M, int N, int act, cudaStream_t st);
 void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
                 const TcW& W, const float* bias, const float* resid, int64_t ldr,
                 const float* g, const float* beta, float* C, int64_t ldc, const float* rowscale,

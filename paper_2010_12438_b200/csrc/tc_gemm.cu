@@ -579,7 +579,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
               y[j] = activate<ACT>(__uint_as_float(u[j]) * ASCALE + bb[e]);
             }
           }
-          store32(a.C, a.ldc, c0, y);
+          if (a.C) store32(a.C, a.ldc, c0, y);
+          if (a.rowscale) {  // C2 = C * rowscale[forward of the row] (trunk modulation)
+            const float* rs = rv ? a.rowscale + (int64_t)a.row_fwd[row] * a.N + n0 + c0 : nullptr;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) y[j] *= (rs && n0 + c0 + j < a.N) ? __ldg(rs + j) : 0.f;
+            store32(a.C2, a.ldc2, c0, y);
+          }
         }
       }
       }  // M halves
@@ -822,6 +828,33 @@ void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda
     case 128: launch_act<128>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
     case 144: launch_act<144>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
     default: launch_act<256>(act, A1, lda1, A2, lda2, a, Wpk, nblk, st); break;
+  }
+}
+
+// C2 = act([A1|A2] @ W + bias) * rowscale[row_fwd[r]] (per-forward row vector of N),
+// optionally also C unscaled (C may be null).
+void tc_gemm_scaled(const float* A1, int64_t lda1, int K1, const TcW& Wpk, const float* bias,
+                    float* C, int64_t ldc, const float* rowscale, const int32_t* row_fwd,
+                    float* C2, int64_t ldc2, int64_t M, int N, int act, cudaStream_t st) {
+  if (M <= 0) return;
+  GO_CHECK(rowscale && row_fwd && C2, "tc_gemm_scaled needs rowscale, row_fwd and C2");
+  tg::Args a{};
+  a.K1 = K1; a.K2 = 0;
+  a.bias = bias; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
+  a.nch = (int)cdiv(K1, tg::BK);
+  a.rowscale = rowscale; a.row_fwd = row_fwd; a.C2 = C2; a.ldc2 = ldc2;
+  a.vec = (C == nullptr || ((uintptr_t)C % 16 == 0 && ldc % 4 == 0)) &&
+          ((uintptr_t)C2 % 16 == 0 && ldc2 % 4 == 0);
+  int BN = tc_gemm_bn(N);
+  int nblk = (int)cdiv(N, BN);
+  switch (BN) {
+    case 16: launch_act<16>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
+    case 32: launch_act<32>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
+    case 48: launch_act<48>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
+    case 64: launch_act<64>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
+    case 128: launch_act<128>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
+    case 144: launch_act<144>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
+    default: launch_act<256>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
   }
 }
 
