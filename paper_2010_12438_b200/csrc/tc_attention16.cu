@@ -95,7 +95,7 @@ __device__ __forceinline__ void named_bar_arrive(int id, int count) {
 // halves double-buffered.  Same TMEM footprint (64 S columns + 16 O columns per tile).
 __device__ int g_attn_debug = 0;
 
-template <int NP, bool S64, bool LP = false>
+template <int NP, bool S64, bool LP = false, bool DEG2 = false>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_f16_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
                     const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         // interleave: polynomial pairs at odd positions first, so MUFU and FMA work mix
         const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
         const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-        pk[i] = poly ? (LP ? exp2_poly_f16x2_lp(x0, x1) : exp2_poly_f16x2(x0, x1))
+        pk[i] = poly ? (DEG2 ? exp2_poly_f16x2_lp2(x0, x1)
+                             : LP ? exp2_poly_f16x2_lp(x0, x1) : exp2_poly_f16x2(x0, x1))
                      : pack_f16x2(ex2f(x0), ex2f(x1));
       }
     };
@@ -874,6 +875,11 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       {t16::attn_f16_db_kernel<0, 2>, t16::attn_f16_db_kernel<1, 2>, t16::attn_f16_db_kernel<2, 2>,
        t16::attn_f16_db_kernel<3, 2>, t16::attn_f16_db_kernel<4, 2>, t16::attn_f16_db_kernel<5, 2>,
        t16::attn_f16_db_kernel<6, 2>}};
+  static const Fn lp2_kernels[7] = {
+      t16::attn_f16_kernel<0, true, true, true>, t16::attn_f16_kernel<1, true, true, true>,
+      t16::attn_f16_kernel<2, true, true, true>, t16::attn_f16_kernel<3, true, true, true>,
+      t16::attn_f16_kernel<4, true, true, true>, t16::attn_f16_kernel<5, true, true, true>,
+      t16::attn_f16_kernel<6, true, true, true>};
   static int np = -1, s64 = 0, use_alt = 0, lp = 0;
   const size_t smem = sizeof(t16::Smem) + 1024;
   const size_t smem64 = sizeof(t16::AltCfg<2, 64>::Smem) + 1024;
@@ -898,7 +904,9 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
       CUDA_CHECK(cudaMemcpyToSymbol(t16::g_attn_debug, &v, sizeof(int)));
     }
     const char* elp = getenv("GO_POLYLP");
-    lp = elp ? (atoi(elp) != 0) : t16::DEFAULT_LP;
+    lp = elp ? atoi(elp) : t16::DEFAULT_LP;  // 2: degree-2 polynomial (experiment)
+    for (Fn f : lp2_kernels)
+      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (Fn f : lp_kernels)
       CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (Fn f : alt64)
@@ -940,7 +948,7 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
     return;
   }
   dim3 grid((unsigned)num_works, (unsigned)n_head);
-  (lp && s64 ? lp_kernels[np] : kernels[s64][std::min(np, 4)])<<<grid, t16::NUM_THREADS, smem, st>>>(
+  (lp == 2 && s64 ? lp2_kernels[np] : lp && s64 ? lp_kernels[np] : kernels[s64][std::min(np, 4)])<<<grid, t16::NUM_THREADS, smem, st>>>(
       static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
       static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
   LAUNCH_CHECK();

@@ -174,6 +174,21 @@ __device__ __forceinline__ uint32_t exp2_poly_f16x2_lp(float x0, float x1) {
   // (borrows between the halves cancel in the shifted sum, both results stay positive)
   return p + ((t - 0x66006600u) << 10);
 }
+// Degree-2 variant of exp2_poly_f16x2_lp (8 instructions per pair, max rel. error
+// 2.0e-3 from the polynomial): an experiment on the accuracy / throughput trade-off.
+__device__ __forceinline__ uint32_t exp2_poly_f16x2_lp2(float x0, float x1) {
+  const uint32_t xh = pack_f16x2_rn(x0, x1);
+  uint32_t t, p;
+  asm("{\n.reg .b32 u, f;\n"
+      "add.rn.f16x2 %0, %2, %3;\n"
+      "sub.rn.f16x2 u, %0, %3;\n"
+      "sub.rn.f16x2 f, %2, u;\n"
+      "fma.rn.f16x2 u, f, %4, %5;\n"
+      "fma.rn.f16x2 %1, u, f, %6;\n}\n"
+      : "=r"(t), "=r"(p)
+      : "r"(xh), "r"(0x66006600u), "r"(0x33AD33ADu), "r"(0x39A039A0u), "r"(0x3C003C00u));
+  return p + ((t - 0x66006600u) << 10);
+}
 __device__ __forceinline__ float tf32_rn(float x) {
   uint32_t y;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
