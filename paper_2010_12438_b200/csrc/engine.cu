@@ -637,6 +637,10 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
                           !strcmp(trunk_env, "tc");
     const bool trunk_mma = !trunk_tc && trunk_mma_supported(dh) &&
                            !(trunk_env && !strcmp(trunk_env, "simt"));
+    // fused FFN for the trunk's 128 -> 512 -> 128 blocks (GO_FFN=0: two GEMMs)
+    const char* ffn_env = getenv("GO_FFN");
+    const bool use_ffn = dm == 128 && di == 512 && !(ffn_env && ffn_env[0] == '0') &&
+                         !(getenv("GO_GEMM_F16") && getenv("GO_GEMM_F16")[0] == '0');
     int32_t* trunk_flags = A.take<int32_t>(Lt + 1);
     if (trunk_tc) CUDA_CHECK(cudaMemsetAsync(trunk_flags, 0, (Lt + 1) * sizeof(int32_t), st));
     {
@@ -681,14 +685,34 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
                    LW, W_(S.blk(l, LN1_G)), W_(S.blk(l, LN1_B)), h1, LW, nullptr, nullptr, nullptr,
                    0, R, dm, st);
       }
-      {
-        KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * di);
-        tc_gemm(h1, LW, dm, nullptr, 0, 0, pack1(W_(S.blk(l, FF_W1)), dm, di), W_(S.blk(l, FF_B1)),
-                F1, LI, R, di, 1, st);
-      }
       bool last = l == Lt - 1;
       float* xm_next = (xm == X[1]) ? X[3] : X[1];
-      {
+      if (use_ffn) {
+        // fused FF1 -> relu -> FF2 -> +h1 -> LN (tc_ffn.cuh); the unfused tf32 GEMMs re-run
+        // the layer only if an operand left the fp16 range (gated on fflag)
+        KTimer kt(ctx, K_GEMM, st, 4.0 * R * dm * di);
+        GO_CHECK(n_packs < MAX_PACKS, "too many packed weights");
+        int32_t* fflag = ovf_flags + n_packs++;
+        void* w1h = A.take<float>((int64_t)cdiv(di, 128) * cdiv(dm, 32) * 128 * 32);
+        void* w2h = A.take<float>((int64_t)cdiv(dm, 128) * cdiv(di, 32) * 128 * 32);
+        tc_gemm_pack16_bn(W_(S.blk(l, FF_W1)), di, dm, di, 128, w1h, st, fflag);
+        tc_gemm_pack16_bn(W_(S.blk(l, FF_W2)), dm, di, dm, 128, w2h, st, fflag);
+        tc_ffn(h1, LW, w1h, w2h, W_(S.blk(l, FF_B1)), W_(S.blk(l, FF_B2)), W_(S.blk(l, LN2_G)),
+               W_(S.blk(l, LN2_B)), last ? hid : nullptr, dm, last ? nullptr : modp, row_fwd,
+               last ? nullptr : xm_next, LW, R, fflag, st);
+        TcW f1 = pack1(W_(S.blk(l, FF_W1)), dm, di), f2 = pack1(W_(S.blk(l, FF_W2)), di, dm);
+        f1.gate = fflag;
+        f2.gate = fflag;
+        tc_gemm(h1, LW, dm, nullptr, 0, 0, f1, W_(S.blk(l, FF_B1)), F1, LI, R, di, 1, st);
+        tc_gemm_ln(F1, LI, di, nullptr, 0, 0, f2, W_(S.blk(l, FF_B2)), h1, LW,
+                   W_(S.blk(l, LN2_G)), W_(S.blk(l, LN2_B)), last ? hid : nullptr, dm,
+                   last ? nullptr : modp, row_fwd, last ? nullptr : xm_next, LW, R, dm, st);
+      } else {
+        {
+          KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * di);
+          tc_gemm(h1, LW, dm, nullptr, 0, 0, pack1(W_(S.blk(l, FF_W1)), dm, di),
+                  W_(S.blk(l, FF_B1)), F1, LI, R, di, 1, st);
+        }
         KTimer kt(ctx, K_GEMM, st, 2.0 * R * di * dm);
         tc_gemm_ln(F1, LI, di, nullptr, 0, 0, pack1(W_(S.blk(l, FF_W2)), di, dm),
                    W_(S.blk(l, FF_B2)), h1, LW, W_(S.blk(l, LN2_G)), W_(S.blk(l, LN2_B)),

@@ -275,6 +275,7 @@ struct TcW {
   const float* w32 = nullptr;
   const void* w16 = nullptr;
   int32_t* ovf = nullptr;
+  const int32_t* gate = nullptr;  // set: tf32 pass only, run only if *gate != 0
 };
 int tc_gemm_bn(int N);
 size_t tc_gemm_packed_floats(int K, int N);
@@ -290,6 +291,14 @@ void tc_gemm(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda
 void tc_gemm_scaled(const float* A1, int64_t lda1, int K1, const TcW& Wpk, const float* bias,
                     float* C, int64_t ldc, const float* rowscale, const int32_t* row_fwd,
                     float* C2, int64_t ldc2, int64_t M, int N, int act, cudaStream_t st);
+void tc_gemm_pack16_bn(const float* W, int64_t ldw, int K, int N, int BN, void* out,
+                       cudaStream_t st, int32_t* ovf);
+// fused trunk FFN: C = LN(X + relu(X W1 + b1) W2 + b2) * g + beta, C2 = C * rowscale
+// (d_model 128, d_inner 512); *ovf set if X / H leave the fp16 range (caller re-runs)
+void tc_ffn(const float* X, int64_t ldx, const void* W1_16, const void* W2_16, const float* b1,
+            const float* b2, const float* g, const float* beta, float* C, int64_t ldc,
+            const float* rowscale, const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M,
+            int32_t* ovf, cudaStream_t st);
 void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
                 const TcW& W, const float* bias, const float* resid, int64_t ldr,
                 const float* g, const float* beta, float* C, int64_t ldc, const float* rowscale,

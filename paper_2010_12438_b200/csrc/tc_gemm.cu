@@ -602,6 +602,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   }
 }
 
+#include "tc_ffn.cuh"
+
 // Pack W[K, N] (row-major, ldw) into [nblk][nch][hi|lo][BN*32] UMMA K-major canonical
 // B tiles: element (n, k) of a block at (k/4)*(BN/8*32) + (n/8)*32 + (n%8)*4 + k%4.
 // Up to three column blocks (W0 | W1 | W2) concatenate into one weight (merged QKV).
@@ -698,6 +700,17 @@ void tc_gemm_pack16(const float* W0, const float* W1, const float* W2, int Nsub,
   LAUNCH_CHECK();
 }
 
+// fp16 pack with an explicit block width (the fused FFN wants 128-column blocks).
+void tc_gemm_pack16_bn(const float* W, int64_t ldw, int K, int N, int BN, void* out,
+                       cudaStream_t st, int32_t* ovf) {
+  int nblk = (int)cdiv(N, BN);
+  int nch = (int)cdiv(K, tg::BK);
+  int64_t total = (int64_t)nblk * nch * BN * tg::BK;
+  tg::pack_b16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+      W, W, W, N, ldw, K, N, BN, nch, nblk, static_cast<__half*>(out), ovf);
+  LAUNCH_CHECK();
+}
+
 // Pack W = [W0 | W1 | W2] (each [K, Nsub] row-major with ldw; N = parts * Nsub).
 void tc_gemm_pack(const float* W0, const float* W1, const float* W2, int Nsub, int64_t ldw, int K,
                   int N, float* out, cudaStream_t st) {
@@ -781,6 +794,12 @@ void launch_all(const float* A1, int64_t lda1, const float* A2, int64_t lda2, tg
   const CUtensorMap m1 = a_map(A1, a.M, a.K1, lda1);
   const CUtensorMap m2 = A2 ? a_map(A2, a.M, a.K2, lda2) : m1;
   constexpr bool can2 = BN <= 128;
+  if (W.gate) {  // tf32 re-run of a fused kernel's layer, gated on its range flag
+    a.gate = W.gate;
+    a.Bpk = W.w32;
+    launch<BN, 1, LN, ACT, false>(m1, m2, a, nblk, st);
+    return;
+  }
   const bool f16 = W.w16 && W.ovf && use_f16();
   if (f16) {
     tg::Args a16 = a;
@@ -856,6 +875,39 @@ void tc_gemm_scaled(const float* A1, int64_t lda1, int K1, const TcW& Wpk, const
     case 144: launch_act<144>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
     default: launch_act<256>(act, A1, lda1, nullptr, 0, a, Wpk, nblk, st); break;
   }
+}
+
+// Fused trunk feed-forward block (tc_ffn.cuh).  W1_16: [128, 512] packed by
+// tc_gemm_pack16_bn(.., BN = 128); W2_16: [512, 128] packed by tc_gemm_pack16.
+void tc_ffn(const float* X, int64_t ldx, const void* W1_16, const void* W2_16, const float* b1,
+            const float* b2, const float* g, const float* beta, float* C, int64_t ldc,
+            const float* rowscale, const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M,
+            int32_t* ovf, cudaStream_t st) {
+  if (M <= 0) return;
+  GO_CHECK(ovf, "tc_ffn needs a range flag");
+  GO_CHECK((C == nullptr || ((uintptr_t)C % 16 == 0 && ldc % 4 == 0)) &&
+               (C2 == nullptr || ((uintptr_t)C2 % 16 == 0 && ldc2 % 4 == 0)) && ldx % 4 == 0 &&
+               (uintptr_t)X % 16 == 0,
+           "tc_ffn rows must be 16-B aligned");
+  GO_CHECK(rowscale == nullptr || (row_fwd && C2), "tc_ffn rowscale needs row_fwd and C2");
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(tg::ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)tg::FF_SMEM));
+    attr = true;
+  }
+  tg::FfnArgs a{};
+  a.X = X; a.ldx = ldx;
+  a.W1 = static_cast<const uint8_t*>(W1_16);
+  a.W2 = static_cast<const uint8_t*>(W2_16);
+  a.b1 = b1; a.b2 = b2; a.ln_g = g; a.ln_b = beta;
+  a.C = C; a.ldc = ldc; a.rowscale = rowscale; a.row_fwd = row_fwd; a.C2 = C2; a.ldc2 = ldc2;
+  a.M = M; a.ovf = ovf;
+  const CUtensorMap mx = a_map(X, M, 128, ldx);
+  const int ntiles = (int)cdiv(M, tg::BM);
+  const int grid = std::min(ntiles, num_sms());
+  tg::ffn_kernel<<<grid, tg::G_THREADS, tg::FF_SMEM, st>>>(mx, a, ntiles);
+  LAUNCH_CHECK();
 }
 
 // C = LN(resid + [A1|A2] @ W + bias) * g + b  (N == 128); optional C2 = C * rowscale[f].

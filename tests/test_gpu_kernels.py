@@ -293,3 +293,28 @@ def _fp16_gemm_case(store, ecfg, pcfg, sizes, graphs, seeds, scale):
     tol = 1e-5 if scale == 1.0 else 1e-4
     assert rel_err(h16, h32) < tol, scale
     assert rel_err(lg16, lg32) < tol, scale
+
+
+def test_fused_ffn_matches_unfused_and_reruns_out_of_range():
+    """The fused trunk feed-forward kernel (tc_ffn.cuh) issues the same 3-pass fp16 MMAs
+    in the same order as the two unfused GEMMs, so the forward is bit-identical; with
+    FF weights scaled so the 512-wide intermediate leaves the fp16 range, the fused pass
+    flags itself and the unfused tf32 re-run produces the layer (finite, close to the
+    unfused path)."""
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    sizes = {"placement": 8}
+    ecfg, pcfg, store = _store(sizes)
+    graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 120, 1, 64, seed=5), node_cap=10**6),
+              gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))]
+    seeds = [21, 22]
+    h_f, lg_f = _forward_env("GO_FFN", None, store, ecfg, pcfg, sizes, graphs, seeds)
+    h_u, lg_u = _forward_env("GO_FFN", "0", store, ecfg, pcfg, sizes, graphs, seeds)
+    assert np.array_equal(h_f, h_u)
+    assert np.array_equal(lg_f, lg_u)
+    store["policy/block1/ff_w1"].data = store["policy/block1/ff_w1"].data * 4e5
+    store.touch()
+    h_f, lg_f = _forward_env("GO_FFN", None, store, ecfg, pcfg, sizes, graphs, seeds)
+    h_u, lg_u = _forward_env("GO_FFN", "0", store, ecfg, pcfg, sizes, graphs, seeds)
+    assert np.isfinite(h_f).all() and np.isfinite(lg_f).all()
+    assert rel_err(h_f, h_u) < 1e-4
+    assert rel_err(lg_f, lg_u) < 1e-4
