@@ -30,7 +30,8 @@ def des(K):
     pr = torch.zeros(g.num_nodes, dtype=torch.int32, device="cuda")
     fg = singleton_fused(g)
     top = uniform_topology(8)
-    for mode in ("lane", "warp"):
+    ref = None
+    for mode, smem in (("lane", "-"), ("warp", "-")):
         os.environ["GO_DES_MODE"] = mode
         simulate_many(fg, pl[:32], pr, top)
         torch.cuda.synchronize()
@@ -38,8 +39,11 @@ def des(K):
         r = simulate_many(fg, pl, pr, top)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        st = r.step_time.cpu().numpy()
+        same = "" if ref is None else f" identical={bool((st == ref).all())}"
+        ref = st if ref is None else ref
         print(f"DES mode={mode} K={K}: {dt*1e3:.1f} ms  ({K/dt:.1f} placements/s)  "
-              f"step[0]={float(r.step_time[0]):.6g}", flush=True)
+              f"step[0]={float(r.step_time[0]):.6g}{same}", flush=True)
 
 
 def forward(F, modes=("tc", "simt"), env=None):
