@@ -541,6 +541,11 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
   float* meanb = A.take<float>((int64_t)F * dm);
   float* part = A.take<float>((m.n_chunks + 1) * 128);
   row_fwd_fill(m.d_row_off, F, R, row_fwd, st);
+  // fused FFN for the 128 -> 512 -> 128 blocks of the trunk and the task heads
+  // (tc_ffn.cuh; GO_FFN=0: two GEMMs each)
+  const char* ffn_env = getenv("GO_FFN");
+  const bool use_ffn = dm == 128 && di == 512 && !(ffn_env && ffn_env[0] == '0') &&
+                       !(getenv("GO_GEMM_F16") && getenv("GO_GEMM_F16")[0] == '0');
   // every packed weight gets tf32 and fp16 copies and its own fp16 range flag
   constexpr int MAX_PACKS = 96;
   int32_t* ovf_flags = A.take<int32_t>(MAX_PACKS);
@@ -637,10 +642,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
                           !strcmp(trunk_env, "tc");
     const bool trunk_mma = !trunk_tc && trunk_mma_supported(dh) &&
                            !(trunk_env && !strcmp(trunk_env, "simt"));
-    // fused FFN for the trunk's 128 -> 512 -> 128 blocks (GO_FFN=0: two GEMMs)
-    const char* ffn_env = getenv("GO_FFN");
-    const bool use_ffn = dm == 128 && di == 512 && !(ffn_env && ffn_env[0] == '0') &&
-                         !(getenv("GO_GEMM_F16") && getenv("GO_GEMM_F16")[0] == '0');
+
     int32_t* trunk_flags = A.take<int32_t>(Lt + 1);
     if (trunk_tc) CUDA_CHECK(cudaMemsetAsync(trunk_flags, 0, (Lt + 1) * sizeof(int32_t), st));
     {
@@ -771,19 +773,39 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
                     st);
       }
       float* o = X[2];
-      {
-        KTimer kt(ctx, K_GEMM, st, 2.0 * R * (W * dm + 2.0 * dm * di));
-        tc_gemm(Ab, LA, W, nullptr, 0, 0, ta_o, W_(S.ta(O_B)), o, LW, R, dm, 0, st);
-        tc_gemm(o, LW, dm, nullptr, 0, 0, pack1(W_(S.task(t, FC_W1)), dm, di), W_(S.task(t, FC_B1)),
-                F1, LI, R, di, 1, st);
-      }
       float* rep = b.reps ? b.reps + (int64_t)t * R * dm : rep_bufs[t & 1];
       const int64_t ldr = b.reps ? dm : LW;
       int a = cfg.task_sizes[t];
       {
-        KTimer kt(ctx, K_GEMM, st, 2.0 * R * (di * dm + dm * a));
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * W * dm);
+        tc_gemm(Ab, LA, W, nullptr, 0, 0, ta_o, W_(S.ta(O_B)), o, LW, R, dm, 0, st);
+      }
+      if (use_ffn) {
+        // rep = relu(o @ fc_w1 + b1) @ fc_w2 + b2 fused (tc_ffn.cuh, no LayerNorm); the
+        // unfused tf32 GEMMs re-run only if an operand left the fp16 range
+        KTimer kt(ctx, K_GEMM, st, 4.0 * R * dm * di);
+        GO_CHECK(n_packs < MAX_PACKS, "too many packed weights");
+        int32_t* fflag = ovf_flags + n_packs++;
+        void* w1h = A.take<float>((int64_t)cdiv(di, 128) * cdiv(dm, 32) * 128 * 32);
+        void* w2h = A.take<float>((int64_t)cdiv(dm, 128) * cdiv(di, 32) * 128 * 32);
+        tc_gemm_pack16_bn(W_(S.task(t, FC_W1)), di, dm, di, 128, w1h, st, fflag);
+        tc_gemm_pack16_bn(W_(S.task(t, FC_W2)), dm, di, dm, 128, w2h, st, fflag);
+        tc_ffn(o, LW, w1h, w2h, W_(S.task(t, FC_B1)), W_(S.task(t, FC_B2)), nullptr, nullptr,
+               rep, ldr, nullptr, nullptr, nullptr, 0, R, fflag, st, false);
+        TcW f1 = pack1(W_(S.task(t, FC_W1)), dm, di), f2 = pack1(W_(S.task(t, FC_W2)), di, dm);
+        f1.gate = fflag;
+        f2.gate = fflag;
+        tc_gemm(o, LW, dm, nullptr, 0, 0, f1, W_(S.task(t, FC_B1)), F1, LI, R, di, 1, st);
+        tc_gemm(F1, LI, di, nullptr, 0, 0, f2, W_(S.task(t, FC_B2)), rep, ldr, R, dm, 0, st);
+      } else {
+        KTimer kt(ctx, K_GEMM, st, 4.0 * R * dm * di);
+        tc_gemm(o, LW, dm, nullptr, 0, 0, pack1(W_(S.task(t, FC_W1)), dm, di), W_(S.task(t, FC_B1)),
+                F1, LI, R, di, 1, st);
         tc_gemm(F1, LI, di, nullptr, 0, 0, pack1(W_(S.task(t, FC_W2)), di, dm), W_(S.task(t, FC_B2)),
                 rep, ldr, R, dm, 0, st);
+      }
+      {
+        KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * a);
         tc_gemm(rep, ldr, dm, nullptr, 0, 0, pack1(W_(S.task(t, OUT_W)), dm, a), W_(S.task(t, OUT_B)),
                 logits + lcol, a, R, a, 0, st);
       }

@@ -298,7 +298,7 @@ void tc_gemm_pack16_bn(const float* W, int64_t ldw, int K, int N, int BN, void* 
 void tc_ffn(const float* X, int64_t ldx, const void* W1_16, const void* W2_16, const float* b1,
             const float* b2, const float* g, const float* beta, float* C, int64_t ldc,
             const float* rowscale, const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M,
-            int32_t* ovf, cudaStream_t st);
+            int32_t* ovf, cudaStream_t st, bool layernorm = true);
 void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
                 const TcW& W, const float* bias, const float* resid, int64_t ldr,
                 const float* g, const float* beta, float* C, int64_t ldc, const float* rowscale,

@@ -1,6 +1,7 @@
 // Fused feed-forward block of the trunk (policy.py:170-177; transformer_block's
 // out = LN(h + FF(h)), FF(h) = relu(h W1 + b1) W2 + b2, d_model = 128, d_inner = 512):
 //   C = LN(X + relu(X W1 + b1) W2 + b2) * g + b,   C2 = C * rowscale[forward]
+// (or, for a task head, C = relu(X W1 + b1) W2 + b2 without residual / LN, policy.py:212-214)
 // in ONE persistent kernel, so the 512-wide intermediate never leaves the SM (it was
 // 40% of the dense layers' HBM traffic as an fp32 [R, 512] round trip).  Included by
 // tc_gemm.cu (shares its helpers and launch plumbing).
@@ -44,6 +45,7 @@ struct FfnArgs {
   int64_t ldc2;
   int64_t M;
   int32_t* ovf;
+  int ln;  // 1: C = LN(X + FF(X)) (trunk block); 0: C = FF(X) (task head, policy.py:212-214)
 };
 
 constexpr int FF_CHUNK = 16384;  // one 32-k chunk: fp32 TMA box, or fp16 hi (8 KB) + lo
@@ -276,8 +278,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     float* s_g = s_b2 + 128;
     float* s_b = s_g + 128;
     s_b2[et] = a.b2[et];
-    s_g[et] = a.ln_g[et];
-    s_b[et] = a.ln_b[et];
+    s_g[et] = a.ln ? a.ln_g[et] : 1.f;
+    s_b[et] = a.ln ? a.ln_b[et] : 0.f;
     asm volatile("bar.sync 1, 128;" ::: "memory");
     const int rq = lane >> 3, c4 = lane & 7;
     auto ld4 = [](const float* p) { return *reinterpret_cast<const float4*>(p); };
@@ -303,6 +305,22 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       mbar_wait(d2_full, tl & 1);
       fence_after();
       const uint32_t tacc = D2 + lane_off;
+      if (!a.ln) {  // plain C = acc + b2
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t u[32];
+          TG_LD16(tacc + c0, u);
+          TG_LD16(tacc + c0 + 16, (u + 16));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float y[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(u[j]) * ASCALE + s_b2[c0 + j];
+          store32(a.C, a.ldc, c0, y);
+        }
+        fence_before();
+        mbar_arrive(d2_empty);
+        continue;
+      }
       // pass 1: x = acc + b2 + X (residual), kept in TMEM; running sum
       float s = 0.f;
 #pragma unroll 1

@@ -882,9 +882,10 @@ void tc_gemm_scaled(const float* A1, int64_t lda1, int K1, const TcW& Wpk, const
 void tc_ffn(const float* X, int64_t ldx, const void* W1_16, const void* W2_16, const float* b1,
             const float* b2, const float* g, const float* beta, float* C, int64_t ldc,
             const float* rowscale, const int32_t* row_fwd, float* C2, int64_t ldc2, int64_t M,
-            int32_t* ovf, cudaStream_t st) {
+            int32_t* ovf, cudaStream_t st, bool layernorm) {
   if (M <= 0) return;
   GO_CHECK(ovf, "tc_ffn needs a range flag");
+  GO_CHECK(layernorm || (C && !rowscale), "tc_ffn without LayerNorm writes C only");
   GO_CHECK((C == nullptr || ((uintptr_t)C % 16 == 0 && ldc % 4 == 0)) &&
                (C2 == nullptr || ((uintptr_t)C2 % 16 == 0 && ldc2 % 4 == 0)) && ldx % 4 == 0 &&
                (uintptr_t)X % 16 == 0,
@@ -902,7 +903,7 @@ void tc_ffn(const float* X, int64_t ldx, const void* W1_16, const void* W2_16, c
   a.W2 = static_cast<const uint8_t*>(W2_16);
   a.b1 = b1; a.b2 = b2; a.ln_g = g; a.ln_b = beta;
   a.C = C; a.ldc = ldc; a.rowscale = rowscale; a.row_fwd = row_fwd; a.C2 = C2; a.ldc2 = ldc2;
-  a.M = M; a.ovf = ovf;
+  a.M = M; a.ovf = ovf; a.ln = layernorm ? 1 : 0;
   const CUtensorMap mx = a_map(X, M, 128, ldx);
   const int ntiles = (int)cdiv(M, tg::BM);
   const int grid = std::min(ntiles, num_sms());
