@@ -199,17 +199,37 @@ __global__ void mean_partial_kernel(const float* __restrict__ x, int64_t ldx,
                                     const int64_t* __restrict__ chunk_row0,
                                     const int64_t* __restrict__ chunk_row1, int D,
                                     float* __restrict__ part, int32_t* __restrict__ flag) {
-  int64_t c = blockIdx.x;
-  int64_t r0 = chunk_row0[c], r1 = chunk_row1[c];
+  // 4 row groups x (blockDim / 4) columns; 4 independent accumulators per thread (the
+  // serial 256-row chain of one accumulator was latency-bound); fixed combine order
+  __shared__ float red[4][128];
+  const int64_t c = blockIdx.x;
+  const int64_t r0 = chunk_row0[c], r1 = chunk_row1[c];
+  const int ncol = blockDim.x >> 2;
+  const int grp = threadIdx.x / ncol, lc = threadIdx.x % ncol;
   bool bad = false;
-  for (int col = threadIdx.x; col < D; col += blockDim.x) {
-    float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) {
-      const float v = x[r * ldx + col];
-      bad |= !isfinite(v);
-      s += v;
+  for (int col0 = 0; col0 < D; col0 += ncol) {
+    const int col = col0 + lc;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    if (col < D) {
+      int64_t r = r0 + grp;
+      for (; r + 12 < r1; r += 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float v = x[(r + 4 * u) * ldx + col];
+          bad |= !isfinite(v);
+          s[u] += v;
+        }
+      }
+      for (int u = 0; r < r1; r += 4, ++u) {
+        const float v = x[r * ldx + col];
+        bad |= !isfinite(v);
+        s[u & 3] += v;
+      }
     }
-    part[c * D + col] = s;
+    red[grp][lc] = (s[0] + s[1]) + (s[2] + s[3]);
+    __syncthreads();
+    if (grp == 0 && col < D) part[c * D + col] = (red[0][lc] + red[1][lc]) + (red[2][lc] + red[3][lc]);
+    __syncthreads();
   }
   // fused non-finite check of the rows being averaged (embedding.py:96-97)
   if (flag && bad) atomicOr(flag, 1);
@@ -234,7 +254,7 @@ void mean_rows(const float* x, int64_t ldx, const int64_t* row_off_dev, int F,
                float* part, cudaStream_t st, int32_t* finite_flag) {
   // chunk_tab (device): [nc] chunk row0, [nc] chunk row1, [F] first chunk, [F] end chunk
   if (nc > 0)
-    mean_partial_kernel<<<(unsigned)nc, 128, 0, st>>>(x, ldx, chunk_tab, chunk_tab + nc, D,
+    mean_partial_kernel<<<(unsigned)nc, 512, 0, st>>>(x, ldx, chunk_tab, chunk_tab + nc, D,
                                                       part, finite_flag);
   mean_final_kernel<<<F, 128, 0, st>>>(part, chunk_tab + 2 * nc, chunk_tab + 2 * nc + F,
                                        row_off_dev, D, out, ldo);

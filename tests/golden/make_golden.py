@@ -422,8 +422,58 @@ def make_grads():
     np.savez_compressed(OUT / "golden_grads.npz", **out)
 
 
+def make_baselines():
+    """Non-learned optimizers (baselines.py:50-237): fanout priorities, brute force over
+    placement / schedule / fusion priorities, simulated annealing chains."""
+    from graphopt.baselines import SAConfig, brute_force, fanout_priorities, simulated_annealing
+    out = {}
+    rng = np.random.default_rng(77)
+    # fanout priorities
+    graphs = [C.random_graph(rng, int(rng.integers(2, 40)), p_edge=float(p))
+              for p in (0.05, 0.2, 0.5, 0.3, 0.1)]
+    graphs.append(gen_workload(WorkloadSpec("multi-branch-cnn", 40, 1, 64, seed=3), node_cap=10**6))
+    for i, g in enumerate(graphs):
+        p = f"f{i}/"
+        graph_arrays(g, p, out)
+        out[p + "levels"] = fanout_priorities(g).actions
+    out["fanout_count"] = np.int64(len(graphs))
+    # brute force
+    cases = [("placement", 6, 2), ("placement", 5, 3), ("placement", 7, 2),
+             ("schedule_priority", 4, 8), ("placement", 8, 2), ("fusion_priority", 3, 8)]
+    for i, (task, n, d) in enumerate(cases):
+        p = f"b{i}/"
+        g = C.random_graph(rng, n, p_edge=0.4, fusible_only=task == "fusion_priority")
+        top = rand_topology(rng, d if task == "placement" else 2)
+        best, t = brute_force(g, top, task)
+        graph_arrays(g, p, out)
+        topo_arrays(top, p, out)
+        out[p + "task"] = np.array(task)
+        out[p + "actions"] = best.actions
+        out[p + "time"] = np.float64(t)
+    out["brute_count"] = np.int64(len(cases))
+    # simulated annealing
+    sa_cases = [(["placement"], 25, 3, 0), (["placement", "schedule_priority"], 20, 2, 5),
+                (["schedule_priority"], 15, 2, 9), (["fusion_priority", "placement"], 12, 2, 3)]
+    for i, (tasks, n, d, seed) in enumerate(sa_cases):
+        p = f"a{i}/"
+        g = C.random_graph(rng, n, p_edge=0.3, fusible_only="fusion_priority" in tasks)
+        top = rand_topology(rng, d)
+        res, t = simulated_annealing(g, top, tasks, SAConfig(iterations=300, seed=seed,
+                                                             cooling_rate=0.99))
+        graph_arrays(g, p, out)
+        topo_arrays(top, p, out)
+        out[p + "tasks"] = np.array(tasks)
+        out[p + "seed"] = np.int64(seed)
+        out[p + "time"] = np.float64(t)
+        for tk in tasks:
+            out[p + "actions/" + tk] = res[tk].actions
+    out["sa_count"] = np.int64(len(sa_cases))
+    np.savez_compressed(OUT / "golden_baselines.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads"]
+    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads",
+                             "baselines"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)
