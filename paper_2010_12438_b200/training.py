@@ -321,15 +321,30 @@ def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed
               else T.as_tensor(base["schedule_priority"].actions, device=dev).to(T.int32))
         ix = T.as_tensor(ks, device=dev)
         if "fusion_priority" in task_sizes:
+            # the native fusion pass per rollout (threads: the ctypes call releases the
+            # GIL), then ONE batched DES launch per distinct grouping -- on graphs where
+            # no merge succeeds (attention-stack) that is a single launch
+            from concurrent.futures import ThreadPoolExecutor
+
+            from .fusion import fuse_groups
             fus = task_rows("fusion_priority").cpu().numpy()
-            for r, k in enumerate(ks):
-                fg = apply_fusion(g, ActionAssignment("fusion_priority", fus[r],
-                                                      task_sizes["fusion_priority"]), fusion_cfg)
-                res = simulate_many(fg, pl[r:r + 1], pr[r] if pr.dim() == 2 else pr, topology,
-                                    baseline=baselines[g_i])
-                rewards[ix[r:r + 1]] = res.reward
-                steps[ix[r:r + 1]] = res.step_time
-                valid[ix[r:r + 1]] = res.valid
+            a_f = task_sizes["fusion_priority"]
+            for r in range(len(ks)):  # the reference's validation (simulator.py:199-210)
+                ActionAssignment("fusion_priority", fus[r], a_f)
+            with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+                maps = list(ex.map(lambda r: fuse_groups(g, fus[r], fusion_cfg.max_group),
+                                   range(len(ks))))
+            by_map: dict = {}
+            for r, m in enumerate(maps):
+                by_map.setdefault(m.tobytes(), []).append(r)
+            for rs in by_map.values():
+                fg = FusedGraph(g, maps[rs[0]])
+                sel = T.as_tensor(rs, device=dev)
+                res = simulate_many(fg, pl[sel].contiguous(), pr[sel] if pr.dim() == 2 else pr,
+                                    topology, baseline=baselines[g_i])
+                rewards[ix[sel]] = res.reward
+                steps[ix[sel]] = res.step_time
+                valid[ix[sel]] = res.valid
         else:
             fg = apply_fusion(g, base["fusion_priority"], fusion_cfg)
             res = simulate_many(fg, pl.contiguous(), pr, topology, baseline=baselines[g_i])

@@ -422,6 +422,42 @@ def make_grads():
     np.savez_compressed(OUT / "golden_grads.npz", **out)
 
 
+def make_rollouts_joint():
+    """collect_rollouts with the joint task set (placement + schedule + fusion priorities)
+    on a graph where fusion merges happen, so every rollout has its own fused grouping."""
+    out = {}
+    g = gen_workload(WorkloadSpec("multi-branch-cnn", 6, 1, 64, seed=1))
+    from graphopt.costmodel import uniform_topology
+    top = uniform_topology(3)
+    tasks = ["placement", "schedule_priority", "fusion_priority"]
+    sizes = task_action_sizes(top, tasks, 8)
+    ecfg, pcfg = EmbedConfig(), PolicyConfig()
+    store = init_all_params(ecfg, pcfg, sizes, seed=0)
+    randomize(store)
+    base = default_assignments(g, top)
+    from graphopt.baselines import baseline_step_time
+    bl = baseline_step_time(g, top)
+    batch = collect_rollouts(store, [g], top, sizes, [bl], 8, seed=4, hyper=PPOHyper(rollouts=8),
+                             embed_cfg=ecfg, policy_cfg=pcfg, fusion_cfg=FusionConfig(),
+                             base_assignments=[base])
+    graph_arrays(g, "g/", out)
+    out["baseline"] = np.float64(bl)
+    groups = set()
+    for i, s in enumerate(batch.samples):
+        p = f"r{i}/"
+        out[p + "reward"] = np.float64(s.reward)
+        out[p + "step_time"] = np.float64(s.step_time)
+        out[p + "valid"] = np.bool_(s.valid)
+        for t in tasks:
+            out[p + "actions/" + t] = s.bundle.actions[t]
+        fg = apply_fusion(g, ActionAssignment("fusion_priority", s.bundle.actions["fusion_priority"], 8),
+                          FusionConfig())
+        groups.add(tuple(fg.group_map))
+    out["count"] = np.int64(len(batch.samples))
+    out["distinct_groupings"] = np.int64(len(groups))
+    np.savez_compressed(OUT / "golden_rollouts_joint.npz", **out)
+
+
 def make_baselines():
     """Non-learned optimizers (baselines.py:50-237): fanout priorities, brute force over
     placement / schedule / fusion priorities, simulated annealing chains."""
@@ -473,7 +509,7 @@ def make_baselines():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads",
-                             "baselines"]
+                             "baselines", "rollouts_joint"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

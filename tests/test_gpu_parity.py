@@ -200,3 +200,32 @@ def test_nonfinite_embedding_raises():
         embed(g, feats, store, cfg)
     with pytest.raises(ValueError):
         embed(g, np.zeros((1, feats.shape[1])), store, cfg)
+
+
+def test_collect_rollouts_joint_tasks_match_reference():
+    """Joint placement + schedule + fusion rollouts (SURVEY §8(f) F1 reward path): every
+    rollout has its own fused grouping (native fusion pass, grouped DES launches); the
+    sampled actions, step times and rewards are the reference's."""
+    from paper_2010_12438_b200 import (EmbedConfig, FusionConfig, PolicyConfig, PPOHyper,
+                                       init_all_params, randomize_zero_init, uniform_topology)
+    from paper_2010_12438_b200.baselines import baseline_step_time, default_assignments
+    from paper_2010_12438_b200.training import collect_rollouts
+    z = golden("rollouts_joint")
+    g = _g(z, "g/")
+    top = uniform_topology(3)
+    sizes = {"placement": 3, "schedule_priority": 8, "fusion_priority": 8}
+    ecfg, pcfg = EmbedConfig(), PolicyConfig()
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
+    bl = baseline_step_time(g, top)
+    assert bl == float(z["baseline"])
+    n = int(z["count"])
+    batch = collect_rollouts(store, [g], top, sizes, [bl], n, 4, PPOHyper(rollouts=n), ecfg, pcfg,
+                             FusionConfig(), base_assignments=[default_assignments(g, top)])
+    assert int(z["distinct_groupings"]) > 1
+    for i, s in enumerate(batch.samples):
+        p = f"r{i}/"
+        for t in sizes:
+            assert np.array_equal(s.bundle.actions[t], z[p + "actions/" + t]), (i, t)
+        assert s.step_time == float(z[p + "step_time"]), i
+        assert s.reward == float(z[p + "reward"]), i
+        assert s.valid == bool(z[p + "valid"]), i
