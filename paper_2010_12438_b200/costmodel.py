@@ -57,3 +57,37 @@ def as_topology(top) -> Topology:
 def kernel_time(flops: float, nbytes: float, peak: float, bw: float) -> float:
     """costmodel.py:137-139 (host helper; the DES evaluates it on device)."""
     return max(flops / peak, nbytes / bw)
+
+
+def topology_from_dict(data: dict) -> Topology:
+    """costmodel.py:115-128 JSON form: devices (id, peak_flops, mem_bw, mem_capacity)
+    and links either {"uniform_bandwidth": bw} or a list of (src, dst, bandwidth)."""
+    devs = sorted(data["devices"], key=lambda d: int(d["id"]))
+    if [int(d["id"]) for d in devs] != list(range(len(devs))):
+        raise TopologyError("device ids must be dense 0..D-1")
+    d = len(devs)
+    links_field = data.get("links")
+    lb = np.zeros((d, d))
+    have = np.eye(d, dtype=bool)
+    if isinstance(links_field, dict):
+        lb[:] = float(links_field["uniform_bandwidth"])
+        have[:] = True
+    else:
+        for l in links_field or []:
+            s_, t_ = int(l["src"]), int(l["dst"])
+            if not (0 <= s_ < d and 0 <= t_ < d):  # costmodel.py:72-74
+                raise TopologyError(f"link references unknown device: {s_}->{t_}")
+            lb[s_, t_] = float(l["bandwidth"])
+            have[s_, t_] = True
+    if not have.all():  # costmodel.py:75-78
+        i, j = map(int, np.argwhere(~have)[0])
+        raise TopologyError(f"no link for device pair {i}->{j}")
+    return Topology([float(x["peak_flops"]) for x in devs], [float(x["mem_bw"]) for x in devs],
+                    [float(x["mem_capacity"]) for x in devs], lb)
+
+
+def load_topology(path) -> Topology:
+    """costmodel.py:110-112."""
+    import json
+    from pathlib import Path
+    return topology_from_dict(json.loads(Path(path).read_text()))

@@ -156,3 +156,110 @@ def node_features(graph, prev_actions=None, action_space=1) -> np.ndarray:
             feats[rows, col + vec[order]] = 1.0
         col += a
     return feats
+
+
+# ---------------------------------------------------------------------------------------
+# JSON graph format (graph.py:208-259): straight into the struct-of-
+# arrays Graph, same keys, defaults and GraphError conditions as the reference loader.
+_NODE_KEYS = {"id", "op", "shape", "flops", "out_bytes", "colocate"}
+_EDGE_KEYS = {"src", "dst", "bytes"}
+_TOP_KEYS = {"name", "nodes", "edges"}
+
+
+def from_dict(data: dict, name: str | None = None) -> Graph:
+    """graph.py:208-246: unknown keys rejected, unknown ops -> "other", edge bytes
+    default to the source node's output bytes, dense ordered ids, shape-consistent
+    output bytes, non-negative costs, acyclic."""
+    if not isinstance(data, dict):
+        raise GraphError("graph file must contain a JSON object")
+    extra = set(data) - _TOP_KEYS
+    if extra:
+        raise GraphError(f"unknown top-level keys: {sorted(extra)}")
+    ids, ops, flops, obytes, coloc = [], [], [], [], []
+    groups: dict = {}
+    for item in data.get("nodes", []):
+        extra = set(item) - _NODE_KEYS
+        if extra:
+            raise GraphError(f"node entry: unknown keys {sorted(extra)}")
+        if "id" not in item or "op" not in item:
+            raise GraphError("node entry missing 'id' or 'op'")
+        nid = int(item["id"])
+        op = item["op"] if item["op"] in OP_INDEX else "other"
+        shape = tuple(int(d) for d in item.get("shape", []))
+        f = float(item.get("flops", 0.0))
+        ob = float(item.get("out_bytes", 0.0))
+        if f < 0 or ob < 0:  # graph.py:52-53
+            raise GraphError(f"node {nid}: negative cost")
+        if any(d <= 0 for d in shape):
+            raise GraphError(f"node {nid}: non-positive shape dim")
+        if shape and ob != BYTES_PER_ELEMENT * math.prod(shape):
+            raise GraphError(f"node {nid}: output_bytes {ob} inconsistent with shape "
+                             f"{list(shape)} ({BYTES_PER_ELEMENT * math.prod(shape)} expected)")
+        c = item.get("colocate")
+        ids.append(nid)
+        ops.append(OP_INDEX[op])
+        flops.append(f)
+        obytes.append(ob)
+        coloc.append(-1 if c is None else groups.setdefault(c, len(groups)))
+    by_id = {nid: i for i, nid in enumerate(ids)}
+    src, dst, eb = [], [], []
+    for item in data.get("edges", []):
+        extra = set(item) - _EDGE_KEYS
+        if extra:
+            raise GraphError(f"edge entry: unknown keys {sorted(extra)}")
+        s, d = int(item["src"]), int(item["dst"])
+        if s not in by_id or d not in by_id:
+            raise GraphError(f"dangling edge {s}->{d}")
+        b = item.get("bytes")
+        b = float(b) if b is not None else obytes[by_id[s]]
+        if b < 0:
+            raise GraphError(f"edge {s}->{d}: negative bytes")
+        src.append(s)
+        dst.append(d)
+        eb.append(b)
+    n = len(ids)
+    if sorted(ids) != list(range(n)):  # graph.py:101-106
+        dup = sorted({i for i in ids if ids.count(i) > 1})
+        if dup:
+            raise GraphError(f"duplicate id {dup[0]}")
+        raise GraphError(f"node ids not dense 0..{n - 1}: {sorted(ids)[:5]}")
+    if ids != sorted(ids):
+        raise GraphError("nodes must be listed in id order")
+    g = Graph(ops, flops, obytes, src, dst, eb, coloc, name=data.get("name", name or ""))
+    g.topo_order()  # raises GraphError on a cycle, like the reference constructor
+    g.colocation_names = list(groups)
+    return g
+
+
+def loads(text: str, name: str | None = None) -> Graph:
+    """graph.py:249-254."""
+    import json
+    try:
+        data = json.loads(text)
+    except json.JSONDecodeError as exc:
+        raise GraphError(f"parse error: {exc}") from exc
+    return from_dict(data, name=name)
+
+
+def load_graph(path) -> Graph:
+    """graph.py:257-260."""
+    from pathlib import Path
+    path = Path(path)
+    return loads(path.read_text(), name=path.stem)
+
+
+def to_dict(graph) -> dict:
+    """JSON object form of a graph (the inverse of from_dict)."""
+    g = as_graph(graph)
+    names = getattr(g, "colocation_names", None)
+    nodes = []
+    for v in range(g.num_nodes):
+        item = {"id": v, "op": OP_TYPES[int(g.op[v])], "flops": float(g.flops[v]),
+                "out_bytes": float(g.out_bytes[v])}
+        c = int(g.coloc[v])
+        if c >= 0:
+            item["colocate"] = names[c] if names else f"g{c}"
+        nodes.append(item)
+    edges = [{"src": int(s), "dst": int(d), "bytes": float(b)}
+             for s, d, b in zip(g.src, g.dst, g.ebytes)]
+    return {"name": g.name, "nodes": nodes, "edges": edges}

@@ -422,6 +422,67 @@ def make_grads():
     np.savez_compressed(OUT / "golden_grads.npz", **out)
 
 
+def make_json():
+    """JSON graph / topology loader cases (graph.py:208-260, costmodel.py:110-128):
+    documents that parse (arrays of the reference's parse) and documents it rejects."""
+    import json as _json
+    from graphopt.costmodel import topology_from_dict
+    from graphopt.graph import GraphError, from_dict
+    docs = [
+        {"name": "tiny", "nodes": [{"id": 0, "op": "matmul", "flops": 1e9, "out_bytes": 64},
+                                   {"id": 1, "op": "relu", "shape": [4, 4], "out_bytes": 64},
+                                   {"id": 2, "op": "mystery-op", "flops": 5, "colocate": "a"},
+                                   {"id": 3, "op": "concat", "colocate": "a"}],
+         "edges": [{"src": 0, "dst": 1}, {"src": 1, "dst": 2, "bytes": 7},
+                   {"src": 0, "dst": 3}, {"src": 2, "dst": 3}, {"src": 0, "dst": 3}]},
+        {"nodes": [{"id": i, "op": "conv", "flops": float(i)} for i in range(5)],
+         "edges": [{"src": i, "dst": i + 1} for i in range(4)]},
+        {"nodes": [], "edges": []},
+        {"nodes": [{"id": 0, "op": "relu"}], "bogus": 1},
+        {"nodes": [{"id": 0, "op": "relu", "extra": 2}]},
+        {"nodes": [{"id": 1, "op": "relu"}]},
+        {"nodes": [{"id": 0, "op": "relu"}, {"id": 0, "op": "relu"}]},
+        {"nodes": [{"id": 1, "op": "relu"}, {"id": 0, "op": "relu"}]},
+        {"nodes": [{"id": 0, "op": "relu"}], "edges": [{"src": 0, "dst": 4}]},
+        {"nodes": [{"id": 0, "op": "relu"}, {"id": 1, "op": "relu"}],
+         "edges": [{"src": 0, "dst": 1}, {"src": 1, "dst": 0}]},
+        {"nodes": [{"id": 0, "op": "relu", "shape": [2], "out_bytes": 9}]},
+        {"nodes": [{"id": 0, "op": "relu", "flops": -1}]},
+        {"nodes": [{"op": "relu"}]},
+    ]
+    out = {}
+    for i, doc in enumerate(docs):
+        p = f"j{i}/"
+        out[p + "doc"] = np.array(_json.dumps(doc))
+        try:
+            g = from_dict(doc, name="x")
+            graph_arrays(g, p, out)
+            out[p + "gname"] = np.array(g.name)
+            out[p + "ok"] = np.bool_(True)
+        except GraphError:
+            out[p + "ok"] = np.bool_(False)
+    out["json_count"] = np.int64(len(docs))
+    tops = [{"devices": [{"id": 1, "peak_flops": 2e12, "mem_bw": 1e11, "mem_capacity": 8e9},
+                         {"id": 0, "peak_flops": 1e12, "mem_bw": 2e11, "mem_capacity": 16e9}],
+             "links": {"uniform_bandwidth": 5e9}},
+            {"devices": [{"id": 0, "peak_flops": 1e12, "mem_bw": 1e11, "mem_capacity": 1e9},
+                         {"id": 1, "peak_flops": 1e12, "mem_bw": 1e11, "mem_capacity": 1e9}],
+             "links": [{"src": 0, "dst": 1, "bandwidth": 1e9}, {"src": 1, "dst": 0, "bandwidth": 3e9}]},
+            {"devices": [{"id": 0, "peak_flops": 1e12, "mem_bw": 1e11, "mem_capacity": 1e9},
+                         {"id": 1, "peak_flops": 1e12, "mem_bw": 1e11, "mem_capacity": 1e9}],
+             "links": [{"src": 0, "dst": 1, "bandwidth": 1e9}]}]
+    for i, doc in enumerate(tops):
+        p = f"t{i}/"
+        out[p + "doc"] = np.array(_json.dumps(doc))
+        try:
+            topo_arrays(topology_from_dict(doc), p, out)
+            out[p + "ok"] = np.bool_(True)
+        except ValueError:
+            out[p + "ok"] = np.bool_(False)
+    out["top_count"] = np.int64(len(tops))
+    np.savez_compressed(OUT / "golden_json.npz", **out)
+
+
 def make_rollouts_joint():
     """collect_rollouts with the joint task set (placement + schedule + fusion priorities)
     on a graph where fusion merges happen, so every rollout has its own fused grouping."""
@@ -509,7 +570,7 @@ def make_baselines():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads",
-                             "baselines", "rollouts_joint"]
+                             "baselines", "rollouts_joint", "json"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)
