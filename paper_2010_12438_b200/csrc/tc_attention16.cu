@@ -284,22 +284,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       for (int j = 0; j < T; ++j) {
           mbar_wait_sleep(&sm.s_full[t][0], j & 1);
           fence_after();
-          PTX_LD16(base, ra);
+          PTX_LD16_AT(base, 0, ra);
           tmem_wait_ld();
-          PTX_LD16(base + 16, rb);
+          PTX_LD16_AT(base, 16, rb);
           softmax16(ra, pk);
-          PTX_ST8(base, pk);
+          PTX_ST8_AT(base, 0, pk);
           tmem_wait_ld();
-          PTX_LD16(base + 32, ra);
+          PTX_LD16_AT(base, 32, ra);
           softmax16(rb, pk);
-          PTX_ST8(base + 8, pk);
+          PTX_ST8_AT(base, 8, pk);
           tmem_wait_ld();
-          PTX_LD16(base + 48, rb);
+          PTX_LD16_AT(base, 48, rb);
           softmax16(ra, pk);
-          PTX_ST8(base + 16, pk);
+          PTX_ST8_AT(base, 16, pk);
           tmem_wait_ld();
           softmax16(rb, pk);
-          PTX_ST8(base + 24, pk);
+          PTX_ST8_AT(base, 24, pk);
           tmem_wait_st();
           fence_before();
           mbar_arrive(&sm.p_full[t][0]);

@@ -218,3 +218,18 @@ __device__ __forceinline__ float tf32_rn(float x) {
                    taddr),                                                                   \
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),    \
                "r"(r[7]))
+
+// immediate column offsets: one uniform base register for all chunks of a step
+#define PTX_LD16_AT(taddr, OFF, r)                                                           \
+  asm volatile(                                                                              \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%" \
+      "15}, [%16+" #OFF "];"                                                                 \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),  \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                \
+      : "r"(taddr))
+#define PTX_ST8_AT(taddr, OFF, r)                                                            \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0+" #OFF "], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"( \
+                   taddr),                                                                   \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),    \
+               "r"(r[7]))
