@@ -179,19 +179,23 @@ constexpr float A16_LIMIT = 32768.f;  // |A| above this re-runs the GEMM in tf32
 // accumulators, halving the weight bytes pulled from L2 per output row).
 // H: fp16 operands (kind::f16, K=16 per MMA).  The A slot then holds the raw fp32 TMA
 // chunk, which the split warps overwrite with its fp16 hi (first 8 KB) and lo halves.
-template <int BN, int MH, bool H = false>
+// WRCH > 0: the whole packed W (<= WRCH 32-k chunks, one N block) is loaded into shared
+// memory once per CTA and stays resident; the ring then carries only A chunks, so more
+// A bytes are in flight (these GEMMs are HBM-bound) and W is not re-read from L2 per tile.
+template <int BN, int MH, bool H = false, int WRCH = 0>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KB: one fp32 (or tf32 hi / lo) tile
   static constexpr int A_SLOT = H ? A_BYTES : 2 * A_BYTES;
   static constexpr int B_BYTES = BN * BK * (H ? 2 : 4);  // one of W_hi / W_lo
-  static constexpr int STAGE = MH * A_SLOT + 2 * B_BYTES;  // multiple of 1024
+  static constexpr int W_RES = WRCH * 2 * B_BYTES;        // resident W (hi + lo chunks)
+  static constexpr int STAGE = MH * A_SLOT + (WRCH ? 0 : 2 * B_BYTES);  // multiple of 1024
   // epilogue staging (4 warps x [32][36]) + bias[256] + ln gamma/beta[128]
   static constexpr int EPI_BYTES = 4 * 32 * 36 * 4 + 512 * 4;
   static constexpr int ALIGN_PAD = 1024;  // the swizzled A tiles need 1024-B alignment
   // 227 KB opt-in limit minus staging, barriers and alignment; >= 2 stages or the refill
   // schedule (stage of chunk g-1 refilled after chunk g is issued) cannot progress
-  static constexpr int BUDGET = 232448 - EPI_BYTES - 1536 - ALIGN_PAD;
-  static constexpr int NSMAX = H ? 6 : 4;
+  static constexpr int BUDGET = 232448 - EPI_BYTES - 1536 - ALIGN_PAD - W_RES;
+  static constexpr int NSMAX = WRCH ? 12 : H ? 6 : 4;
   static constexpr int NS = (BUDGET / STAGE) < NSMAX ? (BUDGET / STAGE) : NSMAX;
   static_assert(NS >= 2, "tc_gemm needs at least two smem stages");
   static_assert(STAGE % 1024 == 0, "stage must keep 1024-B alignment");
@@ -199,7 +203,7 @@ struct Cfg {
   static constexpr uint32_t ACOLS = MH * TCOLS;   // one accumulator set (all halves)
   static constexpr uint32_t TALLOC = 2 * ACOLS;   // double-buffered
   static_assert(TALLOC <= 512, "accumulators exceed TMEM");
-  static constexpr size_t SMEM = (size_t)NS * STAGE + EPI_BYTES + 1536 + ALIGN_PAD;
+  static constexpr size_t SMEM = (size_t)NS * STAGE + W_RES + EPI_BYTES + 1536 + ALIGN_PAD;
 };
 
 constexpr int G_THREADS = 288;  // warps 0-3 split A, 4-7 epilogue, 8 = TMA producer + MMA
@@ -215,26 +219,29 @@ __device__ __forceinline__ float activate(float x) {
 // (tile t -> m tile t / nblk, n block t % nblk).  The smem ring and the two TMEM
 // accumulators carry their phases across tiles, so the loads and MMAs of tile i+1
 // overlap the epilogue of tile i.
-template <int BN, int MH, bool LN, int ACT, bool H>
+template <int BN, int MH, bool LN, int ACT, bool H, int WRCH = 0>
 __global__ void __launch_bounds__(G_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmA2, Args a, int nblk, int ntiles) {
   static_assert(!H || MH == 1, "fp16 path uses one accumulator per tile");
-  using CF = Cfg<BN, MH, H>;
+  using CF = Cfg<BN, MH, H, WRCH>;
+  static_assert(WRCH == 0 || (H && MH == 1), "resident W: fp16 path only");
   if (a.gate && *a.gate == 0) return;  // tf32 re-run not needed
   constexpr int TM = BM * MH;  // rows per tile
   constexpr int NS = CF::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stage_base =
       smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // 1024-B aligned
-  float* epi = reinterpret_cast<float*>(stage_base + (size_t)NS * CF::STAGE);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_base + (size_t)NS * CF::STAGE + CF::EPI_BYTES);
+  uint8_t* w_res = stage_base + (size_t)NS * CF::STAGE;  // WRCH chunks (hi, lo) if resident
+  float* epi = reinterpret_cast<float*>(w_res + CF::W_RES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w_res + CF::W_RES + CF::EPI_BYTES);
   uint64_t* full = bars;                // [NS] tx bytes: A (TMA) + B (bulk)
   uint64_t* a_full = bars + NS;         // [NS] 128 arrivals: A split into hi/lo
   uint64_t* done = bars + 2 * NS;       // [NS] MMA commit: stage free
   uint64_t* acc_full = bars + 3 * NS;   // [2] MMA commit: accumulator ready
   uint64_t* acc_empty = bars + 3 * NS + 2;  // [2] 128 arrivals: accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 4);
+  uint64_t* w_full = bars + 3 * NS + 4;     // [1] resident W landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto A_hi = [&](int s, int h) {
     return reinterpret_cast<float*>(stage_base + (size_t)s * CF::STAGE + (size_t)h * CF::A_SLOT);
@@ -258,6 +265,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         mbar_init(&acc_full[b], 1);
         mbar_init(&acc_empty[b], 128);
       }
+      mbar_init(w_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA1)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
@@ -286,15 +294,29 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         const int k0 = c * BK;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(a.Bpk) +
                              ((size_t)(t % nblk) * nch + c) * 2 * CF::B_BYTES;
-        mbar_expect_tx(&full[s], MH * CF::A_BYTES + 2 * CF::B_BYTES);
+        mbar_expect_tx(&full[s], MH * CF::A_BYTES + (WRCH ? 0 : 2 * CF::B_BYTES));
         for (int h = 0; h < MH; ++h) {
           if (k0 < a.K1) tma_2d(A_hi(s, h), &tmA1, k0, m0 + h * BM, &full[s]);
           else tma_2d(A_hi(s, h), &tmA2, k0 - a.K1, m0 + h * BM, &full[s]);
         }
-        bulk_g2s(B_hi(s), src, CF::B_BYTES, &full[s]);
-        bulk_g2s(B_lo(s), src + CF::B_BYTES, CF::B_BYTES, &full[s]);
+        if constexpr (WRCH == 0) {
+          bulk_g2s(B_hi(s), src, CF::B_BYTES, &full[s]);
+          bulk_g2s(B_lo(s), src + CF::B_BYTES, CF::B_BYTES, &full[s]);
+        }
       };
+      if constexpr (WRCH > 0) {  // the whole W (one N block): nch x (hi, lo) chunks
+        if (my_tiles > 0) {
+          mbar_expect_tx(w_full, nch * 2 * CF::B_BYTES);
+          for (int c = 0; c < nch; ++c)
+            bulk_g2s(w_res + (size_t)c * 2 * CF::B_BYTES,
+                     reinterpret_cast<const uint8_t*>(a.Bpk) + (size_t)c * 2 * CF::B_BYTES,
+                     2 * CF::B_BYTES, w_full);
+        }
+      }
       for (int g = 0; g < NS && g < total; ++g) load(g);
+      if constexpr (WRCH > 0) {
+        if (my_tiles > 0) mbar_wait(w_full, 0);
+      }
       int g = 0;
       for (int tl = 0; tl < my_tiles; ++tl) {
         const int ab = tl & 1;
@@ -307,7 +329,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           mbar_wait(&full[s], ph);
           mbar_wait(&a_full[s], ph);
           fence_after();
-          const uint32_t bh = smem_u32(B_hi(s)), bl = smem_u32(B_lo(s));
+          const uint32_t bh = WRCH ? smem_u32(w_res + (size_t)c * 2 * CF::B_BYTES) : smem_u32(B_hi(s));
+          const uint32_t bl = bh + CF::B_BYTES;
           if constexpr (H) {
             // fp16 hi at +0, lo at +8 KB; 8-half K chunks 2 KB apart (A) / BN*16 B (B)
             const uint32_t a16 = smem_u32(A_hi(s, 0));
@@ -755,21 +778,27 @@ CUtensorMap a_map(const float* A, int64_t rows, int cols, int64_t ld) {
   return m;
 }
 
-template <int BN, int MH, bool LN, int ACT, bool H>
+template <int BN, int MH, bool LN, int ACT, bool H, int WRCH = 0>
 void launch(const CUtensorMap& m1, const CUtensorMap& m2, const tg::Args& a, int nblk,
             cudaStream_t st) {
-  using CF = tg::Cfg<BN, MH, H>;
+  using CF = tg::Cfg<BN, MH, H, WRCH>;
   static bool attr = false;
   if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, MH, LN, ACT, H>,
+    CUDA_CHECK(cudaFuncSetAttribute(tg::tc_gemm_kernel<BN, MH, LN, ACT, H, WRCH>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr = true;
   }
   const int ntiles = (int)cdiv(a.M, tg::BM * MH) * nblk;
   const int grid = std::min(ntiles, num_sms());
-  tg::tc_gemm_kernel<BN, MH, LN, ACT, H><<<grid, tg::G_THREADS, CF::SMEM, st>>>(m1, m2, a, nblk,
-                                                                              ntiles);
+  tg::tc_gemm_kernel<BN, MH, LN, ACT, H, WRCH><<<grid, tg::G_THREADS, CF::SMEM, st>>>(
+      m1, m2, a, nblk, ntiles);
   LAUNCH_CHECK();
+}
+
+// GO_GEMM_WRES=0 keeps W in the smem ring (streamed from L2 per tile)
+static bool w_resident_ok() {
+  const char* e = getenv("GO_GEMM_WRES");
+  return !(e && e[0] == '0');
 }
 
 // GO_GEMM_MH=2: two 128-row accumulators per tile sharing each W chunk (half the weight
@@ -806,7 +835,12 @@ void launch_all(const float* A1, int64_t lda1, const float* A2, int64_t lda2, tg
     a16.Bpk = static_cast<const float*>(W.w16);
     a16.ovf = W.ovf;
     a16.gate = nullptr;
-    launch<BN, 1, LN, ACT, true>(m1, m2, a16, nblk, st);
+    // resident W when the whole packed W is one N block of <= 4 chunks (K <= 128): the
+    // ring keeps >= 8 A stages (larger K would leave fewer A bytes in flight)
+    if (nblk == 1 && a.nch <= 4 && w_resident_ok() && tg::Cfg<BN, 1, true, 4>::NS >= 6)
+      launch<BN, 1, LN, ACT, true, 4>(m1, m2, a16, nblk, st);
+    else
+      launch<BN, 1, LN, ACT, true>(m1, m2, a16, nblk, st);
     a.gate = W.ovf;
   }
   a.Bpk = W.w32;
