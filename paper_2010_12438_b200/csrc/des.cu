@@ -61,10 +61,26 @@ struct DesCaps {
 
 enum { ST_OK = 0, ST_OVERFLOW = 1, ST_DEADLOCK = 2, ST_MEMLIST = 3 };
 
+template <int M>
+struct DesState {
+  double dev_t[M];
+  double busy[M], cur[M], pk[M], acc_a[M], acc_f[M];
+  double link_t[M * M];
+  int32_t dev_g[M], hs[M], na[M], nf[M];
+  int32_t link_g[M * M], lq_h[M * M], lq_n[M * M];
+  uint64_t lmask[(M * M + 63) / 64];
+  uint64_t amask[(M * M + 63) / 64];  // links with a transfer in flight
+};
+template <bool SH, class A, class B>
+__device__ __forceinline__ auto& pick_state(A& sh, B& lo) {
+  if constexpr (SH) return sh;
+  else return lo;
+}
+
 // MAXD: compile-time bound on the device count (4 / 8 / 16).  The per-placement link
 // arrays live in local memory; sizing them for 8 devices (64 links instead of 256) keeps
 // the 28 warps' working sets in L1: 2.14 -> 1.45 s for 4096 random cfg4 placements.
-template <int MAXD>
+template <int MAXD, bool SH>
 __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
                            int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
                            int d, const double* __restrict__ peakf, const double* __restrict__ mbw,
@@ -103,15 +119,28 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
       }
   }
 
-  double dev_t[MAXD];
-  int32_t dev_g[MAXD];
-  int32_t hs[MAXD];
-  double busy[MAXD], cur[MAXD], pk[MAXD], acc_a[MAXD], acc_f[MAXD];
-  int32_t na[MAXD], nf[MAXD];
-  double link_t[MAXD * MAXD];
-  int32_t link_g[MAXD * MAXD];
-  int32_t lq_h[MAXD * MAXD], lq_n[MAXD * MAXD];
-  uint64_t lmask[(MAXD * MAXD + 63) / 64];
+  // per-placement device / link state: in shared memory when the block is one placement
+  // (warp mode) -- local memory is interleaved across the warp's 32 threads, so a single
+  // active lane pulled a whole 128-B line per word and the warps' frames thrashed L1
+  __shared__ DesState<SH ? MAXD : 1> sh_state;
+  DesState<SH ? 1 : MAXD> lo_state;
+  auto& S = pick_state<SH>(sh_state, lo_state);
+  auto& dev_t = S.dev_t;
+  auto& dev_g = S.dev_g;
+  auto& hs = S.hs;
+  auto& busy = S.busy;
+  auto& cur = S.cur;
+  auto& pk = S.pk;
+  auto& acc_a = S.acc_a;
+  auto& acc_f = S.acc_f;
+  auto& na = S.na;
+  auto& nf = S.nf;
+  auto& link_t = S.link_t;
+  auto& link_g = S.link_g;
+  auto& lq_h = S.lq_h;
+  auto& lq_n = S.lq_n;
+  auto& lmask = S.lmask;
+  auto& amask = S.amask;
   for (int i = 0; i < d; ++i) {
     dev_t[i] = DINF;
     dev_g[i] = -1;
@@ -130,7 +159,6 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
     lq_h[s] = 0;
     lq_n[s] = 0;
   }
-  uint64_t amask[(MAXD * MAXD + 63) / 64];  // links with a transfer in flight
   for (int w = 0; w < (L + 63) / 64; ++w) lmask[w] = amask[w] = 0;
   uint32_t dmask = 0;  // devices with a non-empty ready heap
   int status = ST_OK;
@@ -389,7 +417,12 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
     const char* mode = getenv("GO_DES_MODE");
     const int lanes = (mode && !strcmp(mode, "lane")) ? 1 : 32;
     const int threads = 32;
-    auto kern = d <= 4 ? des_kernel<4> : d <= 8 ? des_kernel<8> : des_kernel<DES_MAXD>;
+    // warp mode: one placement per 32-thread block, its state in shared memory
+    auto kern = lanes == 32
+                    ? (d <= 4 ? des_kernel<4, true> : d <= 8 ? des_kernel<8, true>
+                                                            : des_kernel<DES_MAXD, true>)
+                    : (d <= 4 ? des_kernel<4, false> : d <= 8 ? des_kernel<8, false>
+                                                             : des_kernel<DES_MAXD, false>);
     kern<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
         v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
         dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
