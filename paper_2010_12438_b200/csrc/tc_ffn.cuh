@@ -115,14 +115,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       constexpr uint32_t ID = idesc_f16(BM, 128);
       // job order per tile: G1 0, G1 1, G2 0, G1 2, G2 1, G1 3, G2 2, G2 3 (4 weight
       // chunks each: G1(c) -> W1 block c, k-chunks 0..3; G2(c) -> W2 k-chunks 4c..4c+3)
-      constexpr int JT[8] = {1, 1, 2, 1, 2, 1, 2, 2};
-      constexpr int JC[8] = {0, 1, 0, 2, 1, 3, 2, 3};
+      // (bit-packed tables: a dynamically indexed local array would live in local memory,
+      // where a single active lane pulls a whole line per word)
+      auto job_g1 = [](int j) { return ((0x2Bu >> j) & 1u) != 0; };       // G1 at j = 0,1,3,5
+      auto job_c = [](int j) { return (int)((0x32312010u >> (4 * j)) & 0xFu); };
       const int total = my_tiles * 32;  // weight chunks
       auto load_w = [&](int g) {
         const int s = g % FF_NSW;
         const int i = g % 32, j = i >> 2, kc = i & 3;
-        const uint8_t* src = JT[j] == 1 ? a.W1 + (size_t)(JC[j] * 4 + kc) * 2 * 8192
-                                        : a.W2 + (size_t)(JC[j] * 4 + kc) * 2 * 8192;
+        const uint8_t* src = job_g1(j) ? a.W1 + (size_t)(job_c(j) * 4 + kc) * 2 * 8192
+                                       : a.W2 + (size_t)(job_c(j) * 4 + kc) * 2 * 8192;
         mbar_expect_tx(&w_full[s], FF_CHUNK);
         bulk_g2s(Ws + (size_t)s * FF_CHUNK, src, FF_CHUNK, &w_full[s]);
       };
@@ -136,8 +138,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       int g = 0;
       for (int tl = 0; tl < my_tiles; ++tl) {
         for (int j = 0; j < 8; ++j) {
-          const int c = JC[j];
-          const bool g1 = JT[j] == 1;
+          const int c = job_c(j);
+          const bool g1 = job_g1(j);
           const int u = tl * 4 + c;  // use index of D1[c & 1] and of the H buffer
           uint32_t dacc;
           const uint8_t* abase;
