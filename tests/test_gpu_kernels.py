@@ -318,3 +318,33 @@ def test_fused_ffn_matches_unfused_and_reruns_out_of_range():
     assert np.isfinite(h_f).all() and np.isfinite(lg_f).all()
     assert rel_err(h_f, h_u) < 1e-4
     assert rel_err(lg_f, lg_u) < 1e-4
+
+
+@pytest.mark.parametrize("d", [3, 6, 12, 16])
+def test_des_device_bounds_match_oracle(d):
+    """The DES kernel is instantiated for 4 / 8 / 16 devices with its per-placement state in
+    shared memory; every bound agrees bit-for-bit with the oracle DES (random heterogeneous
+    topologies, random placements and priorities, both policies)."""
+    from oracle import des as od
+    from oracle import graph as og
+    from paper_2010_12438_b200.costmodel import Topology
+    from paper_2010_12438_b200.simulator import ActionAssignment, simulate, singleton_fused
+    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    rng = np.random.default_rng(100 + d)
+    g = gen_workload(WorkloadSpec("multi-branch-cnn", 20, 1, 64, seed=d), node_cap=10**6)
+    ogr = og.make(g.num_nodes, g.op, g.flops, g.out_bytes, g.src, g.dst, g.ebytes)
+    peak = rng.choice([1e11, 5e11, 1e12], d)
+    bw = rng.choice([5e10, 1e11], d)
+    cap = np.full(d, 1e12)
+    lb = rng.choice([1e9, 5e9, 1e10], (d, d))
+    top = Topology(peak, bw, cap, lb)
+    otop = od.Topology(list(peak), list(bw), list(cap), [[float(x) for x in row] for row in lb])
+    fg = singleton_fused(g)
+    for policy in ("priority", "fifo"):
+        pl = rng.integers(0, d, g.num_nodes)
+        pr = rng.integers(0, 8, g.num_nodes)
+        res = simulate(fg, ActionAssignment("placement", pl, d),
+                       ActionAssignment("schedule_priority", pr, 8), top, policy=policy)
+        want = od.simulate(ogr, od.singleton(ogr), pl, pr, otop, policy=policy)
+        assert res.step_time == want["step_time"], (d, policy)
+        assert res.per_device_busy == list(want["busy"]), (d, policy)
