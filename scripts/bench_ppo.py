@@ -13,6 +13,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 def main():
     epochs = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+    big = len(sys.argv) > 2 and sys.argv[2] == "cfg4"
     import torch
 
     from paper_2010_12438_b200 import (EmbedConfig, FusionConfig, PolicyConfig, PPOHyper,
@@ -20,18 +21,24 @@ def main():
     from paper_2010_12438_b200.baselines import baseline_step_time, default_assignments
     from paper_2010_12438_b200.training import collect_rollouts, ppo_update
     from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
-    g = gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))
-    top = uniform_topology(2)
-    sizes = {"placement": 2}
+    if big:  # cfg4 graph: per-sample cost of the device backward at 80,001 nodes
+        g = gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
+        top = uniform_topology(8)
+        sizes = {"placement": 8}
+    else:
+        g = gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))
+        top = uniform_topology(2)
+        sizes = {"placement": 2}
     ecfg, pcfg = EmbedConfig(), PolicyConfig()
     store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
-    hyper = PPOHyper(epochs=epochs)
+    hyper = PPOHyper(epochs=epochs) if not big else PPOHyper(epochs=epochs, rollouts=4, minibatches=2)
     bl = baseline_step_time(g, top)
     base = [default_assignments(g, top)]
     # warm-up (context, graph upload, kernels)
-    b = collect_rollouts(store, [g], top, sizes, [bl], 40, 1, hyper, ecfg, pcfg, FusionConfig(),
+    nw = 2 if big else 40
+    b = collect_rollouts(store, [g], top, sizes, [bl], nw, 1, hyper, ecfg, pcfg, FusionConfig(),
                          base_assignments=base)
-    ppo_update(b, store, [g], top, sizes, PPOHyper(epochs=1, minibatches=1, rollouts=40), ecfg,
+    ppo_update(b, store, [g], top, sizes, PPOHyper(epochs=1, minibatches=1, rollouts=nw), ecfg,
                pcfg, seed=0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -42,7 +49,7 @@ def main():
     stats = ppo_update(batch, store, [g], top, sizes, hyper, ecfg, pcfg, seed=3)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    print(json.dumps({"metric": "PPO step (collect + update), cfg1", "rollouts": hyper.rollouts,
+    print(json.dumps({"metric": "PPO step (collect + update), " + ("cfg4 graph" if big else "cfg1"), "rollouts": hyper.rollouts,
                       "epochs": hyper.epochs, "minibatches": hyper.minibatches,
                       "collect_s": t1 - t0, "update_s": t2 - t1,
                       "minibatch_updates_per_s": hyper.epochs * hyper.minibatches / (t2 - t1),
