@@ -175,3 +175,24 @@ def test_fusion_pass_vs_oracle_workloads(spec):
         want = od.apply_fusion(og_, pri, max_group=8)
         got = fuse_groups(g, pri, 8)
         assert np.array_equal(got, want)
+
+
+def test_bench_reference_arm_json_contract():
+    """`bench.py --impl reference` (the CPU oracle on the host cores) prints one JSON line
+    with the contract's keys (run on the small cfg1 workload so the CPU suite stays fast)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
+                          "--workload", "cfg1", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
