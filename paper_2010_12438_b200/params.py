@@ -111,10 +111,50 @@ class ParamStore:
     def load(self, path):
         with np.load(path) as data:
             for name in data.files:
+                if name.startswith(("__adam_m__/", "__adam_v__/")) or name == "__adam_step__":
+                    continue
                 if name in self._params:
                     self._params[name].data = np.array(data[name], dtype=np.float64)
                 else:
                     self.add(name, data[name])
+        self.version += 1
+
+    # Checkpoint WITH the optimiser state.  The reference's save()
+    # writes parameter values only (tensor.py:456-458), so a resumed reference run
+    # restarts Adam from zero.  save_state() writes the same value arrays under the
+    # same names plus "__adam_m__/<name>", "__adam_v__/<name>" and "__adam_step__";
+    # load() above (the reference's semantics) skips those reserved keys, so either
+    # loader reads either file.  Hand a reference store the plain save() file.
+    _M, _V, _STEP = "__adam_m__/", "__adam_v__/", "__adam_step__"
+
+    def save_state(self, path):
+        arrs = {n: p.data for n, p in self.items()}
+        for n in self.names():
+            arrs[self._M + n] = self._m[n]
+            arrs[self._V + n] = self._v[n]
+        arrs[self._STEP] = np.array(self.step_count, np.int64)
+        np.savez(path, **arrs)
+
+    def load_state(self, path):
+        with np.load(path) as data:
+            files = set(data.files)
+            for name in data.files:
+                if name.startswith((self._M, self._V)) or name == self._STEP:
+                    continue
+                if name in self._params:
+                    self._params[name].data = np.array(data[name], dtype=np.float64)
+                else:
+                    self.add(name, data[name])
+            for name in self.names():
+                shape = self._params[name].data.shape
+                for key, dst in ((self._M + name, self._m), (self._V + name, self._v)):
+                    if key in files:
+                        a = np.array(data[key], dtype=np.float64)
+                        if a.shape != shape:
+                            raise ValueError(f"{key}: shape {a.shape} != parameter {shape}")
+                        dst[name] = a
+            if self._STEP in files:
+                self.step_count = int(data[self._STEP])
         self.version += 1
 
 

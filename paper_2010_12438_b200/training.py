@@ -24,7 +24,8 @@ from .runtime import context, torch
 from .simulator import ActionAssignment, FusedGraph, apply_fusion, simulate_many
 
 __all__ = ["Reward", "reward", "PPOHyper", "RolloutSample", "RolloutBatch", "task_action_sizes",
-           "bundle_assignments", "collect_rollouts", "run_decisions", "INVALID_REWARD"]
+           "bundle_assignments", "collect_rollouts", "run_decisions", "INVALID_REWARD",
+           "ppo_update", "TrainResult", "train", "decode_step_time", "pretrain_finetune_zeroshot"]
 
 
 @dataclass(frozen=True)
@@ -573,3 +574,151 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
         "entropy": stats["entropy_sum"] / max(1, stats["entropy_count"]),
         "value_loss": stats["value_loss_sum"] / max(1, stats["value_count"]),
     }
+
+
+# ---------------------------------------------------------------------------------------
+# training drivers (host orchestration over the device entry points above; SURVEY §8(f) F4:
+# what `graphopt optimize method=rl` runs, cli.py:208-220)
+
+@dataclass
+class TrainResult:
+    """training.py:236-248."""
+    store: object
+    best_store: object
+    curve: list
+    best_step_times: list
+    best_actions: list
+    baselines: list
+    stats_history: list = field(default_factory=list)
+
+    @property
+    def best_step_time(self) -> float:
+        return self.best_step_times[0]
+
+
+def train(graphs, topology, tasks, hyper, steps: int, seed: int, embed_cfg=None,
+          policy_cfg=None, fusion_cfg=None, store=None, incumbent_from_default: bool = True,
+          base_assignments=None) -> TrainResult:
+    """training.py:251-317, same control flow and the same numpy stream for the per-step
+    rollout and update seeds; each step is one device `collect_rollouts` (all rollouts
+    batched, one DES launch per graph) and one device `ppo_update`.  The incumbent /
+    best-store / divergence bookkeeping reads only per-rollout scalars, so the per-sample
+    action arrays are fetched from the device only for a new incumbent.
+    Single-process semantics: under torch.distributed every rank runs the same loop and
+    ppo_update shares the minibatch work (owner-computes + gradient all-reduce)."""
+    from .baselines import baseline_step_time
+    from .params import init_all_params
+    from .simulator import evaluate_assignments
+    embed_cfg = embed_cfg or EmbedConfig()
+    policy_cfg = policy_cfg or PolicyConfig()
+    fusion_cfg = fusion_cfg or FusionConfig()
+    graphs = [as_graph(g) for g in graphs]
+    task_sizes = task_action_sizes(topology, tasks, fusion_cfg.num_levels)
+    if store is None:
+        store = init_all_params(embed_cfg, policy_cfg, task_sizes, seed)
+    baselines = [baseline_step_time(g, topology, fusion_cfg) for g in graphs]
+    start_results = [
+        evaluate_assignments(g, topology,
+                             base_assignments[i] if base_assignments
+                             else default_assignments(g, topology, fusion_cfg.num_levels),
+                             fusion_cfg)
+        for i, g in enumerate(graphs)]
+    valid_exists = any(r.valid for r in start_results)
+    best_times = [r.step_time if (incumbent_from_default and r.valid) else math.inf
+                  for r in start_results]
+    best_actions = [None] * len(graphs)
+    best_store = store.clone()
+    best_mean_reward = -math.inf
+    curve, stats_history = [], []
+    rng = np.random.default_rng(seed)
+    bad_streak = 0
+    for step in range(steps):
+        batch = collect_rollouts(store, graphs, topology, task_sizes, baselines,
+                                 hyper.rollouts, int(rng.integers(2**31)), hyper,
+                                 embed_cfg, policy_cfg, fusion_cfg, base_assignments,
+                                 keep_logits=False)
+        for s in batch.samples:
+            if s.valid and s.step_time < best_times[s.graph_index]:
+                best_times[s.graph_index] = s.step_time
+                best_actions[s.graph_index] = {k: np.array(v, copy=True)
+                                               for k, v in s.bundle.actions.items()}
+        if batch.mean_reward > best_mean_reward:
+            best_mean_reward = batch.mean_reward
+            best_store = store.clone()
+        if batch.mean_reward < -9 and valid_exists:
+            bad_streak += 1
+            if bad_streak >= 50:
+                raise RuntimeError(
+                    f"training diverged: mean reward {batch.mean_reward:.2f} "
+                    f"below -9 for 50 consecutive steps")
+        else:
+            bad_streak = 0
+        stats = ppo_update(batch, store, graphs, topology, task_sizes, hyper,
+                           embed_cfg, policy_cfg, int(rng.integers(2**31)))
+        stats_history.append(stats)
+        finite = [t for t in best_times if math.isfinite(t)]
+        curve.append((step, float(np.mean(finite)) if finite else math.inf))
+    return TrainResult(store=store, best_store=best_store, curve=curve,
+                       best_step_times=best_times, best_actions=best_actions,
+                       baselines=baselines, stats_history=stats_history)
+
+
+def decode_step_time(graph, store, topology, tasks, embed_cfg, policy_cfg, fusion_cfg) -> float:
+    """training.py:320-332: greedy (temperature-0) decode, scored by the simulator;
+    invalid decodes count as +inf."""
+    from .policy import iterate_decisions
+    from .simulator import evaluate_assignments
+    task_sizes = task_action_sizes(topology, tasks, fusion_cfg.num_levels)
+    bundle, _ = iterate_decisions(graph, store, embed_cfg, policy_cfg, task_sizes,
+                                  policy_cfg.iterations, seed=0, temperature=0.0)
+    asg = bundle_assignments(graph, topology, bundle, task_sizes, fusion_cfg)
+    res = evaluate_assignments(graph, topology, asg, fusion_cfg)
+    return res.step_time if res.valid else math.inf
+
+
+def pretrain_finetune_zeroshot(train_graphs: dict, holdout_family: str, holdout_graph, topology,
+                               tasks, hyper, seed: int, pretrain_batches: int = 5,
+                               steps_per_batch: int = 4, batch_size: int = 4,
+                               finetune_steps: int = 20, embed_cfg=None, policy_cfg=None,
+                               fusion_cfg=None) -> dict:
+    """training.py:335-381: pretrain on the training families, then the holdout graph's
+    zero-shot decode, the best within `finetune_steps` of fine-tuning (never worse than
+    zero-shot) and a from-scratch run of the same budget."""
+    from .params import init_all_params
+    if finetune_steps > 50:
+        raise ValueError("fine-tuning budget is capped at 50 steps")
+    if holdout_family in train_graphs:
+        raise ValueError(f"holdout family {holdout_family!r} appears in the training set")
+    hname = getattr(holdout_graph, "name", None)
+    for family, gs in train_graphs.items():
+        for g in gs:
+            if getattr(g, "name", None) == hname:
+                raise ValueError(f"holdout graph {hname!r} appears in the training set")
+    embed_cfg = embed_cfg or EmbedConfig()
+    policy_cfg = policy_cfg or PolicyConfig()
+    fusion_cfg = fusion_cfg or FusionConfig()
+    task_sizes = task_action_sizes(topology, tasks, fusion_cfg.num_levels)
+    pool = [g for family in sorted(train_graphs) for g in train_graphs[family]]
+    rng = np.random.default_rng(seed)
+    store = init_all_params(embed_cfg, policy_cfg, task_sizes, seed)
+    for _ in range(pretrain_batches):
+        take = min(batch_size, len(pool))
+        idx = rng.choice(len(pool), size=take, replace=False)
+        result = train([pool[i] for i in idx], topology, tasks, hyper, steps_per_batch,
+                       int(rng.integers(2**31)), embed_cfg, policy_cfg, fusion_cfg, store=store)
+        store = result.store
+    zeroshot = decode_step_time(holdout_graph, store, topology, tasks, embed_cfg, policy_cfg,
+                                fusion_cfg)
+    finetuned = zeroshot
+    if finetune_steps > 0:
+        ft = train([holdout_graph], topology, tasks, hyper, finetune_steps,
+                   int(rng.integers(2**31)), embed_cfg, policy_cfg, fusion_cfg,
+                   store=store.clone(), incumbent_from_default=False)
+        finetuned = min(finetuned, ft.best_step_time)
+    scratch = math.inf
+    if finetune_steps > 0:
+        sc = train([holdout_graph], topology, tasks, hyper, finetune_steps,
+                   int(rng.integers(2**31)), embed_cfg, policy_cfg, fusion_cfg,
+                   incumbent_from_default=False)
+        scratch = sc.best_step_time
+    return {"zeroshot": zeroshot, "finetuned": finetuned, "scratch": scratch}

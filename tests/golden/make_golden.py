@@ -568,9 +568,40 @@ def make_baselines():
     np.savez_compressed(OUT / "golden_baselines.npz", **out)
 
 
+def make_train():
+    """reference train() (training.py:251-317) for 3 steps on a 12-node graph, plus
+    decode_step_time on the result and a save_state-free checkpoint round trip."""
+    from graphopt.costmodel import uniform_topology
+    from graphopt.training import decode_step_time, train
+    out = {}
+    ecfg = EmbedConfig(1, 8, 4)
+    pcfg = PolicyConfig(1, 8, 2, 3, 16, 8, 2)
+    g = C.random_graph(np.random.default_rng(3), 12, p_edge=0.3)
+    top = uniform_topology(2)
+    hyper = PPOHyper(lr=1e-2, rollouts=6, minibatches=2, epochs=2, entropy_coef=0.01)
+    res = train([g], top, ["placement"], hyper, 3, 11, ecfg, pcfg, FusionConfig())
+    graph_arrays(g, "g/", out)
+    out["baselines"] = np.array(res.baselines, np.float64)
+    out["best_step_times"] = np.array(res.best_step_times, np.float64)
+    out["curve"] = np.array([c for _, c in res.curve], np.float64)
+    out["has_best_actions"] = np.bool_(res.best_actions[0] is not None)
+    if res.best_actions[0] is not None:
+        out["best_actions"] = res.best_actions[0]["placement"]
+    for i, st in enumerate(res.stats_history):
+        for k, v in st.items():
+            out[f"stats{i}/{k}"] = np.float64(v)
+    for n in res.store.names():
+        out["store/" + n] = res.store[n].data
+        out["best/" + n] = res.best_store[n].data
+    out["step_count"] = np.int64(res.store.step_count)
+    out["decode"] = np.float64(decode_step_time(g, res.store, top, ["placement"], ecfg, pcfg,
+                                                FusionConfig()))
+    np.savez_compressed(OUT / "golden_train.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads",
-                             "baselines", "rollouts_joint", "json"]
+                             "baselines", "rollouts_joint", "json", "train"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

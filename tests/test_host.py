@@ -196,3 +196,38 @@ def test_bench_reference_arm_json_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_checkpoint_with_adam_state_roundtrip(tmp_path):
+    """save_state / load_state keep parameters, Adam moments and the
+    step count; the reference-format save() file still loads (values only), and the
+    reference-semantics load() ignores the optimiser keys of a save_state() file."""
+    from paper_2010_12438_b200 import EmbedConfig, PolicyConfig, init_all_params
+    ecfg, pcfg = EmbedConfig(1, 8, 4), PolicyConfig(1, 8, 2, 3, 16, 8, 2)
+    s = init_all_params(ecfg, pcfg, {"placement": 2}, 0)
+    rng = np.random.default_rng(0)
+    for n in s.names():
+        s._m[n] = rng.standard_normal(s[n].data.shape)
+        s._v[n] = rng.random(s[n].data.shape)
+    s.step_count = 17
+    s.save_state(tmp_path / "full.npz")
+    s.save(tmp_path / "plain.npz")
+    t = init_all_params(ecfg, pcfg, {"placement": 2}, 1)
+    t.load_state(tmp_path / "full.npz")
+    assert t.step_count == 17 and t.names() == s.names()
+    for n in s.names():
+        assert np.array_equal(t[n].data, s[n].data)
+        assert np.array_equal(t._m[n], s._m[n]) and np.array_equal(t._v[n], s._v[n])
+    u = init_all_params(ecfg, pcfg, {"placement": 2}, 1)
+    u.load(tmp_path / "full.npz")
+    assert u.names() == s.names() and u.step_count == 0
+    assert all(np.array_equal(u[n].data, s[n].data) for n in s.names())
+    w = init_all_params(ecfg, pcfg, {"placement": 2}, 1)
+    w.load_state(tmp_path / "plain.npz")
+    assert all(np.array_equal(w[n].data, s[n].data) for n in s.names())
+    assert w.step_count == 0 and not any(w._m[n].any() for n in w.names())
+    z = dict(np.load(tmp_path / "full.npz"))
+    z["__adam_m__/embed/in_w"] = np.zeros(3)
+    np.savez(tmp_path / "bad.npz", **z)
+    with pytest.raises(ValueError):
+        init_all_params(ecfg, pcfg, {"placement": 2}, 1).load_state(tmp_path / "bad.npz")
