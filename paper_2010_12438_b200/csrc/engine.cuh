@@ -213,7 +213,8 @@ void trunk_attention_tc(const float* qkv, int64_t ld, int n_head, int d_head, in
 bool trunk_mma_supported(int d_head);
 void trunk_attention_mma(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                          int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
-                         int64_t ldo, int32_t* flag, cudaStream_t st);
+                         int64_t ldo, int32_t* flag, cudaStream_t st, float* lse = nullptr,
+                         bool split = false);
 
 // ---- kernels: tc_attention.cu (tcgen05 / TMEM full attention, d_head <= 16)
 struct TcWork {

@@ -4,6 +4,7 @@
 // GraphSAGE embedding, accumulating parameter gradients into a float32 blob with the
 // parameter layout.  One call handles a whole minibatch as a ragged batch.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "train.cuh"
@@ -129,13 +130,44 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
                    /* backward scratch */ (size_t)(8 * std::max(gs, dm) + 8 * W + 2 * di + 2 * H);
   size_t bytes = (size_t)R * per_row * 4 + (size_t)R * 16 + (size_t)m.gtotal * 4 +
                  (size_t)F * (4 * dm + 2 * gs + 64) * 8 + (size_t)(m.n_chunks + 4) * 512 * 4 +
-                 (size_t)R * T * 64 + (8u << 20);
+                 (size_t)R * T * 64 + (8u << 20) + attention_backward_mma_scratch(R, H);
   Arena2 A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   int32_t* row_fwd = A.take<int32_t>(R);
   int32_t* row_node = A.take<int32_t>(R);
   GO_CHECK(m.gtotal + R < ((int64_t)1 << 31), "neighbour list exceeds 2^31 entries");
   int32_t* gidx = A.take<int32_t>(m.gtotal);
   int32_t* segoff = A.take<int32_t>(R + 1);
+  // attention on mma.sync tensor cores (split-fp16 operands, three MMAs per product:
+  // fp32-class results) with a gated fp32 SIMT re-run on range overflow;
+  // GO_TRAIN_ATTN=simt keeps the fp32 SIMT kernels only, =mma16 one fp16 MMA per product
+  // (faster, ~1e-3 relative gradients); GO_TRAIN_FWD=simt the SIMT tape forward only
+  const char* ta_env = getenv("GO_TRAIN_ATTN");
+  const bool attn_mma = trunk_mma_supported(dh) && !(ta_env && !strcmp(ta_env, "simt"));
+  const char* tf_env = getenv("GO_TRAIN_FWD");
+  const bool attn_mma_fwd = attn_mma && !(tf_env && !strcmp(tf_env, "simt"));
+  const bool attn_split = !(ta_env && !strcmp(ta_env, "mma16"));  // 3-MMA split precision
+  int32_t* aflag = A.take<int32_t>(64);
+  void* abw = A.take<char>((int64_t)attention_backward_mma_scratch(R, H));
+  auto attn_fwd = [&](const float* q, const float* k, const float* v, const AttnTile* tiles,
+                      int64_t nt, float* out, float* lse) {
+    if (attn_mma_fwd) {
+      trunk_attention_mma(q, k, v, W, H, dh, tiles, nt, out, W, aflag, st, lse, attn_split);
+      attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse, aflag);
+    } else {
+      attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse);
+    }
+  };
+  auto attn_bwd = [&](const float* q, const float* k, const float* v, const float* O,
+                      const float* dO_, const float* lse, const AttnTile* qt, int64_t nq,
+                      const KvTile* kt, int64_t nk, float* Db, float* dq_, float* dk_a,
+                      float* dv_a, float* dk_b, float* dv_b) {
+    if (attn_mma)
+      attention_backward_mma(q, k, v, O, dO_, W, lse, H, dh, qt, nq, kt, nk, Db, R, dq_, dk_a,
+                             dv_a, dk_b, dv_b, abw, aflag, st);
+    else
+      attention_backward(q, k, v, O, dO_, W, lse, H, dh, qt, nq, kt, nk, Db, R, dq_, dk_a, dv_a,
+                         dk_b, dv_b, st);
+  };
   row_fwd_fill(m.d_row_off, F, R, row_fwd, st);
   row_node_fill(m.d_views, m.d_row_off, row_fwd, R, row_node, st);
 
@@ -202,7 +234,7 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     gemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, Q_W)), W, Pw(S.blk(l, Q_B)), tqv[l], W, R, W, 0, st);
     gemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, K_W)), W, Pw(S.blk(l, K_B)), tkv[l], W, R, W, 0, st);
     gemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, V_W)), W, Pw(S.blk(l, V_B)), tvv[l], W, R, W, 0, st);
-    attention(tqv[l], tkv[l], tvv[l], W, H, dh, d_tq, (int64_t)tq.size(), tat[l], W, st, tls[l]);
+    attn_fwd(tqv[l], tkv[l], tvv[l], d_tq, (int64_t)tq.size(), tat[l], tls[l]);
     gemm(tat[l], W, W, nullptr, 0, 0, Pw(S.blk(l, O_W)), dm, Pw(S.blk(l, O_B)), tu1[l], dm, R, dm, 0, st);
     add_into(tu1[l], dm, txm[l], dm, R, dm, st);  // u1 = xm + o  (kept for LN1 backward)
     add_layernorm(tu1[l], dm, nullptr, 0, Pw(S.blk(l, LN1_G)), Pw(S.blk(l, LN1_B)), th1[l], dm, R, dm, st);
@@ -246,7 +278,7 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     gemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(Q_W)), W, Pw(S.ta(Q_B)), hqv[t], W, R, W, 0, st);
     gemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(K_W)), W, Pw(S.ta(K_B)), hkv[t], W, R, W, 0, st);
     gemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(V_W)), W, Pw(S.ta(V_B)), hvv[t], W, R, W, 0, st);
-    attention(hqv[t], hkv[t], hvv[t], W, H, dh, d_hq, (int64_t)hq.size(), hat[t], W, st, hls[t]);
+    attn_fwd(hqv[t], hkv[t], hvv[t], d_hq, (int64_t)hq.size(), hat[t], hls[t]);
     gemm(hat[t], W, W, nullptr, 0, 0, Pw(S.ta(O_W)), dm, Pw(S.ta(O_B)), ho[t], dm, R, dm, 0, st);
     gemm(ho[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, FC_W1)), di, Pw(S.task(t, FC_B1)), hf1[t], di, R,
          di, 1, st);
@@ -322,8 +354,8 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     // o = att Wo + bo
     dgemm_nt(dO, dm, Pw(S.ta(O_W)), dm, dAt, W, R, W, dm, false, st);
     wgrad(hat[t], W, W, nullptr, 0, 0, dO, dm, R, dm, Gw(S.ta(O_W)), Gw(S.ta(O_B)), st);
-    attention_backward(hqv[t], hkv[t], hvv[t], hat[t], dAt, W, hls[t], H, dh, d_hq, (int64_t)hq.size(),
-                       d_hk, (int64_t)hk.size(), Dbuf, R, dQ, dK, dV, nullptr, nullptr, st);
+    attn_bwd(hqv[t], hkv[t], hvv[t], hat[t], dAt, hls[t], d_hq, (int64_t)hq.size(), d_hk,
+             (int64_t)hk.size(), Dbuf, dQ, dK, dV, nullptr, nullptr);
     float* dHH = d3;
     dgemm_nt(dQ, W, Pw(S.ta(Q_W)), W, dHH, dm, R, dm, W, false, st);
     dgemm_nt(dK, W, Pw(S.ta(K_W)), W, dHH, dm, R, dm, W, true, st);
@@ -369,8 +401,8 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     // u1 = xm + att Wo + bo
     dgemm_nt(du1, dm, Pw(S.blk(l, O_W)), dm, dAt, W, R, W, dm, false, st);
     wgrad(tat[l], W, W, nullptr, 0, 0, du1, dm, R, dm, Gw(S.blk(l, O_W)), Gw(S.blk(l, O_B)), st);
-    attention_backward(tqv[l], tkv[l], tvv[l], tat[l], dAt, W, tls[l], H, dh, d_tq, (int64_t)tq.size(),
-                       d_tk, (int64_t)tk.size(), Dbuf, R, dQ, dK, dV, dK2, dV2, st);
+    attn_bwd(tqv[l], tkv[l], tvv[l], tat[l], dAt, tls[l], d_tq, (int64_t)tq.size(), d_tk,
+             (int64_t)tk.size(), Dbuf, dQ, dK, dV, dK2, dV2);
     // dxm = du1 + (dq Wq^T + dk_self Wk^T + dv_self Wv^T); weights see self + cache parts
     float* dxm = du1;
     dgemm_nt(dQ, W, Pw(S.blk(l, Q_W)), W, dxm, dm, R, dm, W, true, st);

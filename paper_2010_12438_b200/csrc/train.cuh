@@ -39,6 +39,23 @@ void attention_backward(const float* q, const float* k, const float* v, const fl
                         const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
                         float* Dbuf, int64_t M, float* dq, float* dk_a, float* dv_a, float* dk_b,
                         float* dv_b, cudaStream_t st);
+void attention_backward_D(const float* dO, const float* O, int64_t ld, int n_head, int d_head,
+                          int64_t M, float* Dbuf, cudaStream_t st);
+// the fp32 SIMT dq / dk,dv kernels alone (D already in Dbuf); gate: run only if *gate != 0
+void attention_backward_simt(const float* q, const float* k, const float* v, const float* dO,
+                             int64_t ld, const float* lse, int n_head, int d_head,
+                             const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
+                             const float* Dbuf, float* dq, float* dk_a, float* dv_a, float* dk_b,
+                             float* dv_b, const int32_t* gate, cudaStream_t st);
+// tensor-core (mma.sync fp16) backward, d_head <= 16, with the gated SIMT re-run
+// (csrc/attn_bwd_mma.cu); scratch >= attention_backward_mma_scratch(M, n_head) bytes
+size_t attention_backward_mma_scratch(int64_t M, int n_head);
+void attention_backward_mma(const float* q, const float* k, const float* v, const float* O,
+                            const float* dO, int64_t ld, const float* lse, int n_head,
+                            int d_head, const AttnTile* qtiles, int64_t nq, const KvTile* ktiles,
+                            int64_t nk, float* Dbuf, int64_t M, float* dq, float* dk_a,
+                            float* dv_a, float* dk_b, float* dv_b, void* scratch,
+                            int32_t* flag, cudaStream_t st);
 void ppo_loss(const float* logits, int a, int64_t R, const int32_t* actions,
               const int32_t* row_node, const double* old_logp, const int32_t* row_fwd,
               const int64_t* row_off, const double* fparams, double eps, double c_ent, int T,

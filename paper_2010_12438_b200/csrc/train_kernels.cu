@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(64) attn_bwd_dq_kernel(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     const float* __restrict__ dO, int64_t ld, const float* __restrict__ lse,
     const float* __restrict__ Dv, int n_head, int d_head, const AttnTile* __restrict__ tiles,
-    float* __restrict__ dq, float scale, float scale_log2) {
+    float* __restrict__ dq, float scale, float scale_log2, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ __align__(16) float Ks[64][DH];
   __shared__ __align__(16) float Vs[64][DH];
   const AttnTile tl = tiles[blockIdx.x];
@@ -427,7 +428,8 @@ __global__ void __launch_bounds__(64) attn_bwd_dkv_kernel(
     const float* __restrict__ dO, int64_t ld, const float* __restrict__ lse,
     const float* __restrict__ Dv, int n_head, int d_head, const KvTile* __restrict__ tiles,
     float* __restrict__ dk_a, float* __restrict__ dv_a, float* __restrict__ dk_b,
-    float* __restrict__ dv_b, float scale, float scale_log2) {
+    float* __restrict__ dv_b, float scale, float scale_log2, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ __align__(16) float Qs[64][DH];
   __shared__ __align__(16) float Ds_[64][DH];
   __shared__ float Ls[64], Dd[64];
@@ -490,26 +492,35 @@ __global__ void __launch_bounds__(64) attn_bwd_dkv_kernel(
   }
 }
 
-void attention_backward(const float* q, const float* k, const float* v, const float* O,
-                        const float* dO, int64_t ld, const float* lse, int n_head, int d_head,
-                        const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
-                        float* Dbuf, int64_t M, float* dq, float* dk_a, float* dv_a, float* dk_b,
-                        float* dv_b, cudaStream_t st) {
+void attention_backward_D(const float* dO, const float* O, int64_t ld, int n_head, int d_head,
+                          int64_t M, float* Dbuf, cudaStream_t st) {
   if (M <= 0) return;
-  float scale = (float)(1.0 / std::sqrt((double)d_head));
-  float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   attn_bwd_D_kernel<<<(unsigned)cdiv(M * n_head, 256), 256, 0, st>>>(dO, O, ld, n_head, d_head, M,
                                                                      Dbuf);
   LAUNCH_CHECK();
+}
+
+void attention_backward_simt(const float* q, const float* k, const float* v, const float* dO,
+                             int64_t ld, const float* lse, int n_head, int d_head,
+                             const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
+                             const float* Dbuf, float* dq, float* dk_a, float* dv_a, float* dk_b,
+                             float* dv_b, const int32_t* gate, cudaStream_t st) {
+  float scale = (float)(1.0 / std::sqrt((double)d_head));
+  float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   dim3 gq((unsigned)nq, (unsigned)n_head), gk((unsigned)nk, (unsigned)n_head);
 #define GO_BWD(DHV)                                                                             \
   do {                                                                                          \
-    attn_bwd_dq_kernel<DHV><<<gq, 64, 0, st>>>(q, k, v, dO, ld, lse, Dbuf, n_head, d_head, qtiles, \
-                                               dq, scale, scale_log2);                          \
-    LAUNCH_CHECK();                                                                             \
-    attn_bwd_dkv_kernel<DHV><<<gk, 64, 0, st>>>(q, k, v, dO, ld, lse, Dbuf, n_head, d_head, ktiles,\
-                                                dk_a, dv_a, dk_b, dv_b, scale, scale_log2);     \
-    LAUNCH_CHECK();                                                                             \
+    if (nq > 0) {                                                                               \
+      attn_bwd_dq_kernel<DHV><<<gq, 64, 0, st>>>(q, k, v, dO, ld, lse, Dbuf, n_head, d_head,     \
+                                                 qtiles, dq, scale, scale_log2, gate);          \
+      LAUNCH_CHECK();                                                                           \
+    }                                                                                           \
+    if (nk > 0) {                                                                               \
+      attn_bwd_dkv_kernel<DHV><<<gk, 64, 0, st>>>(q, k, v, dO, ld, lse, Dbuf, n_head, d_head,    \
+                                                  ktiles, dk_a, dv_a, dk_b, dv_b, scale,        \
+                                                  scale_log2, gate);                            \
+      LAUNCH_CHECK();                                                                           \
+    }                                                                                           \
   } while (0)
   if (d_head <= 4) GO_BWD(4);
   else if (d_head <= 8) GO_BWD(8);
@@ -518,6 +529,17 @@ void attention_backward(const float* q, const float* k, const float* v, const fl
   else if (d_head <= 64) GO_BWD(64);
   else GO_THROW(GO_ERR_UNSUPPORTED, "d_head %d > 64", d_head);
 #undef GO_BWD
+}
+
+void attention_backward(const float* q, const float* k, const float* v, const float* O,
+                        const float* dO, int64_t ld, const float* lse, int n_head, int d_head,
+                        const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
+                        float* Dbuf, int64_t M, float* dq, float* dk_a, float* dv_a, float* dk_b,
+                        float* dv_b, cudaStream_t st) {
+  if (M <= 0) return;
+  attention_backward_D(dO, O, ld, n_head, d_head, M, Dbuf, st);
+  attention_backward_simt(q, k, v, dO, ld, lse, n_head, d_head, qtiles, nq, ktiles, nk, Dbuf, dq,
+                          dk_a, dv_a, dk_b, dv_b, nullptr, st);
 }
 
 // ---------------------------------------------------------------------------------

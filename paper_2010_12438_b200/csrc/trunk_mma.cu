@@ -49,12 +49,18 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// SPLIT (the PPO tape's forward): every fp16 operand is a 2-term split x = hi + lo and
+// each product takes three MMAs (hi.hi + hi.lo + lo.hi), ~2^-21 relative -- the update's
+// Adam step needs fp32-class logits and log-sum-exps (see attn_bwd_mma.cu).
+template <bool SPLIT>
 __global__ void __launch_bounds__(128) trunk_mma_kernel(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     int64_t ld, int d_head, const AttnTile* __restrict__ tiles, float* __restrict__ out,
-    int64_t ldo, float qscale, int32_t* __restrict__ flag) {
-  __shared__ __align__(16) __half Ks[KC * KS];
-  __shared__ __align__(16) __half Vt[16 * VS];
+    int64_t ldo, float qscale, int32_t* __restrict__ flag, float* __restrict__ lse, int n_head) {
+  constexpr int KS2 = SPLIT ? 40 : KS;  // halves per key row (hi 0..15, lo 16..31)
+  constexpr int NP = SPLIT ? 2 : 1;
+  __shared__ __align__(16) __half Ks[KC * KS2];
+  __shared__ __align__(16) __half Vt[16 * NP * VS];
   const AttnTile tl = tiles[blockIdx.x];
   const int head = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -63,7 +69,7 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
   bool big = false;
 
   // A fragments of this warp's 16 queries (rows g and g + 8, dims 2tq.. and 2tq+8..)
-  uint32_t qa[4];
+  uint32_t qa[4], ql[4];
   {
     const int64_t r0 = tl.q0 + warp * 16 + g, r1 = r0 + 8;
     float x[8];
@@ -77,10 +83,15 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
       x[i] = val;
     }
     // x[0]=(r0,2tq) x[1]=(r1,2tq) x[2]=(r0,2tq+1) x[3]=(r1,2tq+1) x[4..7] same at +8
-    qa[0] = pack2(x[0], x[2]);
-    qa[1] = pack2(x[1], x[3]);
-    qa[2] = pack2(x[4], x[6]);
-    qa[3] = pack2(x[5], x[7]);
+    const int pi[4][2] = {{0, 2}, {1, 3}, {4, 6}, {5, 7}};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      qa[j] = pack2(x[pi[j][0]], x[pi[j][1]]);
+      if (SPLIT) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qa[j]));
+        ql[j] = pack2(x[pi[j][0]] - f.x, x[pi[j][1]] - f.y);
+      }
+    }
   }
   float o[2][4];
 #pragma unroll
@@ -96,7 +107,7 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
     {
       // stage: thread = (key, 8-dim half); K row-major [key][d], V transposed [d][key]
       const int key = tid >> 1, d0 = (tid & 1) * 8;
-      __align__(16) __half kr[8];
+      __align__(16) __half kr[8], kl[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int d = d0 + i;
@@ -107,9 +118,16 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
           big |= !(fabsf(kv) <= RANGE) || !(fabsf(vv) <= RANGE);
         }
         kr[i] = __float2half_rn(kv);
-        Vt[d * VS + key] = __float2half_rn(vv);
+        const __half vh = __float2half_rn(vv);
+        Vt[d * VS + key] = vh;
+        if (SPLIT) {
+          kl[i] = __float2half_rn(kv - __half2float(kr[i]));
+          Vt[(16 + d) * VS + key] = __float2half_rn(vv - __half2float(vh));
+        }
       }
-      *reinterpret_cast<uint4*>(&Ks[key * KS + d0]) = *reinterpret_cast<const uint4*>(kr);
+      *reinterpret_cast<uint4*>(&Ks[key * KS2 + d0]) = *reinterpret_cast<const uint4*>(kr);
+      if (SPLIT)
+        *reinterpret_cast<uint4*>(&Ks[key * KS2 + 16 + d0]) = *reinterpret_cast<const uint4*>(kl);
     }
     __syncthreads();
     // S = Q K^T: 8 n-tiles of 8 keys
@@ -117,9 +135,14 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
       s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-      const __half* kp = &Ks[(8 * n + g) * KS + 2 * tq];
+      const __half* kp = &Ks[(8 * n + g) * KS2 + 2 * tq];
       const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kp);
       const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kp + 8);
+      if (SPLIT) {
+        mma16816(s[n], ql, b0, b1);
+        mma16816(s[n], qa, *reinterpret_cast<const uint32_t*>(kp + 16),
+                 *reinterpret_cast<const uint32_t*>(kp + 24));
+      }
       mma16816(s[n], qa, b0, b1);
     }
     // online softmax over the chunk (rows g: s[.][0..1], g + 8: s[.][2..3])
@@ -149,7 +172,7 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
       o[n][2] *= f1;
       o[n][3] *= f1;
     }
-    uint32_t pa[8][2];  // P as fp16 pairs: [n-tile][row g | row g+8]
+    uint32_t pa[8][2], pl[8][2];  // P as fp16 pairs: [n-tile][row g | row g+8]
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
       const float p0 = ex2(s[n][0] - m0), p1 = ex2(s[n][1] - m0);
@@ -158,16 +181,29 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
       l1 += p2 + p3;
       pa[n][0] = pack2(p0, p1);
       pa[n][1] = pack2(p2, p3);
+      if (SPLIT) {
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&pa[n][0]));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&pa[n][1]));
+        pl[n][0] = pack2(p0 - a.x, p1 - a.y);
+        pl[n][1] = pack2(p2 - b.x, p3 - b.y);
+      }
     }
     // O += P V: k-steps of 16 keys (n-tiles 2kk, 2kk+1), n-tiles of 8 dims
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
+      const uint32_t al[4] = {pl[2 * kk][0], pl[2 * kk][1], pl[2 * kk + 1][0], pl[2 * kk + 1][1]};
 #pragma unroll
       for (int n = 0; n < 2; ++n) {
         const __half* vp = &Vt[(8 * n + g) * VS + 16 * kk + 2 * tq];
-        mma16816(o[n], a, *reinterpret_cast<const uint32_t*>(vp),
-                 *reinterpret_cast<const uint32_t*>(vp + 8));
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(vp);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(vp + 8);
+        if (SPLIT) {
+          mma16816(o[n], al, b0, b1);
+          mma16816(o[n], a, *reinterpret_cast<const uint32_t*>(vp + 16 * VS),
+                   *reinterpret_cast<const uint32_t*>(vp + 16 * VS + 8));
+        }
+        mma16816(o[n], a, b0, b1);
       }
     }
   }
@@ -177,6 +213,10 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   const float i0 = 1.f / l0, i1 = 1.f / l1;
   const int64_t r0 = tl.q0 + warp * 16 + g, r1 = r0 + 8;
+  if (lse && tq == 0) {  // log2-sum-exp of the scaled scores (the training tape's P recompute)
+    if (r0 < tl.q1) lse[r0 * n_head + head] = m0 + log2f(l0);
+    if (r1 < tl.q1) lse[r1 * n_head + head] = m1 + log2f(l1);
+  }
 #pragma unroll
   for (int n = 0; n < 2; ++n) {
     const int d = 8 * n + 2 * tq;
@@ -198,14 +238,18 @@ bool trunk_mma_supported(int d_head) { return d_head >= 1 && d_head <= 16; }
 
 void trunk_attention_mma(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                          int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
-                         int64_t ldo, int32_t* flag, cudaStream_t st) {
+                         int64_t ldo, int32_t* flag, cudaStream_t st, float* lse, bool split) {
   if (num_tiles <= 0) return;
   GO_CHECK(d_head <= 16, "trunk_attention_mma needs d_head <= 16");
   CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
   const float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   dim3 grid((unsigned)num_tiles, (unsigned)n_head);
-  tm::trunk_mma_kernel<<<grid, 128, 0, st>>>(q, k, v, ld, d_head, tiles_dev, out, ldo, qscale,
-                                             flag);
+  if (split)
+    tm::trunk_mma_kernel<true><<<grid, 128, 0, st>>>(q, k, v, ld, d_head, tiles_dev, out, ldo,
+                                                     qscale, flag, lse, n_head);
+  else
+    tm::trunk_mma_kernel<false><<<grid, 128, 0, st>>>(q, k, v, ld, d_head, tiles_dev, out, ldo,
+                                                      qscale, flag, lse, n_head);
   LAUNCH_CHECK();
 }
 
