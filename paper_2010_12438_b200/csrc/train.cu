@@ -130,7 +130,9 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
                    /* backward scratch */ (size_t)(8 * std::max(gs, dm) + 8 * W + 2 * di + 2 * H);
   size_t bytes = (size_t)R * per_row * 4 + (size_t)R * 16 + (size_t)m.gtotal * 4 +
                  (size_t)F * (4 * dm + 2 * gs + 64) * 8 + (size_t)(m.n_chunks + 4) * 512 * 4 +
-                 (size_t)R * T * 64 + (8u << 20) + attention_backward_mma_scratch(R, H);
+                 (size_t)R * T * 64 + (8u << 20) + attention_backward_mma_scratch(R, H) +
+                 /* packed tape-forward weights */ (size_t)(2 * Lg + 6 * Lt + 8 * T + 4) *
+                     (size_t)tc_gemm_packed_floats(std::max(2 * gs, di), std::max(dm, di)) * 6 + (16u << 20);
   Arena2 A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   int32_t* row_fwd = A.take<int32_t>(R);
   int32_t* row_node = A.take<int32_t>(R);
@@ -156,6 +158,37 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     } else {
       attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse);
     }
+  };
+  // tape forward GEMMs on the tcgen05 split-precision GEMM (tc_gemm: fp16 3-pass with
+  // the tf32 re-run on range overflow, as the inference forward); operands whose rows are
+  // not 16-B aligned (the attention output, ld = H*d_head) stay on the fp32 SIMT GEMM.
+  // GO_TRAIN_GEMM=simt keeps every tape GEMM on SIMT.
+  const char* tg_env = getenv("GO_TRAIN_GEMM");
+  const bool tc_fwd = !(tg_env && !strcmp(tg_env, "simt"));
+  auto fgemm = [&](const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
+                   const float* Wt, int64_t ldw, const float* bias, float* C, int64_t ldc,
+                   int64_t M, int N, int act, cudaStream_t s_) {
+    const auto al = [](const float* p, int64_t ld) {
+      return p == nullptr || ((uintptr_t)p % 16 == 0 && ld % 4 == 0);
+    };
+    const bool ok = tc_fwd && al(A1, lda1) && al(A2, lda2) && (A2 == nullptr || K1 % 32 == 0);
+    if (!ok) {
+      gemm(A1, lda1, K1, A2, lda2, K2, Wt, ldw, bias, C, ldc, M, N, act, s_);
+      return;
+    }
+    const int K = K1 + (A2 ? K2 : 0);
+    const int64_t nf = (int64_t)tc_gemm_packed_floats(K, N);
+    TcW w;
+    float* w32 = A.take<float>(nf);
+    void* w16 = A.take<float>((nf + 1) / 2);
+    int32_t* ovf = A.take<int32_t>(1);
+    CUDA_CHECK(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s_));
+    tc_gemm_pack(Wt, nullptr, nullptr, N, ldw, K, N, w32, s_);
+    tc_gemm_pack16(Wt, nullptr, nullptr, N, ldw, K, N, w16, s_, ovf);
+    w.w32 = w32;
+    w.w16 = w16;
+    w.ovf = ovf;
+    tc_gemm(A1, lda1, K1, A2, lda2, K2, w, bias, C, ldc, M, N, act, s_);
   };
   auto attn_bwd = [&](const float* q, const float* k, const float* v, const float* O,
                       const float* dO_, const float* lse, const AttnTile* qt, int64_t nq,
@@ -195,11 +228,11 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   features_inproj(m.d_views, m.d_row_off, row_fwd, R, b.prev_actions, T, tcol, Pw(S.e_in_w()),
                   Pw(S.e_in_b()), gs, eh[0], gs, st);
   for (int l = 0; l < Lg; ++l) {
-    gemm(eh[l], gs, gs, nullptr, 0, 0, Pw(S.e_layer(l, 0)), gs, Pw(S.e_layer(l, 1)), et[l], gs, R,
+    fgemm(eh[l], gs, gs, nullptr, 0, 0, Pw(S.e_layer(l, 0)), gs, Pw(S.e_layer(l, 1)), et[l], gs, R,
          gs, 2, st);
     segment_max(et[l], gs, segoff, gidx, R, gs, ep[l], gs, st,
                 ea[l]);
-    gemm(eh[l], gs, gs, ep[l], gs, gs, Pw(S.e_layer(l, 2)), gs, Pw(S.e_layer(l, 3)), eh[l + 1], gs,
+    fgemm(eh[l], gs, gs, ep[l], gs, gs, Pw(S.e_layer(l, 2)), gs, Pw(S.e_layer(l, 3)), eh[l + 1], gs,
          R, gs, 1, st);
   }
   mean_rows(eh[Lg], gs, m.d_row_off, F, m.d_chunks, m.n_chunks, gs, ge, gs, part, st);
@@ -227,20 +260,20 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     tf1[l] = A.take<float>(R * di);
     tu2[l] = A.take<float>(R * dm);
   }
-  gemm(node_embed, gs, gs, nullptr, 0, 0, Pw(S.pbase()), dm, Pw(S.pbase() + 1), tx[0], dm, R, dm, 0,
+  fgemm(node_embed, gs, gs, nullptr, 0, 0, Pw(S.pbase()), dm, Pw(S.pbase() + 1), tx[0], dm, R, dm, 0,
        st);
   for (int l = 0; l < Lt; ++l) {
     mul_rowvec(tx[l], dm, mod, dm, row_fwd, txm[l], dm, R, dm, st);
-    gemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, Q_W)), W, Pw(S.blk(l, Q_B)), tqv[l], W, R, W, 0, st);
-    gemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, K_W)), W, Pw(S.blk(l, K_B)), tkv[l], W, R, W, 0, st);
-    gemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, V_W)), W, Pw(S.blk(l, V_B)), tvv[l], W, R, W, 0, st);
+    fgemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, Q_W)), W, Pw(S.blk(l, Q_B)), tqv[l], W, R, W, 0, st);
+    fgemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, K_W)), W, Pw(S.blk(l, K_B)), tkv[l], W, R, W, 0, st);
+    fgemm(txm[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, V_W)), W, Pw(S.blk(l, V_B)), tvv[l], W, R, W, 0, st);
     attn_fwd(tqv[l], tkv[l], tvv[l], d_tq, (int64_t)tq.size(), tat[l], tls[l]);
-    gemm(tat[l], W, W, nullptr, 0, 0, Pw(S.blk(l, O_W)), dm, Pw(S.blk(l, O_B)), tu1[l], dm, R, dm, 0, st);
+    fgemm(tat[l], W, W, nullptr, 0, 0, Pw(S.blk(l, O_W)), dm, Pw(S.blk(l, O_B)), tu1[l], dm, R, dm, 0, st);
     add_into(tu1[l], dm, txm[l], dm, R, dm, st);  // u1 = xm + o  (kept for LN1 backward)
     add_layernorm(tu1[l], dm, nullptr, 0, Pw(S.blk(l, LN1_G)), Pw(S.blk(l, LN1_B)), th1[l], dm, R, dm, st);
-    gemm(th1[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, FF_W1)), di, Pw(S.blk(l, FF_B1)), tf1[l], di, R,
+    fgemm(th1[l], dm, dm, nullptr, 0, 0, Pw(S.blk(l, FF_W1)), di, Pw(S.blk(l, FF_B1)), tf1[l], di, R,
          di, 1, st);
-    gemm(tf1[l], di, di, nullptr, 0, 0, Pw(S.blk(l, FF_W2)), dm, Pw(S.blk(l, FF_B2)), tu2[l], dm, R,
+    fgemm(tf1[l], di, di, nullptr, 0, 0, Pw(S.blk(l, FF_W2)), dm, Pw(S.blk(l, FF_B2)), tu2[l], dm, R,
          dm, 0, st);
     add_into(tu2[l], dm, th1[l], dm, R, dm, st);  // u2 = h1 + ff
     add_layernorm(tu2[l], dm, nullptr, 0, Pw(S.blk(l, LN2_G)), Pw(S.blk(l, LN2_B)), tx[l + 1], dm, R,
@@ -269,23 +302,23 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   for (int t = 0; t < T; ++t) {
     zero_in[t] = (t == 0) || (b.ablate_mask >> t & 1);
     if (zero_in[t])
-      gemm(hid, dm, dm, nullptr, 0, 0, Pw(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, Pw(S.task(t, CAT_B)),
+      fgemm(hid, dm, dm, nullptr, 0, 0, Pw(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, Pw(S.task(t, CAT_B)),
            hc[t], dm, R, dm, 0, st);
     else
-      gemm(hrep[t - 1], dm, dm, hid, dm, dm, Pw(S.task(t, CAT_W)), dm, Pw(S.task(t, CAT_B)), hc[t], dm, R,
+      fgemm(hrep[t - 1], dm, dm, hid, dm, dm, Pw(S.task(t, CAT_W)), dm, Pw(S.task(t, CAT_B)), hc[t], dm, R,
            dm, 0, st);
     add_layernorm(hc[t], dm, nullptr, 0, Pw(S.task(t, LN_G)), Pw(S.task(t, LN_B)), hh[t], dm, R, dm, st);
-    gemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(Q_W)), W, Pw(S.ta(Q_B)), hqv[t], W, R, W, 0, st);
-    gemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(K_W)), W, Pw(S.ta(K_B)), hkv[t], W, R, W, 0, st);
-    gemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(V_W)), W, Pw(S.ta(V_B)), hvv[t], W, R, W, 0, st);
+    fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(Q_W)), W, Pw(S.ta(Q_B)), hqv[t], W, R, W, 0, st);
+    fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(K_W)), W, Pw(S.ta(K_B)), hkv[t], W, R, W, 0, st);
+    fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(V_W)), W, Pw(S.ta(V_B)), hvv[t], W, R, W, 0, st);
     attn_fwd(hqv[t], hkv[t], hvv[t], d_hq, (int64_t)hq.size(), hat[t], hls[t]);
-    gemm(hat[t], W, W, nullptr, 0, 0, Pw(S.ta(O_W)), dm, Pw(S.ta(O_B)), ho[t], dm, R, dm, 0, st);
-    gemm(ho[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, FC_W1)), di, Pw(S.task(t, FC_B1)), hf1[t], di, R,
+    fgemm(hat[t], W, W, nullptr, 0, 0, Pw(S.ta(O_W)), dm, Pw(S.ta(O_B)), ho[t], dm, R, dm, 0, st);
+    fgemm(ho[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, FC_W1)), di, Pw(S.task(t, FC_B1)), hf1[t], di, R,
          di, 1, st);
-    gemm(hf1[t], di, di, nullptr, 0, 0, Pw(S.task(t, FC_W2)), dm, Pw(S.task(t, FC_B2)), hrep[t], dm, R,
+    fgemm(hf1[t], di, di, nullptr, 0, 0, Pw(S.task(t, FC_W2)), dm, Pw(S.task(t, FC_B2)), hrep[t], dm, R,
          dm, 0, st);
     int a = cfg.task_sizes[t];
-    gemm(hrep[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, OUT_W)), a, Pw(S.task(t, OUT_B)), hlog[t], a, R,
+    fgemm(hrep[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, OUT_W)), a, Pw(S.task(t, OUT_B)), hlog[t], a, R,
          a, 0, st);
   }
   mean_rows(hrep[T - 1], dm, m.d_row_off, F, m.d_chunks, m.n_chunks, dm, meanrep, dm, part, st);
