@@ -131,7 +131,8 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   size_t bytes = (size_t)R * per_row * 4 + (size_t)R * 16 + (size_t)m.gtotal * 4 +
                  (size_t)F * (4 * dm + 2 * gs + 64) * 8 + (size_t)(m.n_chunks + 4) * 512 * 4 +
                  (size_t)R * T * 64 + (8u << 20) + attention_backward_mma_scratch(R, H) +
-                 /* packed tape-forward weights */ (size_t)(2 * Lg + 6 * Lt + 8 * T + 4) *
+                 /* backward dX scratch */ (size_t)R * std::max(dm, gs) * 4 +
+                 /* packed tape weights (forward + transposed backward) */ 2 * (size_t)(2 * Lg + 6 * Lt + 8 * T + 4) *
                      (size_t)tc_gemm_packed_floats(std::max(2 * gs, di), std::max(dm, di)) * 6 + (16u << 20);
   Arena2 A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   int32_t* row_fwd = A.take<int32_t>(R);
@@ -189,6 +190,33 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     w.w16 = w16;
     w.ovf = ovf;
     tc_gemm(A1, lda1, K1, A2, lda2, K2, w, bias, C, ldc, M, N, act, s_);
+  };
+  // backward dX = dY W^T on the tcgen05 tf32 3-pass GEMM (fp32-class; gradients keep
+  // fp32's exponent range, so no fp16 pass) for 16-B-aligned dY rows; accumulating calls
+  // go through a scratch tile and an add.  Others stay on the SIMT dgemm_nt.
+  float* dtmp = nullptr;
+  const int tmp_cols = std::max(dm, gs);
+  auto dgemm = [&](const float* dY, int64_t ldd, const float* Wt, int64_t ldw, float* dX,
+                   int64_t ldx, int64_t M, int Kin, int Nout, bool accumulate) {
+    const bool ok = tc_fwd && (uintptr_t)dY % 16 == 0 && ldd % 4 == 0 &&
+                    (!accumulate || Kin <= tmp_cols);
+    if (!ok) {
+      dgemm_nt(dY, ldd, Wt, ldw, dX, ldx, M, Kin, Nout, accumulate, st);
+      return;
+    }
+    float* wt = A.take<float>((int64_t)Nout * Kin);
+    transpose(Wt, ldw, Kin, Nout, wt, st);
+    TcW w;
+    float* w32 = A.take<float>((int64_t)tc_gemm_packed_floats(Nout, Kin));
+    tc_gemm_pack(wt, nullptr, nullptr, Kin, Kin, Nout, Kin, w32, st);
+    w.w32 = w32;
+    if (!accumulate) {
+      tc_gemm(dY, ldd, Nout, nullptr, 0, 0, w, nullptr, dX, ldx, M, Kin, 0, st);
+    } else {
+      if (!dtmp) dtmp = A.take<float>(M * tmp_cols);
+      tc_gemm(dY, ldd, Nout, nullptr, 0, 0, w, nullptr, dtmp, Kin, M, Kin, 0, st);
+      add_into(dX, ldx, dtmp, Kin, M, Kin, st);
+    }
   };
   auto attn_bwd = [&](const float* q, const float* k, const float* v, const float* O,
                       const float* dO_, const float* lse, const AttnTile* qt, int64_t nq,
@@ -370,7 +398,7 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     int a = cfg.task_sizes[t];
     float* drep = d1;
     // logits = rep out_w + out_b
-    dgemm_nt(dlog[t], a, Pw(S.task(t, OUT_W)), a, drep, dm, R, dm, a, false, st);
+    dgemm(dlog[t], a, Pw(S.task(t, OUT_W)), a, drep, dm, R, dm, a, false);
     wgrad(hrep[t], dm, dm, nullptr, 0, 0, dlog[t], a, R, a, Gw(S.task(t, OUT_W)), Gw(S.task(t, OUT_B)), st);
     if (t == T - 1)
       value_backward(value, meanrep, rewards, F, dm, value_coef, C, Pw(S.value_w()), dvalue,
@@ -378,21 +406,21 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
                      m.d_row_off, row_fwd, R, st);
     if (have_dprev) add_into(drep, dm, dprev, dm, R, dm, st);
     // rep = f1 W2 + b2 ; f1 = relu(o W1 + b1)
-    dgemm_nt(drep, dm, Pw(S.task(t, FC_W2)), dm, dF1, di, R, di, dm, false, st);
+    dgemm(drep, dm, Pw(S.task(t, FC_W2)), dm, dF1, di, R, di, dm, false);
     wgrad(hf1[t], di, di, nullptr, 0, 0, drep, dm, R, dm, Gw(S.task(t, FC_W2)), Gw(S.task(t, FC_B2)), st);
     act_backward(dF1, di, hf1[t], di, R, di, 1, st);
     float* dO = d2;
-    dgemm_nt(dF1, di, Pw(S.task(t, FC_W1)), di, dO, dm, R, dm, di, false, st);
+    dgemm(dF1, di, Pw(S.task(t, FC_W1)), di, dO, dm, R, dm, di, false);
     wgrad(ho[t], dm, dm, nullptr, 0, 0, dF1, di, R, di, Gw(S.task(t, FC_W1)), Gw(S.task(t, FC_B1)), st);
     // o = att Wo + bo
-    dgemm_nt(dO, dm, Pw(S.ta(O_W)), dm, dAt, W, R, W, dm, false, st);
+    dgemm(dO, dm, Pw(S.ta(O_W)), dm, dAt, W, R, W, dm, false);
     wgrad(hat[t], W, W, nullptr, 0, 0, dO, dm, R, dm, Gw(S.ta(O_W)), Gw(S.ta(O_B)), st);
     attn_bwd(hqv[t], hkv[t], hvv[t], hat[t], dAt, hls[t], d_hq, (int64_t)hq.size(), d_hk,
              (int64_t)hk.size(), Dbuf, dQ, dK, dV, nullptr, nullptr);
     float* dHH = d3;
-    dgemm_nt(dQ, W, Pw(S.ta(Q_W)), W, dHH, dm, R, dm, W, false, st);
-    dgemm_nt(dK, W, Pw(S.ta(K_W)), W, dHH, dm, R, dm, W, true, st);
-    dgemm_nt(dV, W, Pw(S.ta(V_W)), W, dHH, dm, R, dm, W, true, st);
+    dgemm(dQ, W, Pw(S.ta(Q_W)), W, dHH, dm, R, dm, W, false);
+    dgemm(dK, W, Pw(S.ta(K_W)), W, dHH, dm, R, dm, W, true);
+    dgemm(dV, W, Pw(S.ta(V_W)), W, dHH, dm, R, dm, W, true);
     wgrad(hh[t], dm, dm, nullptr, 0, 0, dQ, W, R, W, Gw(S.ta(Q_W)), Gw(S.ta(Q_B)), st);
     wgrad(hh[t], dm, dm, nullptr, 0, 0, dK, W, R, W, Gw(S.ta(K_W)), Gw(S.ta(K_B)), st);
     wgrad(hh[t], dm, dm, nullptr, 0, 0, dV, W, R, W, Gw(S.ta(V_W)), Gw(S.ta(V_B)), st);
@@ -403,13 +431,13 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     if (zero_in[t]) {
       wgrad(hid, dm, dm, nullptr, 0, 0, dC, dm, R, dm, Gw(S.task(t, CAT_W)) + (int64_t)dm * dm,
             Gw(S.task(t, CAT_B)), st);
-      dgemm_nt(dC, dm, Pw(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, dhid, dm, R, dm, dm, true, st);
+      dgemm(dC, dm, Pw(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, dhid, dm, R, dm, dm, true);
       have_dprev = false;
     } else {
       wgrad(hrep[t - 1], dm, dm, hid, dm, dm, dC, dm, R, dm, Gw(S.task(t, CAT_W)), Gw(S.task(t, CAT_B)),
             st);
-      dgemm_nt(dC, dm, Pw(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, dhid, dm, R, dm, dm, true, st);
-      dgemm_nt(dC, dm, Pw(S.task(t, CAT_W)), dm, dprev, dm, R, dm, dm, false, st);
+      dgemm(dC, dm, Pw(S.task(t, CAT_W)) + (int64_t)dm * dm, dm, dhid, dm, R, dm, dm, true);
+      dgemm(dC, dm, Pw(S.task(t, CAT_W)), dm, dprev, dm, R, dm, dm, false);
       have_dprev = true;
     }
   }
@@ -421,26 +449,26 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     ln_backward(tu2[l], dm, Pw(S.blk(l, LN2_G)), dx, dm, du2, dm, false, R, dm, Gw(S.blk(l, LN2_G)),
                 Gw(S.blk(l, LN2_B)), st);
     // u2 = h1 + f1 W2 + b2
-    dgemm_nt(du2, dm, Pw(S.blk(l, FF_W2)), dm, dF1, di, R, di, dm, false, st);
+    dgemm(du2, dm, Pw(S.blk(l, FF_W2)), dm, dF1, di, R, di, dm, false);
     wgrad(tf1[l], di, di, nullptr, 0, 0, du2, dm, R, dm, Gw(S.blk(l, FF_W2)), Gw(S.blk(l, FF_B2)), st);
     act_backward(dF1, di, tf1[l], di, R, di, 1, st);
     float* dh1 = d2;
     cudaMemcpyAsync(dh1, du2, (size_t)R * dm * 4, cudaMemcpyDeviceToDevice, st);
-    dgemm_nt(dF1, di, Pw(S.blk(l, FF_W1)), di, dh1, dm, R, dm, di, true, st);
+    dgemm(dF1, di, Pw(S.blk(l, FF_W1)), di, dh1, dm, R, dm, di, true);
     wgrad(th1[l], dm, dm, nullptr, 0, 0, dF1, di, R, di, Gw(S.blk(l, FF_W1)), Gw(S.blk(l, FF_B1)), st);
     float* du1 = d3;
     ln_backward(tu1[l], dm, Pw(S.blk(l, LN1_G)), dh1, dm, du1, dm, false, R, dm, Gw(S.blk(l, LN1_G)),
                 Gw(S.blk(l, LN1_B)), st);
     // u1 = xm + att Wo + bo
-    dgemm_nt(du1, dm, Pw(S.blk(l, O_W)), dm, dAt, W, R, W, dm, false, st);
+    dgemm(du1, dm, Pw(S.blk(l, O_W)), dm, dAt, W, R, W, dm, false);
     wgrad(tat[l], W, W, nullptr, 0, 0, du1, dm, R, dm, Gw(S.blk(l, O_W)), Gw(S.blk(l, O_B)), st);
     attn_bwd(tqv[l], tkv[l], tvv[l], tat[l], dAt, tls[l], d_tq, (int64_t)tq.size(), d_tk,
              (int64_t)tk.size(), Dbuf, dQ, dK, dV, dK2, dV2);
     // dxm = du1 + (dq Wq^T + dk_self Wk^T + dv_self Wv^T); weights see self + cache parts
     float* dxm = du1;
-    dgemm_nt(dQ, W, Pw(S.blk(l, Q_W)), W, dxm, dm, R, dm, W, true, st);
-    dgemm_nt(dK, W, Pw(S.blk(l, K_W)), W, dxm, dm, R, dm, W, true, st);
-    dgemm_nt(dV, W, Pw(S.blk(l, V_W)), W, dxm, dm, R, dm, W, true, st);
+    dgemm(dQ, W, Pw(S.blk(l, Q_W)), W, dxm, dm, R, dm, W, true);
+    dgemm(dK, W, Pw(S.blk(l, K_W)), W, dxm, dm, R, dm, W, true);
+    dgemm(dV, W, Pw(S.blk(l, V_W)), W, dxm, dm, R, dm, W, true);
     add_into(dK, W, dK2, W, R, W, st);
     add_into(dV, W, dV2, W, R, W, st);
     wgrad(txm[l], dm, dm, nullptr, 0, 0, dQ, W, R, W, Gw(S.blk(l, Q_W)), Gw(S.blk(l, Q_B)), st);
@@ -456,7 +484,7 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   float* dhB = A.take<float>(R * gs);
   float* dP = A.take<float>(R * gs);
   float* dt = A.take<float>(R * gs);
-  dgemm_nt(dx, dm, Pw(S.pbase()), dm, dne, gs, R, gs, dm, false, st);
+  dgemm(dx, dm, Pw(S.pbase()), dm, dne, gs, R, gs, dm, false);
   wgrad(node_embed, gs, gs, nullptr, 0, 0, dx, dm, R, dm, Gw(S.pbase()), Gw(S.pbase() + 1), st);
   // modulation: mod = 2 sigma(block(ge in_w + in_b))
   BlockG bg{Gw(S.blk(mb, V_W)),  Gw(S.blk(mb, V_B)),  Gw(S.blk(mb, O_W)),  Gw(S.blk(mb, O_B)),
@@ -474,14 +502,14 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     // h_{l+1} = relu([h_l | pool] fc_w + fc_b)
     act_backward(dcur, gs, eh[l + 1], gs, R, gs, 1, st);
     wgrad(eh[l], gs, gs, ep[l], gs, gs, dcur, gs, R, gs, Gw(S.e_layer(l, 2)), Gw(S.e_layer(l, 3)), st);
-    dgemm_nt(dcur, gs, Pw(S.e_layer(l, 2)) + (int64_t)gs * gs, gs, dP, gs, R, gs, gs, false, st);
-    dgemm_nt(dcur, gs, Pw(S.e_layer(l, 2)), gs, other, gs, R, gs, gs, false, st);
+    dgemm(dcur, gs, Pw(S.e_layer(l, 2)) + (int64_t)gs * gs, gs, dP, gs, R, gs, gs, false);
+    dgemm(dcur, gs, Pw(S.e_layer(l, 2)), gs, other, gs, R, gs, gs, false);
     // pool = segmax(t) ; t = sigmoid(h agg_w + agg_b)
     CUDA_CHECK(cudaMemsetAsync(dt, 0, (size_t)R * gs * 4, st));
     segmax_backward(dP, gs, ea[l], R, gs, dt, gs, st);
     act_backward(dt, gs, et[l], gs, R, gs, 2, st);
     wgrad(eh[l], gs, gs, nullptr, 0, 0, dt, gs, R, gs, Gw(S.e_layer(l, 0)), Gw(S.e_layer(l, 1)), st);
-    dgemm_nt(dt, gs, Pw(S.e_layer(l, 0)), gs, other, gs, R, gs, gs, true, st);
+    dgemm(dt, gs, Pw(S.e_layer(l, 0)), gs, other, gs, R, gs, gs, true);
     std::swap(dcur, other);
   }
   // h0 = feats in_w + in_b

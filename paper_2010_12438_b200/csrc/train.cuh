@@ -18,6 +18,7 @@ struct BlockG {
 
 void dgemm_nt(const float* dY, int64_t ldd, const float* W, int64_t ldw, float* dX, int64_t ldx,
               int64_t M, int Kin, int Nout, bool accumulate, cudaStream_t st);
+void transpose(const float* W, int64_t ldw, int rows, int cols, float* out, cudaStream_t st);
 void wgrad(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
            const float* dY, int64_t ldd, int64_t M, int N, float* dW, float* db, cudaStream_t st);
 void ln_backward(const float* u, int64_t ldu, const float* g, const float* dout, int64_t ldd,

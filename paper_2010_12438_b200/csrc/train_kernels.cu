@@ -74,6 +74,29 @@ void dgemm_nt(const float* dY, int64_t ldd, const float* W, int64_t ldw, float* 
   LAUNCH_CHECK();
 }
 
+// out[c][r] = W[r * ldw + c] for a rows x cols weight (the tcgen05 dX GEMM's B = W^T)
+__global__ void transpose_kernel(const float* __restrict__ W, int64_t ldw, int rows, int cols,
+                                 float* __restrict__ out) {
+  __shared__ float t[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    t[i][threadIdx.x] = (r < rows && c < cols) ? W[(int64_t)r * ldw + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) out[(int64_t)c * rows + r] = t[threadIdx.x][i];
+  }
+}
+
+void transpose(const float* W, int64_t ldw, int rows, int cols, float* out, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  transpose_kernel<<<dim3((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32)), dim3(32, 8), 0,
+                     st>>>(W, ldw, rows, cols, out);
+  LAUNCH_CHECK();
+}
+
 // dW[K1+K2, N] += [A1 | A2]^T @ dY ; db[N] += sum_r dY.  Grid: (K tiles, N tiles, row chunks).
 __global__ void __launch_bounds__(256) wgrad_kernel(const float* __restrict__ A1, int64_t lda1,
                                                     int K1, const float* __restrict__ A2,
