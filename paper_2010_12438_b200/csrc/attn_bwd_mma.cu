@@ -15,7 +15,10 @@
 // a 2-term split, three MMAs per product, so the gradients stay fp32-class; GO_TRAIN_ATTN
 // =mma16 keeps one fp16 term): Q pre-scaled by log2(e)/sqrt(d), dO by a power of two
 // that brings max|dO| into [0.5, 1) (gradients are far below fp16's normal range
-// otherwise; undone exactly on output).  P and dS are split the same way in registers.
+// otherwise; undone exactly on output).  P and dS are split the same way in registers,
+// scaled by powers of two (2^15 for P <= 1, 2^(14 - ceil log2 bound) for dS) so small
+// values keep fp16-normal hi and lo terms instead of the subnormals' fixed 2^-24 step,
+// which summed over 80k keys is otherwise the dominant error.
 // Anything outside the fp16 range (or a non-finite dS) sets *flag and the caller re-runs
 // the fp32 SIMT kernels gated on it.
 #include <cmath>
@@ -31,6 +34,7 @@ namespace ab {
 constexpr int TS = 64;      // rows per tile / chunk
 constexpr int TT = TS + 8;  // transposed smem stride (halves)
 constexpr float RANGE = 60000.f;
+constexpr float PSCALE = 32768.f;  // P (<= 1) enters the MMAs as 2^15 P (fp16-normal)
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   uint32_t r;
@@ -97,6 +101,7 @@ __global__ void pack_kernel(const float* __restrict__ q, const float* __restrict
   const float gs = grad_scale(gbits);
   const int64_t src = r * ld + (int64_t)h * d_head;
   bool big = false;
+  float nrm[4] = {0.f, 0.f, 0.f, 0.f};
   const float* srcs[4] = {q, k, v, dO};
   const float mul[4] = {qscale, 1.f, 1.f, gs};
   __half* dsts[4] = {Qh, Kh, Vh, Oh};
@@ -107,6 +112,7 @@ __global__ void pack_kernel(const float* __restrict__ q, const float* __restrict
     for (int d = 0; d < 16; ++d) {
       float x = d < d_head ? srcs[t][src + d] * mul[t] : 0.f;
       big |= !(fabsf(x) <= RANGE);
+      nrm[t] = fmaf(x, x, nrm[t]);
       row[d] = __float2half_rn(x);
       if (SPLIT) row[16 + d] = __float2half_rn(x - __half2float(row[d]));
     }
@@ -114,7 +120,17 @@ __global__ void pack_kernel(const float* __restrict__ q, const float* __restrict
 #pragma unroll
     for (int j = 0; j < RW / 8; ++j) o[j] = reinterpret_cast<const uint4*>(row)[j];
   }
+  // max row norms of V and of the scaled dO: |dO_q.(v_k - o_q)| <= 2 |dO_q| max|v| bounds dS
+  atomicMax(const_cast<unsigned*>(gbits) + 1, __float_as_uint(sqrtf(nrm[2])));
+  atomicMax(const_cast<unsigned*>(gbits) + 2, __float_as_uint(sqrtf(nrm[3])));
   if (big) atomicOr(flag, 1);
+}
+
+// power-of-two scale bringing the dS bound to 2^14 (fp16-normal hi/lo terms for small dS)
+__device__ __forceinline__ float ds_scale(const unsigned* gbits) {
+  const float b = 2.f * __uint_as_float(gbits[1]) * __uint_as_float(gbits[2]);
+  if (!(b > 0.f) || !(b <= 3.0e38f)) return 1.f;
+  return exp2f(fminf(14.f - ceilf(log2f(b)), 60.f));
 }
 
 template <bool SPLIT>
@@ -217,6 +233,7 @@ __global__ void __launch_bounds__(128) dq_kernel(
   const float l1 = r1 < tl.q1 ? lse[r1 * n_head + h] : 0.f;
   const float D0 = r0 < tl.q1 ? Dv[r0 * n_head + h] * gs : 0.f;
   const float D1 = r1 < tl.q1 ? Dv[r1 * n_head + h] * gs : 0.f;
+  const float dsc = SPLIT ? ds_scale(gbits) : 1.f;
   float acc[2][4] = {};
   bool bad = false;
   for (int64_t kc = tl.k0; kc < tl.k1; kc += TS) {
@@ -240,7 +257,7 @@ __global__ void __launch_bounds__(128) dq_kernel(
       for (int e = 0; e < 4; ++e) {
         const bool ok = key + (e & 1) < nk;
         const float p = ok ? ex2(s[e] - (e < 2 ? l0 : l1)) : 0.f;
-        ds[e] = p * (gg[e] - (e < 2 ? D0 : D1));
+        ds[e] = p * (gg[e] - (e < 2 ? D0 : D1)) * dsc;
         bad |= !(fabsf(ds[e]) <= RANGE);
       }
       // n-tile n is half (n & 1) of k-step n >> 1: A regs {0,1} or {2,3}
@@ -248,18 +265,25 @@ __global__ void __launch_bounds__(128) dq_kernel(
       split2<SPLIT>(ds[0], ds[1], pa[n >> 1].h[j], pa[n >> 1].l[j]);
       split2<SPLIT>(ds[2], ds[3], pa[n >> 1].h[j + 1], pa[n >> 1].l[j + 1]);
     }
+    // per-chunk MMA sums, added to acc with IEEE FADDs (two-level accumulation: the
+    // MMA's fp32 accumulate drops the low bits of small addends with a consistent sign)
+    float cacc[2][4] = {};
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
 #pragma unroll
       for (int n = 0; n < 2; ++n) {
         const __half* bp = &Kt[(8 * n + g) * TT + 16 * kk + 2 * tq];
         const __half* bl = bp + 16 * TT;
-        mma3<SPLIT>(acc[n], pa[kk], ld32(bp), ld32(bp + 8), SPLIT ? ld32(bl) : 0u,
+        mma3<SPLIT>(cacc[n], pa[kk], ld32(bp), ld32(bp + 8), SPLIT ? ld32(bl) : 0u,
                     SPLIT ? ld32(bl + 8) : 0u);
       }
     }
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[n][e] += cacc[n][e];
   }
-  const float c = scale / gs;
+  const float c = scale / (gs * dsc);
   const int64_t col0 = (int64_t)h * d_head;
 #pragma unroll
   for (int n = 0; n < 2; ++n) {
@@ -304,6 +328,8 @@ __global__ void __launch_bounds__(128) dkv_kernel(
   load_afrag<SPLIT>(V, r0, r1, tl.k1, tq, va);
   bool bad = false;
   const int64_t col0 = (int64_t)h * d_head;
+  const float dsc = SPLIT ? ds_scale(gbits) : 1.f;
+  const float psc = SPLIT ? PSCALE : 1.f;
   for (int part = 0; part < 2; ++part) {
     const int64_t qa0 = part ? tl.qb0 : tl.qa0, qe = part ? tl.qb1 : tl.qa1;
     float* dko = part ? dk_b : dk_a;
@@ -335,7 +361,8 @@ __global__ void __launch_bounds__(128) dkv_kernel(
         for (int e = 0; e < 4; ++e) {
           const bool ok = qi + (e & 1) < nq;
           p[e] = ok ? ex2(s[e] - ((e & 1) ? lq.y : lq.x)) : 0.f;
-          ds[e] = p[e] * (gg[e] - ((e & 1) ? dq2.y : dq2.x));
+          ds[e] = p[e] * (gg[e] - ((e & 1) ? dq2.y : dq2.x)) * dsc;
+          p[e] *= psc;
           bad |= !(fabsf(ds[e]) <= RANGE);
         }
         const int j = (n & 1) * 2;
@@ -344,20 +371,28 @@ __global__ void __launch_bounds__(128) dkv_kernel(
         split2<SPLIT>(ds[0], ds[1], pd[n >> 1].h[j], pd[n >> 1].l[j]);
         split2<SPLIT>(ds[2], ds[3], pd[n >> 1].h[j + 1], pd[n >> 1].l[j + 1]);
       }
+      float cdv[2][4] = {}, cdk[2][4] = {};  // per-chunk sums (two-level accumulation)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
           const __half* ob = &Ot[(8 * n + g) * TT + 16 * kk + 2 * tq];
           const __half* qb = &Qt[(8 * n + g) * TT + 16 * kk + 2 * tq];
-          mma3<SPLIT>(dv[n], pp[kk], ld32(ob), ld32(ob + 8), SPLIT ? ld32(ob + 16 * TT) : 0u,
+          mma3<SPLIT>(cdv[n], pp[kk], ld32(ob), ld32(ob + 8), SPLIT ? ld32(ob + 16 * TT) : 0u,
                       SPLIT ? ld32(ob + 16 * TT + 8) : 0u);
-          mma3<SPLIT>(dk[n], pd[kk], ld32(qb), ld32(qb + 8), SPLIT ? ld32(qb + 16 * TT) : 0u,
+          mma3<SPLIT>(cdk[n], pd[kk], ld32(qb), ld32(qb + 8), SPLIT ? ld32(qb + 16 * TT) : 0u,
                       SPLIT ? ld32(qb + 16 * TT + 8) : 0u);
         }
       }
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          dv[n][e] += cdv[n][e];
+          dk[n][e] += cdk[n][e];
+        }
     }
-    const float cv = 1.f / gs, ck = kscale / gs;
+    const float cv = 1.f / (gs * psc), ck = kscale / (gs * dsc);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int d = 8 * n + 2 * tq;
@@ -417,7 +452,7 @@ static void launch_bwd(const float* q, const float* k, const float* v, const flo
   unsigned* gbits = reinterpret_cast<unsigned*>(Oh + rows);
   const double sc = 1.0 / std::sqrt((double)d_head);
   const float scale = (float)sc, qscale = (float)(1.4426950408889634 * sc);
-  CUDA_CHECK(cudaMemsetAsync(gbits, 0, sizeof(unsigned), st));
+  CUDA_CHECK(cudaMemsetAsync(gbits, 0, 3 * sizeof(unsigned), st));
   const int64_t W = (int64_t)n_head * d_head;
   ab::absmax_kernel<<<(unsigned)std::min<int64_t>(cdiv(M * W, 256), 148 * 8), 256, 0, st>>>(
       dO, ld, M, (int)W, gbits);

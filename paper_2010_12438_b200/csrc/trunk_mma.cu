@@ -30,6 +30,7 @@ constexpr int KC = 64;      // keys per chunk
 constexpr int KS = 24;      // Ks row stride (halves): 48 B, conflict-free fragment loads
 constexpr int VS = KC + 8;  // Vt row stride (halves): 144 B
 constexpr float RANGE = 60000.f;
+constexpr float PSCALE = 32768.f;  // SPLIT: P (<= 1) is packed as 2^15 P
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   uint32_t r;
@@ -116,6 +117,8 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
           kv = k[(kc + key) * ld + col0 + d];
           vv = v[(kc + key) * ld + col0 + d];
           big |= !(fabsf(kv) <= RANGE) || !(fabsf(vv) <= RANGE);
+        } else if (SPLIT && key < nk && d == d_head) {
+          vv = 1.f;  // ones column: the MMA accumulates the row sum next to O
         }
         kr[i] = __float2half_rn(kv);
         const __half vh = __float2half_rn(vv);
@@ -175,10 +178,16 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
     uint32_t pa[8][2], pl[8][2];  // P as fp16 pairs: [n-tile][row g | row g+8]
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
-      const float p0 = ex2(s[n][0] - m0), p1 = ex2(s[n][1] - m0);
-      const float p2 = ex2(s[n][2] - m1), p3 = ex2(s[n][3] - m1);
+      float p0 = ex2(s[n][0] - m0), p1 = ex2(s[n][1] - m0);
+      float p2 = ex2(s[n][2] - m1), p3 = ex2(s[n][3] - m1);
       l0 += p0 + p1;
       l1 += p2 + p3;
+      if (SPLIT) {  // 2^15 P: small P stay fp16-normal (hi) and the lo term keeps its bits
+        p0 *= PSCALE;
+        p1 *= PSCALE;
+        p2 *= PSCALE;
+        p3 *= PSCALE;
+      }
       pa[n][0] = pack2(p0, p1);
       pa[n][1] = pack2(p2, p3);
       if (SPLIT) {
@@ -188,7 +197,11 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
         pl[n][1] = pack2(p2 - b.x, p3 - b.y);
       }
     }
-    // O += P V: k-steps of 16 keys (n-tiles 2kk, 2kk+1), n-tiles of 8 dims
+    // O += P V: k-steps of 16 keys (n-tiles 2kk, 2kk+1), n-tiles of 8 dims.  SPLIT: the
+    // chunk's PV goes to a fresh accumulator added to O with IEEE FADDs (the MMA's own
+    // fp32 accumulation drops the low bits of small addends with a consistent sign)
+    float oc[2][4] = {};
+    float(*od)[4] = SPLIT ? oc : o;
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
@@ -199,19 +212,35 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
         const uint32_t b0 = *reinterpret_cast<const uint32_t*>(vp);
         const uint32_t b1 = *reinterpret_cast<const uint32_t*>(vp + 8);
         if (SPLIT) {
-          mma16816(o[n], al, b0, b1);
-          mma16816(o[n], a, *reinterpret_cast<const uint32_t*>(vp + 16 * VS),
+          mma16816(od[n], al, b0, b1);
+          mma16816(od[n], a, *reinterpret_cast<const uint32_t*>(vp + 16 * VS),
                    *reinterpret_cast<const uint32_t*>(vp + 16 * VS + 8));
         }
-        mma16816(o[n], a, b0, b1);
+        mma16816(od[n], a, b0, b1);
       }
+    }
+    if (SPLIT) {
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[n][e] += oc[n][e];
     }
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  if (SPLIT && d_head < 16) {
+    // row sums from the ones column (dim d_head), accumulated exactly like O (per-chunk
+    // MMA sums added with FADDs) so numerator and denominator share their rounding
+    const int holder = (lane & ~3) | ((d_head >> 1) & 3);
+    const int n = d_head >> 3, e = d_head & 1;
+    const float s0 = __shfl_sync(0xffffffffu, o[n][e], holder);
+    const float s1 = __shfl_sync(0xffffffffu, o[n][2 + e], holder);
+    l0 = s0 / PSCALE;
+    l1 = s1 / PSCALE;
+  }
+  const float i0 = (SPLIT ? 1.f / PSCALE : 1.f) / l0, i1 = (SPLIT ? 1.f / PSCALE : 1.f) / l1;
   const int64_t r0 = tl.q0 + warp * 16 + g, r1 = r0 + 8;
   if (lse && tq == 0) {  // log2-sum-exp of the scaled scores (the training tape's P recompute)
     if (r0 < tl.q1) lse[r0 * n_head + head] = m0 + log2f(l0);
