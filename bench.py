@@ -36,7 +36,15 @@ WORKLOADS = {
     "cfg4": ("attention-stack", 8000, 1, 64, 0, 8, 4096),
     "cfg2": ("multi-branch-cnn", 1857, 1, 64, 0, 4, 256),
     "cfg1": ("attention-stack", 10, 1, 64, 0, 2, 800),
+    # WaveNet-shaped super-positioned batch of mixed-size dilated stacks
+    # (graph index drawn per rollout, training.py:124), the first graph named here
+    "cfg3": ("dilated-stack", 30, 250, 64, 0, 8, 256),
+    # the cfg4 graph with joint placement + scheduling + fusion tasks
+    # (per-rollout fusion pass on the host, DES per distinct grouping)
+    "cfg5": ("attention-stack", 8000, 1, 64, 0, 8, 256),
 }
+CFG3_EXTRA = [("dilated-stack", 10, 250, 64, 1), ("dilated-stack", 5, 100, 64, 2),
+              ("dilated-stack", 2, 50, 64, 3)]
 
 
 def parse():
@@ -63,12 +71,18 @@ def build_workload(name):
     from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
     fam, L, S, w, seed, d, k = WORKLOADS[name]
     g = gen_workload(WorkloadSpec(fam, L, S, w, seed=seed), node_cap=10**6)
+    graphs = [g]
+    if name == "cfg3":
+        graphs += [gen_workload(WorkloadSpec(*sp[:4], seed=sp[4]), node_cap=10**6)
+                   for sp in CFG3_EXTRA]
     top = uniform_topology(d)
     sizes = {"placement": d}
+    if name == "cfg5":
+        sizes = {"placement": d, "schedule_priority": 8, "fusion_priority": 8}
     ecfg, pcfg = EmbedConfig(), PolicyConfig()
     store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
-    return dict(graph=g, top=top, sizes=sizes, ecfg=ecfg, pcfg=pcfg, store=store, k=k, d=d,
-                spec=(fam, L, S, w, seed))
+    return dict(graph=g, graphs=graphs, top=top, sizes=sizes, ecfg=ecfg, pcfg=pcfg,
+                store=store, k=k, d=d, spec=(fam, L, S, w, seed))
 
 
 # -------------------------------------------------------------------------------------
@@ -268,11 +282,16 @@ def run_reference(args):
 
 def workload_config(args, w):
     fam, L, S, wd, seed = w["spec"]
-    return {"workload": f"{args.workload}: {fam} L={L} ({w['graph'].num_nodes} nodes, "
-                        f"{w['graph'].num_edges} edges), {w['d']}-device placement, "
+    gdesc = f"{fam} L={L} ({w['graph'].num_nodes} nodes, {w['graph'].num_edges} edges)"
+    if len(w["graphs"]) > 1:
+        gdesc = ("super-positioned batch of " + ", ".join(
+            f"{x.num_nodes}" for x in w["graphs"]) + "-node dilated stacks (graph drawn "
+            "per rollout)")
+    tdesc = "+".join(w["sizes"]) if len(w["sizes"]) > 1 else f"{w['d']}-device placement"
+    return {"workload": f"{args.workload}: {gdesc}, {tdesc}, "
                         f"{args.placements or w['k']} placements/step sharded over ranks, "
                         "mode R (own neighbour sample + 2 forwards per placement)",
-            "nodes": w["graph"].num_nodes, "devices": w["d"],
+            "nodes": w["graph"].num_nodes, "devices": w["d"], "tasks": list(w["sizes"]),
             "placements_per_step": args.placements or w["k"], "iterations": 2,
             "weights": "init_all_params(seed=0) + zero-init tensors refilled U(+-1/sqrt(fan_in))",
             "l2": "inputs larger than L2 (per-step activations >> 126 MB); no explicit flush"}
@@ -302,15 +321,16 @@ def main():
     w = build_workload(args.workload)
     K = args.placements or w["k"]
     g, top, sizes = w["graph"], w["top"], w["sizes"]
-    base = [default_assignments(g, top)]
-    bl = [baseline_step_time(g, top)]
+    graphs = w["graphs"]
+    base = [default_assignments(x, top) for x in graphs]
+    bl = [baseline_step_time(x, top) for x in graphs]
     hyper = PPOHyper(rollouts=K)
     ctx = context()
 
     def step(s, store):
         """One step: this rank's shard of the K placements (global rollout ids
         [rank*K/world, (rank+1)*K/world) of the step's outer stream)."""
-        batch = collect_rollouts(store, [g], top, sizes, bl, K, 1000 + s, hyper, w["ecfg"],
+        batch = collect_rollouts(store, graphs, top, sizes, bl, K, 1000 + s, hyper, w["ecfg"],
                                  w["pcfg"], FusionConfig(), base_assignments=base,
                                  keep_logits=False, shard=(rank, world))
         return batch
@@ -428,7 +448,8 @@ def main():
         "kernel_ms": {k: v[1] / max(1, args.steps) for k, v in stats.items()},
         "gpu_launches": int(launches), "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and len(w["graphs"]) == 1 \
+            and len(sizes) == 1:
         per, desc = cpu_placement_sample(w)
         line["cpu_baseline"] = {"value": 1.0 / per, "unit": UNIT, "cores": cpu_threads(),
                                 "kind": "port", "sample": desc}
