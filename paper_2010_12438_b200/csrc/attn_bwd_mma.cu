@@ -107,10 +107,13 @@ __global__ void pack_kernel(const float* __restrict__ q, const float* __restrict
   __half* dsts[4] = {Qh, Kh, Vh, Oh};
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
+    if (srcs[t] == nullptr) continue;  // forward: no dO
     __align__(16) __half row[RW];
 #pragma unroll
     for (int d = 0; d < 16; ++d) {
-      float x = d < d_head ? srcs[t][src + d] * mul[t] : 0.f;
+      // V carries a ones column at d_head: the forward's MMAs accumulate the softmax row
+      // sum next to O (dO's column d_head is 0, so the backward products ignore it)
+      float x = d < d_head ? srcs[t][src + d] * mul[t] : (t == 2 && d == d_head ? 1.f : 0.f);
       big |= !(fabsf(x) <= RANGE);
       nrm[t] = fmaf(x, x, nrm[t]);
       row[d] = __float2half_rn(x);
@@ -178,6 +181,17 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
 template <bool SPLIT>
 constexpr int row_stride() { return SPLIT ? 40 : 24; }  // halves; conflict-free fragments
 
+// B fragments (k = 16 rows of a row-major [row][dim] smem block, n = 8 dims) for both
+// n-tiles of a k-step straight from the row-major block: ldmatrix.x4.trans, lanes 0-7 /
+// 8-15 / 16-23 / 24-31 address rows 0-7 / 8-15 (dims 0-7), rows 0-7 / 8-15 (dims 8-15);
+// b[0], b[1] = n-tile 0's (b0, b1), b[2], b[3] = n-tile 1's.  Replaces a transposed copy.
+__device__ __forceinline__ void ldsm_bT(const __half* blk, int stride, int lane, uint32_t* b) {
+  const __half* p = blk + ((lane & 7) + ((lane >> 3) & 1) * 8) * stride + (lane >> 4) * 8;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+
 // stage rows [c, c+n) of two packed arrays: row-major and transposed ([RW][TT])
 template <bool SPLIT>
 __device__ __forceinline__ void stage(const __half* __restrict__ X, const __half* __restrict__ Y,
@@ -216,7 +230,6 @@ __global__ void __launch_bounds__(128) dq_kernel(
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
   __shared__ __align__(16) __half Ks[TS * RS2];
   __shared__ __align__(16) __half Vs[TS * RS2];
-  __shared__ __align__(16) __half Kt[RW * TT];
   const AttnTile tl = tiles[blockIdx.x];
   const int h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(128) dq_kernel(
   for (int64_t kc = tl.k0; kc < tl.k1; kc += TS) {
     const int nk = (tl.k1 - kc) < TS ? (int)(tl.k1 - kc) : TS;
     __syncthreads();
-    stage<SPLIT>(K, V, kc, nk, Ks, Vs, Kt, nullptr, tid);
+    stage<SPLIT>(K, V, kc, nk, Ks, Vs, nullptr, nullptr, tid);
     __syncthreads();
     Frag<SPLIT> pa[4];  // dS as A fragments, k-steps of 16 keys
 #pragma unroll
@@ -270,13 +283,12 @@ __global__ void __launch_bounds__(128) dq_kernel(
     float cacc[2][4] = {};
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
+      uint32_t bh[4], bl[4] = {0u, 0u, 0u, 0u};
+      ldsm_bT(Ks + 16 * kk * RS2, RS2, lane, bh);
+      if (SPLIT) ldsm_bT(Ks + 16 * kk * RS2 + 16, RS2, lane, bl);
 #pragma unroll
-      for (int n = 0; n < 2; ++n) {
-        const __half* bp = &Kt[(8 * n + g) * TT + 16 * kk + 2 * tq];
-        const __half* bl = bp + 16 * TT;
-        mma3<SPLIT>(cacc[n], pa[kk], ld32(bp), ld32(bp + 8), SPLIT ? ld32(bl) : 0u,
-                    SPLIT ? ld32(bl + 8) : 0u);
-      }
+      for (int n = 0; n < 2; ++n)
+        mma3<SPLIT>(cacc[n], pa[kk], bh[2 * n], bh[2 * n + 1], bl[2 * n], bl[2 * n + 1]);
     }
 #pragma unroll
     for (int n = 0; n < 2; ++n)
@@ -311,8 +323,6 @@ __global__ void __launch_bounds__(128) dkv_kernel(
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
   __shared__ __align__(16) __half Qs[TS * RS2];
   __shared__ __align__(16) __half Os[TS * RS2];
-  __shared__ __align__(16) __half Qt[RW * TT];
-  __shared__ __align__(16) __half Ot[RW * TT];
   __shared__ __align__(8) float Ls[TS], Dd[TS];
   const KvTile tl = tiles[blockIdx.x];
   const int h = blockIdx.y;
@@ -339,7 +349,7 @@ __global__ void __launch_bounds__(128) dkv_kernel(
     for (int64_t qc = qa0; qc < qe; qc += TS) {
       const int nq = (qe - qc) < TS ? (int)(qe - qc) : TS;
       __syncthreads();
-      stage<SPLIT>(Q, O, qc, nq, Qs, Os, Qt, Ot, tid);
+      stage<SPLIT>(Q, O, qc, nq, Qs, Os, nullptr, nullptr, tid);
       if (tid < TS) Ls[tid] = tid < nq ? lse[(qc + tid) * n_head + h] : 0.f;
       else Dd[tid - TS] = tid - TS < nq ? Dv[(qc + tid - TS) * n_head + h] * gs : 0.f;
       __syncthreads();
@@ -374,14 +384,17 @@ __global__ void __launch_bounds__(128) dkv_kernel(
       float cdv[2][4] = {}, cdk[2][4] = {};  // per-chunk sums (two-level accumulation)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
+        uint32_t oh[4], ol[4] = {0u, 0u, 0u, 0u}, qh[4], ql[4] = {0u, 0u, 0u, 0u};
+        ldsm_bT(Os + 16 * kk * RS2, RS2, lane, oh);
+        ldsm_bT(Qs + 16 * kk * RS2, RS2, lane, qh);
+        if (SPLIT) {
+          ldsm_bT(Os + 16 * kk * RS2 + 16, RS2, lane, ol);
+          ldsm_bT(Qs + 16 * kk * RS2 + 16, RS2, lane, ql);
+        }
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
-          const __half* ob = &Ot[(8 * n + g) * TT + 16 * kk + 2 * tq];
-          const __half* qb = &Qt[(8 * n + g) * TT + 16 * kk + 2 * tq];
-          mma3<SPLIT>(cdv[n], pp[kk], ld32(ob), ld32(ob + 8), SPLIT ? ld32(ob + 16 * TT) : 0u,
-                      SPLIT ? ld32(ob + 16 * TT + 8) : 0u);
-          mma3<SPLIT>(cdk[n], pd[kk], ld32(qb), ld32(qb + 8), SPLIT ? ld32(qb + 16 * TT) : 0u,
-                      SPLIT ? ld32(qb + 16 * TT + 8) : 0u);
+          mma3<SPLIT>(cdv[n], pp[kk], oh[2 * n], oh[2 * n + 1], ol[2 * n], ol[2 * n + 1]);
+          mma3<SPLIT>(cdk[n], pd[kk], qh[2 * n], qh[2 * n + 1], ql[2 * n], ql[2 * n + 1]);
         }
       }
 #pragma unroll
@@ -419,6 +432,117 @@ __global__ void __launch_bounds__(128) dkv_kernel(
     }
   }
   if (bad) atomicOr(flag, 1);
+}
+
+// forward with log2-sum-exp on the packed operands (the PPO tape's forward of both the
+// banded trunk and the N x N head attention): S = Q K^T (3 split MMAs per 8-key n-tile),
+// exact online max, P = exp2(S - m) scaled by 2^15 and split, O += P V from the row-major
+// V block through ldmatrix.trans, per-chunk sums added with FADDs, row sums from V's ones
+// column.  d_head <= 15 (the ones column needs a free slot).
+template <bool SPLIT>
+__global__ void __launch_bounds__(128) fwd_kernel(
+    const __half* __restrict__ Qh, const __half* __restrict__ Kh, const __half* __restrict__ Vh,
+    int64_t M, int n_head, int d_head, const AttnTile* __restrict__ tiles,
+    float* __restrict__ out, int64_t ldo, float* __restrict__ lse) {
+  constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
+  __shared__ __align__(16) __half Ks[TS * RS2];
+  __shared__ __align__(16) __half Vs[TS * RS2];
+  const AttnTile tl = tiles[blockIdx.x];
+  const int h = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const __half* Q = Qh + (int64_t)h * M * RW;
+  const __half* K = Kh + (int64_t)h * M * RW;
+  const __half* V = Vh + (int64_t)h * M * RW;
+  const int64_t r0 = tl.q0 + warp * 16 + g, r1 = r0 + 8;
+  Frag<SPLIT> qa;
+  load_afrag<SPLIT>(Q, r0, r1, tl.q1, tq, qa);
+  float o[2][4] = {};
+  float m0 = -INFINITY, m1 = -INFINITY;
+  const float psc = SPLIT ? PSCALE : 1.f;
+  for (int64_t kc = tl.k0; kc < tl.k1; kc += TS) {
+    const int nk = (tl.k1 - kc) < TS ? (int)(tl.k1 - kc) : TS;
+    __syncthreads();
+    stage<SPLIT>(K, V, kc, nk, Ks, Vs, nullptr, nullptr, tid);
+    __syncthreads();
+    float s[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+      const __half* kp = &Ks[(8 * n + g) * RS2 + 2 * tq];
+      mma3<SPLIT>(s[n], qa, ld32(kp), ld32(kp + 8), SPLIT ? ld32(kp + 16) : 0u,
+                  SPLIT ? ld32(kp + 24) : 0u);
+    }
+    float c0 = -INFINITY, c1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int key = 8 * n + 2 * tq;
+      if (key >= nk) s[n][0] = s[n][2] = -INFINITY;
+      if (key + 1 >= nk) s[n][1] = s[n][3] = -INFINITY;
+      c0 = fmaxf(c0, fmaxf(s[n][0], s[n][1]));
+      c1 = fmaxf(c1, fmaxf(s[n][2], s[n][3]));
+    }
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 1));
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 2));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 1));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 2));
+    const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+    const float f0 = ex2(m0 - n0), f1 = ex2(m1 - n1);  // 0 on the first chunk
+    m0 = n0;
+    m1 = n1;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      o[n][0] *= f0;
+      o[n][1] *= f0;
+      o[n][2] *= f1;
+      o[n][3] *= f1;
+    }
+    Frag<SPLIT> pa[4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float p0 = ex2(s[n][0] - m0) * psc, p1 = ex2(s[n][1] - m0) * psc;
+      const float p2 = ex2(s[n][2] - m1) * psc, p3 = ex2(s[n][3] - m1) * psc;
+      const int j = (n & 1) * 2;
+      split2<SPLIT>(p0, p1, pa[n >> 1].h[j], pa[n >> 1].l[j]);
+      split2<SPLIT>(p2, p3, pa[n >> 1].h[j + 1], pa[n >> 1].l[j + 1]);
+    }
+    float oc[2][4] = {};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t bh[4], bl[4] = {0u, 0u, 0u, 0u};
+      ldsm_bT(Vs + 16 * kk * RS2, RS2, lane, bh);
+      if (SPLIT) ldsm_bT(Vs + 16 * kk * RS2 + 16, RS2, lane, bl);
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+        mma3<SPLIT>(oc[n], pa[kk], bh[2 * n], bh[2 * n + 1], bl[2 * n], bl[2 * n + 1]);
+    }
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[n][e] += oc[n][e];
+  }
+  // row sums (x 2^15) from the ones column d_head, held by lane quad member (d_head/2)&3
+  const int holder = (lane & ~3) | ((d_head >> 1) & 3);
+  const int cn = d_head >> 3, ce = d_head & 1;
+  const float l0 = __shfl_sync(0xffffffffu, o[cn][ce], holder);
+  const float l1 = __shfl_sync(0xffffffffu, o[cn][2 + ce], holder);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  if (lse && tq == 0) {
+    if (r0 < tl.q1) lse[r0 * n_head + h] = m0 + log2f(l0 / psc);
+    if (r1 < tl.q1) lse[r1 * n_head + h] = m1 + log2f(l1 / psc);
+  }
+  const int64_t col0 = (int64_t)h * d_head;
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+    const int d = 8 * n + 2 * tq;
+    if (r0 < tl.q1) {
+      if (d < d_head) out[r0 * ldo + col0 + d] = o[n][0] * i0;
+      if (d + 1 < d_head) out[r0 * ldo + col0 + d + 1] = o[n][1] * i0;
+    }
+    if (r1 < tl.q1) {
+      if (d < d_head) out[r1 * ldo + col0 + d] = o[n][2] * i1;
+      if (d + 1 < d_head) out[r1 * ldo + col0 + d + 1] = o[n][3] * i1;
+    }
+  }
 }
 
 }  // namespace ab
@@ -472,6 +596,28 @@ static void launch_bwd(const float* q, const float* k, const float* v, const flo
         (float)(1.0 / 1.4426950408889634), gbits, flag);
     LAUNCH_CHECK();
   }
+}
+
+void attention_forward_mma(const float* q, const float* k, const float* v, int64_t ld,
+                                int n_head, int d_head, const AttnTile* tiles, int64_t nt,
+                                int64_t M, float* out, int64_t ldo, float* lse, void* scratch,
+                                int32_t* flag, cudaStream_t st) {
+  if (nt <= 0 || M <= 0) return;
+  GO_CHECK(d_head >= 1 && d_head <= 15, "attention_forward_mma needs d_head <= 15");
+  const size_t rows = (size_t)M * n_head * 32;
+  __half* Qh = reinterpret_cast<__half*>(scratch);
+  __half* Kh = Qh + rows;
+  __half* Vh = Kh + rows;
+  unsigned* gbits = reinterpret_cast<unsigned*>(Vh + 2 * rows);
+  const float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
+  CUDA_CHECK(cudaMemsetAsync(gbits, 0, 3 * sizeof(unsigned), st));
+  CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
+  ab::pack_kernel<true><<<(unsigned)cdiv(M * n_head, 128), 128, 0, st>>>(
+      q, k, v, nullptr, ld, M, n_head, d_head, qscale, gbits, Qh, Kh, Vh, nullptr, flag);
+  LAUNCH_CHECK();
+  ab::fwd_kernel<true><<<dim3((unsigned)nt, (unsigned)n_head), 128, 0, st>>>(
+      Qh, Kh, Vh, M, n_head, d_head, tiles, out, ldo, lse);
+  LAUNCH_CHECK();
 }
 
 void attention_backward_mma(const float* q, const float* k, const float* v, const float* O,

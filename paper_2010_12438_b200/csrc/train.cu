@@ -154,7 +154,10 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   auto attn_fwd = [&](const float* q, const float* k, const float* v, const AttnTile* tiles,
                       int64_t nt, float* out, float* lse) {
     if (attn_mma_fwd) {
-      trunk_attention_mma(q, k, v, W, H, dh, tiles, nt, out, W, aflag, st, lse, attn_split);
+      if (attn_split && dh <= 15)
+        attention_forward_mma(q, k, v, W, H, dh, tiles, nt, R, out, W, lse, abw, aflag, st);
+      else
+        trunk_attention_mma(q, k, v, W, H, dh, tiles, nt, out, W, aflag, st, lse, attn_split);
       attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse, aflag);
     } else {
       attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse);

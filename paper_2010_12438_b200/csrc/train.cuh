@@ -48,6 +48,12 @@ void attention_backward_simt(const float* q, const float* k, const float* v, con
                              const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
                              const float* Dbuf, float* dq, float* dk_a, float* dv_a, float* dk_b,
                              float* dv_b, const int32_t* gate, cudaStream_t st);
+// tensor-core (split-fp16 mma.sync) forward with lse over packed operands (rows 0..M-1,
+// d_head <= 15); scratch as for attention_backward_mma; *flag set on fp16 range overflow
+void attention_forward_mma(const float* q, const float* k, const float* v, int64_t ld,
+                           int n_head, int d_head, const AttnTile* tiles, int64_t nt, int64_t M,
+                           float* out, int64_t ldo, float* lse, void* scratch, int32_t* flag,
+                           cudaStream_t st);
 // tensor-core (mma.sync fp16) backward, d_head <= 16, with the gated SIMT re-run
 // (csrc/attn_bwd_mma.cu); scratch >= attention_backward_mma_scratch(M, n_head) bytes
 size_t attention_backward_mma_scratch(int64_t M, int n_head);
