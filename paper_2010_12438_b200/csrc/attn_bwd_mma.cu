@@ -181,6 +181,32 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
 template <bool SPLIT>
 constexpr int row_stride() { return SPLIT ? 40 : 24; }  // halves; conflict-free fragments
 
+// asynchronous staging (cp.async, zero-filled rows past n) into one of two buffers, so
+// the next chunk's rows load while this chunk computes
+template <bool SPLIT>
+__device__ __forceinline__ void stage_cp(const __half* __restrict__ X,
+                                         const __half* __restrict__ Y, int64_t c, int n,
+                                         __half* Xs, __half* Ys, int tid) {
+  constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
+  const int row = tid >> 1, half = (tid & 1) * 8;
+  const bool ok = row < n;
+  const int64_t r = ok ? c + row : 0;
+#pragma unroll
+  for (int p = 0; p < (SPLIT ? 2 : 1); ++p) {
+    const uint32_t xs = static_cast<uint32_t>(__cvta_generic_to_shared(Xs + row * RS2 + p * 16 + half));
+    const uint32_t ys = static_cast<uint32_t>(__cvta_generic_to_shared(Ys + row * RS2 + p * 16 + half));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xs),
+                 "l"(X + r * RW + p * 16 + half), "r"(ok ? 16 : 0));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ys),
+                 "l"(Y + r * RW + p * 16 + half), "r"(ok ? 16 : 0));
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // B fragments (k = 16 rows of a row-major [row][dim] smem block, n = 8 dims) for both
 // n-tiles of a k-step straight from the row-major block: ldmatrix.x4.trans, lanes 0-7 /
 // 8-15 / 16-23 / 24-31 address rows 0-7 / 8-15 (dims 0-7), rows 0-7 / 8-15 (dims 8-15);
@@ -228,8 +254,8 @@ __global__ void __launch_bounds__(128) dq_kernel(
     float* __restrict__ dq, int64_t ld, float scale, const unsigned* __restrict__ gbits,
     int32_t* __restrict__ flag) {
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
-  __shared__ __align__(16) __half Ks[TS * RS2];
-  __shared__ __align__(16) __half Vs[TS * RS2];
+  __shared__ __align__(16) __half Ks2[2][TS * RS2];
+  __shared__ __align__(16) __half Vs2[2][TS * RS2];
   const AttnTile tl = tiles[blockIdx.x];
   const int h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
@@ -249,11 +275,23 @@ __global__ void __launch_bounds__(128) dq_kernel(
   const float dsc = SPLIT ? ds_scale(gbits) : 1.f;
   float acc[2][4] = {};
   bool bad = false;
-  for (int64_t kc = tl.k0; kc < tl.k1; kc += TS) {
+  if (tl.k0 < tl.k1)
+    stage_cp<SPLIT>(K, V, tl.k0, (tl.k1 - tl.k0) < TS ? (int)(tl.k1 - tl.k0) : TS, Ks2[0],
+                    Vs2[0], tid);
+  int buf = 0;
+  for (int64_t kc = tl.k0; kc < tl.k1; kc += TS, buf ^= 1) {
     const int nk = (tl.k1 - kc) < TS ? (int)(tl.k1 - kc) : TS;
+    const int64_t kn = kc + TS;
+    if (kn < tl.k1) {
+      stage_cp<SPLIT>(K, V, kn, (tl.k1 - kn) < TS ? (int)(tl.k1 - kn) : TS, Ks2[buf ^ 1],
+                      Vs2[buf ^ 1], tid);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
     __syncthreads();
-    stage<SPLIT>(K, V, kc, nk, Ks, Vs, nullptr, nullptr, tid);
-    __syncthreads();
+    const __half* Ks = Ks2[buf];
+    const __half* Vs = Vs2[buf];
     Frag<SPLIT> pa[4];  // dS as A fragments, k-steps of 16 keys
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
@@ -294,6 +332,7 @@ __global__ void __launch_bounds__(128) dq_kernel(
     for (int n = 0; n < 2; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[n][e] += cacc[n][e];
+    __syncthreads();  // buffer `buf` is refilled by the staging two chunks ahead
   }
   const float c = scale / (gs * dsc);
   const int64_t col0 = (int64_t)h * d_head;
@@ -321,9 +360,9 @@ __global__ void __launch_bounds__(128) dkv_kernel(
     float* __restrict__ dv_b, int64_t ld, float kscale, const unsigned* __restrict__ gbits,
     int32_t* __restrict__ flag) {
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
-  __shared__ __align__(16) __half Qs[TS * RS2];
-  __shared__ __align__(16) __half Os[TS * RS2];
-  __shared__ __align__(8) float Ls[TS], Dd[TS];
+  __shared__ __align__(16) __half Qs2[2][TS * RS2];
+  __shared__ __align__(16) __half Os2[2][TS * RS2];
+  __shared__ __align__(8) float Ls2[2][TS], Dd2[2][TS];
   const KvTile tl = tiles[blockIdx.x];
   const int h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
@@ -346,13 +385,27 @@ __global__ void __launch_bounds__(128) dkv_kernel(
     float* dvo = part ? dv_b : dv_a;
     if (!dko) continue;
     float dk[2][4] = {}, dv[2][4] = {};
-    for (int64_t qc = qa0; qc < qe; qc += TS) {
+    __syncthreads();  // the previous part's last chunk is done with both buffers
+    if (qa0 < qe)
+      stage_cp<SPLIT>(Q, O, qa0, (qe - qa0) < TS ? (int)(qe - qa0) : TS, Qs2[0], Os2[0], tid);
+    int buf = 0;
+    for (int64_t qc = qa0; qc < qe; qc += TS, buf ^= 1) {
       const int nq = (qe - qc) < TS ? (int)(qe - qc) : TS;
-      __syncthreads();
-      stage<SPLIT>(Q, O, qc, nq, Qs, Os, nullptr, nullptr, tid);
+      const int64_t qn = qc + TS;
+      if (qn < qe) {
+        stage_cp<SPLIT>(Q, O, qn, (qe - qn) < TS ? (int)(qe - qn) : TS, Qs2[buf ^ 1],
+                        Os2[buf ^ 1], tid);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      float* Ls = Ls2[buf];
+      float* Dd = Dd2[buf];
       if (tid < TS) Ls[tid] = tid < nq ? lse[(qc + tid) * n_head + h] : 0.f;
       else Dd[tid - TS] = tid - TS < nq ? Dv[(qc + tid - TS) * n_head + h] * gs : 0.f;
       __syncthreads();
+      const __half* Qs = Qs2[buf];
+      const __half* Os = Os2[buf];
       Frag<SPLIT> pp[4], pd[4];
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
@@ -404,6 +457,7 @@ __global__ void __launch_bounds__(128) dkv_kernel(
           dv[n][e] += cdv[n][e];
           dk[n][e] += cdk[n][e];
         }
+      __syncthreads();  // buffer `buf` is refilled by the staging two chunks ahead
     }
     const float cv = 1.f / (gs * psc), ck = kscale / (gs * dsc);
 #pragma unroll
@@ -445,8 +499,8 @@ __global__ void __launch_bounds__(128) fwd_kernel(
     int64_t M, int n_head, int d_head, const AttnTile* __restrict__ tiles,
     float* __restrict__ out, int64_t ldo, float* __restrict__ lse) {
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
-  __shared__ __align__(16) __half Ks[TS * RS2];
-  __shared__ __align__(16) __half Vs[TS * RS2];
+  __shared__ __align__(16) __half Ks2[2][TS * RS2];
+  __shared__ __align__(16) __half Vs2[2][TS * RS2];
   const AttnTile tl = tiles[blockIdx.x];
   const int h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
@@ -459,11 +513,23 @@ __global__ void __launch_bounds__(128) fwd_kernel(
   float o[2][4] = {};
   float m0 = -INFINITY, m1 = -INFINITY;
   const float psc = SPLIT ? PSCALE : 1.f;
-  for (int64_t kc = tl.k0; kc < tl.k1; kc += TS) {
+  if (tl.k0 < tl.k1)
+    stage_cp<SPLIT>(K, V, tl.k0, (tl.k1 - tl.k0) < TS ? (int)(tl.k1 - tl.k0) : TS, Ks2[0],
+                    Vs2[0], tid);
+  int buf = 0;
+  for (int64_t kc = tl.k0; kc < tl.k1; kc += TS, buf ^= 1) {
     const int nk = (tl.k1 - kc) < TS ? (int)(tl.k1 - kc) : TS;
+    const int64_t kn = kc + TS;
+    if (kn < tl.k1) {
+      stage_cp<SPLIT>(K, V, kn, (tl.k1 - kn) < TS ? (int)(tl.k1 - kn) : TS, Ks2[buf ^ 1],
+                      Vs2[buf ^ 1], tid);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
     __syncthreads();
-    stage<SPLIT>(K, V, kc, nk, Ks, Vs, nullptr, nullptr, tid);
-    __syncthreads();
+    const __half* Ks = Ks2[buf];
+    const __half* Vs = Vs2[buf];
     float s[8][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
@@ -519,6 +585,7 @@ __global__ void __launch_bounds__(128) fwd_kernel(
     for (int n = 0; n < 2; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) o[n][e] += oc[n][e];
+    __syncthreads();  // buffer `buf` is refilled by the staging two chunks ahead
   }
   // row sums (x 2^15) from the ones column d_head, held by lane quad member (d_head/2)&3
   const int holder = (lane & ~3) | ((d_head >> 1) & 3);
