@@ -292,41 +292,44 @@ __global__ void __launch_bounds__(128) dq_kernel(
     __syncthreads();
     const __half* Ks = Ks2[buf];
     const __half* Vs = Vs2[buf];
-    Frag<SPLIT> pa[4];  // dS as A fragments, k-steps of 16 keys
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      float s[4] = {0.f, 0.f, 0.f, 0.f}, gg[4] = {0.f, 0.f, 0.f, 0.f};
-      const __half* kp = &Ks[(8 * n + g) * RS2 + 2 * tq];
-      const __half* vp = &Vs[(8 * n + g) * RS2 + 2 * tq];
-      mma3<SPLIT>(s, qa, ld32(kp), ld32(kp + 8), SPLIT ? ld32(kp + 16) : 0u,
-                  SPLIT ? ld32(kp + 24) : 0u);
-      mma3<SPLIT>(gg, oa, ld32(vp), ld32(vp + 8), SPLIT ? ld32(vp + 16) : 0u,
-                  SPLIT ? ld32(vp + 24) : 0u);
-      const int key = 8 * n + 2 * tq;
-      float ds[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool ok = key + (e & 1) < nk;
-        const float p = ok ? ex2(s[e] - (e < 2 ? l0 : l1)) : 0.f;
-        ds[e] = p * (gg[e] - (e < 2 ? D0 : D1)) * dsc;
-        bad |= !(fabsf(ds[e]) <= RANGE);
-      }
-      // n-tile n is half (n & 1) of k-step n >> 1: A regs {0,1} or {2,3}
-      const int j = (n & 1) * 2;
-      split2<SPLIT>(ds[0], ds[1], pa[n >> 1].h[j], pa[n >> 1].l[j]);
-      split2<SPLIT>(ds[2], ds[3], pa[n >> 1].h[j + 1], pa[n >> 1].l[j + 1]);
-    }
-    // per-chunk MMA sums, added to acc with IEEE FADDs (two-level accumulation: the
-    // MMA's fp32 accumulate drops the low bits of small addends with a consistent sign)
+    // streamed per 16-key k-step: S and G for its two n-tiles, dS as the A fragment, then
+    // the dq MMAs; per-chunk MMA sums are added to acc with IEEE FADDs (two-level
+    // accumulation: the MMA's fp32 accumulate drops the low bits of small addends with a
+    // consistent sign)
     float cacc[2][4] = {};
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
+      Frag<SPLIT> pa;
+#pragma unroll
+      for (int hn = 0; hn < 2; ++hn) {
+        const int n = 2 * kk + hn;
+        float s[4] = {0.f, 0.f, 0.f, 0.f}, gg[4] = {0.f, 0.f, 0.f, 0.f};
+        const __half* kp = &Ks[(8 * n + g) * RS2 + 2 * tq];
+        const __half* vp = &Vs[(8 * n + g) * RS2 + 2 * tq];
+        mma3<SPLIT>(s, qa, ld32(kp), ld32(kp + 8), SPLIT ? ld32(kp + 16) : 0u,
+                    SPLIT ? ld32(kp + 24) : 0u);
+        mma3<SPLIT>(gg, oa, ld32(vp), ld32(vp + 8), SPLIT ? ld32(vp + 16) : 0u,
+                    SPLIT ? ld32(vp + 24) : 0u);
+        const int key = 8 * n + 2 * tq;
+        float ds[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool ok = key + (e & 1) < nk;
+          const float p = ok ? ex2(s[e] - (e < 2 ? l0 : l1)) : 0.f;
+          ds[e] = p * (gg[e] - (e < 2 ? D0 : D1)) * dsc;
+          bad |= !(fabsf(ds[e]) <= RANGE);
+        }
+        // n-tile 2kk + hn is half hn of the k-step: A regs {0,1} or {2,3}
+        const int j = hn * 2;
+        split2<SPLIT>(ds[0], ds[1], pa.h[j], pa.l[j]);
+        split2<SPLIT>(ds[2], ds[3], pa.h[j + 1], pa.l[j + 1]);
+      }
       uint32_t bh[4], bl[4] = {0u, 0u, 0u, 0u};
       ldsm_bT(Ks + 16 * kk * RS2, RS2, lane, bh);
       if (SPLIT) ldsm_bT(Ks + 16 * kk * RS2 + 16, RS2, lane, bl);
 #pragma unroll
       for (int n = 0; n < 2; ++n)
-        mma3<SPLIT>(cacc[n], pa[kk], bh[2 * n], bh[2 * n + 1], bl[2 * n], bl[2 * n + 1]);
+        mma3<SPLIT>(cacc[n], pa, bh[2 * n], bh[2 * n + 1], bl[2 * n], bl[2 * n + 1]);
     }
 #pragma unroll
     for (int n = 0; n < 2; ++n)
