@@ -189,7 +189,12 @@ int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards,
  * layout, ACCUMULATED (caller zeroes per minibatch); the loss is the sum over the F
  * samples divided by loss_denominator (<= 0: F), so ranks holding parts of one
  * minibatch produce gradients that all-reduce(sum) to the minibatch mean.  stats_out: host float64 [14*F]: [F][3][4] (sum surr, sum entropy, sum
- * ratio, clipped count) per task slot, then [F] (value - reward)^2, then [F] value. */
+ * ratio, clipped count) per task slot, then [F] (value - reward)^2, then [F] value.
+ * Kernels: attention forward (with log-sum-exp) and dq / dk,dv backward on split-fp16
+ * mma.sync tensor cores (fp32-class, csrc/attn_bwd_mma.cu), forward and dX GEMMs on the
+ * tcgen05 split-precision GEMM; fp32 SIMT re-runs gated on the fp16 range flags.
+ * Environment: GO_TRAIN_ATTN=simt|mma16, GO_TRAIN_FWD=simt, GO_TRAIN_GEMM=simt select
+ * the fp32 SIMT / single-fp16 variants (testing and A/B timing only). */
 int go_ppo_grad(go_ctx_t ctx, const go_config_t* cfg, const float* params,
                 const int64_t* param_offsets, const go_batch_t* batch, const int32_t* actions,
                 const double* old_logp, const double* fparams, double clip_eps,
