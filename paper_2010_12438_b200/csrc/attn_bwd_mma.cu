@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(128) dq_kernel(
 }
 
 template <bool SPLIT>
-__global__ void __launch_bounds__(128) dkv_kernel(
+__global__ void __launch_bounds__(128, 4) dkv_kernel(
     const __half* __restrict__ Qh, const __half* __restrict__ Kh, const __half* __restrict__ Vh,
     const __half* __restrict__ Oh, int64_t M, const float* __restrict__ lse,
     const float* __restrict__ Dv, int n_head, int d_head, const KvTile* __restrict__ tiles,
