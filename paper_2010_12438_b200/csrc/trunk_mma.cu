@@ -28,7 +28,6 @@ namespace tm {
 constexpr int QT = 64;      // queries per CTA
 constexpr int KC = 64;      // keys per chunk
 constexpr int KS = 24;      // Ks row stride (halves): 48 B, conflict-free fragment loads
-constexpr int VS = KC + 8;  // Vt row stride (halves): 144 B
 constexpr float RANGE = 60000.f;
 constexpr float PSCALE = 32768.f;  // SPLIT: P (<= 1) is packed as 2^15 P
 
@@ -43,6 +42,15 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// B fragments of both 8-dim n-tiles of a 16-row k-step from a row-major [row][dim] smem
+// block: ldmatrix.x4.trans (lanes 0-7 / 8-15 / 16-23 / 24-31 address rows 0-7 / 8-15 of
+// dims 0-7, then of dims 8-15); b[0..1] n-tile 0, b[2..3] n-tile 1
+__device__ __forceinline__ void ldsm_bT(const __half* blk, int stride, int lane, uint32_t* b) {
+  const __half* p = blk + ((lane & 7) + ((lane >> 3) & 1) * 8) * stride + (lane >> 4) * 8;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
 }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -59,9 +67,8 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
     int64_t ld, int d_head, const AttnTile* __restrict__ tiles, float* __restrict__ out,
     int64_t ldo, float qscale, int32_t* __restrict__ flag, float* __restrict__ lse, int n_head) {
   constexpr int KS2 = SPLIT ? 40 : KS;  // halves per key row (hi 0..15, lo 16..31)
-  constexpr int NP = SPLIT ? 2 : 1;
   __shared__ __align__(16) __half Ks[KC * KS2];
-  __shared__ __align__(16) __half Vt[16 * NP * VS];
+  __shared__ __align__(16) __half Vs[KC * KS2];  // row-major [key][d] (lo at +16)
   const AttnTile tl = tiles[blockIdx.x];
   const int head = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -106,9 +113,10 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
     const int nk = rem < KC ? (int)rem : KC;
     __syncthreads();
     {
-      // stage: thread = (key, 8-dim half); K row-major [key][d], V transposed [d][key]
+      // stage: thread = (key, 8-dim half); K and V row-major [key][d] (V's B fragments
+      // come out transposed through ldmatrix.trans)
       const int key = tid >> 1, d0 = (tid & 1) * 8;
-      __align__(16) __half kr[8], kl[8];
+      __align__(16) __half kr[8], kl[8], vr[8], vl[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int d = d0 + i;
@@ -121,16 +129,18 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
           vv = 1.f;  // ones column: the MMA accumulates the row sum next to O
         }
         kr[i] = __float2half_rn(kv);
-        const __half vh = __float2half_rn(vv);
-        Vt[d * VS + key] = vh;
+        vr[i] = __float2half_rn(vv);
         if (SPLIT) {
           kl[i] = __float2half_rn(kv - __half2float(kr[i]));
-          Vt[(16 + d) * VS + key] = __float2half_rn(vv - __half2float(vh));
+          vl[i] = __float2half_rn(vv - __half2float(vr[i]));
         }
       }
       *reinterpret_cast<uint4*>(&Ks[key * KS2 + d0]) = *reinterpret_cast<const uint4*>(kr);
-      if (SPLIT)
+      *reinterpret_cast<uint4*>(&Vs[key * KS2 + d0]) = *reinterpret_cast<const uint4*>(vr);
+      if (SPLIT) {
         *reinterpret_cast<uint4*>(&Ks[key * KS2 + 16 + d0]) = *reinterpret_cast<const uint4*>(kl);
+        *reinterpret_cast<uint4*>(&Vs[key * KS2 + 16 + d0]) = *reinterpret_cast<const uint4*>(vl);
+      }
     }
     __syncthreads();
     // S = Q K^T: 8 n-tiles of 8 keys
@@ -206,17 +216,16 @@ __global__ void __launch_bounds__(128) trunk_mma_kernel(
     for (int kk = 0; kk < 4; ++kk) {
       const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
       const uint32_t al[4] = {pl[2 * kk][0], pl[2 * kk][1], pl[2 * kk + 1][0], pl[2 * kk + 1][1]};
+      uint32_t bh[4], bl[4] = {0u, 0u, 0u, 0u};
+      ldsm_bT(Vs + 16 * kk * KS2, KS2, lane, bh);
+      if (SPLIT) ldsm_bT(Vs + 16 * kk * KS2 + 16, KS2, lane, bl);
 #pragma unroll
       for (int n = 0; n < 2; ++n) {
-        const __half* vp = &Vt[(8 * n + g) * VS + 16 * kk + 2 * tq];
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(vp);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(vp + 8);
         if (SPLIT) {
-          mma16816(od[n], al, b0, b1);
-          mma16816(od[n], a, *reinterpret_cast<const uint32_t*>(vp + 16 * VS),
-                   *reinterpret_cast<const uint32_t*>(vp + 16 * VS + 8));
+          mma16816(od[n], al, bh[2 * n], bh[2 * n + 1]);
+          mma16816(od[n], a, bl[2 * n], bl[2 * n + 1]);
         }
-        mma16816(od[n], a, b0, b1);
+        mma16816(od[n], a, bh[2 * n], bh[2 * n + 1]);
       }
     }
     if (SPLIT) {
