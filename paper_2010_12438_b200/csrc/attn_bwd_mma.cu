@@ -10,7 +10,10 @@
 //         G = dO V^T (8 + 8 MMAs per warp), dS in registers, dq += dS K (8 MMAs);
 //   dkv : key-major, CTA = 64 keys x head; per 64-query chunk S^T = K Q^T and
 //         G^T = V dO^T, dv += P^T dO and dk += dS^T Q (the C fragments of S^T / G^T are
-//         reused directly as the A fragments of P^T / dS^T).
+//         reused directly as the A fragments of P^T / dS^T; the B fragments of dO / Q /
+//         K come from the row-major staged chunk through ldmatrix.trans).
+// Chunks are staged with double-buffered cp.async; a forward kernel (fwd_kernel, with
+// the log2-sum-exp) shares the packed operands.
 // Operands are pre-packed once per call into fp16 rows ([H][M][32]: hi and lo halves of
 // a 2-term split, three MMAs per product, so the gradients stay fp32-class; GO_TRAIN_ATTN
 // =mma16 keeps one fp16 term): Q pre-scaled by log2(e)/sqrt(d), dO by a power of two
@@ -32,7 +35,6 @@ namespace go {
 namespace ab {
 
 constexpr int TS = 64;      // rows per tile / chunk
-constexpr int TT = TS + 8;  // transposed smem stride (halves)
 constexpr float RANGE = 60000.f;
 constexpr float PSCALE = 32768.f;  // P (<= 1) enters the MMAs as 2^15 P (fp16-normal)
 
@@ -216,34 +218,6 @@ __device__ __forceinline__ void ldsm_bT(const __half* blk, int stride, int lane,
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
                : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
-}
-
-// stage rows [c, c+n) of two packed arrays: row-major and transposed ([RW][TT])
-template <bool SPLIT>
-__device__ __forceinline__ void stage(const __half* __restrict__ X, const __half* __restrict__ Y,
-                                      int64_t c, int n, __half* Xs, __half* Ys, __half* Xt,
-                                      __half* Yt, int tid) {
-  constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
-  const int row = tid >> 1, half = (tid & 1) * 8;
-#pragma unroll
-  for (int p = 0; p < (SPLIT ? 2 : 1); ++p) {
-    uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
-    if (row < n) {
-      x = *reinterpret_cast<const uint4*>(X + (c + row) * RW + p * 16 + half);
-      y = *reinterpret_cast<const uint4*>(Y + (c + row) * RW + p * 16 + half);
-    }
-    *reinterpret_cast<uint4*>(Xs + row * RS2 + p * 16 + half) = x;
-    *reinterpret_cast<uint4*>(Ys + row * RS2 + p * 16 + half) = y;
-    if (Xt) {
-      const __half* xh = reinterpret_cast<const __half*>(&x);
-      const __half* yh = reinterpret_cast<const __half*>(&y);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        Xt[(p * 16 + half + i) * TT + row] = xh[i];
-        if (Yt) Yt[(p * 16 + half + i) * TT + row] = yh[i];
-      }
-    }
-  }
 }
 
 template <bool SPLIT>
