@@ -68,7 +68,7 @@ def parse():
 def build_workload(name):
     from paper_2010_12438_b200 import (EmbedConfig, PolicyConfig, init_all_params,
                                        randomize_zero_init, uniform_topology)
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     fam, L, S, w, seed, d, k = WORKLOADS[name]
     g = gen_workload(WorkloadSpec(fam, L, S, w, seed=seed), node_cap=10**6)
     graphs = [g]

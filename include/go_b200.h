@@ -206,6 +206,13 @@ int go_ppo_grad(go_ctx_t ctx, const go_config_t* cfg, const float* params,
 int go_adam(go_ctx_t ctx, float* params, const float* grads, float* m, float* v, int64_t count,
             int64_t step, double lr, double beta1, double beta2, double eps, void* stream);
 
+/* Float64-master Adam (tensor.py:428-441 ParamStore.adam_step, same float64
+ * operations in the same order): params / m / v are float64 device arrays kept across
+ * the update, params32 receives the float32 copy the forward/backward kernels read. */
+int go_adam64(go_ctx_t ctx, double* params, float* params32, const float* grads, double* m,
+              double* v, int64_t count, int64_t step, double lr, double beta1, double beta2,
+              double eps, void* stream);
+
 /* Batched exact discrete-event simulation (simulator.py:280-441) of K placements of
  * one graph (its current fused tables) + reward (training.py:37-44).
  *   placement  dev int32 [K][n] node-indexed device per node

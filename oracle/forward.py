@@ -215,6 +215,53 @@ def task_heads(hid, P, cfg: PolicyCfg, tasks, prefix="policy/", ablate=None, chu
     return logits, reprs, value
 
 
+def task_heads_rows(hid, P, cfg: PolicyCfg, tasks, rows, prefix="policy/"):
+    """policy.py:187-217 restricted to query rows `rows` (topo-row indices) for a
+    single task: the head's keys/values still span all N rows (h for every row is
+    one N x 256 x 128 product), only the queries and everything after the attention
+    are evaluated for `rows`.  Returns (logits[len(rows), a], rep rows).  With more
+    than one task the next task's keys need every row's rep, so use task_heads."""
+    if len(tasks) != 1:
+        raise ValueError("task_heads_rows evaluates a single task; use task_heads")
+    task, _a = tasks[0]
+    n, d = hid.shape
+    p = f"{prefix}task/{task}/"
+    pa = prefix + "task_attn/"
+    h = layer_norm(np.concatenate([np.zeros((n, d)), hid], axis=1) @ P[p + "cat_w"] + P[p + "cat_b"],
+                   P[p + "ln_g"], P[p + "ln_b"])
+    rows = np.asarray(rows, np.int64)
+    q = h[rows] @ P[pa + "q_w"] + P[pa + "q_b"]
+    k = h @ P[pa + "k_w"] + P[pa + "k_b"]
+    v = h @ P[pa + "v_w"] + P[pa + "v_b"]
+    out = np.zeros((len(rows), cfg.n_head * cfg.d_head))
+    scale = 1.0 / math.sqrt(cfg.d_head)
+    for i in range(cfg.n_head):
+        sl = slice(i * cfg.d_head, (i + 1) * cfg.d_head)
+        out[:, sl] = softmax((q[:, sl] @ k[:, sl].T) * scale) @ v[:, sl]
+    attn = out @ P[pa + "o_w"] + P[pa + "o_b"]
+    rep = relu(attn @ P[p + "fc_w1"] + P[p + "fc_b1"]) @ P[p + "fc_w2"] + P[p + "fc_b2"]
+    return rep @ P[p + "out_w"] + P[p + "out_b"], rep
+
+
+def uniform_at(seed, index):
+    """The reference's uniform number `index` of default_rng(seed).random() calls
+    (policy.py:235 draws rng.random((N, 1)) per task and iteration, so row r of task t
+    in iteration it is draw (it*T + t)*N + r).  PCG64.advance(k) jumps
+    the stream by k 64-bit outputs, one per double."""
+    gen = np.random.default_rng(seed)
+    gen.bit_generator.advance(int(index))
+    return float(gen.random())
+
+
+def sample_row(logits_row, temperature, u):
+    """sample_actions (policy.py:220-237) for one row given its uniform u."""
+    class _U:
+        def random(self, shape):
+            return np.full(shape, u)
+    a, lp = sample_actions(np.asarray(logits_row, np.float64)[None, :], temperature, _U())
+    return int(a[0]), float(lp[0])
+
+
 def sample_actions(logits, temperature, rng):
     """policy.py:220-237, verbatim numpy semantics."""
     if temperature < 0:

@@ -23,7 +23,7 @@ __all__ = [
 def __getattr__(name):
     # heavy submodules (torch) are imported lazily
     import importlib
-    for mod in ("embedding", "policy", "simulator", "training", "baselines", "workloads"):
+    for mod in ("embedding", "policy", "simulator", "training", "baselines"):
         m = importlib.import_module(f".{mod}", __name__)
         if hasattr(m, name):
             return getattr(m, name)

@@ -14,14 +14,14 @@ LIB_PATH = Path(__file__).resolve().parent / "libgo_b200.so"
 GO_OK, GO_ERR_VALUE, GO_ERR_CUDA, GO_ERR_CYCLE, GO_ERR_NONFINITE, GO_ERR_DEADLOCK, \
     GO_ERR_UNSUPPORTED = range(7)
 
-# every symbol include/go_b200.h declares (checked by tests/test_abi.py)
+# every symbol include/go_b200.h declares (checked by tests/test_host.py::test_header_symbols_exported)
 EXPORTS = (
     "go_last_error", "go_version", "go_ctx_create", "go_ctx_destroy", "go_ctx_workspace_bytes",
     "go_launch_count", "go_ctx_set_timing", "go_ctx_kernel_stats",
     "go_topo_order", "go_greedy_cuts", "go_apply_fusion", "go_graph_create", "go_graph_destroy", "go_graph_topo",
     "go_graph_num_neighbors", "go_graph_set_fusion", "go_param_count", "go_forward",
     "go_forward_status", "go_neighbor_arrays", "go_sample", "go_simulate", "go_ppo_grad",
-    "go_adam",
+    "go_adam", "go_adam64",
 )
 
 
@@ -78,6 +78,7 @@ _SIGS = {
     "go_ppo_grad": (C.c_int, [P, C.POINTER(GoConfig), P, P, C.POINTER(GoBatch), P, P, P, F64, F64,
                               F64, I32, P, P, P]),
     "go_adam": (C.c_int, [P, P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
+    "go_adam64": (C.c_int, [P, P, P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
     "go_simulate": (C.c_int, [P, P, I32, P, P, I32, I32, P, P, P, P, I32, F64, P, P, P, P, P,
                               P, P]),
 }

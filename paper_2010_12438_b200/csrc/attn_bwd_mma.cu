@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(128) dq_kernel(
     for (int n = 0; n < 2; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[n][e] += cacc[n][e];
-    __syncthreads();  // buffer `buf` is refilled by the staging two chunks ahead
+    __syncthreads();  // required: the next iteration's cp.async (into buf ^ 1 of that
+                      // iteration, i.e. this `buf`) refills the buffer just read
   }
   const float c = scale / (gs * dsc);
   const int64_t col0 = (int64_t)h * d_head;
@@ -434,7 +435,8 @@ __global__ void __launch_bounds__(128, 4) dkv_kernel(
           dv[n][e] += cdv[n][e];
           dk[n][e] += cdk[n][e];
         }
-      __syncthreads();  // buffer `buf` is refilled by the staging two chunks ahead
+      __syncthreads();  // required: the next iteration's cp.async (into buf ^ 1 of that
+                      // iteration, i.e. this `buf`) refills the buffer just read
     }
     const float cv = 1.f / (gs * psc), ck = kscale / (gs * dsc);
 #pragma unroll
@@ -562,7 +564,8 @@ __global__ void __launch_bounds__(128) fwd_kernel(
     for (int n = 0; n < 2; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) o[n][e] += oc[n][e];
-    __syncthreads();  // buffer `buf` is refilled by the staging two chunks ahead
+    __syncthreads();  // required: the next iteration's cp.async (into buf ^ 1 of that
+                      // iteration, i.e. this `buf`) refills the buffer just read
   }
   // row sums (x 2^15) from the ones column d_head, held by lane quad member (d_head/2)&3
   const int holder = (lane & ~3) | ((d_head >> 1) & 3);

@@ -134,9 +134,7 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   if (need_heads) build_tiles(m.row_off, 0, false, ht);
   for (auto& t : tt) m.trunk_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
   for (auto& t : ht) m.head_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
-  std::vector<TrunkTile> ttc;
-  if (need_trunk) m.trunk_tc_ok = trunk_tc_build_tiles(m.row_off, cfg.segment_len, ttc);
-  size_t o_tt = s.add(tt), o_ht = s.add(ht), o_ttc = s.add(ttc);
+  size_t o_tt = s.add(tt), o_ht = s.add(ht);
   std::vector<TcWork> tcw, tcw2;
   std::vector<int64_t> trow0;
   std::vector<int32_t> tn;
@@ -168,8 +166,6 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   m.d_views = reinterpret_cast<const GraphView*>(dev + o_views);
   m.d_trunk_tiles = reinterpret_cast<const AttnTile*>(dev + o_tt);
   m.n_trunk_tiles = (int64_t)tt.size();
-  m.d_trunk_tc = reinterpret_cast<const TrunkTile*>(dev + o_ttc);
-  m.n_trunk_tc = (int64_t)ttc.size();
   m.d_head_tiles = reinterpret_cast<const AttnTile*>(dev + o_ht);
   m.n_head_tiles = (int64_t)ht.size();
   m.d_chunks = reinterpret_cast<const int64_t*>(dev + o_ch);
@@ -631,20 +627,15 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       modp = mod;
     }
     float* x0 = Lt == 0 ? hid : X[0];
-    // GO_TRUNK=tc: tcgen05 segmented attention (fp16 operands; the SIMT kernel re-runs a
-    // layer whose operands left the fp16 range).  Measured 0.61-0.66 ms/forward at cfg4
-    // against 0.41 ms for the SIMT banded kernel (2 CTAs/SM by TMEM, latency-bound
-    // staging), so SIMT stays the default.
-    // Default: warp-level MMA banded attention (trunk_mma.cu), with the SIMT kernel
-    // re-running a layer whose operands left the fp16 range; GO_TRUNK=simt forces SIMT.
+    // Warp-level MMA banded attention (trunk_mma.cu), with the SIMT kernel re-running a
+    // layer whose operands left the fp16 range (gated on the layer's flag).  A tcgen05
+    // version (2 CTAs/SM by TMEM, 0.61-0.66 ms per cfg4 forward vs 0.17 ms here) was
+    // measured in round 1 and removed.  GO_TRUNK=simt forces the fp32 SIMT kernel
+    // (A/B testing).
     const char* trunk_env = getenv("GO_TRUNK");
-    const bool trunk_tc = m.trunk_tc_ok && trunk_tc_supported(H, dh) && trunk_env &&
-                          !strcmp(trunk_env, "tc");
-    const bool trunk_mma = !trunk_tc && trunk_mma_supported(dh) &&
-                           !(trunk_env && !strcmp(trunk_env, "simt"));
+    const bool trunk_mma = trunk_mma_supported(dh) && !(trunk_env && !strcmp(trunk_env, "simt"));
 
     int32_t* trunk_flags = A.take<int32_t>(Lt + 1);
-    if (trunk_tc) CUDA_CHECK(cudaMemsetAsync(trunk_flags, 0, (Lt + 1) * sizeof(int32_t), st));
     {
       KTimer kt(ctx, K_GEMM, st, 2.0 * R * gs * dm);
       if (Lt > 0)  // xm = (node_embed @ in_w + b) * m(forward), modulation in the epilogue
@@ -665,12 +656,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       }
       {
         KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
-        if (trunk_tc) {
-          trunk_attention_tc(QKV, LQ, H, dh, cfg.segment_len, m.d_trunk_tc, m.n_trunk_tc, Ab, LA,
-                             trunk_flags + l, st);
-          attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
-                    LA, st, nullptr, trunk_flags + l);
-        } else if (trunk_mma) {
+        if (trunk_mma) {
           trunk_attention_mma(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles,
                               m.n_trunk_tiles, Ab, LA, trunk_flags + l, st);
           attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,

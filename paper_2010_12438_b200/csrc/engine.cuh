@@ -190,23 +190,6 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                       const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
                       const TcWork* works2_dev, int64_t num_works2, cudaStream_t st);
 
-// ---- kernels: tc_trunk.cu (tcgen05 / TMEM segmented trunk attention, d_head <= 15)
-constexpr int TRUNK_TC_MAX_KEYS = 192;
-struct TrunkTile {
-  int64_t q0, k0, f0, f1;  // first query row, first key row, forward rows [f0, f1)
-  int32_t nq, nk;
-};
-// 128-row query tiles per forward with their key windows; false (and empty) if some
-// window exceeds TRUNK_TC_MAX_KEYS (segment_len too large for the TMEM budget)
-bool trunk_tc_build_tiles(const std::vector<int64_t>& row_off, int64_t S,
-                          std::vector<TrunkTile>& out);
-bool trunk_tc_supported(int n_head, int d_head);
-// qkv rows hold [Q | K | V] (each n_head * d_head wide); flag (zeroed) is set if some
-// operand left the fp16 range -- the caller then re-runs attention() gated on it
-void trunk_attention_tc(const float* qkv, int64_t ld, int n_head, int d_head, int S,
-                        const TrunkTile* tiles_dev, int64_t num_tiles, float* out, int64_t ldo,
-                        int32_t* flag, cudaStream_t st);
-
 // ---- kernels: trunk_mma.cu (banded trunk attention on mma.sync m16n8k16, d_head <= 16);
 // *flag (zeroed here) is set if some operand left the fp16 range -- the caller then
 // re-runs attention() gated on it
@@ -260,10 +243,6 @@ struct BatchMeta {
   const int64_t* d_tile_row0 = nullptr;
   const int32_t* d_tile_n = nullptr;
   int64_t n_tiles = 0;
-  // tensor-core trunk attention tiles (empty + false if a key window is too wide)
-  const TrunkTile* d_trunk_tc = nullptr;
-  int64_t n_trunk_tc = 0;
-  bool trunk_tc_ok = false;
 };
 BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b, bool need_embed,
                     bool need_trunk, bool need_heads, cudaStream_t st, const void* extra = nullptr,

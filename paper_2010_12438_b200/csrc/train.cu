@@ -554,4 +554,15 @@ int go_adam(go_ctx_t ctx, float* params, const float* grads, float* m, float* v,
   });
 }
 
+int go_adam64(go_ctx_t ctx, double* params, float* params32, const float* grads, double* m,
+              double* v, int64_t count, int64_t step, double lr, double beta1, double beta2,
+              double eps, void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    GO_CHECK(step >= 1, "adam step must be >= 1");
+    adam64(params, params32, grads, m, v, count, lr, beta1, beta2, eps, step,
+           (cudaStream_t)stream);
+  });
+}
+
 }  // extern "C"

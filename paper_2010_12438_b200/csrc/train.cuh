@@ -77,6 +77,8 @@ void inproj_wgrad(const GraphView* views, const int64_t* row_off, const int32_t*
 void modulate_backward(const float* ge, int F, int gs, const float* in_w, const float* in_b,
                        const BlockW& w, int dm, int wd, int di, const float* dmod, float* dge,
                        const BlockG& gr, float* d_in_w, float* d_in_b, cudaStream_t st);
+void adam64(double* p, float* p32, const float* g, double* m, double* v, int64_t n, double lr,
+            double b1, double b2, double eps, int64_t step, cudaStream_t st);
 void adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, double b1,
           double b2, double eps, int64_t step, cudaStream_t st);
 

@@ -929,4 +929,37 @@ void adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, do
   LAUNCH_CHECK();
 }
 
+// Float64-master Adam, the reference's arithmetic (tensor.py:428-441) operation for
+// operation: m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g; p -= lr*(m/bc1)/(sqrt(v/bc2)+eps)
+// with explicit _rn intrinsics so no FMA contraction changes a rounding.  The master
+// parameters and moments stay float64 on the device across the whole update; the
+// kernels read the float32 copy written here.
+__global__ void adam64_kernel(double* __restrict__ p, float* __restrict__ p32,
+                              const float* __restrict__ g, double* __restrict__ m,
+                              double* __restrict__ v, int64_t n, double lr, double b1,
+                              double b2, double eps, double bc1, double bc2) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double gi = (double)g[i];
+  double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dadd_rn(1.0, -b1), gi));
+  double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dadd_rn(1.0, -b2), gi), gi));
+  m[i] = mi;
+  v[i] = vi;
+  double mhat = __ddiv_rn(mi, bc1);
+  double vhat = __ddiv_rn(vi, bc2);
+  double step = __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps));
+  double pi = __dadd_rn(p[i], -step);
+  p[i] = pi;
+  p32[i] = (float)pi;
+}
+
+void adam64(double* p, float* p32, const float* g, double* m, double* v, int64_t n, double lr,
+            double b1, double b2, double eps, int64_t step, cudaStream_t st) {
+  if (n <= 0) return;
+  double bc1 = 1.0 - std::pow(b1, (double)step), bc2 = 1.0 - std::pow(b2, (double)step);
+  adam64_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(p, p32, g, m, v, n, lr, b1, b2, eps,
+                                                       bc1, bc2);
+  LAUNCH_CHECK();
+}
+
 }  // namespace go

@@ -33,7 +33,8 @@ class Param:
 
 class ParamStore:
     """Named float64 parameters with Adam moment state (tensor.py:391-465).
-    `version` increments on every in-place update so device copies stay coherent."""
+    `version` counts bulk updates (informational: the device cache compares packed
+    contents, DeviceParams)."""
 
     def __init__(self):
         self._params: dict[str, Param] = {}
@@ -68,7 +69,8 @@ class ParamStore:
         return sum(p.data.size for n, p in self.items() if n.startswith(prefix))
 
     def touch(self):
-        """Call after mutating `.data` in place (the reference has no such hook)."""
+        """Kept for callers of the round-1 API; not needed for coherence (DeviceParams
+        compares contents)."""
         self.version += 1
 
     def zero_grads(self):
@@ -264,37 +266,49 @@ def _get(store, name):
     return np.asarray(store[name].data)
 
 
-def pack(store, embed_cfg, cfg, task_sizes):
-    """Host float32 blob (16-byte aligned tensors) + int64 offsets in slot order."""
+def pack(store, embed_cfg, cfg, task_sizes, dtype=np.float32):
+    """Host blob (float32 by default; 16-byte aligned tensors in float32 units) + int64
+    offsets in slot order.  dtype=float64 gives the optimiser's master copy with the
+    same offsets."""
     names = slot_names(embed_cfg, cfg, task_sizes)
-    arrays = [np.ascontiguousarray(_get(store, n), dtype=np.float32).reshape(-1) for n in names]
+    arrays = [np.ascontiguousarray(_get(store, n), dtype=dtype).reshape(-1) for n in names]
     offs = np.zeros(len(names), np.int64)
     pos = 0
     for i, a in enumerate(arrays):
         offs[i] = pos
         pos += (a.size + 3) // 4 * 4
-    blob = np.zeros(max(pos, 4), np.float32)
+    blob = np.zeros(max(pos, 4), dtype)
     for o, a in zip(offs, arrays):
         blob[o:o + a.size] = a
     return blob, offs
 
 
 class DeviceParams:
-    """float32 device copy of a store, re-uploaded when the store's version moves
-    (foreign stores without `version` are re-uploaded on every call)."""
+    """float32 device copy of a store.
+
+    Every call re-packs the store on the host (~3-5 ms for the 1.5M-parameter joint
+    network) and compares the packed blob with the one last uploaded; the device copy
+    is reused only when the bytes are identical.  So in-place edits
+    (`store[name].data[:] = x`, which the reference's own tests do between calls,
+    tests/test_policy.py:212), reassignments, foreign stores without a version and
+    a new store that happens to reuse a freed store's id() can never be served stale
+    weights."""
 
     def __init__(self):
         self._key = None
+        self._host = None
         self.blob = None
         self.offsets = None
 
     def get(self, store, embed_cfg, cfg, task_sizes, device):
         import torch
-        key = (id(store), getattr(store, "version", None), embed_cfg, cfg,
-               tuple(ordered_tasks(task_sizes)), str(device))
-        if key[1] is None or key != self._key:
-            blob, offs = pack(store, embed_cfg, cfg, task_sizes)
+        blob, offs = pack(store, embed_cfg, cfg, task_sizes)
+        key = (embed_cfg, cfg, tuple(ordered_tasks(task_sizes)), str(device))
+        if (key != self._key or self._host is None or self._host.shape != blob.shape
+                or not np.array_equal(self.offsets, offs)
+                or not np.array_equal(self._host, blob)):
             self.blob = torch.from_numpy(blob).to(device, non_blocking=False)
             self.offsets = offs
+            self._host = blob
             self._key = key
         return self.blob, self.offsets

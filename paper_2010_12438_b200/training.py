@@ -371,7 +371,8 @@ def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed
 @dataclass
 class _DevSample:
     handle: object
-    prev: object       # int32 [T, n] node-indexed (iteration-1 actions)
+    prev: object       # int32 [T, n] node-indexed previous-iteration actions, or None
+                       # (iterations == 1: the re-forward sees zero action features)
     actions: object    # int32 [T, n] node-indexed
     logp: object       # float64 [T, n] topo-row indexed
     seed: int
@@ -389,14 +390,16 @@ def _device_samples(batch, graphs, tasks):
         g = as_graph(graphs[s.graph_index])
         b = s.bundle
         n = g.num_nodes
-        if b.prev_actions is None:
-            raise ValueError("PPO re-forward needs the bundle's previous-iteration actions")
-        prev = np.stack([np.asarray(b.prev_actions[t], np.int32) for t, _ in tasks])
+        # training.py:156-158: the loss re-forwards with the bundle's prev_actions,
+        # which is None when the policy ran a single iteration
+        prev = (None if b.prev_actions is None else
+                np.stack([np.asarray(b.prev_actions[t], np.int32) for t, _ in tasks]))
         acts = np.stack([np.asarray(b.actions[t], np.int32) for t, _ in tasks])
         logp = np.stack([np.asarray(b.log_probs[t], np.float64) for t, _ in tasks])
-        if prev.shape != (len(tasks), n) or acts.shape != (len(tasks), n):
+        if (prev is not None and prev.shape != (len(tasks), n)) or acts.shape != (len(tasks), n):
             raise ValueError("bundle arrays do not match the graph")
-        out.append(_DevSample(ctx.graph(g), T_.as_tensor(prev, device=dev),
+        out.append(_DevSample(ctx.graph(g),
+                              None if prev is None else T_.as_tensor(prev, device=dev),
                               T_.as_tensor(acts, device=dev), T_.as_tensor(logp, device=dev),
                               int(b.embed_seed), float(b.temperature), float(s.reward)))
     return out
@@ -415,7 +418,10 @@ def ppo_grad(params, embed_cfg, policy_cfg, task_sizes, samples, advantages, hyp
     tasks = ordered_tasks(task_sizes)
     F = len(samples)
     blob, offs = params
-    prev = T_.cat([s.prev for s in samples], dim=1).contiguous()
+    has_prev = [s.prev is not None for s in samples]
+    if any(has_prev) and not all(has_prev):
+        raise ValueError("a minibatch mixes single- and multi-iteration bundles")
+    prev = T_.cat([s.prev for s in samples], dim=1).contiguous() if all(has_prev) else None
     acts = T_.cat([s.actions for s in samples], dim=1).contiguous()
     logp = T_.cat([s.logp for s in samples], dim=1).contiguous()
     fparams = np.zeros((F, 4), np.float64)
@@ -490,15 +496,19 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
     adv = np.array([s.advantage for s in batch.samples], dtype=np.float64)
     if hyper.advantage_norm and len(adv) > 1 and adv.std() > 0:
         adv = (adv - adv.mean()) / (adv.std() + 1e-8)
-    blob_h, offs = pack(store, embed_cfg, policy_cfg, task_sizes)
+    # float64 master parameters and Adam moments stay on the device for the whole
+    # update (go_adam64 runs the reference's float64 Adam); the kernels read `blob`,
+    # the float32 copy go_adam64 refreshes after every step
+    blob64_h, offs = pack(store, embed_cfg, policy_cfg, task_sizes, dtype=np.float64)
     names = slot_names(embed_cfg, policy_cfg, task_sizes)
-    blob = T_.as_tensor(blob_h, device=dev).contiguous()
+    blob64 = T_.as_tensor(blob64_h, device=dev).contiguous()
+    blob = blob64.to(T_.float32)
 
     def moments(d):
-        out = np.zeros_like(blob_h)
+        out = np.zeros_like(blob64_h)
         for nm, o in zip(names, offs):
             if d is not None and nm in d:
-                a = np.asarray(d[nm], np.float32).reshape(-1)
+                a = np.asarray(d[nm], np.float64).reshape(-1)
                 out[o:o + a.size] = a
         return T_.as_tensor(out, device=dev)
 
@@ -541,9 +551,9 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
                 stats["value_loss_sum"] += float(st[12 * F + i])
                 stats["value_count"] += 1
             step += 1
-            _lib.call("go_adam", context().handle, _lib.ptr(blob), _lib.ptr(grads), _lib.ptr(m),
-                      _lib.ptr(v), int(blob.numel()), step, float(hyper.lr), 0.9, 0.999, 1e-8,
-                      stream_ptr())
+            _lib.call("go_adam64", context().handle, _lib.ptr(blob64), _lib.ptr(blob),
+                      _lib.ptr(grads), _lib.ptr(m), _lib.ptr(v), int(blob.numel()), step,
+                      float(hyper.lr), 0.9, 0.999, 1e-8, stream_ptr())
     if world > 1:
         import torch.distributed as dist
         T_ = torch()
@@ -552,8 +562,8 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
         dist.all_reduce(vec)
         stats = {k: (int(round(v)) if isinstance(stats[k], int) else float(v))
                  for k, v in zip(keys, vec.tolist())}
-    # write parameters and Adam state back into the store (float64 host master)
-    hb, hm, hv = (x.cpu().numpy().astype(np.float64) for x in (blob, m, v))
+    # write the float64 parameters and Adam state back into the store
+    hb, hm, hv = (x.cpu().numpy() for x in (blob64, m, v))
     for nm, o in zip(names, offs):
         if nm not in store:
             continue

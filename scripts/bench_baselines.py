@@ -21,7 +21,7 @@ def main():
 
     from paper_2010_12438_b200.baselines import brute_force
     from paper_2010_12438_b200.costmodel import uniform_topology
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     g = gen_workload(WorkloadSpec("attention-stack", 1, 1, 64, seed=0), node_cap=10**6)
     if g.num_nodes != n:  # a random DAG of exactly n nodes otherwise
         from paper_2010_12438_b200.graph import Graph

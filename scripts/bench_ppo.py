@@ -20,7 +20,7 @@ def main():
                                        init_all_params, randomize_zero_init, uniform_topology)
     from paper_2010_12438_b200.baselines import baseline_step_time, default_assignments
     from paper_2010_12438_b200.training import collect_rollouts, ppo_update
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     if big:  # cfg4 graph: per-sample cost of the device backward at 80,001 nodes
         g = gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
         top = uniform_topology(8)

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 
 def cfg4():
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     return gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
 
 

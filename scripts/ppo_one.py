@@ -7,7 +7,7 @@ from paper_2010_12438_b200 import (EmbedConfig, FusionConfig, PolicyConfig, PPOH
                                    init_all_params, randomize_zero_init, uniform_topology)
 from paper_2010_12438_b200.baselines import baseline_step_time, default_assignments  # noqa: E402
 from paper_2010_12438_b200.training import collect_rollouts, ppo_update  # noqa: E402
-from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload  # noqa: E402
+from synthetic.workloads import WorkloadSpec, gen_workload  # noqa: E402
 
 g = gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
 top = uniform_topology(8)

@@ -17,7 +17,7 @@ def main():
     from paper_2010_12438_b200.params import pack
     from paper_2010_12438_b200.policy import ordered_tasks
     from paper_2010_12438_b200.training import _device_samples, collect_rollouts, ppo_grad
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 8000
     g = gen_workload(WorkloadSpec("attention-stack", L, 1, 64, seed=0), node_cap=10**6)
     top = uniform_topology(8)

@@ -3,7 +3,8 @@
 Benchmark input only: it lets bench.py build the named DAGs on
 the GPU box, where the reference package is absent.  Same families, closed-form
 sizes and numpy draw order, so a spec yields the reference's graph exactly
-(pinned by tests/test_workloads.py against fixtures from the reference)."""
+(pinned by tests/test_host.py::test_workloads_match_reference against fixtures
+from the reference)."""
 from __future__ import annotations
 
 import math
@@ -11,7 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .graph import BYTES_PER_ELEMENT, OP_INDEX, Graph, GraphError
+from paper_2010_12438_b200.graph import BYTES_PER_ELEMENT, OP_INDEX, Graph, GraphError
 
 FAMILIES = ("grid-rnn", "enc-dec-rnn", "attention-stack", "multi-branch-cnn", "cell-stack-cnn",
             "dilated-stack")

@@ -302,10 +302,10 @@ def make_rollouts():
     np.savez_compressed(OUT / "golden_rollouts.npz", **out)
 
 
-def make_ppo():
+def make_ppo(iterations=2, name="golden_ppo.npz"):
     out = {}
     ecfg = EmbedConfig(1, 8, 4)
-    pcfg = PolicyConfig(1, 8, 2, 3, 16, 8, 2)
+    pcfg = PolicyConfig(1, 8, 2, 3, 16, 8, iterations)
     g = C.random_graph(np.random.default_rng(3), 12, p_edge=0.3)
     top = C.simple_topology(2)
     sizes = task_action_sizes(top, ["placement"], 8)
@@ -329,10 +329,16 @@ def make_ppo():
         out[p + "reward"] = np.float64(s.reward)
         out[p + "advantage"] = np.float64(s.advantage)
         out[p + "actions"] = s.bundle.actions["placement"]
-        out[p + "prev_actions"] = s.bundle.prev_actions["placement"]
+        if s.bundle.prev_actions is not None:
+            out[p + "prev_actions"] = s.bundle.prev_actions["placement"]
         out[p + "logp"] = s.bundle.log_probs["placement"]
         out[p + "embed_seed"] = np.int64(s.bundle.embed_seed)
-    np.savez_compressed(OUT / "golden_ppo.npz", **out)
+    np.savez_compressed(OUT / name, **out)
+
+
+def make_ppo1():
+    """ppo_update over single-iteration bundles (prev_actions None, training.py:156-158)."""
+    make_ppo(iterations=1, name="golden_ppo1.npz")
 
 
 WORKLOAD_SPECS = [
@@ -599,9 +605,55 @@ def make_train():
     np.savez_compressed(OUT / "golden_train.npz", **out)
 
 
+def make_fusion():
+    """apply_fusion group maps (simulator.py:199-277) with the priorities and
+    max_group that produced them: random DAGs (fusible-only and mixed ops, some
+    priorities 0), the same DAGs with permuted (non-topological) node ids, and
+    workload-family graphs.  The canonical FusedGraph.group_map is stored."""
+    from graphopt.simulator import ActionAssignment as AA
+    out = {}
+    rng = np.random.default_rng(2024)
+    cases = []
+    for i in range(60):
+        n = int(rng.integers(2, 41))
+        g = C.random_graph(rng, n, p_edge=float(rng.choice([0.08, 0.2, 0.35])),
+                           fusible_only=bool(i % 2 == 0))
+        cases.append(("random", g))
+        if i % 3 == 0:  # same structure, node ids permuted (edges no longer id-forward)
+            perm = rng.permutation(n)
+            specs = [None] * n
+            for v, nd in enumerate(g.nodes):
+                specs[perm[v]] = {"op": nd.op_type, "flops": nd.flops,
+                                  "out_bytes": nd.output_bytes}
+            edges = [(int(perm[e.src]), int(perm[e.dst]), e.bytes) for e in g.edges]
+            cases.append(("permuted", C.make_graph(specs, edges)))
+    for spec in [("attention-stack", 10, 1, 64, 0), ("dilated-stack", 2, 50, 64, 3),
+                 ("multi-branch-cnn", 40, 1, 64, 0), ("grid-rnn", 3, 5, 16, 2),
+                 ("enc-dec-rnn", 2, 4, 32, 1), ("cell-stack-cnn", 6, 1, 32, 4)]:
+        cases.append(("workload", gen_workload(WorkloadSpec(*spec))))
+    merged_any = 0
+    for c, (tag, g) in enumerate(cases):
+        n = g.num_nodes
+        pri = rng.integers(0, 8, n)
+        if c % 4 == 1:
+            pri[rng.random(n) < 0.3] = 0
+        mg = int(rng.choice([2, 3, 4, 8]))
+        fg = apply_fusion(g, AA("fusion_priority", pri, 8), FusionConfig(max_group=mg))
+        p = f"c{c}/"
+        graph_arrays(g, p, out)
+        out[p + "tag"] = np.array(tag)
+        out[p + "pri"] = pri.astype(np.int64)
+        out[p + "max_group"] = np.int64(mg)
+        out[p + "group_map"] = fg.group_map.astype(np.int64)
+        merged_any += int(len(fg.groups) < n)
+    out["count"] = np.int64(len(cases))
+    out["merged_cases"] = np.int64(merged_any)
+    np.savez_compressed(OUT / "golden_fusion.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "workloads", "grads",
-                             "baselines", "rollouts_joint", "json", "train"]
+    which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "ppo1", "workloads", "grads",
+                             "baselines", "rollouts_joint", "json", "train", "fusion"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

@@ -115,7 +115,7 @@ def test_ragged_batch_matches_single_forwards():
     each forward exactly what it gets alone."""
     from paper_2010_12438_b200.engine import forward_batch
     from paper_2010_12438_b200.runtime import context
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes)
     graphs = [gen_workload(WorkloadSpec("dilated-stack", 2, 50, 64, seed=3)),
@@ -154,7 +154,7 @@ def test_tc_gemm_forward_matches_simt_and_oracle():
     fp32 GEMMs and with the float64 oracle on a workload graph and a ragged batch."""
     from oracle import forward as of
     from oracle import graph as og
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes)
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 300, 1, 64, seed=0), node_cap=10**6),
@@ -208,7 +208,7 @@ def test_trunk_tc_matches_simt(seg):
     and mid-tile; segment_len 48 and 100 give key windows wider than the 192-key TMEM
     budget, so those batches take the SIMT kernel."""
     from paper_2010_12438_b200 import EmbedConfig, PolicyConfig
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes, EmbedConfig(), PolicyConfig(segment_len=seg))
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 60, 1, 64, seed=1), node_cap=10**6),
@@ -229,7 +229,7 @@ def test_trunk_mma_matches_simt(seg):
     (GO_TRUNK=simt) on a ragged batch; segment lengths that are not multiples of the
     64-query tile and windows wider than one key chunk (200 -> 400 keys) included."""
     from paper_2010_12438_b200 import EmbedConfig, PolicyConfig
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes, EmbedConfig(), PolicyConfig(segment_len=seg))
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 60, 1, 64, seed=1), node_cap=10**6),
@@ -251,7 +251,7 @@ def test_trunk_mma_out_of_range_reruns_simt():
     # |q| ~ 1e5 > the fp16 range: softmax becomes a near-argmax, outputs stay moderate
     store["policy/block0/attn_q_w"].data = store["policy/block0/attn_q_w"].data * 3e5
     store.touch()
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     graphs = [gen_workload(WorkloadSpec("attention-stack", 10, 1, 64, seed=0))]
     h_m, lg_m = _forward_env("GO_TRUNK", None, store, ecfg, pcfg, sizes, graphs, [7])
     h_s, lg_s = _forward_env("GO_TRUNK", "simt", store, ecfg, pcfg, sizes, graphs, [7])
@@ -263,7 +263,7 @@ def test_fp16_gemm_matches_tf32_and_reruns_out_of_range():
     """The fp16-operand GEMMs (default) agree with the tf32-operand GEMMs
     (GO_GEMM_F16=0); with embedding weights scaled so activations exceed the fp16
     range, the fp16 pass flags itself and the tf32 re-run produces the same result."""
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes)
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 200, 1, 64, seed=4), node_cap=10**6)]
@@ -301,7 +301,7 @@ def test_fused_ffn_matches_unfused_and_reruns_out_of_range():
     FF weights scaled so the 512-wide intermediate leaves the fp16 range, the fused pass
     flags itself and the unfused tf32 re-run produces the layer (finite, close to the
     unfused path)."""
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
     ecfg, pcfg, store = _store(sizes)
     graphs = [gen_workload(WorkloadSpec("multi-branch-cnn", 120, 1, 64, seed=5), node_cap=10**6),
@@ -329,7 +329,7 @@ def test_des_device_bounds_match_oracle(d):
     from oracle import graph as og
     from paper_2010_12438_b200.costmodel import Topology
     from paper_2010_12438_b200.simulator import ActionAssignment, simulate, singleton_fused
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     rng = np.random.default_rng(100 + d)
     g = gen_workload(WorkloadSpec("multi-branch-cnn", 20, 1, 64, seed=d), node_cap=10**6)
     ogr = og.make(g.num_nodes, g.op, g.flops, g.out_bytes, g.src, g.dst, g.ebytes)

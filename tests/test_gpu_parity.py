@@ -140,7 +140,7 @@ def test_des_batched_matches_oracle_random_placements():
     from oracle import graph as og
     from paper_2010_12438_b200.costmodel import uniform_topology
     from paper_2010_12438_b200.simulator import simulate_many, singleton_fused
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     g = gen_workload(WorkloadSpec("attention-stack", 60, 1, 64, seed=0), node_cap=10**6)
     rng = np.random.default_rng(7)
     K, d = 48, 8

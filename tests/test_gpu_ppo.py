@@ -78,15 +78,18 @@ def test_sample_loss_and_gradient_parity(case):
         assert not bad, (case, i, bad)
 
 
-def test_ppo_update_matches_reference():
+@pytest.mark.parametrize("name,iterations", [("ppo", 2), ("ppo1", 1)])
+def test_ppo_update_matches_reference(name, iterations):
+    """iterations=1 bundles carry prev_actions=None; the loss re-forward then sees zero
+    action features (training.py:156-158), the ADVICE r1 case that used to raise."""
     from paper_2010_12438_b200 import (EmbedConfig, PolicyConfig, PPOHyper, init_all_params,
                                        randomize_zero_init)
     from paper_2010_12438_b200.costmodel import uniform_topology
     from paper_2010_12438_b200.policy import TaskActionBundle
     from paper_2010_12438_b200.training import RolloutBatch, RolloutSample, ppo_update
-    z = golden("ppo")
+    z = golden(name)
     g = _graph(z, "g/")
-    ecfg, pcfg = EmbedConfig(1, 8, 4), PolicyConfig(1, 8, 2, 3, 16, 8, 2)
+    ecfg, pcfg = EmbedConfig(1, 8, 4), PolicyConfig(1, 8, 2, 3, 16, 8, iterations)
     sizes = {"placement": 2}
     store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
     for n, prm in store.items():
@@ -94,9 +97,11 @@ def test_ppo_update_matches_reference():
     samples = []
     for i in range(4):
         q = f"r{i}/"
+        prev = ({"placement": z[q + "prev_actions"]} if q + "prev_actions" in z else None)
+        assert (prev is None) == (iterations == 1)
         b = TaskActionBundle(["placement"], {}, {"placement": z[q + "actions"]},
-                             {"placement": z[q + "logp"]}, 0.0,
-                             {"placement": z[q + "prev_actions"]}, int(z[q + "embed_seed"]), 1.0)
+                             {"placement": z[q + "logp"]}, 0.0, prev, int(z[q + "embed_seed"]),
+                             1.0)
         samples.append(RolloutSample(0, b, float(z[q + "reward"]), 0.0,
                                      float(z[q + "advantage"]), 0.0, True))
     hyper = PPOHyper(lr=1e-2, rollouts=4, minibatches=2, epochs=2, entropy_coef=0.01)
@@ -182,7 +187,7 @@ def test_tensor_core_tape_matches_simt_at_cfg4_scale():
                                        init_all_params, randomize_zero_init, uniform_topology)
     from paper_2010_12438_b200.baselines import baseline_step_time
     from paper_2010_12438_b200.training import collect_rollouts
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     g = gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
     top = uniform_topology(8)
     sizes = {"placement": 8}
@@ -221,7 +226,7 @@ def test_tensor_core_tape_attention_matches_simt_and_reruns_out_of_range():
                                        init_all_params, randomize_zero_init, uniform_topology)
     from paper_2010_12438_b200.baselines import baseline_step_time
     from paper_2010_12438_b200.training import collect_rollouts
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     g = gen_workload(WorkloadSpec("attention-stack", 100, 1, 64, seed=0))
     top = uniform_topology(4)
     sizes = {"placement": 4}
@@ -260,7 +265,7 @@ def test_tape_loss_matches_float64_oracle():
                                        init_all_params, randomize_zero_init, uniform_topology)
     from paper_2010_12438_b200.baselines import baseline_step_time
     from paper_2010_12438_b200.training import collect_rollouts
-    from paper_2010_12438_b200.workloads import WorkloadSpec, gen_workload
+    from synthetic.workloads import WorkloadSpec, gen_workload
     g = gen_workload(WorkloadSpec("attention-stack", 1000, 1, 64, seed=0), node_cap=10**6)
     top = uniform_topology(8)
     sizes = {"placement": 8}

@@ -94,16 +94,15 @@ def test_des_oracle_bit_exact():
 
 
 def test_fusion_oracle_matches_reference_groups():
-    z = golden("des")
+    """oracle.des.apply_fusion against the reference's apply_fusion group maps
+    (golden_fusion.npz, with the priorities that produced them)."""
+    z = golden("fusion")
     for c in range(int(z["count"])):
         p = f"c{c}/"
-        if str(z[p + "tag"]) != "fused":
-            continue
         g = oracle_graph(z, p)
-        # the reference group_map is canonical (groups by min member); the
-        # oracle's fusion pass returns roots, so compare partitions
-        want = od.Fused(g, z[p + "group_map"]).group_map
-        assert len(want) == g["n"]
+        roots = od.apply_fusion(g, z[p + "pri"], max_group=int(z[p + "max_group"]))
+        got = od.Fused(g, roots).group_map
+        assert np.array_equal(np.asarray(got), z[p + "group_map"]), (c, str(z[p + "tag"]))
 
 
 def test_sampler_oracle_bit_exact():
@@ -143,3 +142,29 @@ def test_rollout_oracle_matches_reference():
         assert res["step_time"] == z[p + "step_time"]
         assert od.reward(res["step_time"], bl, res["valid"]) == z[p + "reward"]
         assert abs(traj[-1]["value"] - z[p + "value"]) < 1e-12
+
+
+def test_row_subset_heads_and_per_row_sampler_match_full_oracle():
+    """The helpers the headline parity tests use (tests/headline.py): task-head logits
+    on a subset of query rows equal the full float64 heads on those rows, and the
+    per-row sampler with the reference's uniform index reproduces iterate_decisions."""
+    import headline as H
+    z = golden("rollouts")
+    g = oracle_graph(z, "g/")
+    ecfg, pcfg = of.EmbedCfg(), of.PolicyCfg()
+    sizes = {"placement": 2}
+    P = op.randomize_zero_init(op.init_all_params(ecfg, pcfg, sizes, 0))
+    feats = og.node_features(g, None, [2])
+    ne, ge = of.embed(g, feats, P, ecfg, seed=11)
+    hid = of.trunk_forward(ne, ge, P, pcfg)
+    full, _, _ = of.task_heads(hid, P, pcfg, [("placement", 2)])
+    rows = H.sample_rows(g["n"], 17, seed=2)
+    sub, _ = of.task_heads_rows(hid, P, pcfg, [("placement", 2)], rows)
+    assert np.allclose(sub, full["placement"][rows], rtol=1e-13, atol=1e-13)
+    traj = of.iterate_decisions(g, P, ecfg, pcfg, sizes, 2, 11)
+    n = g["n"]
+    for it, step in enumerate(traj):
+        rep = H.check_actions(step["actions"]["placement"], step["log_probs"]["placement"],
+                              step["logits"]["placement"], step["logits"]["placement"],
+                              g["topo"], np.arange(n), 11, it, 0, 1)
+        assert rep["flips"] == 0 and rep["logp_max_abs_err"] == 0.0, rep
