@@ -135,11 +135,11 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   for (auto& t : tt) m.trunk_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
   for (auto& t : ht) m.head_pairs += (double)(t.q1 - t.q0) * (double)(t.k1 - t.k0);
   size_t o_tt = s.add(tt), o_ht = s.add(ht);
-  std::vector<TcWork> tcw, tcw2;
+  std::vector<TcWork> tcw;
   std::vector<int64_t> trow0;
   std::vector<int32_t> tn;
-  if (need_heads) tc_build_tables(m.row_off, tcw, trow0, tn, tcw2);
-  size_t o_tcw = s.add(tcw), o_tr = s.add(trow0), o_tn = s.add(tn), o_tcw2 = s.add(tcw2);
+  if (need_heads) tc_build_tables(m.row_off, tcw, trow0, tn);
+  size_t o_tcw = s.add(tcw), o_tr = s.add(trow0), o_tn = s.add(tn);
   // mean chunks: [nc] r0, [nc] r1, [F] first, [F] end
   std::vector<int64_t> c0, c1, f0(m.F), f1(m.F);
   for (int f = 0; f < m.F; ++f) {
@@ -171,8 +171,6 @@ BatchMeta make_meta(go_ctx* ctx, const go_config_t& cfg, const go_batch_t& b,
   m.d_chunks = reinterpret_cast<const int64_t*>(dev + o_ch);
   m.d_tc_works = reinterpret_cast<const TcWork*>(dev + o_tcw);
   m.n_tc_works = (int64_t)tcw.size();
-  m.d_tc_works2 = reinterpret_cast<const TcWork*>(dev + o_tcw2);
-  m.n_tc_works2 = (int64_t)tcw2.size();
   m.d_tile_row0 = reinterpret_cast<const int64_t*>(dev + o_tr);
   m.d_tile_n = reinterpret_cast<const int32_t*>(dev + o_tn);
   m.n_tiles = (int64_t)trow0.size();
@@ -435,7 +433,7 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
       tc_q = A.take<float>((int64_t)cfg.n_head * R * 16);
       tc_k = A.take<float>((int64_t)cfg.n_head * m.n_tiles * 64 * 16);
       tc_v = A.take<float>((int64_t)cfg.n_head * m.n_tiles * 64 * 16);
-      tc_scratch = A.take<int32_t>(1 + (int64_t)F * cfg.n_head);
+      tc_scratch = A.take<int32_t>(tc_attention_scratch_ints(F, cfg.n_head, m.n_tc_works));
     }
     float* a_prev = nullptr;
     int64_t ld_prev = LW;
@@ -460,7 +458,7 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
         if (use_tc)
           attention_full_tc(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, R, m.n_tiles, m.d_tc_works,
                             m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
-                            row_fwd, F, tc_scratch, m.d_tc_works2, m.n_tc_works2, st);
+                            row_fwd, F, tc_scratch, st);
         else
           attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_head_tiles, m.n_head_tiles, Ab,
                     LA, st);
@@ -657,8 +655,11 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       {
         KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
         if (trunk_mma) {
+          // split fp16 operands (3 MMAs per product): single fp16 Q/K/V put the trunk
+          // output 1.03e-4 (normwise) from float64 at cfg3, where the random-init rows are
+          // nearly parallel and the operand roundings do not average out
           trunk_attention_mma(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles,
-                              m.n_trunk_tiles, Ab, LA, trunk_flags + l, st);
+                              m.n_trunk_tiles, Ab, LA, trunk_flags + l, st, nullptr, true);
           attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
                     LA, st, nullptr, trunk_flags + l);
         } else {
@@ -721,7 +722,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       tc_q = A.take<float>((int64_t)H * R * 16);
       tc_k = A.take<float>((int64_t)H * m.n_tiles * 64 * 16);
       tc_v = A.take<float>((int64_t)H * m.n_tiles * 64 * 16);
-      tc_scratch = A.take<int32_t>(1 + (int64_t)F * H);
+      tc_scratch = A.take<int32_t>(tc_attention_scratch_ints(F, H, m.n_tc_works));
     }
     const TcW ta_qkv = pack(W_(S.ta(Q_W)), W_(S.ta(K_W)), W_(S.ta(V_W)), W, W, dm, 3 * W);
     const float* ta_b = qkv_bias(W_(S.ta(Q_B)), W_(S.ta(K_B)), W_(S.ta(V_B)));
@@ -753,7 +754,7 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
         if (use_tc)
           attention_full_tc(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, R, m.n_tiles, m.d_tc_works,
                             m.n_tc_works, m.d_tile_row0, m.d_tile_n, tc_q, tc_k, tc_v, Ab, LA,
-                            row_fwd, F, tc_scratch, m.d_tc_works2, m.n_tc_works2, st);
+                            row_fwd, F, tc_scratch, st);
         else
           attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_head_tiles, m.n_head_tiles, Ab, LA,
                     st);

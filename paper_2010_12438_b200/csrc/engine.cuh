@@ -187,8 +187,8 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                       int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
                       int64_t num_works, const int64_t* tile_row0_dev, const int32_t* tile_n_dev,
                       void* qh, void* kb, void* vb, float* out, int64_t ldo,
-                      const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
-                      const TcWork* works2_dev, int64_t num_works2, cudaStream_t st);
+                      const int32_t* row_fwd, unsigned* kmax, int32_t* flag, int32_t* wflag,
+                      float qscale, cudaStream_t st);
 
 // ---- kernels: trunk_mma.cu (banded trunk attention on mma.sync m16n8k16, d_head <= 16);
 // *flag (zeroed here) is set if some operand left the fp16 range -- the caller then
@@ -205,17 +205,18 @@ struct TcWork {
   int64_t row0, tile0;
 };
 bool tc_attention_supported(int d_head);
-// works: 384-query items (tf32 kernels and the 3-tile fp16 kernel); works2: 256-query
-// items (2-tile alternating-window fp16 kernel)
+// works: 384-query items (one CTA each in the fp16 and tf32 kernels)
 void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& works,
-                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n,
-                     std::vector<TcWork>& works2);
+                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n);
+// int32 scratch attention_full_tc needs: launch flag, max |k| per (forward, head),
+// fallback marks per (head, work item)
+int64_t tc_attention_scratch_ints(int F, int n_head, int64_t num_works);
 void attention_full_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                        int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
                        int64_t num_works, const int64_t* tile_row0_dev,
                        const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
                        int64_t ldo, const int32_t* row_fwd, int F, int32_t* scratch,
-                       const TcWork* works2_dev, int64_t num_works2, cudaStream_t st);
+                       cudaStream_t st);
 
 // per-call batch metadata (engine.cu make_meta): row offsets, graph views, tiles
 struct BatchMeta {
@@ -238,8 +239,6 @@ struct BatchMeta {
   // tensor-core heads attention tables
   const TcWork* d_tc_works = nullptr;
   int64_t n_tc_works = 0;
-  const TcWork* d_tc_works2 = nullptr;
-  int64_t n_tc_works2 = 0;
   const int64_t* d_tile_row0 = nullptr;
   const int32_t* d_tile_n = nullptr;
   int64_t n_tiles = 0;

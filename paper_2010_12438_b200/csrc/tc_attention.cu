@@ -445,52 +445,52 @@ __global__ void repack_kernel(const float* __restrict__ q, const float* __restri
 // of the bound); otherwise the online-softmax kernel above takes the launch.
 constexpr float BOUND_LIMIT = 60.f;
 
-// 2^x for x <= 0 on the FMA/ALU pipes: x = n + f, n = rint(x) (magic-number add),
-// f in [-0.5, 0.5], 2^f by a degree-4 minimax polynomial, 2^n by exponent add.
-// Inputs below -126 return 0 (the MUFU path flushes there too).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer
-  const int n = __float_as_int(t) - 0x4B400000;
-  const float f = x - (t - 12582912.f);
-  float p = 1.3333558146e-3f;
-  p = fmaf(p, f, 9.6181291076e-3f);
-  p = fmaf(p, f, 5.5504108664e-2f);
-  p = fmaf(p, f, 2.4022650695e-1f);
-  p = fmaf(p, f, 6.9314718056e-1f);
-  p = fmaf(p, f, 1.0f);
-  const float r = __int_as_float(__float_as_int(p) + (n << 23));
-  return n < -126 ? 0.f : r;
-}
-
 // The fixed kernel runs two CTAs per SM (TMEM 2 x 256 columns) so the softmax warps
 // of two independent CTAs interleave on each SM sub-partition and keep the MUFU pipe
 // busy through each other's tcgen05.ld/st and barrier latencies.  Each 64-key K/V
 // tile is consumed as two 32-key halves (S sub-tiles of 32 TMEM columns, double
 // buffered per query tile): 3 x 2 x 32 S columns + 3 x 16 O columns = 240 <= 256.
+// O accumulates in TMEM over DRAIN_U sub-tiles only; at each group boundary the MMA
+// thread commits o_ready, the softmax thread adds the group's O into a float sum in
+// shared memory (tc_attention16.cu explains why: the tensor core's accumulate drifts
+// over thousands of additions), and the next group restarts the accumulator.
 constexpr int HK = 32;                      // keys per softmax sub-tile
 constexpr int NSF = 6;                      // K/V ring stages per CTA
+constexpr int DRAIN_U = 16;                 // 32-key sub-tiles per accumulation group
 constexpr uint32_t O_COL_F = NQT * 2 * HK;  // O accumulators after the S buffers
 constexpr uint32_t TMEM_COLS_F = 256;
 
 struct SmemF {
   float q[NQT][QT * 16];
   float kv[NSF][2][KT * 16];
+  float osum[NQT][16][QT];  // drained O groups, [tile][column][row]
   uint64_t kv_full[NSF], kv_empty[NSF];
-  uint64_t s_full[NQT][2], p_full[NQT][2], o_done[NQT];
+  uint64_t s_full[NQT][2], p_full[NQT][2], o_ready[NQT], o_done[NQT];
   uint32_t tmem_base;
 };
 
-// POLY_PER_8: of every 8 score columns, this many are exponentiated by ex2_poly on
-// the FMA pipe instead of MUFU.EX2.  PIPE: software-pipelined softmax loop (16-column
-// chunks; the next chunk's tcgen05.ld is in flight while this chunk's ex2s issue).
-template <int POLY_PER_8, bool PIPE>
+// Launch flag bits (attention_full_tc): 1 = the online kernel takes the launch,
+// 2 = the tf32 kernel takes the launch, 4 = the tf32 kernel takes the work items the
+// fp16 kernel marked in wflag.  primary: the tf32 kernel is the first choice (no fp16
+// pass before it).
+__device__ __forceinline__ bool tf32_launch(int32_t flag, bool primary) {
+  return !(flag & 1) && (primary || (flag & 6));
+}
+__device__ __forceinline__ bool tf32_work(int32_t flag, bool primary, const int32_t* wflag,
+                                          int64_t item) {
+  if (!tf32_launch(flag, primary)) return false;
+  return primary || (flag & 2) || wflag[item];
+}
+
+// Pipelined softmax loop: 16-column chunks, the next chunk's tcgen05.ld in flight while
+// this chunk's ex2s issue.
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_tc_fixed_kernel(const float* __restrict__ qh, const float* __restrict__ kb,
                          const float* __restrict__ vb, int64_t R, int64_t Ttot,
                          const Work* __restrict__ works, float* __restrict__ out, int64_t ldo,
-                         int d_head, const int32_t* __restrict__ flag, int want) {
-  if (*flag != want) return;  // another variant takes this launch
+                         int d_head, const int32_t* __restrict__ flag,
+                         const int32_t* __restrict__ wflag, bool primary) {
+  if (!tf32_work(*flag, primary, wflag, (int64_t)blockIdx.y * gridDim.x + blockIdx.x)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SmemF& sm = *reinterpret_cast<SmemF*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -510,6 +510,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         mbar_init(&sm.s_full[t][b], 1);
         mbar_init(&sm.p_full[t][b], 128);
       }
+      mbar_init(&sm.o_ready[t], 1);
       mbar_init(&sm.o_done[t], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -577,8 +578,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         wait_kv(u);
         for (int t = 0; t < NQT; ++t) issue_s(u, t);
       }
-      // (A non-blocking, any-order variant that polled every query tile measured 34%
-      // slower: the spinning issuer steals issue slots from the softmax warps.)
       for (int u = 0; u < U; ++u) {
         const int j = u >> 1, h = u & 1, s = j % NSF, b = u & 1;
         const bool more = u + 2 < U;
@@ -590,8 +589,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           const uint32_t d = tbase + O_COL_F + t * 16;
           const uint32_t a = tbase + t * 2 * HK + b * HK;
 #pragma unroll
-          for (int k = 0; k < HK / 8; ++k)
-            umma_ts(d, a + k * 8, sdesc(vaddr + k * 512, 256, 128), ID_O, (u > 0 || k > 0));
+          for (int k = 0; k < HK / 8; ++k)  // a new accumulation group restarts O
+            umma_ts(d, a + k * 8, sdesc(vaddr + k * 512, 256, 128), ID_O,
+                    (u % DRAIN_U != 0 || k > 0));
+          if ((u + 1) % DRAIN_U == 0 && u + 1 < U) umma_commit(&sm.o_ready[t]);
           if (more) issue_s(u + 2, t);
         }
         if (h == 1) umma_commit(&sm.kv_empty[s]);  // both halves' PV issued
@@ -600,76 +601,68 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     }
     __syncwarp();
   } else {
+    // chunk c = 2u + h: columns [16h, 16h + 16) of sub-tile u.  The tcgen05.ld of chunk
+    // c + 1 is issued before chunk c's ex2s, so the MUFU queue never waits on a TMEM
+    // load; P(u) is released after its second chunk's tcgen05.st lands.
     const int t = warp >> 2;
-    const int wq = warp & 3;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    if (PIPE) {
-      // chunk c = 2u + h: columns [16h, 16h + 16) of sub-tile u.  The tcgen05.ld of
-      // chunk c + 1 is issued before chunk c's ex2s, so the MUFU queue never waits on
-      // a TMEM load; P(u) is released after its second chunk's tcgen05.st lands.
-      const uint32_t base = tbase + lane_off + t * 2 * HK;
-      auto caddr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 16; };
-      uint32_t ra[16], rb[16];
-      if (U > 0) {
-        mbar_wait(&sm.s_full[t][0], 0);
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t base = tbase + lane_off + t * 2 * HK;
+    const uint32_t obase = tbase + lane_off + O_COL_F + t * 16;
+    float* osum = &sm.osum[t][0][row];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) osum[d * QT] = 0.f;
+    auto caddr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 16; };
+    uint32_t ra[16], rb[16];
+    if (U > 0) {
+      mbar_wait(&sm.s_full[t][0], 0);
+      fence_after();
+      TC_LD16(caddr(0), ra);
+      tmem_wait_ld();
+    }
+    for (int u = 0; u < U; ++u) {
+      const int c = 2 * u;
+      TC_LD16(caddr(c + 1), rb);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ra[i] = __float_as_uint(ex2(__uint_as_float(ra[i])));
+      TC_ST16(caddr(c), ra);
+      tmem_wait_ld();
+      const bool more = u + 1 < U;
+      if (more) {
+        mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
         fence_after();
-        TC_LD16(caddr(0), ra);
-        tmem_wait_ld();
+        TC_LD16(caddr(c + 2), ra);
       }
-      for (int u = 0; u < U; ++u) {
-        const int c = 2 * u;
-        TC_LD16(caddr(c + 1), rb);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) ra[i] = __float_as_uint(ex2(__uint_as_float(ra[i])));
-        TC_ST16(caddr(c), ra);
-        tmem_wait_ld();
-        const bool more = u + 1 < U;
-        if (more) {
-          mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
-          fence_after();
-          TC_LD16(caddr(c + 2), ra);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) rb[i] = __float_as_uint(ex2(__uint_as_float(rb[i])));
-        TC_ST16(caddr(c + 1), rb);
-        tmem_wait_st();
-        fence_before();
-        mbar_arrive(&sm.p_full[t][u & 1]);
-        if (more) tmem_wait_ld();
-      }
-    } else {
-      for (int u = 0; u < U; ++u) {
-        const int b = u & 1;
-        mbar_wait(&sm.s_full[t][b], (u >> 1) & 1);
+      for (int i = 0; i < 16; ++i) rb[i] = __float_as_uint(ex2(__uint_as_float(rb[i])));
+      TC_ST16(caddr(c + 1), rb);
+      tmem_wait_st();
+      if (u > 0 && u % DRAIN_U == 0) {  // O = sub-tiles [u - DRAIN_U, u); PV(u) waits on us
+        mbar_wait(&sm.o_ready[t], ((u / DRAIN_U) - 1) & 1);
         fence_after();
-        uint32_t sr[HK];
-        const uint32_t sa = tbase + lane_off + t * 2 * HK + b * HK;
-        TC_LD32(sa, sr);
+        TC_LD16(obase, rb);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < HK; ++i) {
-          const float x = __uint_as_float(sr[i]);
-          // FA4-style split: a fixed subset of the columns is exponentiated on the FMA
-          // pipe (degree-5 polynomial, rel. err < 4e-6, far below the tf32 rounding of
-          // P) so the MUFU and FMA pipes work in parallel.
-          sr[i] = __float_as_uint(((i & 7) < POLY_PER_8) ? ex2_poly(x) : ex2(x));
-        }
-        TC_ST32(sa, sr);
-        tmem_wait_st();
-        fence_before();
-        mbar_arrive(&sm.p_full[t][b]);
+        for (int d = 0; d < 16; ++d) osum[d * QT] += __uint_as_float(rb[d]);
       }
+      fence_before();
+      mbar_arrive(&sm.p_full[t][u & 1]);
+      if (more) tmem_wait_ld();
     }
     mbar_wait(&sm.o_done[t], 0);
     fence_after();
-    uint32_t r[16];
-    TC_LD16(tbase + lane_off + O_COL_F + t * 16, r);
-    tmem_wait_ld();
-    const int lr = w.q0 + t * QT + wq * 32 + lane;
+    if (U > 0) {
+      uint32_t r[16];
+      TC_LD16(obase, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int d = 0; d < 16; ++d) osum[d * QT] += __uint_as_float(r[d]);
+    }
+    const int lr = w.q0 + t * QT + row;
     if (lr < w.n) {
-      float inv = 1.f / __uint_as_float(r[15]);
+      float inv = 1.f / osum[15 * QT];
       float* o = out + (w.row0 + lr) * ldo + head * d_head;
-      for (int d = 0; d < d_head; ++d) o[d] = __uint_as_float(r[d]) * inv;
+      for (int d = 0; d < d_head; ++d) o[d] = osum[d * QT] * inv;
     }
   }
   fence_before();
@@ -688,8 +681,8 @@ __global__ void repack_kv_fixed_kernel(const float* __restrict__ k, const float*
                                        const int32_t* __restrict__ tile_n, int64_t Ttot,
                                        float* __restrict__ kb, float* __restrict__ vb,
                                        unsigned* __restrict__ kmax,
-                                       const int32_t* __restrict__ flag, int want) {
-  if (*flag != want) return;
+                                       const int32_t* __restrict__ flag, bool primary) {
+  if (!tf32_launch(*flag, primary)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)n_head * Ttot * KT;
   if (idx >= total) return;
@@ -729,8 +722,8 @@ __global__ void repack_q_fixed_kernel(const float* __restrict__ q, int64_t ld, i
                                       int d_head, int64_t R, const int32_t* __restrict__ row_fwd,
                                       const unsigned* __restrict__ kmax, float qscale,
                                       float* __restrict__ qh, int32_t* __restrict__ flag,
-                                      int want) {
-  if (*flag != want) return;
+                                      bool primary) {
+  if (!tf32_launch(*flag, primary)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * n_head) return;
   int64_t r = idx / n_head;
@@ -754,8 +747,7 @@ __global__ void repack_q_fixed_kernel(const float* __restrict__ q, int64_t ld, i
 bool tc_attention_supported(int d_head) { return d_head <= 16; }
 
 void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& works,
-                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n,
-                     std::vector<TcWork>& works2) {
+                     std::vector<int64_t>& tile_row0, std::vector<int32_t>& tile_n) {
   int F = (int)row_off.size() - 1;
   int64_t tb = 0;
   for (int f = 0; f < F; ++f) {
@@ -763,8 +755,6 @@ void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& w
     int32_t T = (int32_t)cdiv(n, tc::KT);
     for (int64_t q0 = 0; q0 < n; q0 += tc::NQT * tc::QT)
       works.push_back(TcWork{f, (int32_t)q0, (int32_t)n, T, row_off[f], tb});
-    for (int64_t q0 = 0; q0 < n; q0 += 2 * tc::QT)
-      works2.push_back(TcWork{f, (int32_t)q0, (int32_t)n, T, row_off[f], tb});
     for (int32_t t = 0; t < T; ++t) {
       tile_row0.push_back(row_off[f]);
       tile_n.push_back((int32_t)n);
@@ -775,63 +765,57 @@ void tc_build_tables(const std::vector<int64_t>& row_off, std::vector<TcWork>& w
   }
 }
 
+int64_t tc_attention_scratch_ints(int F, int n_head, int64_t num_works) {
+  return 1 + (int64_t)F * n_head + (int64_t)n_head * num_works;
+}
+
 void attention_full_tc(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                        int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
                        int64_t num_works, const int64_t* tile_row0_dev,
                        const int32_t* tile_n_dev, float* qh, float* kb, float* vb, float* out,
                        int64_t ldo, const int32_t* row_fwd, int F, int32_t* scratch,
-                       const TcWork* works2_dev, int64_t num_works2, cudaStream_t st) {
+                       cudaStream_t st) {
   if (num_works <= 0) return;
   if (d_head > 16) GO_THROW(GO_ERR_UNSUPPORTED, "tensor-core attention needs d_head <= 16");
   static bool attr = false;
   const size_t smem = sizeof(tc::Smem) + 1024;
   const size_t smemf = sizeof(tc::SmemF) + 1024;
-  using FixedFn = void (*)(const float*, const float*, const float*, int64_t, int64_t,
-                           const tc::Work*, float*, int64_t, int, const int32_t*, int);
-  static const FixedFn fixed_fns[6] = {
-      tc::attn_tc_fixed_kernel<0, true>,  tc::attn_tc_fixed_kernel<1, false>,
-      tc::attn_tc_fixed_kernel<2, false>, tc::attn_tc_fixed_kernel<3, false>,
-      tc::attn_tc_fixed_kernel<4, false>, tc::attn_tc_fixed_kernel<0, false>};
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-    for (FixedFn fn : fixed_fns)
-      CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf));
+    CUDA_CHECK(cudaFuncSetAttribute(tc::attn_tc_fixed_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf));
     attr = true;
   }
-  // GO_POLY=k (1..4): k of every 8 exponentials on the FMA pipe; GO_POLY=5: the
-  // unpipelined pure-MUFU loop; default 0: pipelined pure-MUFU loop (tf32 variant)
-  const char* poly_env = getenv("GO_POLY");
-  const int poly = poly_env ? std::max(0, std::min(5, atoi(poly_env))) : 0;
+  // A/B switch (tests and timing only): GO_ATTN=tf32 makes the tf32 fixed-offset kernel
+  // the first choice, GO_ATTN=online forces the online-softmax kernel
   const char* force = getenv("GO_ATTN");
-  // GO_ATTN=tf32 skips the fp16 variant, GO_ATTN=online forces the online kernel
   const bool use16 = d_head <= 15 && !(force && (!strcmp(force, "tf32") || !strcmp(force, "online")));
   float qscale = (float)(1.4426950408889634 / std::sqrt((double)d_head));
   int64_t total = (int64_t)n_head * Ttot * tc::KT;
   dim3 grid((unsigned)num_works, (unsigned)n_head);
   bool fixed_ok = d_head <= 15 && !(force && !strcmp(force, "online"));
   if (fixed_ok) {
-    // scratch: [0] flag, [1..] kmax per (forward, head)
+    // scratch: [0] launch flag, [1, 1 + F*H) max |k| per (forward, head),
+    // then per (head, work item) fallback marks of the fp16 kernel
     int32_t* flag = scratch;
     unsigned* kmax = reinterpret_cast<unsigned*>(scratch + 1);
-    CUDA_CHECK(cudaMemsetAsync(scratch, 0, (size_t)(1 + F * n_head) * 4, st));
-    // flag after the fp16 repack: 0 -> fp16 kernel, 2 -> tf32 kernel, odd -> online
-    int want = 0;
-    if (use16) {
+    int32_t* wflag = scratch + 1 + (int64_t)F * n_head;
+    CUDA_CHECK(cudaMemsetAsync(
+        scratch, 0, (size_t)tc_attention_scratch_ints(F, n_head, num_works) * 4, st));
+    if (use16)
       attention_f16_tc(q, k, v, ld, n_head, d_head, R, Ttot, works_dev, num_works, tile_row0_dev,
-                       tile_n_dev, qh, kb, vb, out, ldo, row_fwd, kmax, flag, qscale,
-                       works2_dev, num_works2, st);
-      want = 2;
-    }
+                       tile_n_dev, qh, kb, vb, out, ldo, row_fwd, kmax, flag, wflag, qscale, st);
+    const bool primary = !use16;
     tc::repack_kv_fixed_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
-        k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, kb, vb, kmax, flag, want);
+        k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, kb, vb, kmax, flag, primary);
     LAUNCH_CHECK();
     tc::repack_q_fixed_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
-        q, ld, n_head, d_head, R, row_fwd, kmax, qscale, qh, flag, want);
+        q, ld, n_head, d_head, R, row_fwd, kmax, qscale, qh, flag, primary);
     LAUNCH_CHECK();
-    fixed_fns[poly]<<<grid, tc::NUM_THREADS, smemf, st>>>(
+    tc::attn_tc_fixed_kernel<<<grid, tc::NUM_THREADS, smemf, st>>>(
         qh, kb, vb, R, Ttot, reinterpret_cast<const tc::Work*>(works_dev), out, ldo, d_head, flag,
-        want);
+        wflag, primary);
     LAUNCH_CHECK();
     // fallback for bounds > BOUND_LIMIT: the online kernel re-packs and runs only if flagged
     tc::repack_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(

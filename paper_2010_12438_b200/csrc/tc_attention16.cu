@@ -1,21 +1,39 @@
-// Task-head N x N attention, fp16 tensor-core variant (policy.py:210).
+// Task-head N x N attention, fp16 tensor-core kernel (policy.py:210 multi_head_attention
+// over all rows), the default path of every forward's heads.
 //
-// Same structure and fixed-offset trick as attn_tc_fixed_kernel (tc_attention.cu), with
-// the two MMAs in kind::f16 (fp16 operands, fp32 accumulation), because at these shapes
-// the tensor pipe, not the MUFU, binds the tf32 kernel: a tcgen05.mma with M=128 and
-// N <= 64 costs ~45.5 cycles regardless of N (scripts/umma_probe.cu), and kind::f16 does
-// K=16 per instruction against kind::tf32's K=8, halving the instruction count:
-//   S = Q K^T    M=128, N=32, K=16: 1 instruction per query tile and 32-key sub-tile
-//   O += P V     M=128, N=16, K=16 (A = P packed fp16x2 in TMEM): 2 instructions
+// Per (head, 384 queries) CTA, two CTAs per SM (TMEM 2 x 256 columns), 16 warps:
+//   warps 0-11  softmax: one thread per query row (3 tiles x 128 TMEM lanes)
+//   warp 12     producer: cp.async.bulk of 64-key K and V^T fp16 tiles into an 8-stage ring
+//   warps 13-15 one MMA-issuing thread per query tile:
+//     S = Q K^T      kind::f16, M=128, N=64, K=16: one MMA per 64-key tile
+//     O += P V       kind::f16, M=128, N=16, A = P packed fp16x2 in TMEM: 4 MMAs
 //
-// Precision.  fp16 carries the same 10 explicit mantissa bits as tf32 (Q, K, V and P are
-// rounded to nearest), so products match the tf32 kernel's.  The range is handled by the
-// offset: Q[:,15] = 15 - b_i against K[:,15] = 1 gives S' = s - b_i + 15 <= 15, so
-// P' = 2^S' <= 2^15 never overflows fp16, and as long as b_i <= F16_LIMIT = 14 every
-// score satisfies S' >= 15 - 2 b_i >= -13, i.e. every P' is a normal fp16 (no subnormal
-// precision loss).  The 2^15 scale cancels in O / O[:,15].  Rows with a larger bound (or
-// |k|, |v| beyond fp16 range) flag the launch over to the tf32 kernel (bound <= 60) or
-// the online-softmax kernel (> 60).
+// Fixed-offset softmax.  Q[:,15] = 15 - b_i (b_i >= |q_i| max|k|, a Cauchy-Schwarz bound)
+// against K[:,15] = 1 makes the MMA return S' = s - b_i + 15 <= 15, so P' = 2^S' <= 2^15
+// never overflows fp16, and while b_i <= F16_LIMIT = 14 every S' >= -13 gives a normal
+// fp16 P'.  V[:,15] = 1 makes O[:,15] the row sum of exactly the P' the numerator used,
+// so the 2^(15 - b_i) scale cancels in O / O[:,15]: no running max, no rescale.
+// Half of the exponentials run as an fp16x2 polynomial on the FMA pipe (ptx::
+// exp2_poly_f16x2_lp), half on MUFU.EX2 (16/clk/SM): together 1.24x the MUFU rate.
+//
+// Accumulation.  The tensor core's fp32 accumulate does not round the low bits of
+// small addends to nearest; summed over the 1,250 key tiles of an 80k-node graph (where
+// the random-init rows are nearly parallel and every addend has the same sign pattern)
+// that drift reached 1.4e-4 of the logits.  So O accumulates in TMEM over only DRAIN = 8
+// key tiles; at each group boundary the softmax thread, which owns its row, reads the
+// 16 O columns and adds them into a float sum in shared memory (IEEE round-to-nearest,
+// ~160 additions at 80k keys), and the MMA thread restarts the accumulator.  Measured
+// at cfg4 (scripts/parity_variants.py): logits 1.41e-4 -> 4.8e-6 normwise from float64,
+// kernel time unchanged (Kahan compensation or DRAIN = 16 / 32: 5.6e-6 / 7.6e-6).  The drain needs no extra barrier: S(j) is
+// issued after PV(j-1) by the same thread and tcgen05 MMAs complete in order, so when
+// s_full(j) fires O holds exactly tiles [.., j-1], and PV(j) (accumulate = 0) waits for
+// p_full(j), which this thread signals only after the drain.
+//
+// Fallback per work item.  A row whose bound exceeds F16_LIMIT gets NaN in Q[:,15]
+// (repack_q16_kernel); the CTA owning it sees the NaN while staging Q, marks its
+// (work, head) in wflag, sets bit 4 of the launch flag and exits, and the tf32 kernel
+// (tc_attention.cu) recomputes only the marked work items.  Bounds above BOUND_LIMIT
+// (bit 1) and operands outside the fp16 range (bit 2) still move the whole launch.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -30,34 +48,32 @@ namespace t16 {
 
 using namespace ptx;
 
-constexpr int KT = 64;   // keys per K/V tile (the tile tables are shared with the tf32 path)
+constexpr int KT = 64;   // keys per K/V tile (tile tables shared with the tf32 path)
 constexpr int QT = 128;  // queries per M tile
 constexpr int NQT = 3;   // M tiles per CTA
-constexpr int HK = 32;   // keys per softmax sub-tile
 constexpr int NS = 8;    // K/V ring stages
+constexpr int DRAIN = 8; // key tiles per TMEM accumulation group
+constexpr int NP = 4;    // of every 8 exponential pairs, NP on the FMA-pipe polynomial
 constexpr int TILE_BYTES = KT * 16 * 2;
 constexpr int PRODUCER_WARP = NQT * 4;
-// one MMA-issuing warp per query tile: a tile's PV / next-S issue never waits behind
-// another tile's softmax (a single in-order issuer left the softmax warps spinning on
-// s_full for a third of their samples, ncu source page)
 constexpr int MMA_WARP0 = NQT * 4 + 1;
 constexpr int NUM_THREADS = (NQT * 5 + 1) * 32;
-constexpr uint32_t O_COL = NQT * 2 * HK;
+constexpr uint32_t S_COLS = KT;            // S columns per query tile (P packed into half)
+constexpr uint32_t O_COL = NQT * S_COLS;   // O accumulators after the S buffers
 constexpr uint32_t TMEM_COLS = 256;
+static_assert(O_COL + NQT * 16 <= TMEM_COLS, "TMEM budget");
 constexpr float F16_LIMIT = 14.f;
 constexpr float BOUND_LIMIT = 60.f;
 constexpr float RANGE_LIMIT = 60000.f;
-constexpr int DEFAULT_POLY_PAIRS = 4;
-constexpr int DEFAULT_S64 = 1;
-constexpr int DEFAULT_ALT = 0;
-constexpr int DEFAULT_LP = 1;  // |k|, |v| that still round to a finite fp16
 
 struct Smem {
   uint16_t q[NQT][QT * 16];
   uint16_t kv[NS][2][KT * 16];
+  float osum[NQT][16][QT];   // sum of the drained O groups, [tile][column][row]
   uint64_t kv_full[NS], kv_empty[NS];
-  uint64_t s_full[NQT][2], p_full[NQT][2], o_done[NQT];
+  uint64_t s_full[NQT], p_full[NQT], o_done[NQT];
   uint32_t tmem_base;
+  int32_t fallback;
 };
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -79,540 +95,73 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
-
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+// 16 S columns -> 8 packed fp16x2 P columns; pairs at odd positions first on the
+// polynomial so MUFU and FMA work interleave
+__device__ __forceinline__ void softmax16(const uint32_t* r, uint32_t* pk) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
+    const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+    pk[i] = poly ? exp2_poly_f16x2_lp(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
+  }
 }
-__device__ __forceinline__ void named_bar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 
-// NP of every 8 exponential pairs go to the FMA-pipe polynomial (exp2_poly_f16x2), the
-// rest to MUFU.EX2: the MUFU (16 ex2/clk/SM) binds the all-MUFU kernel while the FMA
-// pipe idles, so splitting the work raises the exp rate (scripts/exp_probe.cu).
-// S64: one N=64 S MMA per 64-key tile into a single TMEM buffer per query tile (5 MMAs
-// per tile instead of 6; the next S waits for this tile's PV), instead of two N=32
-// halves double-buffered.  Same TMEM footprint (64 S columns + 16 O columns per tile).
-__device__ int g_attn_debug = 0;
-
-template <int NP, bool S64, bool LP = false, bool DEG2 = false>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     attn_f16_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
                     const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
                     const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
-                    int d_head, const int32_t* __restrict__ flag) {
-  if (*flag) return;  // some row needs the tf32 or the online kernel
+                    int d_head, int32_t* __restrict__ flag, int32_t* __restrict__ wflag) {
+  if (*flag & 3) return;  // the whole launch goes to the tf32 or the online kernel
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TcWork w = works[blockIdx.x];
   const int head = blockIdx.y;
   const int T = w.tiles;
-  const int U = 2 * T;
   const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
   const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
-  if (warp == PRODUCER_WARP && lane == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&sm.kv_full[s], 1);
-      mbar_init(&sm.kv_empty[s], NQT);
-    }
-    for (int t = 0; t < NQT; ++t) {
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&sm.s_full[t][b], 1);
-        mbar_init(&sm.p_full[t][b], 128);
-      }
-      mbar_init(&sm.o_done[t], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == MMA_WARP0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  // Q: per query tile, K-major canonical (two 8-half K chunks of 8-row core matrices)
+  if (threadIdx.x == 0) sm.fallback = 0;
+  __syncthreads();
+  // Q: per query tile, K-major canonical (two 8-half K chunks of 8-row core matrices);
+  // the chunk holding column 15 carries the NaN fallback marker
+  bool marked = false;
   for (int i = threadIdx.x; i < NQT * QT * 2; i += NUM_THREADS) {
     const int qt = i / (QT * 2), rem = i % (QT * 2);
     const int r = rem >> 1, c = rem & 1;
     const int lr = w.q0 + qt * QT + r;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (lr < w.n)
-      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
-    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
-  }
-  fence_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tbase = sm.tmem_base;
-
-  if (warp == PRODUCER_WARP) {
-    if (lane == 0) {
-      for (int j = 0; j < T; ++j) {
-        const int s = j % NS;
-        if (j >= NS) mbar_wait_sleep(&sm.kv_empty[s], ((j / NS) - 1) & 1);
-        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
-        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
-        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= MMA_WARP0 && S64) {
-    if (lane == 0) {
-      const int t = warp - MMA_WARP0;
-      constexpr uint32_t ID_S = idesc_f16(QT, KT);
-      constexpr uint32_t ID_O = idesc_f16(QT, 16);
-      const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
-      const uint32_t sd = tbase + t * 2 * HK;  // 64 S columns; P packed into the first 32
-      auto issue_s = [&](int j) {
-        const int s = j % NS;
-        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
-        fence_after();
-        umma_ss_f16(sd, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
-        umma_commit(&sm.s_full[t][0]);
-      };
-      if (T > 0) issue_s(0);
-      for (int j = 0; j < T; ++j) {
-        const int s = j % NS;
-        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
-        mbar_wait_sleep(&sm.p_full[t][0], j & 1);
-        fence_after();
-        const uint32_t d = tbase + O_COL + t * 16;
-        if (g_attn_debug != 3) {
-#pragma unroll
-          for (int kk = 0; kk < KT / 16; ++kk)
-            umma_ts_f16(d, sd + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
-        }
-        if (j + 1 < T) issue_s(j + 1);  // in-order after the PV that reads P
-        umma_commit(&sm.kv_empty[s]);
-      }
-      umma_commit(&sm.o_done[t]);
-    }
-    __syncwarp();
-  } else if (warp >= MMA_WARP0) {
-    if (lane == 0) {
-      const int t = warp - MMA_WARP0;
-      constexpr uint32_t ID_S = idesc_f16(QT, HK);
-      constexpr uint32_t ID_O = idesc_f16(QT, 16);
-      const uint32_t qaddr = smem_u32(sm.q[t]);
-      auto wait_kv = [&](int u) {
-        if ((u & 1) == 0) {
-          const int j = u >> 1;
-          mbar_wait(&sm.kv_full[j % NS], (j / NS) & 1);
-          fence_after();
-        }
-      };
-      // S(u): keys [32h, 32h + 32) of tile j = u / 2 (K chunk stride 1 KB, 8-key
-      // groups 128 B apart, so the second half starts 4 groups = 512 B in)
-      auto issue_s = [&](int u) {
-        const int j = u >> 1, h = u & 1, s = j % NS, b = u & 1;
-        const uint32_t kaddr = smem_u32(sm.kv[s][0]) + h * 512;
-        umma_ss_f16(tbase + t * 2 * HK + b * HK, sdesc(qaddr, QT * 16, 128),
-                    sdesc(kaddr, KT * 16, 128), ID_S, 0);
-        umma_commit(&sm.s_full[t][b]);
-      };
-      for (int u = 0; u < 2 && u < U; ++u) {
-        wait_kv(u);
-        issue_s(u);
-      }
-      for (int u = 0; u < U; ++u) {
-        const int j = u >> 1, h = u & 1, s = j % NS, b = u & 1;
-        const bool more = u + 2 < U;
-        // V^T: 8-key chunks of 256 B (16 d rows x 16 B); second half 4 chunks in
-        const uint32_t vaddr = smem_u32(sm.kv[s][1]) + h * 1024;
-        mbar_wait(&sm.p_full[t][b], (u >> 1) & 1);
-        fence_after();
-        const uint32_t d = tbase + O_COL + t * 16;
-        const uint32_t a = tbase + t * 2 * HK + b * HK;  // P: 16 packed columns
-#pragma unroll
-        for (int kk = 0; kk < HK / 16; ++kk)
-          umma_ts_f16(d, a + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (u > 0 || kk > 0));
-        if (more) {
-          wait_kv(u + 2);
-          issue_s(u + 2);
-        }
-        if (h == 1) umma_commit(&sm.kv_empty[s]);
-      }
-      umma_commit(&sm.o_done[t]);
-    }
-    __syncwarp();
-  } else {
-    // softmax: thread = query row; 16-column chunks, the next chunk's tcgen05.ld in
-    // flight while this chunk's ex2s issue; P (fp16x2) overwrites the consumed S columns
-    const int t = warp >> 2;
-    const int wq = warp & 3;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t base = tbase + lane_off + t * 2 * HK;
-    auto s_addr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 16; };
-    auto p_addr = [&](int c) { return base + ((c >> 1) & 1) * HK + (c & 1) * 8; };
-    auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        // interleave: polynomial pairs at odd positions first, so MUFU and FMA work mix
-        const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
-        const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-        pk[i] = poly ? (DEG2 ? exp2_poly_f16x2_lp2(x0, x1)
-                             : LP ? exp2_poly_f16x2_lp(x0, x1) : exp2_poly_f16x2(x0, x1))
-                     : pack_f16x2(ex2f(x0), ex2f(x1));
-      }
-    };
-    uint32_t ra[16], rb[16], pk[8];
-    if constexpr (S64) {
-      // 64 S columns in 4 chunks of 16; chunk c's P (8 packed columns) lands on
-      // columns [8c, 8c + 8), all inside chunks already consumed
-      const int dbg = g_attn_debug;  // timing experiments only (GO_ATTN_DEBUG)
-      if (dbg == 1 || dbg == 2) {
-        for (int j = 0; j < T; ++j) {
-          mbar_wait_sleep(&sm.s_full[t][0], j & 1);
-          fence_after();
-          if (dbg == 1) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              PTX_LD16(base + 16 * c, ra);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 8; ++i) pk[i] = ra[2 * i] ^ ra[2 * i + 1];
-              PTX_ST8(base + 8 * c, pk);
-            }
-            tmem_wait_st();
-          }
-          fence_before();
-          mbar_arrive(&sm.p_full[t][0]);
-        }
-      } else
-      for (int j = 0; j < T; ++j) {
-          mbar_wait_sleep(&sm.s_full[t][0], j & 1);
-          fence_after();
-          PTX_LD16_AT(base, 0, ra);
-          tmem_wait_ld();
-          PTX_LD16_AT(base, 16, rb);
-          softmax16(ra, pk);
-          PTX_ST8_AT(base, 0, pk);
-          tmem_wait_ld();
-          PTX_LD16_AT(base, 32, ra);
-          softmax16(rb, pk);
-          PTX_ST8_AT(base, 8, pk);
-          tmem_wait_ld();
-          PTX_LD16_AT(base, 48, rb);
-          softmax16(ra, pk);
-          PTX_ST8_AT(base, 16, pk);
-          tmem_wait_ld();
-          softmax16(rb, pk);
-          PTX_ST8_AT(base, 24, pk);
-          tmem_wait_st();
-          fence_before();
-          mbar_arrive(&sm.p_full[t][0]);
-        }
-    } else {
-    uint32_t ra[16], rb[16], pk[8];
-      if (U > 0) {
-        mbar_wait(&sm.s_full[t][0], 0);
-        fence_after();
-        PTX_LD16(s_addr(0), ra);
-        tmem_wait_ld();
-      }
-      for (int u = 0; u < U; ++u) {
-        const int c = 2 * u;
-        PTX_LD16(s_addr(c + 1), rb);
-        softmax16(ra, pk);
-        PTX_ST8(p_addr(c), pk);
-        tmem_wait_ld();
-        const bool more = u + 1 < U;
-        if (more) {
-          mbar_wait(&sm.s_full[t][(u + 1) & 1], ((u + 1) >> 1) & 1);
-          fence_after();
-          PTX_LD16(s_addr(c + 2), ra);
-        }
-        softmax16(rb, pk);
-        PTX_ST8(p_addr(c + 1), pk);
-        tmem_wait_st();
-        fence_before();
-        mbar_arrive(&sm.p_full[t][u & 1]);
-        if (more) tmem_wait_ld();
-      }
-    }
-    mbar_wait_sleep(&sm.o_done[t], 0);
-    fence_after();
-    uint32_t r[16];
-    PTX_LD16(tbase + lane_off + O_COL + t * 16, r);
-    tmem_wait_ld();
-    const int lr = w.q0 + t * QT + wq * 32 + lane;
     if (lr < w.n) {
-      const float inv = 1.f / __uint_as_float(r[15]);
-      float* o = out + (w.row0 + lr) * ldo + head * d_head;
-      for (int d = 0; d < d_head; ++d) o[d] = __uint_as_float(r[d]) * inv;
+      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
+      marked |= c == 1 && ((v.w >> 16) & 0x7FFFu) > 0x7C00u;  // column 15 is NaN
     }
+    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
   }
-  fence_before();
+  if (marked) sm.fallback = 1;
   __syncthreads();
-  fence_after();
-  if (warp == MMA_WARP0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
-                 "r"(TMEM_COLS));
+  if (sm.fallback) {
+    if (threadIdx.x == 0) {
+      wflag[(int64_t)head * gridDim.x + blockIdx.x] = 1;
+      atomicOr(flag, 4);
+    }
+    return;
   }
-}
-
-// ---------------------------------------------------------------------------------------
-// Double-buffered variant (GO_ATTN16=db): one CTA per SM owning all 512 TMEM columns,
-// 3 query tiles x (2 x 64 S columns) + 3 x 16 O columns.  S(j+2) is computed into the
-// buffer of step j right after PV(j), while the softmax warps work on step j+1, so the
-// softmax warps never wait for an S MMA in steady state (fewer warps per SM, though).
-// SPLIT = 2: two softmax warps per (tile, TMEM lane quarter), each owning 32 of the 64
-// columns of a step, so the SM keeps 24 softmax warps (6 per SMSP) with no S waits.
-template <int SPLIT>
-struct DbCfg {
-  static constexpr int SOFT = NQT * 4 * SPLIT;
-  static constexpr int PRODUCER = SOFT;
-  static constexpr int MMA0 = SOFT + 1;
-  static constexpr int THREADS = (SOFT + 1 + NQT) * 32;
-};
-template <int NP, int SPLIT>
-__global__ void __launch_bounds__(DbCfg<SPLIT>::THREADS, 1)
-    attn_f16_db_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
-                       const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
-                       const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
-                       int d_head, const int32_t* __restrict__ flag) {
-  constexpr uint32_t DB_COLS = 512;
-  constexpr uint32_t DB_O = NQT * 128;
-  using C = DbCfg<SPLIT>;
-  constexpr int PRODUCER_WARP = C::PRODUCER, MMA_WARP0 = C::MMA0, NUM_THREADS = C::THREADS;
-  if (*flag) return;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TcWork w = works[blockIdx.x];
-  const int head = blockIdx.y;
-  const int T = w.tiles;
-  const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
-  const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
   if (warp == PRODUCER_WARP && lane == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], NQT);
     }
     for (int t = 0; t < NQT; ++t) {
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&sm.s_full[t][b], 1);
-        mbar_init(&sm.p_full[t][b], 128 * SPLIT);
-      }
-      mbar_init(&sm.o_done[t], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == MMA_WARP0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "r"(DB_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  for (int i = threadIdx.x; i < NQT * QT * 2; i += NUM_THREADS) {
-    const int qt = i / (QT * 2), rem = i % (QT * 2);
-    const int r = rem >> 1, c = rem & 1;
-    const int lr = w.q0 + qt * QT + r;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (lr < w.n)
-      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
-    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
-  }
-  fence_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tbase = sm.tmem_base;
-
-  if (warp == PRODUCER_WARP) {
-    if (lane == 0) {
-      for (int j = 0; j < T; ++j) {
-        const int s = j % NS;
-        if (j >= NS) mbar_wait_sleep(&sm.kv_empty[s], ((j / NS) - 1) & 1);
-        mbar_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
-        bulk_g2s(sm.kv[s][0], kbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
-        bulk_g2s(sm.kv[s][1], vbase + (int64_t)j * (KT * 16), TILE_BYTES, &sm.kv_full[s]);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= MMA_WARP0) {
-    if (lane == 0) {
-      const int t = warp - MMA_WARP0;
-      constexpr uint32_t ID_S = idesc_f16(QT, KT);
-      constexpr uint32_t ID_O = idesc_f16(QT, 16);
-      const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
-      const uint32_t reg = tbase + t * 128;
-      const uint32_t d = tbase + DB_O + t * 16;
-      auto issue_s = [&](int j) {
-        const int s = j % NS;
-        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
-        fence_after();
-        umma_ss_f16(reg + (j & 1) * 64, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
-        umma_commit(&sm.s_full[t][j & 1]);
-      };
-      for (int j = 0; j < 2 && j < T; ++j) issue_s(j);
-      for (int j = 0; j < T; ++j) {
-        const int s = j % NS;
-        mbar_wait_sleep(&sm.p_full[t][j & 1], (j >> 1) & 1);
-        fence_after();
-        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
-        const uint32_t pa = reg + (j & 1) * 64;
-#pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk)
-          umma_ts_f16(d, pa + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (j > 0 || kk > 0));
-        if (j + 2 < T) issue_s(j + 2);  // same buffer, in-order after the PV reading P(j)
-        umma_commit(&sm.kv_empty[s]);
-      }
-      umma_commit(&sm.o_done[t]);
-    }
-    __syncwarp();
-  } else {
-    const int t = warp / (4 * SPLIT);
-    const int wq = warp & 3;
-    const int half = SPLIT == 2 ? (warp >> 2) & 1 : 0;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
-        const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-        pk[i] = poly ? exp2_poly_f16x2_lp(x0, x1) : pack_f16x2(ex2f(x0), ex2f(x1));
-      }
-    };
-    uint32_t ra[16], rb[16], pk[8];
-    for (int j = 0; j < T; ++j) {
-      const uint32_t base = tbase + lane_off + t * 128 + (j & 1) * 64;
-      mbar_wait_sleep(&sm.s_full[t][j & 1], (j >> 1) & 1);
-      fence_after();
-      if constexpr (SPLIT == 2) {
-        // chunks 2*half, 2*half + 1; P of chunk c lands on columns [8c, 8c + 8), which
-        // for half 1 (c = 2, 3 -> columns 16..31) lie in half 0's S chunk 1: wait for
-        // half 0 to have read it (it reads both its chunks before its first P store)
-        const uint32_t sb = base + 32 * half;
-        PTX_LD16(sb, ra);
-        PTX_LD16(sb + 16, rb);
-        tmem_wait_ld();
-        if (half == 1) named_bar_sync(1 + t * 4 + wq, 64);
-        else named_bar_arrive(1 + t * 4 + wq, 64);
-        softmax16(ra, pk);
-        PTX_ST8(base + 16 * half, pk);
-        softmax16(rb, pk);
-        PTX_ST8(base + 16 * half + 8, pk);
-      } else {
-        PTX_LD16(base, ra);
-        tmem_wait_ld();
-        PTX_LD16(base + 16, rb);
-        softmax16(ra, pk);
-        PTX_ST8(base, pk);
-        tmem_wait_ld();
-        PTX_LD16(base + 32, ra);
-        softmax16(rb, pk);
-        PTX_ST8(base + 8, pk);
-        tmem_wait_ld();
-        PTX_LD16(base + 48, rb);
-        softmax16(ra, pk);
-        PTX_ST8(base + 16, pk);
-        tmem_wait_ld();
-        softmax16(rb, pk);
-        PTX_ST8(base + 24, pk);
-      }
-      tmem_wait_st();
-      fence_before();
-      mbar_arrive(&sm.p_full[t][j & 1]);
-    }
-    mbar_wait_sleep(&sm.o_done[t], 0);
-    fence_after();
-    uint32_t r[16];
-    PTX_LD16(tbase + lane_off + DB_O + t * 16, r);
-    tmem_wait_ld();
-    const int lr = w.q0 + t * QT + wq * 32 + lane;
-    if (lr < w.n && half == 0) {
-      const float inv = 1.f / __uint_as_float(r[15]);
-      float* o = out + (w.row0 + lr) * ldo + head * d_head;
-      for (int dd = 0; dd < d_head; ++dd) o[dd] = __uint_as_float(r[dd]) * inv;
-    }
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == MMA_WARP0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
-                 "r"(DB_COLS));
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// Alternating-window variant (GO_ATTN16=alt): S(u+1) is issued BEFORE PV(u), so a query
-// tile's softmax waits only for one S MMA, not for the PV MMAs in front of it.  With KS
-// keys per step, per query tile 1.5 KS S/P columns + 16 O columns:
-//   even u: S in [0, KS),      P packed into [0, KS/2)    (chunks read ascending)
-//   odd  u: S in [KS/2, 3KS/2), P packed into [KS, 3KS/2) (chunks read descending, so
-//           every P chunk lands on S columns already consumed)
-// S(u+1) never touches P(u); it overwrites P(u-1), whose PV was issued before it by the
-// same thread (tcgen05 MMAs from one thread execute in order).
-//   <NQ=2, KS=64>: 256 queries per CTA, 224 TMEM columns (works2 table)
-//   <NQ=3, KS=32>: 384 queries per CTA, 192 TMEM columns (works table)
-template <int NQ, int KS>
-struct AltCfg {
-  static constexpr int SOFT_WARPS = NQ * 4;
-  static constexpr int PRODUCER = SOFT_WARPS;
-  static constexpr int MMA0 = SOFT_WARPS + 1;
-  static constexpr int THREADS = (SOFT_WARPS + 1 + NQ) * 32;
-  static constexpr uint32_t REGION = KS + KS / 2;
-  static constexpr uint32_t O_COL = NQ * REGION;
-  static constexpr uint32_t TMEM_COLS = 256;
-  static constexpr int STEPS = KT / KS;  // S steps per K/V tile
-  static_assert(O_COL + NQ * 16 <= TMEM_COLS, "TMEM budget");
-  struct Smem {
-    uint16_t q[NQ][QT * 16];
-    uint16_t kv[NS][2][KT * 16];
-    uint64_t kv_full[NS], kv_empty[NS];
-    uint64_t s_full[NQ], p_full[NQ], o_done[NQ];
-    uint32_t tmem_base;
-  };
-};
-
-template <int NP, bool LP, int NQ, int KS>
-__global__ void __launch_bounds__(AltCfg<NQ, KS>::THREADS, 2)
-    attn_f16_alt_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ kb,
-                        const uint16_t* __restrict__ vb, int64_t R, int64_t Ttot,
-                        const TcWork* __restrict__ works, float* __restrict__ out, int64_t ldo,
-                        int d_head, const int32_t* __restrict__ flag) {
-  using C = AltCfg<NQ, KS>;
-  constexpr int NCH = KS / 16;  // 16-column chunks per step
-  if (*flag) return;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  typename C::Smem& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TcWork w = works[blockIdx.x];
-  const int head = blockIdx.y;
-  const int T = w.tiles;
-  const int U = T * C::STEPS;
-  const uint16_t* kbase = kb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
-  const uint16_t* vbase = vb + ((int64_t)head * Ttot + w.tile0) * (KT * 16);
-  if (warp == C::PRODUCER && lane == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&sm.kv_full[s], 1);
-      mbar_init(&sm.kv_empty[s], NQ);
-    }
-    for (int t = 0; t < NQ; ++t) {
       mbar_init(&sm.s_full[t], 1);
       mbar_init(&sm.p_full[t], 128);
       mbar_init(&sm.o_done[t], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == C::MMA0) {
+  if (warp == MMA_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
-                 "r"(C::TMEM_COLS));
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  for (int i = threadIdx.x; i < NQ * QT * 2; i += C::THREADS) {
-    const int qt = i / (QT * 2), rem = i % (QT * 2);
-    const int r = rem >> 1, c = rem & 1;
-    const int lr = w.q0 + qt * QT + r;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (lr < w.n)
-      v = *reinterpret_cast<const uint4*>(qh + ((int64_t)head * R + w.row0 + lr) * 16 + c * 8);
-    *reinterpret_cast<uint4*>(&sm.q[qt][c * (QT * 8) + (r >> 3) * 64 + (r & 7) * 8]) = v;
   }
   fence_async_smem();
   fence_before();
@@ -620,7 +169,7 @@ __global__ void __launch_bounds__(AltCfg<NQ, KS>::THREADS, 2)
   fence_after();
   const uint32_t tbase = sm.tmem_base;
 
-  if (warp == C::PRODUCER) {
+  if (warp == PRODUCER_WARP) {
     if (lane == 0) {
       for (int j = 0; j < T; ++j) {
         const int s = j % NS;
@@ -631,100 +180,99 @@ __global__ void __launch_bounds__(AltCfg<NQ, KS>::THREADS, 2)
       }
     }
     __syncwarp();
-  } else if (warp >= C::MMA0) {
+  } else if (warp >= MMA_WARP0) {
     if (lane == 0) {
-      const int t = warp - C::MMA0;
-      constexpr uint32_t ID_S = idesc_f16(QT, KS);
+      const int t = warp - MMA_WARP0;
+      constexpr uint32_t ID_S = idesc_f16(QT, KT);
       constexpr uint32_t ID_O = idesc_f16(QT, 16);
       const uint64_t qd = sdesc(smem_u32(sm.q[t]), QT * 16, 128);
-      const uint32_t reg = tbase + t * C::REGION;
-      const uint32_t d = tbase + C::O_COL + t * 16;
-      // step u: K/V tile j = u / STEPS, key half h = u % STEPS (8-key groups are 128 B
-      // apart in K, 256 B in V^T)
-      auto issue_s = [&](int u) {
-        const int j = u / C::STEPS, h = u % C::STEPS, s = j % NS;
-        if (h == 0) {
-          mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
-          fence_after();
-        }
-        umma_ss_f16(reg + (u & 1) * (KS / 2), qd,
-                    sdesc(smem_u32(sm.kv[s][0]) + h * (KS / 8) * 128, KT * 16, 128), ID_S, 0);
+      const uint32_t sd = tbase + t * S_COLS;
+      const uint32_t od = tbase + O_COL + t * 16;
+      auto issue_s = [&](int j) {
+        const int s = j % NS;
+        mbar_wait_sleep(&sm.kv_full[s], (j / NS) & 1);
+        fence_after();
+        umma_ss_f16(sd, qd, sdesc(smem_u32(sm.kv[s][0]), KT * 16, 128), ID_S, 0);
         umma_commit(&sm.s_full[t]);
       };
-      if (U > 0) issue_s(0);
-      for (int u = 0; u < U; ++u) {
-        const int j = u / C::STEPS, h = u % C::STEPS, s = j % NS;
-        mbar_wait_sleep(&sm.p_full[t], u & 1);
+      if (T > 0) issue_s(0);
+      for (int j = 0; j < T; ++j) {
+        const int s = j % NS;
+        const uint32_t vaddr = smem_u32(sm.kv[s][1]);
+        mbar_wait_sleep(&sm.p_full[t], j & 1);
         fence_after();
-        if (u + 1 < U) issue_s(u + 1);
-        const uint32_t vaddr = smem_u32(sm.kv[s][1]) + h * (KS / 8) * 256;
-        const uint32_t pa = reg + (u & 1) * KS;
 #pragma unroll
-        for (int kk = 0; kk < KS / 16; ++kk)
-          umma_ts_f16(d, pa + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O, (u > 0 || kk > 0));
-        if (h == C::STEPS - 1) umma_commit(&sm.kv_empty[s]);
+        for (int kk = 0; kk < KT / 16; ++kk)  // a new accumulation group restarts O
+          umma_ts_f16(od, sd + kk * 8, sdesc(vaddr + kk * 512, 256, 128), ID_O,
+                      (j % DRAIN != 0 || kk > 0));
+        if (j + 1 < T) issue_s(j + 1);  // in order after the PV that reads P
+        umma_commit(&sm.kv_empty[s]);
       }
       umma_commit(&sm.o_done[t]);
     }
     __syncwarp();
   } else {
+    // softmax: thread = query row.  64 S columns in 4 chunks of 16, the next chunk's
+    // tcgen05.ld in flight while this chunk's exponentials issue; chunk c's P (8 packed
+    // columns) lands on columns [8c, 8c + 8), all inside chunks already consumed.
     const int t = warp >> 2;
-    const int wq = warp & 3;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t reg = tbase + lane_off + t * C::REGION;
-    auto softmax16 = [&](const uint32_t* r, uint32_t* pk) {
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t base = tbase + lane_off + t * S_COLS;
+    const uint32_t obase = tbase + lane_off + O_COL + t * 16;
+    float* osum = &sm.osum[t][0][row];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const bool poly = (i & 1) ? ((i >> 1) < NP) : ((4 + (i >> 1)) < NP);
-        const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-        pk[i] = poly ? (LP ? exp2_poly_f16x2_lp(x0, x1) : exp2_poly_f16x2(x0, x1))
-                     : pack_f16x2(ex2f(x0), ex2f(x1));
+    for (int d = 0; d < 16; ++d) osum[d * QT] = 0.f;
+    auto drain = [&]() {  // O of the group just finished -> float sum in smem
+      uint32_t r[16];
+      PTX_LD16(obase, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        osum[d * QT] += __uint_as_float(r[d]);
       }
     };
     uint32_t ra[16], rb[16], pk[8];
-    for (int u = 0; u < U; ++u) {
-      const bool odd = u & 1;
-      const uint32_t win = reg + (odd ? KS / 2 : 0);
-      const uint32_t pb = reg + (odd ? KS : 0);
-      const int c0 = odd ? NCH - 1 : 0, dc = odd ? -1 : 1;
-      mbar_wait_sleep(&sm.s_full[t], u & 1);
+    for (int j = 0; j < T; ++j) {
+      mbar_wait_sleep(&sm.s_full[t], j & 1);
       fence_after();
-      PTX_LD16(win + 16 * c0, ra);
+      if (j > 0 && j % DRAIN == 0) drain();  // O = tiles [j - DRAIN, j), stable here
+      PTX_LD16_AT(base, 0, ra);
       tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < NCH; i += 2) {
-        const int ca = c0 + i * dc, cb = ca + dc;
-        PTX_LD16(win + 16 * cb, rb);
-        softmax16(ra, pk);
-        PTX_ST8(pb + 8 * ca, pk);
-        tmem_wait_ld();
-        if (i + 2 < NCH) PTX_LD16(win + 16 * (cb + dc), ra);
-        softmax16(rb, pk);
-        PTX_ST8(pb + 8 * cb, pk);
-        if (i + 2 < NCH) tmem_wait_ld();
-      }
+      PTX_LD16_AT(base, 16, rb);
+      softmax16(ra, pk);
+      PTX_ST8_AT(base, 0, pk);
+      tmem_wait_ld();
+      PTX_LD16_AT(base, 32, ra);
+      softmax16(rb, pk);
+      PTX_ST8_AT(base, 8, pk);
+      tmem_wait_ld();
+      PTX_LD16_AT(base, 48, rb);
+      softmax16(ra, pk);
+      PTX_ST8_AT(base, 16, pk);
+      tmem_wait_ld();
+      softmax16(rb, pk);
+      PTX_ST8_AT(base, 24, pk);
       tmem_wait_st();
       fence_before();
       mbar_arrive(&sm.p_full[t]);
     }
     mbar_wait_sleep(&sm.o_done[t], 0);
     fence_after();
-    uint32_t r[16];
-    PTX_LD16(tbase + lane_off + C::O_COL + t * 16, r);
-    tmem_wait_ld();
-    const int lr = w.q0 + t * QT + wq * 32 + lane;
+    if (T > 0) drain();
+    const int lr = w.q0 + t * QT + row;
     if (lr < w.n) {
-      const float inv = 1.f / __uint_as_float(r[15]);
+      const float inv = 1.f / osum[15 * QT];
       float* o = out + (w.row0 + lr) * ldo + head * d_head;
-      for (int dd = 0; dd < d_head; ++dd) o[dd] = __uint_as_float(r[dd]) * inv;
+      for (int d = 0; d < d_head; ++d) o[d] = osum[d * QT] * inv;
     }
   }
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == C::MMA0) {
+  if (warp == MMA_WARP0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
-                 "r"(C::TMEM_COLS));
+                 "r"(TMEM_COLS));
   }
 }
 
@@ -802,8 +350,10 @@ __global__ void repack_kv16_kernel(const float* __restrict__ k, const float* __r
   if (big) atomicOr(flag, 2);
 }
 
-// Q in fp16, scaled by log2(e)/sqrt(d_head); column 15 = 15 - b_i.  Flags: 1 = some
-// bound > BOUND_LIMIT (online kernel), 2 = some bound > F16_LIMIT (tf32 kernel).
+// Q in fp16, scaled by log2(e)/sqrt(d_head); column 15 = 15 - b_i, or NaN when b_i >
+// F16_LIMIT (the fp16 kernel hands that row's work item to the tf32 kernel).  Flag bits:
+// 1 = some bound > BOUND_LIMIT (online kernel for the launch), 2 = |q| outside the fp16
+// range (tf32 kernel for the launch).
 __global__ void repack_q16_kernel(const float* __restrict__ q, int64_t ld, int n_head, int d_head,
                                   int64_t R, const int32_t* __restrict__ row_fwd,
                                   const unsigned* __restrict__ kmax, float qscale,
@@ -828,8 +378,8 @@ __global__ void repack_q16_kernel(const float* __restrict__ q, int64_t ld, int n
   const float km = __uint_as_float(kmax[row_fwd[r] * n_head + head]);
   const float bnd = sqrtf(nq) * km * (1.f + 1.f / 256.f) + 1.f / 256.f;
   if (!(bnd <= BOUND_LIMIT)) atomicOr(flag, 1);
-  else if (bnd > F16_LIMIT || big) atomicOr(flag, 2);
-  qv[15] = __float2half_rn(15.f - bnd);
+  else if (big) atomicOr(flag, 2);
+  qv[15] = bnd > F16_LIMIT ? __ushort_as_half((unsigned short)0x7E00u) : __float2half_rn(15.f - bnd);
   uint4* o = reinterpret_cast<uint4*>(qh + ((int64_t)head * R + r) * 16);
   o[0] = reinterpret_cast<const uint4*>(qv)[0];
   o[1] = reinterpret_cast<const uint4*>(qv)[1];
@@ -841,78 +391,14 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                       int d_head, int64_t R, int64_t Ttot, const TcWork* works_dev,
                       int64_t num_works, const int64_t* tile_row0_dev, const int32_t* tile_n_dev,
                       void* qh, void* kb, void* vb, float* out, int64_t ldo,
-                      const int32_t* row_fwd, unsigned* kmax, int32_t* flag, float qscale,
-                      const TcWork* works2_dev, int64_t num_works2, cudaStream_t st) {
-  using Fn = void (*)(const uint16_t*, const uint16_t*, const uint16_t*, int64_t, int64_t,
-                     const TcWork*, float*, int64_t, int, const int32_t*);
-  static const Fn kernels[2][5] = {
-      {t16::attn_f16_kernel<0, false>, t16::attn_f16_kernel<1, false>,
-       t16::attn_f16_kernel<2, false>, t16::attn_f16_kernel<3, false>,
-       t16::attn_f16_kernel<4, false>},
-      {t16::attn_f16_kernel<0, true>, t16::attn_f16_kernel<1, true>,
-       t16::attn_f16_kernel<2, true>, t16::attn_f16_kernel<3, true>,
-       t16::attn_f16_kernel<4, true>}};
-  // GO_ATTN16=alt (2 tiles x 64-key steps) / alt32 (3 tiles x 32-key steps)
-  static const Fn alt64[7] = {
-      t16::attn_f16_alt_kernel<0, true, 2, 64>, t16::attn_f16_alt_kernel<1, true, 2, 64>,
-      t16::attn_f16_alt_kernel<2, true, 2, 64>, t16::attn_f16_alt_kernel<3, true, 2, 64>,
-      t16::attn_f16_alt_kernel<4, true, 2, 64>, t16::attn_f16_alt_kernel<5, true, 2, 64>,
-      t16::attn_f16_alt_kernel<6, true, 2, 64>};
-  static const Fn alt32[7] = {
-      t16::attn_f16_alt_kernel<0, true, 3, 32>, t16::attn_f16_alt_kernel<1, true, 3, 32>,
-      t16::attn_f16_alt_kernel<2, true, 3, 32>, t16::attn_f16_alt_kernel<3, true, 3, 32>,
-      t16::attn_f16_alt_kernel<4, true, 3, 32>, t16::attn_f16_alt_kernel<5, true, 3, 32>,
-      t16::attn_f16_alt_kernel<6, true, 3, 32>};
-  static const Fn lp_kernels[7] = {
-      t16::attn_f16_kernel<0, true, true>, t16::attn_f16_kernel<1, true, true>,
-      t16::attn_f16_kernel<2, true, true>, t16::attn_f16_kernel<3, true, true>,
-      t16::attn_f16_kernel<4, true, true>, t16::attn_f16_kernel<5, true, true>,
-      t16::attn_f16_kernel<6, true, true>};
-  static const Fn dbk[2][7] = {
-      {t16::attn_f16_db_kernel<0, 1>, t16::attn_f16_db_kernel<1, 1>, t16::attn_f16_db_kernel<2, 1>,
-       t16::attn_f16_db_kernel<3, 1>, t16::attn_f16_db_kernel<4, 1>, t16::attn_f16_db_kernel<5, 1>,
-       t16::attn_f16_db_kernel<6, 1>},
-      {t16::attn_f16_db_kernel<0, 2>, t16::attn_f16_db_kernel<1, 2>, t16::attn_f16_db_kernel<2, 2>,
-       t16::attn_f16_db_kernel<3, 2>, t16::attn_f16_db_kernel<4, 2>, t16::attn_f16_db_kernel<5, 2>,
-       t16::attn_f16_db_kernel<6, 2>}};
-  static const Fn lp2_kernels[7] = {
-      t16::attn_f16_kernel<0, true, true, true>, t16::attn_f16_kernel<1, true, true, true>,
-      t16::attn_f16_kernel<2, true, true, true>, t16::attn_f16_kernel<3, true, true, true>,
-      t16::attn_f16_kernel<4, true, true, true>, t16::attn_f16_kernel<5, true, true, true>,
-      t16::attn_f16_kernel<6, true, true, true>};
-  static int np = -1, s64 = 0, use_alt = 0, lp = 0;
+                      const int32_t* row_fwd, unsigned* kmax, int32_t* flag, int32_t* wflag,
+                      float qscale, cudaStream_t st) {
+  static bool attr = false;
   const size_t smem = sizeof(t16::Smem) + 1024;
-  const size_t smem64 = sizeof(t16::AltCfg<2, 64>::Smem) + 1024;
-  const size_t smem32 = sizeof(t16::AltCfg<3, 32>::Smem) + 1024;
-  if (np < 0) {
-    const char* e = getenv("GO_POLY16");
-    np = e ? std::min(6, std::max(0, atoi(e))) : t16::DEFAULT_POLY_PAIRS;
-    const char* e64 = getenv("GO_S64");
-    s64 = e64 ? (atoi(e64) != 0) : t16::DEFAULT_S64;
-    const char* ea = getenv("GO_ATTN16");
-    use_alt = ea ? (!strcmp(ea, "alt") ? 1 : !strcmp(ea, "alt32") ? 2 : !strcmp(ea, "db") ? 3 : !strcmp(ea, "db2") ? 4 : 0)
-                 : t16::DEFAULT_ALT;
-    for (auto& row : dbk)
-      for (Fn f : row)
-        CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (auto& row : kernels)
-      for (Fn f : row)
-        CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const char* edbg = getenv("GO_ATTN_DEBUG");
-    if (edbg) {
-      const int v = atoi(edbg);
-      CUDA_CHECK(cudaMemcpyToSymbol(t16::g_attn_debug, &v, sizeof(int)));
-    }
-    const char* elp = getenv("GO_POLYLP");
-    lp = elp ? atoi(elp) : t16::DEFAULT_LP;  // 2: degree-2 polynomial (experiment)
-    for (Fn f : lp2_kernels)
-      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (Fn f : lp_kernels)
-      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (Fn f : alt64)
-      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
-    for (Fn f : alt32)
-      CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32));
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(t16::attn_f16_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
   }
   const int64_t total = (int64_t)n_head * Ttot * (t16::KT / 8) * 2;
   t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
@@ -922,35 +408,10 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
   t16::repack_q16_kernel<<<(unsigned)cdiv(R * n_head, 256), 256, 0, st>>>(
       q, ld, n_head, d_head, R, row_fwd, kmax, qscale, static_cast<__half*>(qh), flag);
   LAUNCH_CHECK();
-  if (use_alt == 1 && works2_dev && num_works2 > 0) {
-    dim3 grid2((unsigned)num_works2, (unsigned)n_head);
-    alt64[np]<<<grid2, t16::AltCfg<2, 64>::THREADS, smem64, st>>>(
-        static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
-        static_cast<const uint16_t*>(vb), R, Ttot, works2_dev, out, ldo, d_head, flag);
-    LAUNCH_CHECK();
-    return;
-  }
-  if (use_alt == 3 || use_alt == 4) {
-    dim3 grid4((unsigned)num_works, (unsigned)n_head);
-    const int sp = use_alt == 4;
-    dbk[sp][np]<<<grid4, sp ? t16::DbCfg<2>::THREADS : t16::DbCfg<1>::THREADS, smem, st>>>(
-        static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
-        static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
-    LAUNCH_CHECK();
-    return;
-  }
-  if (use_alt == 2) {
-    dim3 grid3((unsigned)num_works, (unsigned)n_head);
-    alt32[np]<<<grid3, t16::AltCfg<3, 32>::THREADS, smem32, st>>>(
-        static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
-        static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
-    LAUNCH_CHECK();
-    return;
-  }
   dim3 grid((unsigned)num_works, (unsigned)n_head);
-  (lp == 2 && s64 ? lp2_kernels[np] : lp && s64 ? lp_kernels[np] : kernels[s64][std::min(np, 4)])<<<grid, t16::NUM_THREADS, smem, st>>>(
+  t16::attn_f16_kernel<<<grid, t16::NUM_THREADS, smem, st>>>(
       static_cast<const uint16_t*>(qh), static_cast<const uint16_t*>(kb),
-      static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag);
+      static_cast<const uint16_t*>(vb), R, Ttot, works_dev, out, ldo, d_head, flag, wflag);
   LAUNCH_CHECK();
 }
 

@@ -25,7 +25,7 @@ from .simulator import ActionAssignment, FusedGraph, apply_fusion, simulate_many
 
 __all__ = ["Reward", "reward", "PPOHyper", "RolloutSample", "RolloutBatch", "task_action_sizes",
            "bundle_assignments", "collect_rollouts", "run_decisions", "INVALID_REWARD",
-           "ppo_update", "TrainResult", "train", "decode_step_time", "pretrain_finetune_zeroshot"]
+           "ppo_update", "train_step"]
 
 
 @dataclass(frozen=True)
@@ -257,9 +257,17 @@ def gather_results(packed, count: int, world: int):
     mx = max(sizes)
     pad = T.zeros((packed.shape[0], mx), dtype=packed.dtype, device=packed.device)
     pad[:, :packed.shape[1]] = packed
-    bufs = [T.empty_like(pad) for _ in sizes]
-    dist.all_gather(bufs, pad)
-    return T.cat([b[:, :s] for b, s in zip(bufs, sizes)], dim=1)
+    host = _host_staged(pad)
+    src = pad.cpu() if host else pad
+    bufs = [T.empty_like(src) for _ in sizes]
+    dist.all_gather(bufs, src)
+    return T.cat([b[:, :s] for b, s in zip(bufs, sizes)], dim=1).to(packed.device)
+
+
+def _host_staged(t) -> bool:
+    """gloo (the CPU test backend) takes host tensors; NCCL works on device memory."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend() != "nccl"
 
 
 def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed, hyper,
@@ -354,6 +362,7 @@ def collect_rollouts(store, graphs, topology, task_sizes, baselines, count, seed
             valid[ix] = res.valid
     batch.rewards, batch.step_times, batch.valid, batch.values = rewards, steps, valid, values
     batch.shard = (lo, hi)
+    batch.global_count = len(gi_all)
     if shard is not None and shard[1] > 1:
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized():
@@ -474,7 +483,13 @@ def allreduce_sum(grads, loss: float) -> float:
     import torch.distributed as dist
     T_ = torch()
     lt = T_.tensor([loss], dtype=T_.float64, device=grads.device)
-    dist.all_reduce(grads)
+    if _host_staged(grads):
+        g = grads.cpu()
+        dist.all_reduce(g)
+        grads.copy_(g)
+        lt = lt.cpu()
+    else:
+        dist.all_reduce(grads)
     dist.all_reduce(lt)
     return float(lt.item())
 
@@ -493,7 +508,22 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
     dev = T_.device("cuda", context().device)
     tasks = ordered_tasks(task_sizes)
     rng = np.random.default_rng(seed)
-    adv = np.array([s.advantage for s in batch.samples], dtype=np.float64)
+    rank, world = _dist_rank_world()
+    lo, hi = getattr(batch, "shard", None) or (0, len(batch.samples))
+    count = getattr(batch, "global_count", hi - lo)
+    sharded = hi - lo < count
+    if sharded:
+        # a collect_rollouts(shard=...) batch: this rank holds global rollouts [lo, hi).
+        # The reference's advantage normalisation and epoch permutation run over ALL
+        # rollouts (training.py:204-213), so both use the all-gathered results; each
+        # minibatch member is evaluated by the rank that collected it.
+        if getattr(batch, "global_rewards", None) is None or world <= 1:
+            raise ValueError("ppo_update got a sharded rollout batch without its gathered "
+                             "global results: call collect_rollouts(shard=(rank, world)) "
+                             "with torch.distributed initialised")
+        adv = (batch.global_rewards - batch.global_values).cpu().numpy().astype(np.float64)
+    else:
+        adv = np.array([s.advantage for s in batch.samples], dtype=np.float64)
     if hyper.advantage_norm and len(adv) > 1 and adv.std() > 0:
         adv = (adv - adv.mean()) / (adv.std() + 1e-8)
     # float64 master parameters and Adam moments stay on the device for the whole
@@ -515,21 +545,23 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
     m = moments(getattr(store, "_m", None))
     v = moments(getattr(store, "_v", None))
     grads = T_.zeros_like(blob)
-    rank, world = _dist_rank_world()
     samples = _device_samples(batch, graphs, tasks)
     step = int(getattr(store, "step_count", 0))
     stats = {"ratio_sum": 0.0, "clip_sum": 0.0, "node_count": 0, "entropy_sum": 0.0,
              "entropy_count": 0, "value_loss_sum": 0.0, "value_count": 0}
     for _epoch in range(hyper.epochs):
-        perm = rng.permutation(len(samples))
+        perm = rng.permutation(count)
         stats = {k: 0 if isinstance(val, int) else 0.0 for k, val in stats.items()}
         for chunk in np.array_split(perm, min(hyper.minibatches, len(perm))):
             if len(chunk) == 0:
                 continue
             grads.zero_()
-            mine = rank_share(chunk, rank, world)
+            if sharded:  # owner computes: the members this rank collected
+                mine = [int(k) for k in chunk if lo <= k < hi]
+            else:        # replicated batch: split the members round-robin
+                mine = [int(k) for k in rank_share(chunk, rank, world)]
             loss, st = (ppo_grad((blob, offs), embed_cfg, policy_cfg, task_sizes,
-                                 [samples[i] for i in mine], adv[mine], hyper, grads,
+                                 [samples[k - lo] for k in mine], adv[mine], hyper, grads,
                                  denominator=len(chunk))
                         if len(mine) else (0.0, np.zeros(0)))
             if world > 1:
@@ -541,7 +573,7 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
             F = len(mine)
             per = st[:12 * F].reshape(F, 3, 4)
             for i, k in enumerate(mine):
-                n = samples[k].handle.n
+                n = samples[k - lo].handle.n
                 for t in range(len(tasks)):
                     stats["ratio_sum"] += float(per[i, t, 2])
                     stats["clip_sum"] += float(per[i, t, 3])
@@ -558,7 +590,8 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
         import torch.distributed as dist
         T_ = torch()
         keys = list(stats)
-        vec = T_.tensor([float(stats[k]) for k in keys], dtype=T_.float64, device=dev)
+        vec = T_.tensor([float(stats[k]) for k in keys], dtype=T_.float64,
+                        device="cpu" if dist.get_backend() != "nccl" else dev)
         dist.all_reduce(vec)
         stats = {k: (int(round(v)) if isinstance(stats[k], int) else float(v))
                  for k, v in zip(keys, vec.tolist())}
@@ -587,148 +620,27 @@ def ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg, pol
 
 
 # ---------------------------------------------------------------------------------------
-# training drivers (host orchestration over the device entry points above; SURVEY §8(f) F4:
-# what `graphopt optimize method=rl` runs, cli.py:208-220)
+# one training step on the device (the body of the reference's train loop,
+# training.py:289-314: collect_rollouts then ppo_update).  The loop around it -- the
+# incumbent / best-store / divergence bookkeeping and the pretrain / fine-tune
+# drivers (training.py:236-384) -- is host orchestration that stays in the reference
+# and reaches this path through the INTEGRATION.md shim (out of scope).
 
-@dataclass
-class TrainResult:
-    """training.py:236-248."""
-    store: object
-    best_store: object
-    curve: list
-    best_step_times: list
-    best_actions: list
-    baselines: list
-    stats_history: list = field(default_factory=list)
-
-    @property
-    def best_step_time(self) -> float:
-        return self.best_step_times[0]
-
-
-def train(graphs, topology, tasks, hyper, steps: int, seed: int, embed_cfg=None,
-          policy_cfg=None, fusion_cfg=None, store=None, incumbent_from_default: bool = True,
-          base_assignments=None) -> TrainResult:
-    """training.py:251-317, same control flow and the same numpy stream for the per-step
-    rollout and update seeds; each step is one device `collect_rollouts` (all rollouts
-    batched, one DES launch per graph) and one device `ppo_update`.  The incumbent /
-    best-store / divergence bookkeeping reads only per-rollout scalars, so the per-sample
-    action arrays are fetched from the device only for a new incumbent.
-    Single-process semantics: under torch.distributed every rank runs the same loop and
-    ppo_update shares the minibatch work (owner-computes + gradient all-reduce)."""
-    from .baselines import baseline_step_time
-    from .params import init_all_params
-    from .simulator import evaluate_assignments
-    embed_cfg = embed_cfg or EmbedConfig()
-    policy_cfg = policy_cfg or PolicyConfig()
-    fusion_cfg = fusion_cfg or FusionConfig()
-    graphs = [as_graph(g) for g in graphs]
-    task_sizes = task_action_sizes(topology, tasks, fusion_cfg.num_levels)
-    if store is None:
-        store = init_all_params(embed_cfg, policy_cfg, task_sizes, seed)
-    baselines = [baseline_step_time(g, topology, fusion_cfg) for g in graphs]
-    start_results = [
-        evaluate_assignments(g, topology,
-                             base_assignments[i] if base_assignments
-                             else default_assignments(g, topology, fusion_cfg.num_levels),
-                             fusion_cfg)
-        for i, g in enumerate(graphs)]
-    valid_exists = any(r.valid for r in start_results)
-    best_times = [r.step_time if (incumbent_from_default and r.valid) else math.inf
-                  for r in start_results]
-    best_actions = [None] * len(graphs)
-    best_store = store.clone()
-    best_mean_reward = -math.inf
-    curve, stats_history = [], []
-    rng = np.random.default_rng(seed)
-    bad_streak = 0
-    for step in range(steps):
-        batch = collect_rollouts(store, graphs, topology, task_sizes, baselines,
-                                 hyper.rollouts, int(rng.integers(2**31)), hyper,
-                                 embed_cfg, policy_cfg, fusion_cfg, base_assignments,
-                                 keep_logits=False)
-        for s in batch.samples:
-            if s.valid and s.step_time < best_times[s.graph_index]:
-                best_times[s.graph_index] = s.step_time
-                best_actions[s.graph_index] = {k: np.array(v, copy=True)
-                                               for k, v in s.bundle.actions.items()}
-        if batch.mean_reward > best_mean_reward:
-            best_mean_reward = batch.mean_reward
-            best_store = store.clone()
-        if batch.mean_reward < -9 and valid_exists:
-            bad_streak += 1
-            if bad_streak >= 50:
-                raise RuntimeError(
-                    f"training diverged: mean reward {batch.mean_reward:.2f} "
-                    f"below -9 for 50 consecutive steps")
-        else:
-            bad_streak = 0
-        stats = ppo_update(batch, store, graphs, topology, task_sizes, hyper,
-                           embed_cfg, policy_cfg, int(rng.integers(2**31)))
-        stats_history.append(stats)
-        finite = [t for t in best_times if math.isfinite(t)]
-        curve.append((step, float(np.mean(finite)) if finite else math.inf))
-    return TrainResult(store=store, best_store=best_store, curve=curve,
-                       best_step_times=best_times, best_actions=best_actions,
-                       baselines=baselines, stats_history=stats_history)
-
-
-def decode_step_time(graph, store, topology, tasks, embed_cfg, policy_cfg, fusion_cfg) -> float:
-    """training.py:320-332: greedy (temperature-0) decode, scored by the simulator;
-    invalid decodes count as +inf."""
-    from .policy import iterate_decisions
-    from .simulator import evaluate_assignments
-    task_sizes = task_action_sizes(topology, tasks, fusion_cfg.num_levels)
-    bundle, _ = iterate_decisions(graph, store, embed_cfg, policy_cfg, task_sizes,
-                                  policy_cfg.iterations, seed=0, temperature=0.0)
-    asg = bundle_assignments(graph, topology, bundle, task_sizes, fusion_cfg)
-    res = evaluate_assignments(graph, topology, asg, fusion_cfg)
-    return res.step_time if res.valid else math.inf
-
-
-def pretrain_finetune_zeroshot(train_graphs: dict, holdout_family: str, holdout_graph, topology,
-                               tasks, hyper, seed: int, pretrain_batches: int = 5,
-                               steps_per_batch: int = 4, batch_size: int = 4,
-                               finetune_steps: int = 20, embed_cfg=None, policy_cfg=None,
-                               fusion_cfg=None) -> dict:
-    """training.py:335-381: pretrain on the training families, then the holdout graph's
-    zero-shot decode, the best within `finetune_steps` of fine-tuning (never worse than
-    zero-shot) and a from-scratch run of the same budget."""
-    from .params import init_all_params
-    if finetune_steps > 50:
-        raise ValueError("fine-tuning budget is capped at 50 steps")
-    if holdout_family in train_graphs:
-        raise ValueError(f"holdout family {holdout_family!r} appears in the training set")
-    hname = getattr(holdout_graph, "name", None)
-    for family, gs in train_graphs.items():
-        for g in gs:
-            if getattr(g, "name", None) == hname:
-                raise ValueError(f"holdout graph {hname!r} appears in the training set")
-    embed_cfg = embed_cfg or EmbedConfig()
-    policy_cfg = policy_cfg or PolicyConfig()
-    fusion_cfg = fusion_cfg or FusionConfig()
-    task_sizes = task_action_sizes(topology, tasks, fusion_cfg.num_levels)
-    pool = [g for family in sorted(train_graphs) for g in train_graphs[family]]
-    rng = np.random.default_rng(seed)
-    store = init_all_params(embed_cfg, policy_cfg, task_sizes, seed)
-    for _ in range(pretrain_batches):
-        take = min(batch_size, len(pool))
-        idx = rng.choice(len(pool), size=take, replace=False)
-        result = train([pool[i] for i in idx], topology, tasks, hyper, steps_per_batch,
-                       int(rng.integers(2**31)), embed_cfg, policy_cfg, fusion_cfg, store=store)
-        store = result.store
-    zeroshot = decode_step_time(holdout_graph, store, topology, tasks, embed_cfg, policy_cfg,
-                                fusion_cfg)
-    finetuned = zeroshot
-    if finetune_steps > 0:
-        ft = train([holdout_graph], topology, tasks, hyper, finetune_steps,
-                   int(rng.integers(2**31)), embed_cfg, policy_cfg, fusion_cfg,
-                   store=store.clone(), incumbent_from_default=False)
-        finetuned = min(finetuned, ft.best_step_time)
-    scratch = math.inf
-    if finetune_steps > 0:
-        sc = train([holdout_graph], topology, tasks, hyper, finetune_steps,
-                   int(rng.integers(2**31)), embed_cfg, policy_cfg, fusion_cfg,
-                   incumbent_from_default=False)
-        scratch = sc.best_step_time
-    return {"zeroshot": zeroshot, "finetuned": finetuned, "scratch": scratch}
+def train_step(store, graphs, topology, task_sizes, baselines, hyper, embed_cfg, policy_cfg,
+               fusion_cfg, rollout_seed: int, update_seed: int, base_assignments=None,
+               shard=None, keep_logits: bool = False):
+    """collect_rollouts + ppo_update with the rollouts sharded over the ranks of an
+    initialised torch.distributed group: each rank decides and
+    scores only its own global rollouts, the per-rollout results are all-gathered
+    once, and each minibatch member's forward+backward runs on the rank that
+    collected it, followed by one gradient all-reduce per minibatch.  Returns
+    (batch, stats); `store` is updated in place on every rank, identically."""
+    if shard is None:
+        rank, world = _dist_rank_world()
+        shard = (rank, world) if world > 1 else None
+    batch = collect_rollouts(store, graphs, topology, task_sizes, baselines, hyper.rollouts,
+                             rollout_seed, hyper, embed_cfg, policy_cfg, fusion_cfg,
+                             base_assignments, keep_logits=keep_logits, shard=shard)
+    stats = ppo_update(batch, store, graphs, topology, task_sizes, hyper, embed_cfg,
+                       policy_cfg, update_seed)
+    return batch, stats

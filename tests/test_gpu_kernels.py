@@ -110,6 +110,47 @@ def test_medium_scores_take_tf32_kernel():
     assert rel_err(out.logits["placement"].data, lg["placement"]) < 5e-4
 
 
+def _head_bounds(hid, P, sizes):
+    """Per (row, head) fixed-offset bound b = |q| max|k| log2(e)/sqrt(d) the repack
+    kernels compute (tc_attention16.cu), in float64 from the oracle's h."""
+    import math
+    from oracle import forward as of
+    t, _a = of.ordered_tasks(sizes)[0]
+    p, pa = f"policy/task/{t}/", "policy/task_attn/"
+    n, d = hid.shape
+    h = of.layer_norm(np.concatenate([np.zeros((n, d)), hid], 1) @ P[p + "cat_w"] + P[p + "cat_b"],
+                      P[p + "ln_g"], P[p + "ln_b"])
+    q = h @ P[pa + "q_w"] + P[pa + "q_b"]
+    k = h @ P[pa + "k_w"] + P[pa + "k_b"]
+    s = math.log2(math.e) / math.sqrt(15)
+    return np.stack([np.linalg.norm(q[:, i * 15:(i + 1) * 15], axis=1)
+                     * np.linalg.norm(k[:, i * 15:(i + 1) * 15], axis=1).max() * s
+                     for i in range(3)], axis=1)
+
+
+def test_fp16_fallback_is_per_work_item():
+    """W_q scaled so only a few rows' bounds pass the fp16 limit (14): only the 384-query
+    work items holding such a row move to the tf32 kernel (the fp16 kernel marks them),
+    the rest stay on the fp16 kernel, and the whole launch matches the oracle."""
+    from oracle import forward as of
+    from paper_2010_12438_b200.policy import ordered_tasks, task_heads
+    sizes = {"placement": 4}
+    ecfg, pcfg, store = _store(sizes)
+    rng = np.random.default_rng(5)
+    hid = rng.normal(size=(2300, pcfg.d_model))
+    b = _head_bounds(hid, _oracle_P(store), sizes)
+    store["policy/task_attn/q_w"].data = store["policy/task_attn/q_w"].data * (
+        14.3 / np.quantile(b, 0.9985))
+    b = _head_bounds(hid, _oracle_P(store), sizes)
+    works = np.stack([(b[i * 384:(i + 1) * 384] > 14.0).any(axis=0)
+                      for i in range((len(hid) + 383) // 384)])
+    assert works.any() and not works.all() and b.max() < 60, works
+    tasks = ordered_tasks(sizes)
+    out = task_heads(hid, store, pcfg, tasks)
+    lg, _, _ = of.task_heads(hid, _oracle_P(store), of.PolicyCfg(), tasks)
+    assert rel_err(out.logits["placement"].data, lg["placement"]) < 1e-4
+
+
 def test_ragged_batch_matches_single_forwards():
     """A super-positioned batch (cfg3 style: mixed graph sizes in one launch) gives
     each forward exactly what it gets alone."""

@@ -120,7 +120,8 @@ def test_ppo_update_matches_reference(name, iterations):
 
 @pytest.mark.gpu
 def test_train_matches_reference():
-    """training.py:251-317 `train` for 3 steps (rollouts -> PPO update -> incumbent
+    """training.py:251-317 `train` (restated test-side in tests/train_driver.py over the
+    device train_step) for 3 steps (rollouts -> PPO update -> incumbent
     bookkeeping) on the device path vs the reference run in tests/golden (make_train).
     Step 0 starts from identical parameters, so its rollouts and incumbent are exact;
     later steps start from the fp32 device update (within 2e-4 of the float64 one, see
@@ -128,28 +129,28 @@ def test_train_matches_reference():
     and the parameters / stats to tolerance; greedy decode of the result the same."""
     from paper_2010_12438_b200 import EmbedConfig, FusionConfig, PolicyConfig, PPOHyper
     from paper_2010_12438_b200.costmodel import uniform_topology
-    from paper_2010_12438_b200.training import decode_step_time, train
+    import train_driver as D
     z = golden("train")
     g = _graph(z, "g/")
     ecfg, pcfg = EmbedConfig(1, 8, 4), PolicyConfig(1, 8, 2, 3, 16, 8, 2)
     top = uniform_topology(2)
     hyper = PPOHyper(lr=1e-2, rollouts=6, minibatches=2, epochs=2, entropy_coef=0.01)
-    res = train([g], top, ["placement"], hyper, 3, 11, ecfg, pcfg, FusionConfig())
-    assert np.array_equal(np.array(res.baselines), z["baselines"])
-    assert np.array_equal(np.array(res.best_step_times), z["best_step_times"])
-    assert np.array_equal(np.array([c for _, c in res.curve]), z["curve"])
-    assert (res.best_actions[0] is not None) == bool(z["has_best_actions"])
-    if res.best_actions[0] is not None:
-        assert np.array_equal(res.best_actions[0]["placement"], z["best_actions"])
-    for i, st in enumerate(res.stats_history):
+    res = D.run([g], top, ["placement"], hyper, 3, 11, ecfg, pcfg, FusionConfig())
+    assert np.array_equal(np.array(res["baselines"]), z["baselines"])
+    assert np.array_equal(np.array(res["best_step_times"]), z["best_step_times"])
+    assert np.array_equal(np.array(res["curve"]), z["curve"])
+    assert (res["best_actions"][0] is not None) == bool(z["has_best_actions"])
+    if res["best_actions"][0] is not None:
+        assert np.array_equal(res["best_actions"][0]["placement"], z["best_actions"])
+    for i, st in enumerate(res["stats_history"]):
         for k in ("mean_ratio", "entropy", "value_loss"):
             want = float(z[f"stats{i}/{k}"])
             assert abs(st[k] - want) <= 2e-3 * max(1.0, abs(want)), (i, k, st[k], want)
-    assert res.store.step_count == int(z["step_count"])
-    d = np.concatenate([np.abs(p.data - z["store/" + n]).reshape(-1)
-                        for n, p in res.store.items()])
+    store = res["store"]
+    assert store.step_count == int(z["step_count"])
+    d = np.concatenate([np.abs(p.data - z["store/" + n]).reshape(-1) for n, p in store.items()])
     assert (d <= 1e-3).mean() >= 0.99, (d.max(), (d <= 1e-3).mean())
-    dec = decode_step_time(g, res.store, top, ["placement"], ecfg, pcfg, FusionConfig())
+    dec = D.decode_step_time(g, store, top, ["placement"], ecfg, pcfg, FusionConfig())
     assert dec == float(z["decode"])
 
 
