@@ -146,6 +146,16 @@ typedef struct {
   const float* features;
   int32_t feature_dim;
   float* reps;
+  /* optional trunk cache hook (policy.py:137,170-172 cache_perturb, diagnostics): when
+   * set, before layer l's attention the library copies that layer's inputs xm
+   * (host float32 [rows, d_model]) and calls cache_hook(user, l, xm, prefix, rows,
+   * d_model); prefix (host, pre-filled with xm) receives, for every segment s >= 1,
+   * the values its queries use as the previous segment's cached keys/values in place
+   * of xm's rows of segment s-1.  Single forward, segment_len <= 64; the layer then
+   * runs on the fp32 SIMT attention kernel. */
+  void (*cache_hook)(void* user, int32_t layer, const float* xm, float* prefix,
+                     int64_t rows, int32_t d_model);
+  void* cache_hook_user;
 } go_batch_t;
 
 int go_forward(go_ctx_t ctx, const go_config_t* cfg, const float* params,
@@ -228,6 +238,26 @@ int go_simulate(go_ctx_t ctx, go_graph_t g, int32_t num_placements, const int32_
                 const double* link_bw, int32_t policy, double baseline,
                 double* step_time, uint8_t* valid, int8_t* violation, double* busy,
                 double* peak_mem, double* reward, void* stream);
+
+/* One started compute or transfer of a traced simulation (simulator.py:61-67
+ * TraceEvent): kind 0 = compute on device `src_or_device`, kind 1 = transfer on link
+ * src_or_device -> dst; group_id = the computing group / the receiving group. */
+typedef struct {
+  double t_start, t_end;
+  int32_t kind, src_or_device, dst, group_id;
+} go_trace_event_t;
+
+/* simulate(..., record_trace=True) for ONE placement (simulator.py:280-441 with the
+ * trace appends of :360-373): same results as go_simulate (priorities per node,
+ * device pointers) plus the device event log in start order; trace_count receives the
+ * number of events (at most groups + cross-device edges; events past trace_capacity are
+ * counted but not written).  The caller sorts them as simulator.py:432-433 does. */
+int go_simulate_trace(go_ctx_t ctx, go_graph_t g, const int32_t* placement,
+                      const int32_t* priorities, int32_t d, const double* peak,
+                      const double* mem_bw, const double* cap, const double* link_bw,
+                      int32_t policy, double* step_time, uint8_t* valid, int8_t* violation,
+                      double* busy, double* peak_mem, go_trace_event_t* trace,
+                      int64_t trace_capacity, int64_t* trace_count, void* stream);
 
 #ifdef __cplusplus
 }

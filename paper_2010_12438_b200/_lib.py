@@ -21,7 +21,7 @@ EXPORTS = (
     "go_topo_order", "go_greedy_cuts", "go_apply_fusion", "go_graph_create", "go_graph_destroy", "go_graph_topo",
     "go_graph_num_neighbors", "go_graph_set_fusion", "go_param_count", "go_forward",
     "go_forward_status", "go_neighbor_arrays", "go_sample", "go_simulate", "go_ppo_grad",
-    "go_adam", "go_adam64",
+    "go_adam", "go_adam64", "go_simulate_trace",
 )
 
 
@@ -37,7 +37,13 @@ class GoBatch(C.Structure):
                 ("row_counts", C.POINTER(C.c_int64)), ("embed_seeds", C.POINTER(C.c_int64)), ("prev_actions", C.c_void_p),
                 ("stage_mask", C.c_int32), ("ablate_mask", C.c_int32),
                 ("mod_override", C.c_void_p), ("features", C.c_void_p),
-                ("feature_dim", C.c_int32), ("reps", C.c_void_p)]
+                ("feature_dim", C.c_int32), ("reps", C.c_void_p),
+                ("cache_hook", C.c_void_p), ("cache_hook_user", C.c_void_p)]
+
+
+# void cache_hook(void* user, int32 layer, const float* xm, float* prefix, int64 rows, int32 dm)
+CACHE_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_float),
+                         C.POINTER(C.c_float), C.c_int64, C.c_int32)
 
 
 class GoError(RuntimeError):
@@ -81,6 +87,8 @@ _SIGS = {
     "go_adam64": (C.c_int, [P, P, P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
     "go_simulate": (C.c_int, [P, P, I32, P, P, I32, I32, P, P, P, P, I32, F64, P, P, P, P, P,
                               P, P]),
+    "go_simulate_trace": (C.c_int, [P, P, P, P, I32, P, P, P, P, I32, P, P, P, P, P, P, I64, P,
+                                    P]),
 }
 
 

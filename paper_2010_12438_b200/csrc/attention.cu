@@ -19,7 +19,9 @@ __global__ void __launch_bounds__(ATT_Q) attn_kernel(const float* __restrict__ q
                                                      float* __restrict__ out, int64_t ldo,
                                                      float scale_log2,
                                                      float* __restrict__ lse, int n_head,
-                                                     const int32_t* __restrict__ gate) {
+                                                     const int32_t* __restrict__ gate,
+                                                     const float* __restrict__ kalt,
+                                                     const float* __restrict__ valt) {
   if (gate && *gate == 0) return;
   __shared__ __align__(16) float Ks[ATT_KC][DH];
   __shared__ __align__(16) float Vs[ATT_KC][DH];
@@ -41,8 +43,11 @@ __global__ void __launch_bounds__(ATT_Q) attn_kernel(const float* __restrict__ q
     for (int idx = threadIdx.x; idx < ATT_KC * DH; idx += ATT_Q) {
       int j = idx / DH, d = idx % DH;
       bool ok = j < nk && d < d_head;
-      Ks[j][d] = ok ? k[(kc + j) * ld + col0 + d] : 0.f;
-      Vs[j][d] = ok ? v[(kc + j) * ld + col0 + d] : 0.f;
+      // kalt / valt: the keys before the tile's first query (the previous segment of
+      // a banded trunk tile) come from the cache-hook buffers (policy.py:170-172)
+      const bool pre = kalt && kc + j < tl.q0;
+      Ks[j][d] = ok ? (pre ? kalt : k)[(kc + j) * ld + col0 + d] : 0.f;
+      Vs[j][d] = ok ? (pre ? valt : v)[(kc + j) * ld + col0 + d] : 0.f;
     }
     __syncthreads();
     float s[ATT_KC];
@@ -80,13 +85,14 @@ __global__ void __launch_bounds__(ATT_Q) attn_kernel(const float* __restrict__ q
 
 void attention(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
-               int64_t ldo, cudaStream_t st, float* lse, const int32_t* gate) {
+               int64_t ldo, cudaStream_t st, float* lse, const int32_t* gate,
+               const float* kalt, const float* valt) {
   if (num_tiles <= 0) return;
   float scale_log2 = (float)(1.4426950408889634 / sqrt((double)d_head));
   dim3 grid((unsigned)num_tiles, (unsigned)n_head);
 #define GO_ATT(DHV)                                                                          \
   attn_kernel<DHV><<<grid, ATT_Q, 0, st>>>(q, k, v, ld, d_head, tiles_dev, out, ldo,           \
-                                           scale_log2, lse, n_head, gate)
+                                           scale_log2, lse, n_head, gate, kalt, valt)
   if (d_head <= 4) GO_ATT(4);
   else if (d_head <= 8) GO_ATT(8);
   else if (d_head <= 16) GO_ATT(16);

@@ -61,6 +61,16 @@ struct DesCaps {
 
 enum { ST_OK = 0, ST_OVERFLOW = 1, ST_DEADLOCK = 2, ST_MEMLIST = 3 };
 
+// Optional event log (simulate(record_trace=True), simulator.py:61-67, 360-373): one
+// record per started compute (kind 0, a = device) and per started transfer (kind 1,
+// a -> b the link), in the order schedule() starts them; the host sorts them the way
+// the reference does (simulator.py:432-433).
+struct DesTraceLog {
+  DesTraceRec* rec;  // capacity cap; nullptr: no trace
+  int64_t cap;
+  int64_t* count;
+};
+
 template <int M>
 struct DesState {
   double dev_t[M];
@@ -90,7 +100,8 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
                            double* __restrict__ o_step, uint8_t* __restrict__ o_valid,
                            int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
                            double* __restrict__ o_peak, double* __restrict__ o_reward,
-                           int32_t* __restrict__ o_status, int lanes_per_placement) {
+                           int32_t* __restrict__ o_status, int lanes_per_placement,
+                           DesTraceLog tr) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gtid % lanes_per_placement) return;
   const int tid = gtid / lanes_per_placement;
@@ -107,6 +118,11 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
   double* mlist = reinterpret_cast<double*>(lq + (int64_t)d * d * caps.cl);
 
   auto gdev = [&](int g) { return pl[V.grp_rep[g]]; };
+  int64_t n_trace = 0;  // events logged (the single-placement trace launch only)
+  auto log_event = [&](double t0, double t1, int kind, int a, int b, int g) {
+    if (tr.rec && n_trace < tr.cap) tr.rec[n_trace] = DesTraceRec{t0, t1, kind, a, b, g};
+    ++n_trace;
+  };
 
   // colocation (simulator.py:308-315): checked on group devices, simulation continues
   int8_t viol = 0;
@@ -278,6 +294,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
         double dt = __ddiv_rn(V.out_bytes[e.edge], lbw[s]);
         link_t[s] = __dadd_rn(t, dt);
         link_g[s] = e.grp;
+        if (tr.rec) log_event(t, link_t[s], 1, s / d, s % d, e.grp);
         amask[w] |= 1ull << b;
       }
     }
@@ -293,6 +310,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
       busy[dev] = __dadd_rn(busy[dev], dt);
       dev_t[dev] = __dadd_rn(t, dt);
       dev_g[dev] = g;
+      if (tr.rec) log_event(t, dev_t[dev], 0, dev, -1, g);
     }
   };
 
@@ -365,6 +383,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
     if (done != G) status = ST_DEADLOCK;
   }
   o_status[tid] = status;
+  if (tr.rec) *tr.count = n_trace;
   if (status != ST_OK) return;
   if (!viol)
     for (int dev = 0; dev < d; ++dev)
@@ -388,7 +407,8 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
                    const double* mem_bw, const double* cap, const double* link_bw, int policy,
                    double baseline, double* step_time, uint8_t* valid, int8_t* violation,
                    double* busy, double* peak_mem, double* reward, go_ctx* ctx,
-                   cudaStream_t st) {
+                   cudaStream_t st, DesTraceRec* trace, int64_t trace_cap, int64_t* trace_count) {
+  GO_CHECK(!trace || K == 1, "event traces are recorded for one placement per call");
   if (K <= 0) return GO_OK;
   if (d > DES_MAXD) GO_THROW(GO_ERR_UNSUPPORTED, "%d devices > %d", d, DES_MAXD);
   // topology -> device (small; part of the DES workspace head)
@@ -426,7 +446,8 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
     kern<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
         v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
         dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
-        step_time, valid, violation, busy, peak_mem, reward, dstatus, lanes);
+        step_time, valid, violation, busy, peak_mem, reward, dstatus, lanes,
+        DesTraceLog{trace, trace_cap, trace_count});
     LAUNCH_CHECK();
     std::vector<int32_t> hstat(count);
     CUDA_CHECK(cudaMemcpyAsync(hstat.data(), dstatus, (size_t)count * 4, cudaMemcpyDeviceToHost,

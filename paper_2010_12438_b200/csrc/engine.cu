@@ -312,7 +312,10 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
   const int gs = cfg.gs_dim, dm = cfg.d_model, W = cfg.n_head * cfg.d_head, di = cfg.d_inner;
   const int64_t wmax = std::max(gs, dm);
   const int64_t LW = ldp((int)wmax), LA = ldp(W), LI = ldp(di);
-  Arena A{reinterpret_cast<char*>(ctx->ensure(forward_ws_bytes(cfg, R, m.gtotal, F, m.n_chunks))),
+  const size_t hook_bytes =
+      b.cache_hook ? (size_t)cfg.trf_layers * R * (ldp(cfg.d_model) + 2 * LA + 192) * 4 : 0;
+  Arena A{reinterpret_cast<char*>(
+              ctx->ensure(forward_ws_bytes(cfg, R, m.gtotal, F, m.n_chunks) + hook_bytes)),
           0, ctx->ws_bytes};
   float* X[6];
   for (int i = 0; i < 6; ++i) X[i] = A.take<float>(R * LW);
@@ -378,6 +381,8 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
 
   // ---- trunk (policy.py:122-177), layer-major block-banded attention
   if (do_t) {
+    GO_CHECK(!b.cache_hook || (F == 1 && cfg.segment_len <= 64),
+             "the trunk cache hook needs one forward and segment_len <= 64");
     GO_CHECK(node_embed && graph_embed && hid, "trunk inputs/outputs required");
     const float* modp = b.mod_override;
     if (!modp) {
@@ -399,7 +404,25 @@ static void run_forward(go_ctx* ctx, const go_config_t& cfg, const float* P,
       gemm(xm, LW, dm, nullptr, 0, 0, W_(S.blk(l, Q_W)), W, W_(S.blk(l, Q_B)), Qb, LA, R, W, 0, st);
       gemm(xm, LW, dm, nullptr, 0, 0, W_(S.blk(l, K_W)), W, W_(S.blk(l, K_B)), Kb, LA, R, W, 0, st);
       gemm(xm, LW, dm, nullptr, 0, 0, W_(S.blk(l, V_W)), W, W_(S.blk(l, V_B)), Vb, LA, R, W, 0, st);
-      {
+      if (b.cache_hook) {  // cache_perturb (policy.py:170-172), see run_forward_tc
+        std::vector<float> hx((size_t)R * dm);
+        CUDA_CHECK(cudaMemcpy2DAsync(hx.data(), dm * 4, xm, LW * 4, dm * 4, R,
+                                     cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        std::vector<float> hp = hx;
+        b.cache_hook(b.cache_hook_user, l, hx.data(), hp.data(), R, dm);
+        float* pfx = A.take<float>(R * dm);
+        float* kp = A.take<float>(R * LA);
+        float* vp = A.take<float>(R * LA);
+        CUDA_CHECK(cudaMemcpyAsync(pfx, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice, st));
+        gemm(pfx, dm, dm, nullptr, 0, 0, W_(S.blk(l, K_W)), W, W_(S.blk(l, K_B)), kp, LA, R, W, 0,
+             st);
+        gemm(pfx, dm, dm, nullptr, 0, 0, W_(S.blk(l, V_W)), W, W_(S.blk(l, V_B)), vp, LA, R, W, 0,
+             st);
+        attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
+                  LA, st, nullptr, nullptr, kp, vp);
+        CUDA_CHECK(cudaStreamSynchronize(st));
+      } else {
         KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
         attention(Qb, Kb, Vb, LA, cfg.n_head, cfg.d_head, m.d_trunk_tiles, m.n_trunk_tiles, Ab,
                   LA, st);
@@ -520,7 +543,8 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
           tc_gemm_packed_floats(dm, di) + tc_gemm_packed_floats(di, dm) +
           tc_gemm_packed_floats(dm, cfg.task_sizes[t]);
   size_t bytes = forward_ws_bytes(cfg, R, m.gtotal, F, m.n_chunks) + (size_t)R * (LQ + 16) * 4 +
-                 pk * 6 + (size_t)(Lt + 2) * 4 * 160 + (4u << 20);
+                 pk * 6 + (size_t)(Lt + 2) * 4 * 160 + (4u << 20) +
+                 (b.cache_hook ? (size_t)Lt * R * (dm + LQ + 128) * 4 : 0);
   Arena A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   float* X[6];
   for (int i = 0; i < 6; ++i) X[i] = A.take<float>(R * LW);
@@ -613,6 +637,8 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
   }
 
   if (do_t) {
+    GO_CHECK(!b.cache_hook || (F == 1 && cfg.segment_len <= 64),
+             "the trunk cache hook needs one forward and segment_len <= 64");
     GO_CHECK(node_embed && graph_embed && hid, "trunk inputs/outputs required");
     const float* modp = b.mod_override;
     if (!modp) {
@@ -646,13 +672,29 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
     float* xm = X[1];
     for (int l = 0; l < Lt; ++l) {
       const float* bq = qkv_bias(W_(S.blk(l, Q_B)), W_(S.blk(l, K_B)), W_(S.blk(l, V_B)));
+      const TcW wqkv = pack(W_(S.blk(l, Q_W)), W_(S.blk(l, K_W)), W_(S.blk(l, V_W)), W, W, dm, 3 * W);
       {
         KTimer kt(ctx, K_GEMM, st, 2.0 * R * dm * 3 * W);
-        tc_gemm(xm, LW, dm, nullptr, 0, 0,
-                pack(W_(S.blk(l, Q_W)), W_(S.blk(l, K_W)), W_(S.blk(l, V_W)), W, W, dm, 3 * W), bq,
-                QKV, LQ, R, 3 * W, 0, st);
+        tc_gemm(xm, LW, dm, nullptr, 0, 0, wqkv, bq, QKV, LQ, R, 3 * W, 0, st);
       }
-      {
+      if (b.cache_hook) {
+        // cache_perturb (policy.py:170-172): the host hook rewrites the previous-segment
+        // keys/values of every segment; their K/V projections go to QKVp and the SIMT
+        // kernel reads rows before each tile's first query from there
+        std::vector<float> hx((size_t)R * dm), hp;
+        CUDA_CHECK(cudaMemcpy2DAsync(hx.data(), dm * 4, xm, LW * 4, dm * 4, R,
+                                     cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        hp = hx;
+        b.cache_hook(b.cache_hook_user, l, hx.data(), hp.data(), R, dm);
+        float* pfx = A.take<float>(R * dm);
+        float* qkvp = A.take<float>(R * LQ);
+        CUDA_CHECK(cudaMemcpyAsync(pfx, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice, st));
+        tc_gemm(pfx, dm, dm, nullptr, 0, 0, wqkv, bq, qkvp, LQ, R, 3 * W, 0, st);
+        attention(QKV, QKV + W, QKV + 2 * W, LQ, H, dh, m.d_trunk_tiles, m.n_trunk_tiles, Ab, LA,
+                  st, nullptr, nullptr, qkvp + W, qkvp + 2 * W);
+        CUDA_CHECK(cudaStreamSynchronize(st));  // the host buffers above go out of scope
+      } else {
         KTimer kt(ctx, K_TRUNK_ATTN, st, 4.0 * m.trunk_pairs * W);
         if (trunk_mma) {
           // split fp16 operands (3 MMAs per product): single fp16 Q/K/V put the trunk
@@ -993,6 +1035,39 @@ int go_simulate(go_ctx_t ctx, go_graph_t g, int32_t K, const int32_t* placement,
     simulate_batch(g->des, K, placement, g->n, priorities, prio_per_placement ? g->n : 0, d, peak,
                    mem_bw, cap, link_bw, policy, baseline, step_time, valid, violation, busy,
                    peak_mem, reward, ctx, st);
+  });
+}
+
+int go_simulate_trace(go_ctx_t ctx, go_graph_t g, const int32_t* placement,
+                      const int32_t* priorities, int32_t d, const double* peak,
+                      const double* mem_bw, const double* cap, const double* link_bw,
+                      int32_t policy, double* step_time, uint8_t* valid, int8_t* violation,
+                      double* busy, double* peak_mem, go_trace_event_t* trace,
+                      int64_t trace_capacity, int64_t* trace_count, void* stream) {
+  return guarded([&] {
+    static_assert(sizeof(go_trace_event_t) == sizeof(DesTraceRec), "trace record layout");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    GO_CHECK(policy == 0 || policy == 1, "unknown policy");
+    GO_CHECK(d >= 1, "need at least one device");
+    GO_CHECK(trace && trace_count && trace_capacity >= 0, "trace buffers required");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!g->acyclic) {  // simulator.py:317-319: no events, (0, invalid, zeros)
+      std::vector<double> z((size_t)d, 0.0), zk(1, 0.0);
+      uint8_t v = 0;
+      int8_t vi = 3;
+      int64_t zero = 0;
+      CUDA_CHECK(cudaMemcpyAsync(step_time, zk.data(), 8, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(valid, &v, 1, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(violation, &vi, 1, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(busy, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(peak_mem, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaMemcpyAsync(trace_count, &zero, 8, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      return;
+    }
+    simulate_batch(g->des, 1, placement, g->n, priorities, 0, d, peak, mem_bw, cap, link_bw,
+                   policy, 0.0, step_time, valid, violation, busy, peak_mem, nullptr, ctx, st,
+                   reinterpret_cast<DesTraceRec*>(trace), trace_capacity, trace_count);
   });
 }
 

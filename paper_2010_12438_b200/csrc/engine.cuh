@@ -178,7 +178,8 @@ struct AttnTile {
 void attention(const float* q, const float* k, const float* v, int64_t ld, int n_head,
                int d_head, const AttnTile* tiles_dev, int64_t num_tiles, float* out,
                int64_t ldo, cudaStream_t st, float* lse = nullptr,
-               const int32_t* gate = nullptr);
+               const int32_t* gate = nullptr, const float* kalt = nullptr,
+               const float* valt = nullptr);
 
 // ---- kernels: tc_attention16.cu (fp16 operands, fixed-offset softmax; flags the launch
 // over to the tf32 / online kernels when a bound exceeds the fp16-exact range)
@@ -291,11 +292,16 @@ void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t
                  int32_t* actions, double* logp, cudaStream_t st);
 
 // ---- kernels: des.cu
+struct DesTraceRec {  // one started compute / transfer of a traced simulation
+  double t0, t1;
+  int32_t kind, a, b, grp;
+};
 int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t pstride,
                    const int32_t* prio, int64_t prio_stride, int d, const double* peak,
                    const double* mem_bw, const double* cap, const double* link_bw, int policy,
                    double baseline, double* step_time, uint8_t* valid, int8_t* violation,
                    double* busy, double* peak_mem, double* reward, go_ctx* ctx,
-                   cudaStream_t st);
+                   cudaStream_t st, DesTraceRec* trace = nullptr, int64_t trace_cap = 0,
+                   int64_t* trace_count = nullptr);
 
 }  // namespace go

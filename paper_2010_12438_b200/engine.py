@@ -63,7 +63,7 @@ def forward_batch(store, embed_cfg: EmbedConfig, cfg: PolicyConfig, task_sizes: 
                   handles: list, seeds, prev_actions=None, stage_mask=EMBED | TRUNK | HEADS,
                   node_embed=None, graph_embed=None, hid=None, mod_override=None,
                   ablate_mask=0, params=None, features=None, row_counts=None,
-                  want_reps=False) -> ForwardOut:
+                  want_reps=False, cache_hook=None) -> ForwardOut:
     """One go_forward_status call over a ragged batch.  `handles` are GraphHandles
     (or None with `row_counts` for graph-less trunk/heads calls)."""
     T = torch()
@@ -125,6 +125,8 @@ def forward_batch(store, embed_cfg: EmbedConfig, cfg: PolicyConfig, task_sizes: 
     b.stage_mask = stage_mask
     b.ablate_mask = ablate_mask
     b.mod_override = _lib.ptr(mod_override)
+    if cache_hook is not None:  # a _lib.CACHE_HOOK; the caller keeps it alive
+        b.cache_hook = C.cast(cache_hook, C.c_void_p)
     _lib.call("go_forward_status", ctx.handle, C.byref(cfg_c), _lib.ptr(blob),
               offs.ctypes.data, C.byref(b), _lib.ptr(node_embed), _lib.ptr(graph_embed),
               _lib.ptr(hid), _lib.ptr(logits), _lib.ptr(value), _lib.ptr(status), stream_ptr())
@@ -228,3 +230,40 @@ def simulate_batch(handle, placement, priorities, topology, policy="priority",
               _lib.ptr(out.step_time), _lib.ptr(out.valid), _lib.ptr(out.violation),
               _lib.ptr(out.busy), _lib.ptr(out.peak), _lib.ptr(out.reward), stream_ptr())
     return out
+
+
+class GoTraceEvent(C.Structure):
+    _fields_ = [("t_start", C.c_double), ("t_end", C.c_double), ("kind", C.c_int32),
+                ("src_or_device", C.c_int32), ("dst", C.c_int32), ("group_id", C.c_int32)]
+
+
+def simulate_trace(handle, placement, priorities, topology, policy="priority",
+                   capacity: int = 0):
+    """One placement through go_simulate_trace: (SimBatch of K=1, event records as a
+    numpy structured array in start order)."""
+    T = torch()
+    ctx = context()
+    dev = T.device("cuda", ctx.device)
+    if policy not in ("fifo", "priority"):
+        raise ValueError(f"unknown policy {policy!r}")
+    d = topology.num_devices
+    out = SimBatch(step_time=T.empty(1, dtype=T.float64, device=dev),
+                   valid=T.empty(1, dtype=T.uint8, device=dev),
+                   violation=T.empty(1, dtype=T.int8, device=dev),
+                   busy=T.empty((1, d), dtype=T.float64, device=dev),
+                   peak=T.empty((1, d), dtype=T.float64, device=dev), reward=None)
+    rec = T.empty((max(1, capacity), C.sizeof(GoTraceEvent)), dtype=T.uint8, device=dev)
+    count = T.zeros(1, dtype=T.int64, device=dev)
+    _lib.call("go_simulate_trace", ctx.handle, handle.handle, _lib.ptr(placement.contiguous()),
+              _lib.ptr(priorities.contiguous()), d, _lib.ptr(topology.peak),
+              _lib.ptr(topology.mem_bw), _lib.ptr(topology.cap), _lib.ptr(topology.link_bw),
+              0 if policy == "priority" else 1, _lib.ptr(out.step_time), _lib.ptr(out.valid),
+              _lib.ptr(out.violation), _lib.ptr(out.busy), _lib.ptr(out.peak), _lib.ptr(rec),
+              int(capacity), _lib.ptr(count), stream_ptr())
+    n = int(count.item())
+    if n > capacity:
+        raise AssertionError(f"trace overflow: {n} events > capacity {capacity}")
+    dt = np.dtype([("t_start", "<f8"), ("t_end", "<f8"), ("kind", "<i4"),
+                   ("src_or_device", "<i4"), ("dst", "<i4"), ("group_id", "<i4")])
+    events = rec[:n].cpu().numpy().reshape(-1).view(dt) if n else np.zeros(0, dt)
+    return out, events

@@ -51,12 +51,16 @@ def modulation_gate(x):
 
 def trunk_forward(node_embed, graph_embed, store, cfg: PolicyConfig, prefix: str = "policy/",
                   modulation_override=None, cache_perturb=None):
-    """policy.py:135-177 (layer-major block-banded attention on device)."""
+    """policy.py:135-177 (layer-major block-banded attention on device).
+
+    cache_perturb(segment_index, layer, array) -> array (policy.py:146-147, 170-172), the
+    reference's diagnostics hook on the cached previous-segment states: the device
+    trunk hands each layer's inputs to the hook (go_batch_t.cache_hook) and the
+    segment's queries attend to the returned keys/values.  Calls arrive layer-major
+    (every segment of layer 0, then layer 1, ...), not segment-major; a pure hook sees
+    the same arrays (float32 values as float64) and gives the same result."""
     if prefix != "policy/":
         raise ValueError("only the 'policy/' parameter prefix is supported")
-    if cache_perturb is not None:
-        raise NotImplementedError("cache_perturb is a host diagnostics hook of the reference "
-                                  "tape; the device trunk does not expose per-segment caches")
     ne = _dev32(node_embed)
     ge = _dev32(graph_embed).reshape(1, -1)
     n = int(ne.shape[0])
@@ -65,8 +69,29 @@ def trunk_forward(node_embed, graph_embed, store, cfg: PolicyConfig, prefix: str
     mod = None
     if modulation_override is not None:
         mod = _dev32(modulation_override).reshape(1, cfg.d_model)
+    hook, errors = None, []
+    if cache_perturb is not None:
+        from . import _lib
+        S = cfg.segment_len
+
+        def _hook(_user, layer, xm_p, pfx_p, rows, dm):
+            try:
+                xm = np.ctypeslib.as_array(xm_p, shape=(rows, dm))
+                pfx = np.ctypeslib.as_array(pfx_p, shape=(rows, dm))
+                for s in range(1, (rows + S - 1) // S):
+                    lo, hi = (s - 1) * S, s * S
+                    arr = np.asarray(cache_perturb(s, int(layer), xm[lo:hi].astype(np.float64)),
+                                     dtype=np.float64)
+                    pfx[lo:hi] = arr.reshape(hi - lo, dm)
+            except BaseException as exc:  # ctypes drops exceptions raised in callbacks
+                errors.append(exc)
+
+        hook = _lib.CACHE_HOOK(_hook)
     out = forward_batch(store, ecfg, cfg, {"placement": 1}, None, [0], stage_mask=TRUNK,
-                        node_embed=ne, graph_embed=ge, mod_override=mod, row_counts=[n])
+                        node_embed=ne, graph_embed=ge, mod_override=mod, row_counts=[n],
+                        cache_hook=hook)
+    if errors:
+        raise errors[0]
     return DeviceArray(out.hid)
 
 

@@ -18,6 +18,7 @@ from .graph import OP_INDEX, as_graph
 from .runtime import context, torch
 
 __all__ = ["TASKS", "NUM_PRIORITY_LEVELS", "NON_FUSIBLE", "ActionAssignment", "SimResult",
+           "TraceEvent",
            "FusionConfig", "FusedGraph", "singleton_fused", "apply_fusion", "simulate",
            "simulate_many", "evaluate_assignments", "check_validity"]
 
@@ -47,6 +48,16 @@ class ActionAssignment:
 
     def __len__(self):
         return len(self.actions)
+
+
+@dataclass
+class TraceEvent:
+    """simulator.py:61-67."""
+    time_start: float
+    time_end: float
+    device: str
+    kind: str  # "compute" | "transfer"
+    group_id: int
 
 
 @dataclass
@@ -139,14 +150,16 @@ def simulate_many(fg: FusedGraph, placements, priorities, topology, policy="prio
 
 def simulate(fg: FusedGraph, placement: ActionAssignment, priorities: ActionAssignment, topology,
              policy: str = "priority", record_trace: bool = False) -> SimResult:
-    """simulator.py:280-441 on device (bit-exact step time, busy, peak memory)."""
+    """simulator.py:280-441 on device (bit-exact step time, busy, peak memory).
+    record_trace=True records every started compute / transfer on the device
+    (go_simulate_trace) and returns them as TraceEvents sorted like the reference
+    (simulator.py:432-433: by start, end, kind, device string, group)."""
     if policy not in ("fifo", "priority"):
         raise ValueError(f"unknown policy {policy!r}")
-    if record_trace:
-        raise NotImplementedError("event traces are a reference diagnostic (simulator.py:61-67)"
-                                  " outside the device path")
     top = as_topology(topology)
     _check_inputs(fg.graph.num_nodes, top.num_devices, placement, priorities)
+    if record_trace:
+        return _simulate_traced(fg, placement, priorities, top, policy)
     out = simulate_many(fg, placement.actions.reshape(1, -1), priorities.actions, top, policy)
     step = float(out.step_time.cpu().numpy()[0])
     vio = VIOLATIONS[int(out.violation.cpu().numpy()[0])]
@@ -154,6 +167,27 @@ def simulate(fg: FusedGraph, placement: ActionAssignment, priorities: ActionAssi
     peak = out.peak.cpu().numpy()[0].tolist()
     return SimResult(step_time=step, valid=vio is None, violation=vio, per_device_busy=busy,
                      peak_mem=peak, trace=None)
+
+
+def _simulate_traced(fg, placement, priorities, top, policy) -> SimResult:
+    from .engine import simulate_trace
+    T = torch()
+    dev = T.device("cuda", context().device)
+    h = fg.install()
+    g = fg.graph
+    pl = T.as_tensor(placement.actions).to(device=dev, dtype=T.int32)
+    pr = T.as_tensor(priorities.actions).to(device=dev, dtype=T.int32)
+    out, ev = simulate_trace(h, pl, pr, top, policy, capacity=g.num_nodes + g.num_edges)
+    trace = [TraceEvent(float(e["t_start"]), float(e["t_end"]),
+                        str(int(e["src_or_device"])) if e["kind"] == 0
+                        else f"{int(e['src_or_device'])}->{int(e['dst'])}",
+                        "compute" if e["kind"] == 0 else "transfer", int(e["group_id"]))
+             for e in ev]
+    trace.sort(key=lambda t: (t.time_start, t.time_end, t.kind, t.device, t.group_id))
+    vio = VIOLATIONS[int(out.violation.cpu().numpy()[0])]
+    return SimResult(step_time=float(out.step_time.cpu().numpy()[0]), valid=vio is None,
+                     violation=vio, per_device_busy=out.busy.cpu().numpy()[0].tolist(),
+                     peak_mem=out.peak.cpu().numpy()[0].tolist(), trace=trace)
 
 
 def check_validity(graph, placement: ActionAssignment, topology) -> list[str]:

@@ -651,9 +651,106 @@ def make_fusion():
     np.savez_compressed(OUT / "golden_fusion.npz", **out)
 
 
+def make_trace():
+    """simulate(record_trace=True) event logs (simulator.py:61-67, 360-373, 432-433):
+    random graphs and placements (both policies, tight memory), fused groupings, a
+    colocation violation, a cycle after fusion and a workload-scale graph."""
+    out = {}
+    rng = np.random.default_rng(77)
+    cases = 0
+
+    def record(g, fg_map, top, placement, pri, policy, tag):
+        nonlocal cases
+        p = f"c{cases}/"
+        graph_arrays(g, p, out)
+        topo_arrays(top, p, out)
+        fg = FusedGraph(g, fg_map)
+        res = simulate(fg, ActionAssignment("placement", placement, top.num_devices),
+                       ActionAssignment("schedule_priority", pri, 8), top, policy=policy,
+                       record_trace=True)
+        out[p + "group_map"] = np.asarray(fg_map, np.int64)
+        out[p + "placement"] = np.asarray(placement, np.int64)
+        out[p + "priorities"] = np.asarray(pri, np.int64)
+        out[p + "policy"] = np.array(policy)
+        out[p + "tag"] = np.array(tag)
+        out[p + "step_time"] = np.float64(res.step_time)
+        tr = res.trace
+        out[p + "t_start"] = np.array([e.time_start for e in tr], np.float64)
+        out[p + "t_end"] = np.array([e.time_end for e in tr], np.float64)
+        out[p + "device"] = np.array([e.device for e in tr], dtype="U16")
+        out[p + "kind"] = np.array([e.kind for e in tr], dtype="U16")
+        out[p + "group"] = np.array([e.group_id for e in tr], np.int64)
+        cases += 1
+
+    for _ in range(40):
+        n = int(rng.integers(1, 40))
+        g = C.random_graph(rng, n, p_edge=float(rng.choice([0.05, 0.2, 0.5])))
+        d = int(rng.integers(1, 12))  # >= 10 devices: "10" sorts before "2"
+        top = rand_topology(rng, d, tight=bool(rng.random() < 0.3))
+        record(g, np.arange(n), top, rng.integers(0, d, n),
+               rng.integers(0, 8, n) if rng.random() < 0.7 else np.zeros(n, np.int64),
+               "priority" if rng.random() < 0.7 else "fifo", "random")
+    for _ in range(10):
+        n = int(rng.integers(2, 30))
+        g = C.random_graph(rng, n, p_edge=0.3, fusible_only=True)
+        fg = apply_fusion(g, ActionAssignment("fusion_priority", rng.integers(0, 8, n), 8),
+                          FusionConfig())
+        record(g, fg.group_map, rand_topology(rng, 3), rng.integers(0, 3, n),
+               rng.integers(0, 8, n), "priority", "fused")
+    specs = [{"op": "relu", "flops": 1e9, "out_bytes": 8, "colocate": "g"},
+             {"op": "relu", "flops": 1e9, "out_bytes": 8, "colocate": "g"},
+             {"op": "relu", "flops": 1e9, "out_bytes": 8}]
+    record(C.make_graph(specs, [(0, 2)]), np.arange(3), C.simple_topology(2), np.array([0, 1, 0]),
+           np.zeros(3, np.int64), "priority", "coloc")
+    g = C.make_graph([{"op": "relu", "out_bytes": 4}] * 3, [(0, 1), (1, 2), (0, 2)])
+    record(g, np.array([0, 1, 0]), C.simple_topology(1), np.zeros(3, np.int64),
+           np.zeros(3, np.int64), "priority", "cycle")
+    from graphopt.costmodel import uniform_topology
+    g = gen_workload(WorkloadSpec("dilated-stack", 3, 60, 64, seed=1), node_cap=10**6)
+    record(g, np.arange(g.num_nodes), uniform_topology(8), rng.integers(0, 8, g.num_nodes),
+           rng.integers(0, 8, g.num_nodes), "priority", "workload")
+    out["count"] = np.int64(cases)
+    np.savez_compressed(OUT / "golden_trace.npz", **out)
+
+
+def perturb_a(seg_index, layer, arr):  # the reference test's hook (test_policy.py:140-143)
+    return arr + 0.5 if (seg_index == 1 and layer == 0) else arr
+
+
+def perturb_b(seg_index, layer, arr):  # every segment and layer, position dependent
+    return arr * (1.0 - 0.05 * layer) + 0.01 * seg_index
+
+
+def make_perturb():
+    """trunk_forward(cache_perturb=...) (policy.py:137, 170-172) from the reference on the
+    reference tests' small configuration and on the default network (segment_len 64,
+    150 rows), with the parameters' init seed and the node / graph embeddings stored."""
+    from graphopt.tensor import Tensor
+    out = {}
+    rng = np.random.default_rng(99)
+    cases = [("small", EmbedConfig(gs_layers=1, gs_dim=8, gs_knn=4),
+              PolicyConfig(trf_layers=2, d_model=8, n_head=2, d_head=3, d_inner=16,
+                           segment_len=4, iterations=2), 12),
+             ("default", EmbedConfig(), PolicyConfig(), 150)]
+    for name, ecfg, pcfg, n in cases:
+        store = init_all_params(ecfg, pcfg, {"placement": 3}, seed=0)
+        randomize(store)
+        ne = rng.normal(size=(n, ecfg.gs_dim))
+        ge = rng.normal(size=(1, ecfg.gs_dim)) * 0.1
+        p = name + "/"
+        out[p + "meta"] = np.array(json.dumps({"ecfg": ecfg.__dict__, "pcfg": pcfg.__dict__}))
+        out[p + "node_embed"] = ne
+        out[p + "graph_embed"] = ge
+        out[p + "base"] = trunk_forward(Tensor(ne), Tensor(ge), store, pcfg).data
+        for tag, fn in (("a", perturb_a), ("b", perturb_b)):
+            out[p + tag] = trunk_forward(Tensor(ne), Tensor(ge), store, pcfg,
+                                         cache_perturb=fn).data
+    np.savez_compressed(OUT / "golden_perturb.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "ppo1", "workloads", "grads",
-                             "baselines", "rollouts_joint", "json", "train", "fusion"]
+                             "baselines", "rollouts_joint", "json", "train", "fusion", "trace", "perturb"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

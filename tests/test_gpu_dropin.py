@@ -94,3 +94,53 @@ def test_adam64_is_the_reference_adam_bit_for_bit():
         assert np.array_equal(m.cpu().numpy(), store._m["w"])
         assert np.array_equal(v.cpu().numpy(), store._v["w"])
         assert np.array_equal(p32.cpu().numpy(), got.astype(np.float32))
+
+
+def _perturb_a(seg_index, layer, arr):  # tests/golden/make_golden.py perturb_a
+    return arr + 0.5 if (seg_index == 1 and layer == 0) else arr
+
+
+def _perturb_b(seg_index, layer, arr):
+    return arr * (1.0 - 0.05 * layer) + 0.01 * seg_index
+
+
+@pytest.mark.parametrize("case", ["small", "default"])
+def test_trunk_cache_perturb_matches_reference(case):
+    """trunk_forward(cache_perturb=...) (policy.py:137, 170-172): the hook rewrites the
+    previous segment's cached states; outputs match the reference's (golden_perturb)
+    within 1e-4, and the reference test's own assertions hold
+    (test_policy.py:134-149: segment 0 intact, segment 1 and downstream moved)."""
+    import json
+
+    from conftest import golden
+    from paper_2010_12438_b200 import EmbedConfig, PolicyConfig, init_all_params, randomize_zero_init
+    from paper_2010_12438_b200.policy import trunk_forward
+    z = golden("perturb")
+    p = case + "/"
+    meta = json.loads(str(z[p + "meta"]))
+    ecfg, pcfg = EmbedConfig(**meta["ecfg"]), PolicyConfig(**meta["pcfg"])
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, {"placement": 3}, 0))
+    ne, ge = z[p + "node_embed"], z[p + "graph_embed"]
+    base = trunk_forward(ne, ge, store, pcfg).data
+    assert rel_err(base, z[p + "base"]) < 1e-4
+    for tag, fn in (("a", _perturb_a), ("b", _perturb_b)):
+        got = trunk_forward(ne, ge, store, pcfg, cache_perturb=fn).data
+        assert rel_err(got, z[p + tag]) < 1e-4, (case, tag, rel_err(got, z[p + tag]))
+    S = pcfg.segment_len
+    bumped = trunk_forward(ne, ge, store, pcfg, cache_perturb=_perturb_a).data
+    assert np.allclose(base[:S], bumped[:S], rtol=0, atol=1e-5)
+    assert not np.allclose(base[S:2 * S], bumped[S:2 * S])
+    assert not np.allclose(base[2 * S:], bumped[2 * S:])
+
+
+def test_cache_perturb_errors_propagate():
+    from paper_2010_12438_b200 import EmbedConfig, PolicyConfig, init_all_params, randomize_zero_init
+    from paper_2010_12438_b200.policy import trunk_forward
+    ecfg = EmbedConfig(gs_layers=1, gs_dim=8, gs_knn=4)
+    pcfg = PolicyConfig(trf_layers=2, d_model=8, n_head=2, d_head=3, d_inner=16, segment_len=4)
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, {"placement": 3}, 0))
+
+    def bad(seg, layer, arr):
+        raise KeyError("boom")
+    with pytest.raises(KeyError):
+        trunk_forward(np.ones((12, 8)), np.zeros((1, 8)), store, pcfg, cache_perturb=bad)

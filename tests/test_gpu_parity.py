@@ -229,3 +229,33 @@ def test_collect_rollouts_joint_tasks_match_reference():
         assert s.step_time == float(z[p + "step_time"]), i
         assert s.reward == float(z[p + "reward"]), i
         assert s.valid == bool(z[p + "valid"]), i
+
+
+def test_simulate_record_trace_matches_reference():
+    """simulate(record_trace=True): the device event log (go_simulate_trace), sorted
+    like simulator.py:432-433, equals the reference's TraceEvent list exactly (starts,
+    ends, device / link strings incl. >= 10 devices, kinds, groups), together with the
+    untraced results (golden_trace.npz from make_golden.py make_trace)."""
+    from paper_2010_12438_b200.simulator import ActionAssignment, FusedGraph, simulate
+    z = golden("trace")
+    total = 0
+    for c in range(int(z["count"])):
+        p = f"c{c}/"
+        g = _g(z, p)
+        top = _topology(z, p)
+        d = top.num_devices
+        fg = FusedGraph(g, z[p + "group_map"])
+        pl = ActionAssignment("placement", z[p + "placement"], d)
+        pr = ActionAssignment("schedule_priority", z[p + "priorities"], 8)
+        res = simulate(fg, pl, pr, top, policy=str(z[p + "policy"]), record_trace=True)
+        plain = simulate(fg, pl, pr, top, policy=str(z[p + "policy"]))
+        assert res.step_time == float(z[p + "step_time"]) == plain.step_time, c
+        assert res.per_device_busy == plain.per_device_busy and res.peak_mem == plain.peak_mem
+        tr = res.trace
+        assert [e.time_start for e in tr] == list(z[p + "t_start"]), c
+        assert [e.time_end for e in tr] == list(z[p + "t_end"]), c
+        assert [e.device for e in tr] == [str(x) for x in z[p + "device"]], c
+        assert [e.kind for e in tr] == [str(x) for x in z[p + "kind"]], c
+        assert [e.group_id for e in tr] == list(z[p + "group"]), c
+        total += len(tr)
+    assert total > 1000
