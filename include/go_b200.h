@@ -259,6 +259,23 @@ int go_simulate_trace(go_ctx_t ctx, go_graph_t g, const int32_t* placement,
                       double* busy, double* peak_mem, go_trace_event_t* trace,
                       int64_t trace_capacity, int64_t* trace_count, void* stream);
 
+/* Simulated annealing (baselines.py:146-206) of `chains` independent chains on the
+ * device DES, one chain per 32-thread block.  rng_words (host) holds each chain's numpy
+ * PCG64 state (state_hi, state_lo, inc_hi, inc_lo of default_rng(seed)); the chain
+ * consumes it draw for draw like the reference (task index, node, value per move,
+ * a uniform for an uphill move).  state / best: dev int32 [chains][2][n] (placement,
+ * priorities), both set to the start assignment by the caller; best receives each
+ * chain's best state and best_time (dev f64 [chains]) its step time (inf: none
+ * valid).  Annealed tasks: task_slots[t] 0 = placement, 1 = schedule_priority, in the
+ * caller's task order, with task_sizes[t] actions.  initial_temperature NaN = 10% of
+ * the initial step time (1.0 if infinite). */
+int go_anneal(go_ctx_t ctx, go_graph_t g, int32_t chains, const uint64_t* rng_words,
+              int32_t* state, int32_t* best, int32_t d, const double* peak, const double* mem_bw,
+              const double* cap, const double* link_bw, int32_t policy, int32_t iterations,
+              int32_t moves_per_step, double initial_temperature, double cooling_rate,
+              int32_t num_tasks, const int32_t* task_slots, const int32_t* task_sizes,
+              double* best_time, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

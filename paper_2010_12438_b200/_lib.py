@@ -21,7 +21,7 @@ EXPORTS = (
     "go_topo_order", "go_greedy_cuts", "go_apply_fusion", "go_graph_create", "go_graph_destroy", "go_graph_topo",
     "go_graph_num_neighbors", "go_graph_set_fusion", "go_param_count", "go_forward",
     "go_forward_status", "go_neighbor_arrays", "go_sample", "go_simulate", "go_ppo_grad",
-    "go_adam", "go_adam64", "go_simulate_trace",
+    "go_adam", "go_adam64", "go_simulate_trace", "go_anneal",
 )
 
 
@@ -87,6 +87,8 @@ _SIGS = {
     "go_adam64": (C.c_int, [P, P, P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
     "go_simulate": (C.c_int, [P, P, I32, P, P, I32, I32, P, P, P, P, I32, F64, P, P, P, P, P,
                               P, P]),
+    "go_anneal": (C.c_int, [P, P, I32, P, P, P, I32, P, P, P, P, I32, I32, I32, F64, F64, I32,
+                            P, P, P, P]),
     "go_simulate_trace": (C.c_int, [P, P, P, P, I32, P, P, P, P, I32, P, P, P, P, P, P, I64, P,
                                     P]),
 }

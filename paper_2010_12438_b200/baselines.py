@@ -3,7 +3,8 @@ baselines.py:24-237).
 
 greedy_placement uses the native O(D N log N) DP (go_greedy_cuts) that returns the
 reference's exact cuts; baseline_step_time, brute_force and simulated_annealing score
-candidates with the device DES (brute force batched, 65,536 placements per launch)."""
+candidates with the device DES (brute force batched, 65,536 placements per launch;
+annealing chains run on the device, many at once: anneal_chains)."""
 from __future__ import annotations
 
 from dataclasses import dataclass
@@ -178,17 +179,25 @@ class SAConfig:
 
 def simulated_annealing(graph, topology, tasks: list, sa: SAConfig | None = None,
                         fusion_config: FusionConfig | None = None):
-    """baselines.py:146-206: anneal over the concatenated action vectors of `tasks`,
-    one uniform single-node move per step, Metropolis acceptance under geometric
-    cooling, best state returned.  The chain is sequential and its random stream
-    (np.random.default_rng(seed): task index, node, value, then a uniform only for an
-    uphill move) is the reference's draw for draw; each candidate is scored by the
-    device DES (bit-exact step times, so the chain takes the same path), the fusion pass
-    re-run only when fusion priorities are annealed."""
-    import math
+    """baselines.py:146-206 -> (assignments, best step time): the reference's chain for
+    seed sa.seed, run by anneal_chains."""
+    sa = sa or SAConfig()
+    return anneal_chains(graph, topology, tasks, sa, fusion_config, seeds=[sa.seed])[0]
 
+
+def anneal_chains(graph, topology, tasks: list, sa: SAConfig | None = None,
+                  fusion_config: FusionConfig | None = None, seeds=None) -> list:
+    """Many simulated-annealing chains at once: chain k is the
+    reference's simulated_annealing (baselines.py:146-206) with SAConfig.seed =
+    seeds[k], bit for bit -- same moves, same acceptance, same best state -- and the
+    chains run concurrently.  Returns [(assignments, best step time)] per seed.
+
+    Placement and schedule-priority chains run entirely on the device (go_anneal: one
+    chain per 32-thread block, candidate simulations by the device DES, the numpy
+    stream regenerated on the device).  Chains that anneal fusion priorities re-run the
+    native fusion pass per candidate on the host and score each iteration's candidates
+    of all chains with batched device simulations."""
     from .config import TASKS
-    from .simulator import apply_fusion, simulate
     if not tasks:
         raise ValueError("tasks must be non-empty")
     for t in tasks:
@@ -196,49 +205,112 @@ def simulated_annealing(graph, topology, tasks: list, sa: SAConfig | None = None
             raise ValueError(f"unknown task {t!r}")
     sa = sa or SAConfig()
     fusion_config = fusion_config or FusionConfig()
+    seeds = [sa.seed] if seeds is None else [int(x) for x in seeds]
     g = as_graph(graph)
     top = as_topology(topology)
-    rng = np.random.default_rng(sa.seed)
-    n = g.num_nodes
-    state = default_assignments(g, top, fusion_config.num_levels)
+    start = default_assignments(g, top, fusion_config.num_levels)
     sizes = {t: _task_action_size(t, top, fusion_config.num_levels) for t in tasks}
-    fixed_fg = None if "fusion_priority" in tasks else apply_fusion(g, state["fusion_priority"],
-                                                                   fusion_config)
+    if "fusion_priority" in tasks:
+        bests = _anneal_host_fusion(g, top, tasks, sa, fusion_config, seeds, start, sizes)
+    else:
+        bests = _anneal_device(g, top, tasks, sa, fusion_config, seeds, start, sizes)
+    out = []
+    for best, t in bests:
+        res = dict(start)
+        for task in tasks:
+            res[task] = ActionAssignment(task, best[task], sizes[task])
+        out.append((res, t))
+    return out
 
-    def evaluate(asg) -> float:
-        fg = fixed_fg or apply_fusion(g, asg["fusion_priority"], fusion_config)
-        res = simulate(fg, asg["placement"], asg["schedule_priority"], top)
-        return res.step_time if res.valid else math.inf
 
-    current = {t: state[t].actions.copy() for t in tasks}
-    cur_time = evaluate(state)
-    best = {t: current[t].copy() for t in tasks}
-    best_time = cur_time
-    temp = sa.initial_temperature
-    if temp is None:
-        temp = 0.1 * cur_time if math.isfinite(cur_time) else 1.0
+def _anneal_device(g, top, tasks, sa, fusion_config, seeds, start, sizes):
+    import ctypes as C
+    import math
+
+    from . import _lib
+    from .engine import pcg_words
+    from .runtime import context, stream_ptr, torch
+    from .simulator import apply_fusion
+    T = torch()
+    dev = T.device("cuda", context().device)
+    h = apply_fusion(g, start["fusion_priority"], fusion_config).install()
+    n, k = g.num_nodes, len(seeds)
+    init = np.stack([start["placement"].actions, start["schedule_priority"].actions]).astype(np.int32)
+    state = T.as_tensor(np.broadcast_to(init, (k, 2, n)).copy(), device=dev)
+    best = state.clone()
+    best_time = T.empty(k, dtype=T.float64, device=dev)
+    words = np.array([pcg_words(np.random.default_rng(s)) for s in seeds], dtype=np.uint64)
+    slot = {"placement": 0, "schedule_priority": 1}
+    slots = (C.c_int32 * 2)(*[slot[t] for t in tasks])
+    sz = (C.c_int32 * 2)(*[sizes[t] for t in tasks])
+    t0 = math.nan if sa.initial_temperature is None else float(sa.initial_temperature)
+    _lib.call("go_anneal", context().handle, h.handle, k, words.ctypes.data, _lib.ptr(state),
+              _lib.ptr(best), top.num_devices, _lib.ptr(top.peak), _lib.ptr(top.mem_bw),
+              _lib.ptr(top.cap), _lib.ptr(top.link_bw), 0, int(sa.iterations),
+              int(sa.moves_per_step), t0, float(sa.cooling_rate), len(tasks), slots, sz,
+              _lib.ptr(best_time), stream_ptr())
+    bh = best.cpu().numpy().astype(np.int64)
+    th = best_time.cpu().numpy()
+    return [({t: bh[i, slot[t]].copy() for t in tasks}, float(th[i])) for i in range(k)]
+
+
+def _anneal_host_fusion(g, top, tasks, sa, fusion_config, seeds, start, sizes):
+    """Iteration-synchronous chains: every chain proposes from its own numpy stream, the
+    candidates' fusion passes run natively on host threads and their simulations are
+    batched on the device per distinct grouping, then every chain applies its
+    Metropolis test (baselines.py:183-204)."""
+    import math
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .fusion import fuse_groups
+    from .simulator import FusedGraph, simulate_many
+    n, k = g.num_nodes, len(seeds)
+    rngs = [np.random.default_rng(s) for s in seeds]
+    base = {t: start[t].actions for t in ("placement", "schedule_priority", "fusion_priority")}
+    cur = [{t: base[t].copy() for t in tasks} for _ in range(k)]
+
+    def score(states):
+        full = [{**base, **st} for st in states]
+        with ThreadPoolExecutor(max_workers=8) as ex:
+            maps = list(ex.map(lambda a: fuse_groups(g, a["fusion_priority"],
+                                                     fusion_config.max_group), full))
+        times = np.empty(len(full))
+        groups: dict = {}
+        for i, m in enumerate(maps):
+            groups.setdefault(m.tobytes(), []).append(i)
+        for ids in groups.values():
+            res = simulate_many(FusedGraph(g, maps[ids[0]]),
+                                np.stack([full[i]["placement"] for i in ids]),
+                                np.stack([full[i]["schedule_priority"] for i in ids]), top)
+            st, va = res.step_time.cpu().numpy(), res.valid.cpu().numpy()
+            for j, i in enumerate(ids):
+                times[i] = st[j] if va[j] else math.inf
+        return times
+
+    cur_t = score(cur)
+    best = [{t: c[t].copy() for t in tasks} for c in cur]
+    best_t = cur_t.copy()
+    temp = [sa.initial_temperature if sa.initial_temperature is not None
+            else (0.1 * x if math.isfinite(x) else 1.0) for x in cur_t]
     for _ in range(sa.iterations):
-        cand = {t: current[t].copy() for t in tasks}
-        for _ in range(sa.moves_per_step):
-            t = tasks[int(rng.integers(len(tasks)))]
-            v = int(rng.integers(n))
-            cand[t][v] = int(rng.integers(sizes[t]))
-        asg = dict(state)
-        for t in tasks:
-            asg[t] = ActionAssignment(t, cand[t], sizes[t])
-        cand_time = evaluate(asg)
-        delta = cand_time - cur_time
-        accept = delta <= 0
-        if not accept and temp > 0 and math.isfinite(delta):
-            accept = rng.random() < math.exp(-delta / temp)
-        if accept:
-            current = cand
-            cur_time = cand_time
-            if cur_time < best_time:
-                best_time = cur_time
-                best = {t: current[t].copy() for t in tasks}
-        temp *= sa.cooling_rate
-    result = dict(state)
-    for t in tasks:
-        result[t] = ActionAssignment(t, best[t], sizes[t])
-    return result, best_time
+        cand = []
+        for i in range(k):
+            c = {t: cur[i][t].copy() for t in tasks}
+            for _m in range(sa.moves_per_step):
+                t = tasks[int(rngs[i].integers(len(tasks)))]
+                v = int(rngs[i].integers(n))
+                c[t][v] = int(rngs[i].integers(sizes[t]))
+            cand.append(c)
+        cand_t = score(cand)
+        for i in range(k):
+            delta = cand_t[i] - cur_t[i]
+            ok = delta <= 0
+            if not ok and temp[i] > 0 and math.isfinite(delta):
+                ok = rngs[i].random() < math.exp(-delta / temp[i])
+            if ok:
+                cur[i], cur_t[i] = cand[i], cand_t[i]
+                if cur_t[i] < best_t[i]:
+                    best_t[i] = cur_t[i]
+                    best[i] = {t: cur[i][t].copy() for t in tasks}
+            temp[i] *= sa.cooling_rate
+    return [(best[i], float(best_t[i])) for i in range(k)]

@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include "engine.cuh"
+#include "rng.cuh"
 
 namespace go {
 
@@ -87,36 +88,28 @@ __device__ __forceinline__ auto& pick_state(A& sh, B& lo) {
   else return lo;
 }
 
-// MAXD: compile-time bound on the device count (4 / 8 / 16).  The per-placement link
-// arrays live in local memory; sizing them for 8 devices (64 links instead of 256) keeps
-// the 28 warps' working sets in L1: 2.14 -> 1.45 s for 4096 random cfg4 placements.
-template <int MAXD, bool SH>
-__global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
-                           int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
-                           int d, const double* __restrict__ peakf, const double* __restrict__ mbw,
-                           const double* __restrict__ cap, const double* __restrict__ lbw,
-                           int policy, double baseline, DesCaps caps, char* __restrict__ scratch,
-                           int64_t scratch_stride, const int32_t* __restrict__ which,
-                           double* __restrict__ o_step, uint8_t* __restrict__ o_valid,
-                           int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
-                           double* __restrict__ o_peak, double* __restrict__ o_reward,
-                           int32_t* __restrict__ o_status, int lanes_per_placement,
-                           DesTraceLog tr) {
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gtid % lanes_per_placement) return;
-  const int tid = gtid / lanes_per_placement;
-  if (tid >= K) return;
-  const int kk = which ? which[tid] : tid;
-  const int32_t* pl = placement + (int64_t)kk * pstride;
-  const int32_t* pr = prio + (int64_t)kk * prio_stride;
+// One placement's simulation: the reference's event loop (simulator.py:320-441) run by
+// one thread.  S (the per-placement device / link state) lives in shared memory when
+// the block is one placement (warp mode) -- local memory is interleaved across the
+// warp's 32 threads, so a single active lane pulled a whole 128-B line per word and
+// the warps' frames thrashed L1; `base` is this placement's global scratch (pending
+// counts, ready heaps, link FIFOs, memory lists).  Returns the status; step time and
+// violation (0 none, 1 colocation, 2 oom) through the references, busy / peak in S.
+// MAXD: compile-time bound on the device count (4 / 8 / 16): sizing the link arrays
+// for 8 devices (64 links instead of 256) took 4,096 random cfg4 placements from 2.14
+// to 1.45 s before the state moved to shared memory (0.56 s).
+template <int MAXD>
+__device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
+                       const int32_t* __restrict__ pr, int d, const double* __restrict__ peakf,
+                       const double* __restrict__ mbw, const double* __restrict__ cap,
+                       const double* __restrict__ lbw, int policy, DesCaps caps, char* base,
+                       DesState<MAXD>& S, DesTraceLog tr, double& step, int8_t& viol_out) {
   const int G = V.G;
-  char* base = scratch + (int64_t)tid * scratch_stride;
   int32_t* pending = reinterpret_cast<int32_t*>(base);
   int32_t* rem = pending + G;
   HeapEnt* heaps = reinterpret_cast<HeapEnt*>(base + round_up(2 * (int64_t)G * 4, 16));
   LinkEnt* lq = reinterpret_cast<LinkEnt*>(heaps + (int64_t)d * caps.cq);
   double* mlist = reinterpret_cast<double*>(lq + (int64_t)d * d * caps.cl);
-
   auto gdev = [&](int g) { return pl[V.grp_rep[g]]; };
   int64_t n_trace = 0;  // events logged (the single-placement trace launch only)
   auto log_event = [&](double t0, double t1, int kind, int a, int b, int g) {
@@ -135,12 +128,6 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
       }
   }
 
-  // per-placement device / link state: in shared memory when the block is one placement
-  // (warp mode) -- local memory is interleaved across the warp's 32 threads, so a single
-  // active lane pulled a whole 128-B line per word and the warps' frames thrashed L1
-  __shared__ DesState<SH ? MAXD : 1> sh_state;
-  DesState<SH ? 1 : MAXD> lo_state;
-  auto& S = pick_state<SH>(sh_state, lo_state);
   auto& dev_t = S.dev_t;
   auto& dev_g = S.dev_g;
   auto& hs = S.hs;
@@ -316,7 +303,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
 
   schedule(0.0);
   int done = 0;
-  double step = 0.0;
+  double step_t = 0.0;
   double mem_time = -1.0;
   while (status == ST_OK) {
     double now = DINF;
@@ -336,7 +323,7 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
       dev_t[dev] = DINF;
       dev_g[dev] = -1;
       ++done;
-      step = now;
+      step_t = now;
       for (int64_t e = V.out_off[g]; e < V.out_off[g + 1]; ++e) {
         int gd = V.out_grp[e];
         int dd = gdev(gd);
@@ -382,21 +369,54 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
     mem_flush();
     if (done != G) status = ST_DEADLOCK;
   }
-  o_status[tid] = status;
   if (tr.rec) *tr.count = n_trace;
-  if (status != ST_OK) return;
+  step = 0.0;
+  viol_out = viol;
+  if (status != ST_OK) return status;
+  step = step_t;
   if (!viol)
     for (int dev = 0; dev < d; ++dev)
       if (pk[dev] > cap[dev]) {
-        viol = 2;
+        viol_out = 2;
         break;
       }
+  return status;
+}
+
+template <int MAXD, bool SH>
+__global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
+                           int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
+                           int d, const double* __restrict__ peakf, const double* __restrict__ mbw,
+                           const double* __restrict__ cap, const double* __restrict__ lbw,
+                           int policy, double baseline, DesCaps caps, char* __restrict__ scratch,
+                           int64_t scratch_stride, const int32_t* __restrict__ which,
+                           double* __restrict__ o_step, uint8_t* __restrict__ o_valid,
+                           int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
+                           double* __restrict__ o_peak, double* __restrict__ o_reward,
+                           int32_t* __restrict__ o_status, int lanes_per_placement,
+                           DesTraceLog tr) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gtid % lanes_per_placement) return;
+  const int tid = gtid / lanes_per_placement;
+  if (tid >= K) return;
+  const int kk = which ? which[tid] : tid;
+  __shared__ DesState<SH ? MAXD : 1> sh_state;
+  DesState<SH ? 1 : MAXD> lo_state;
+  auto& S = pick_state<SH>(sh_state, lo_state);
+  double step;
+  int8_t viol;
+  const int status =
+      des_run<MAXD>(V, placement + (int64_t)kk * pstride, prio + (int64_t)kk * prio_stride, d,
+                    peakf, mbw, cap, lbw, policy, caps, scratch + (int64_t)tid * scratch_stride, S,
+                    tr, step, viol);
+  o_status[tid] = status;
+  if (status != ST_OK) return;
   o_step[kk] = step;
   o_valid[kk] = viol == 0;
   o_viol[kk] = viol;
   for (int dev = 0; dev < d; ++dev) {
-    if (o_busy) o_busy[(int64_t)kk * d + dev] = busy[dev];
-    if (o_peak) o_peak[(int64_t)kk * d + dev] = pk[dev];
+    if (o_busy) o_busy[(int64_t)kk * d + dev] = S.busy[dev];
+    if (o_peak) o_peak[(int64_t)kk * d + dev] = S.pk[dev];
   }
   if (o_reward && baseline > 0.0)
     o_reward[kk] = viol == 0 ? -sqrt(__ddiv_rn(step, baseline)) : -10.0;
@@ -475,6 +495,183 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
     }
   }
   return GO_OK;
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Simulated annealing on the device DES (baselines.py:146-206), many chains at once.
+//
+// One chain per 32-thread block: lane 0 runs the chain's numpy stream (PCG64 with the
+// Generator's buffered next_uint32 and Lemire bounded draws, rng.cuh), proposes the
+// move(s), simulates the candidate with des_run and applies the Metropolis test; the
+// warp copies the state into the best-so-far arrays on an improvement.  Every draw,
+// the float64 acceptance arithmetic and the geometric cooling follow the reference
+// line for line, so a chain seeded like SAConfig.seed walks exactly the reference's
+// chain (the step times it compares are bit-exact); the other chains are independent
+// restarts.  Moves are applied in place and undone on rejection.  Tasks annealed here:
+// placement and schedule_priority over a fixed grouping (fusion priorities change the
+// grouping, whose tables are built on the host).
+namespace {
+constexpr int SA_MAX_TASKS = 2;
+constexpr int SA_MAX_MOVES = 16;
+}
+
+template <int MAXD>
+__global__ void anneal_kernel(DesView V, int C, const uint64_t* __restrict__ rng_words,
+                              int32_t* __restrict__ cur, int32_t* __restrict__ best, int d,
+                              const double* __restrict__ peakf, const double* __restrict__ mbw,
+                              const double* __restrict__ cap, const double* __restrict__ lbw,
+                              int policy, int iterations, int moves, double t_init,
+                              double cooling, int ntasks, int task_slot0, int task_slot1,
+                              int size0, int size1, DesCaps caps, char* __restrict__ scratch,
+                              int64_t scratch_stride, double* __restrict__ o_best,
+                              int32_t* __restrict__ o_status) {
+  const int c = blockIdx.x;
+  if (c >= C) return;
+  const int lane = threadIdx.x;
+  const int n = V.n;
+  // arrays per chain: [placement | priorities], current and best
+  int32_t* cs = cur + (int64_t)c * 2 * n;
+  int32_t* bs = best + (int64_t)c * 2 * n;
+  __shared__ DesState<MAXD> S;
+  __shared__ double sh_time;
+  __shared__ int sh_flag;  // 1 = copy current -> best, -1 = stop (DES failure)
+  const int slot[SA_MAX_TASKS] = {task_slot0, task_slot1};
+  const int size[SA_MAX_TASKS] = {size0, size1};
+  Pcg64 rng;
+  char* base = scratch + (int64_t)c * scratch_stride;
+  double cur_time = 0.0, best_time = 0.0, temp = 0.0;
+  auto evaluate = [&](double& t) -> int {
+    double step;
+    int8_t viol;
+    const int stt = des_run<MAXD>(V, cs, cs + n, d, peakf, mbw, cap, lbw, policy, caps, base, S,
+                                  DesTraceLog{nullptr, 0, nullptr}, step, viol);
+    t = viol == 0 ? step : DINF;
+    return stt;
+  };
+  if (lane == 0) {
+    rng.state = ((u128)rng_words[4 * c] << 64) | rng_words[4 * c + 1];
+    rng.inc = ((u128)rng_words[4 * c + 2] << 64) | rng_words[4 * c + 3];
+    rng.has32 = false;
+    rng.buf32 = 0;
+    const int stt = evaluate(cur_time);
+    best_time = cur_time;
+    temp = t_init == t_init ? t_init : (isfinite(cur_time) ? 0.1 * cur_time : 1.0);
+    sh_flag = stt == ST_OK ? 0 : -1;
+    o_status[c] = stt;
+  }
+  __syncwarp();
+  if (sh_flag < 0) return;
+  int mv_slot[SA_MAX_MOVES], mv_node[SA_MAX_MOVES], mv_old[SA_MAX_MOVES];
+  for (int it = 0; it < iterations; ++it) {
+    if (lane == 0) {
+      for (int m = 0; m < moves; ++m) {
+        const int t = (int)rng.bounded((uint32_t)(ntasks - 1));  // rng.integers(len(tasks))
+        const int v = (int)rng.bounded((uint32_t)(n - 1));       // rng.integers(n)
+        const int val = (int)rng.bounded((uint32_t)(size[t] - 1));
+        int32_t* arr = cs + (int64_t)slot[t] * n;
+        mv_slot[m] = slot[t];
+        mv_node[m] = v;
+        mv_old[m] = arr[v];
+        arr[v] = val;
+      }
+      double cand;
+      const int stt = evaluate(cand);
+      int flag = 0;
+      if (stt != ST_OK) {
+        o_status[c] = stt;
+        flag = -1;
+      } else {
+        const double delta = cand - cur_time;
+        bool accept = delta <= 0.0;
+        if (!accept && temp > 0.0 && isfinite(delta))
+          accept = rng.random() < exp(__ddiv_rn(-delta, temp));
+        if (accept) {
+          cur_time = cand;
+          if (cur_time < best_time) {
+            best_time = cur_time;
+            flag = 1;
+          }
+        } else {
+          for (int m = moves - 1; m >= 0; --m) cs[(int64_t)mv_slot[m] * n + mv_node[m]] = mv_old[m];
+        }
+        temp = __dmul_rn(temp, cooling);
+      }
+      sh_flag = flag;
+    }
+    __syncwarp();
+    const int flag = sh_flag;
+    if (flag < 0) return;
+    if (flag == 1) {
+      for (int64_t i = lane; i < 2 * (int64_t)n; i += 32) bs[i] = cs[i];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) o_best[c] = best_time;
+}
+
+int anneal_chains(const DesView& v, int C, const uint64_t* rng_words_host, int32_t* cur,
+                  int32_t* best, int d, const double* peak, const double* mem_bw,
+                  const double* cap, const double* link_bw, int policy, int iterations,
+                  int moves, double t_init, double cooling, int ntasks, const int* slots,
+                  const int* sizes, double* best_time, go_ctx* ctx, cudaStream_t st) {
+  GO_CHECK(C >= 1 && ntasks >= 1 && ntasks <= SA_MAX_TASKS, "bad annealing configuration");
+  GO_CHECK(moves >= 1 && moves <= SA_MAX_MOVES, "moves_per_step must be in [1, %d]", SA_MAX_MOVES);
+  if (d > DES_MAXD) GO_THROW(GO_ERR_UNSUPPORTED, "%d devices > %d", d, DES_MAXD);
+  std::vector<double> topo(3 * d + d * d);
+  for (int i = 0; i < d; ++i) {
+    topo[i] = peak[i];
+    topo[d + i] = mem_bw[i];
+    topo[2 * d + i] = cap[i];
+  }
+  for (int i = 0; i < d * d; ++i) topo[3 * d + i] = link_bw[i];
+  const int G = v.G;
+  auto run = [&](DesCaps caps) {
+    const int64_t stride = caps.per_placement_bytes(G, d);
+    const int64_t head = round_up((int64_t)topo.size() * 8, 256) + round_up((int64_t)C * 32, 256) +
+                         round_up((int64_t)C * 4, 256);
+    char* ws = reinterpret_cast<char*>(ctx->ensure_des(head + stride * C));
+    double* dtopo = reinterpret_cast<double*>(ws);
+    uint64_t* dwords = reinterpret_cast<uint64_t*>(ws + round_up((int64_t)topo.size() * 8, 256));
+    int32_t* dstatus =
+        reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dwords) + round_up((int64_t)C * 32, 256));
+    CUDA_CHECK(cudaMemcpyAsync(dtopo, topo.data(), topo.size() * 8, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(dwords, rng_words_host, (size_t)C * 32, cudaMemcpyHostToDevice, st));
+    auto kern = d <= 4 ? anneal_kernel<4> : d <= 8 ? anneal_kernel<8> : anneal_kernel<DES_MAXD>;
+    kern<<<C, 32, 0, st>>>(v, C, dwords, cur, best, d, dtopo, dtopo + d, dtopo + 2 * d,
+                           dtopo + 3 * d, policy, iterations, moves, t_init, cooling, ntasks,
+                           slots[0], ntasks > 1 ? slots[1] : 0, sizes[0],
+                           ntasks > 1 ? sizes[1] : 1, caps, ws + head, stride, best_time, dstatus);
+    LAUNCH_CHECK();
+    std::vector<int32_t> hs(C);
+    CUDA_CHECK(cudaMemcpyAsync(hs.data(), dstatus, (size_t)C * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    return hs;
+  };
+  // small queues first; a chain whose heap / link FIFO overflowed makes the whole launch
+  // re-run from the saved initial state with capacities that cannot overflow
+  const size_t state_bytes = (size_t)C * 2 * v.n * sizeof(int32_t);
+  int32_t* saved = nullptr;
+  CUDA_CHECK(cudaMallocAsync(&saved, state_bytes, st));
+  CUDA_CHECK(cudaMemcpyAsync(saved, cur, state_bytes, cudaMemcpyDeviceToDevice, st));
+  std::vector<int32_t> stat = run(DesCaps{64, 64, 64});
+  bool redo = false;
+  for (int s : stat) {
+    if (s == ST_DEADLOCK) GO_THROW(GO_ERR_DEADLOCK, "simulation deadlocked");
+    redo |= s != ST_OK;
+  }
+  if (redo) {
+    CUDA_CHECK(cudaMemcpyAsync(cur, saved, state_bytes, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(best, saved, state_bytes, cudaMemcpyDeviceToDevice, st));
+    stat = run(DesCaps{std::max<int64_t>(G, 1), std::max<int64_t>(v.num_edges, 1),
+                       std::max<int64_t>(G, 1)});
+    for (int s : stat)
+      if (s != ST_OK)
+        GO_THROW(s == ST_DEADLOCK ? GO_ERR_DEADLOCK : GO_ERR_UNSUPPORTED,
+                 "simulation failed (status %d)", s);
+  }
+  CUDA_CHECK(cudaFreeAsync(saved, st));
+  return 0;
 }
 
 }  // namespace go

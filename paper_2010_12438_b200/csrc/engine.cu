@@ -1071,4 +1071,31 @@ int go_simulate_trace(go_ctx_t ctx, go_graph_t g, const int32_t* placement,
   });
 }
 
+int go_anneal(go_ctx_t ctx, go_graph_t g, int32_t chains, const uint64_t* rng_words,
+              int32_t* state, int32_t* best, int32_t d, const double* peak, const double* mem_bw,
+              const double* cap, const double* link_bw, int32_t policy, int32_t iterations,
+              int32_t moves_per_step, double initial_temperature, double cooling_rate,
+              int32_t num_tasks, const int32_t* task_slots, const int32_t* task_sizes,
+              double* best_time, void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    GO_CHECK(policy == 0 || policy == 1, "unknown policy");
+    GO_CHECK(iterations >= 1, "iterations must be >= 1");
+    GO_CHECK(cooling_rate > 0.0 && cooling_rate < 1.0, "cooling_rate must be in (0,1)");
+    GO_CHECK(g->acyclic, "the annealed grouping has a cycle");
+    GO_CHECK(num_tasks >= 1 && num_tasks <= 2, "1 or 2 annealed tasks");
+    int slots[2] = {0, 0}, sizes[2] = {1, 1};
+    for (int t = 0; t < num_tasks; ++t) {
+      GO_CHECK(task_slots[t] == 0 || task_slots[t] == 1, "task slot must be 0 or 1");
+      GO_CHECK(task_sizes[t] >= 1, "empty action space");
+      slots[t] = task_slots[t];
+      sizes[t] = task_sizes[t];
+    }
+    GO_CHECK(g->n >= 1, "empty graph");
+    anneal_chains(g->des, chains, rng_words, state, best, d, peak, mem_bw, cap, link_bw, policy,
+                  iterations, moves_per_step, initial_temperature, cooling_rate, num_tasks, slots,
+                  sizes, best_time, ctx, (cudaStream_t)stream);
+  });
+}
+
 }  // extern "C"

@@ -292,6 +292,13 @@ void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t
                  int32_t* actions, double* logp, cudaStream_t st);
 
 // ---- kernels: des.cu
+// device simulated annealing, C chains (des.cu anneal_kernel); cur / best: dev
+// [C][2][n] (placement | priorities), both initialised to the start state by the caller
+int anneal_chains(const DesView& v, int C, const uint64_t* rng_words_host, int32_t* cur,
+                  int32_t* best, int d, const double* peak, const double* mem_bw,
+                  const double* cap, const double* link_bw, int policy, int iterations,
+                  int moves, double t_init, double cooling, int ntasks, const int* slots,
+                  const int* sizes, double* best_time, go_ctx* ctx, cudaStream_t st);
 struct DesTraceRec {  // one started compute / transfer of a traced simulation
   double t0, t1;
   int32_t kind, a, b, grp;

@@ -22,9 +22,10 @@
 // that drift reached 1.4e-4 of the logits.  So O accumulates in TMEM over only DRAIN = 8
 // key tiles; at each group boundary the softmax thread, which owns its row, reads the
 // 16 O columns and adds them into a float sum in shared memory (IEEE round-to-nearest,
-// ~160 additions at 80k keys), and the MMA thread restarts the accumulator.  Measured
-// at cfg4 (scripts/parity_variants.py): logits 1.41e-4 -> 4.8e-6 normwise from float64,
-// kernel time unchanged (Kahan compensation or DRAIN = 16 / 32: 5.6e-6 / 7.6e-6).  The drain needs no extra barrier: S(j) is
+// ~80 additions at 80k keys, two columns per packed FADD2), and the MMA thread restarts
+// the accumulator.  Measured at cfg4 (scripts/parity_variants.py): logits 1.41e-4 ->
+// 5.6e-6 normwise from float64 (DRAIN = 8: 4.8e-6 for twice the drain instructions;
+// 32: 7.6e-6).  The drain needs no extra barrier: S(j) is
 // issued after PV(j-1) by the same thread and tcgen05 MMAs complete in order, so when
 // s_full(j) fires O holds exactly tiles [.., j-1], and PV(j) (accumulate = 0) waits for
 // p_full(j), which this thread signals only after the drain.
@@ -52,7 +53,7 @@ constexpr int KT = 64;   // keys per K/V tile (tile tables shared with the tf32 
 constexpr int QT = 128;  // queries per M tile
 constexpr int NQT = 3;   // M tiles per CTA
 constexpr int NS = 8;    // K/V ring stages
-constexpr int DRAIN = 8; // key tiles per TMEM accumulation group
+constexpr int DRAIN = 16;  // key tiles per TMEM accumulation group
 constexpr int NP = 4;    // of every 8 exponential pairs, NP on the FMA-pipe polynomial
 constexpr int TILE_BYTES = KT * 16 * 2;
 constexpr int PRODUCER_WARP = NQT * 4;
@@ -69,7 +70,7 @@ constexpr float RANGE_LIMIT = 60000.f;
 struct Smem {
   uint16_t q[NQT][QT * 16];
   uint16_t kv[NS][2][KT * 16];
-  float osum[NQT][16][QT];   // sum of the drained O groups, [tile][column][row]
+  float4 osum[NQT][4][QT];   // sum of the drained O groups, [tile][column/4][row]
   uint64_t kv_full[NS], kv_empty[NS];
   uint64_t s_full[NQT], p_full[NQT], o_done[NQT];
   uint32_t tmem_base;
@@ -89,6 +90,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// {a.x + b.x, a.y + b.y} in one packed fp32 add (FADD2), IEEE round-to-nearest
+__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+  return *reinterpret_cast<const float2*>(&r);
 }
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   uint32_t r;
@@ -220,23 +229,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t base = tbase + lane_off + t * S_COLS;
     const uint32_t obase = tbase + lane_off + O_COL + t * 16;
-    float* osum = &sm.osum[t][0][row];
+    float4* osum = &sm.osum[t][0][row];
 #pragma unroll
-    for (int d = 0; d < 16; ++d) osum[d * QT] = 0.f;
+    for (int c = 0; c < 4; ++c) osum[c * QT] = make_float4(0.f, 0.f, 0.f, 0.f);
     auto drain = [&]() {  // O of the group just finished -> float sum in smem
       uint32_t r[16];
       PTX_LD16(obase, r);
       tmem_wait_ld();
 #pragma unroll
-      for (int d = 0; d < 16; ++d) {
-        osum[d * QT] += __uint_as_float(r[d]);
+      for (int c = 0; c < 4; ++c) {
+        float4 a = osum[c * QT];
+        const float2 lo = add_f32x2(make_float2(a.x, a.y),
+                                    make_float2(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1])));
+        const float2 hi = add_f32x2(make_float2(a.z, a.w),
+                                    make_float2(__uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3])));
+        osum[c * QT] = make_float4(lo.x, lo.y, hi.x, hi.y);
       }
     };
     uint32_t ra[16], rb[16], pk[8];
-    for (int j = 0; j < T; ++j) {
+    auto tile = [&](int j, bool drain_first) {
       mbar_wait_sleep(&sm.s_full[t], j & 1);
       fence_after();
-      if (j > 0 && j % DRAIN == 0) drain();  // O = tiles [j - DRAIN, j), stable here
+      if (drain_first) drain();  // O = tiles [j - DRAIN, j), stable once s_full(j) fired
       PTX_LD16_AT(base, 0, ra);
       tmem_wait_ld();
       PTX_LD16_AT(base, 16, rb);
@@ -256,15 +270,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       tmem_wait_st();
       fence_before();
       mbar_arrive(&sm.p_full[t]);
+    };
+    for (int g0 = 0; g0 < T; g0 += DRAIN) {  // groups of DRAIN key tiles
+      const int g1 = min(g0 + DRAIN, T);
+      for (int j = g0; j < g1; ++j) tile(j, j == g0 && g0 > 0);
     }
     mbar_wait_sleep(&sm.o_done[t], 0);
     fence_after();
     if (T > 0) drain();
     const int lr = w.q0 + t * QT + row;
     if (lr < w.n) {
-      const float inv = 1.f / osum[15 * QT];
+      float v[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 a = osum[c * QT];
+        v[4 * c] = a.x;
+        v[4 * c + 1] = a.y;
+        v[4 * c + 2] = a.z;
+        v[4 * c + 3] = a.w;
+      }
+      const float inv = 1.f / v[15];
       float* o = out + (w.row0 + lr) * ldo + head * d_head;
-      for (int d = 0; d < d_head; ++d) o[d] = osum[d * QT] * inv;
+      for (int d = 0; d < d_head; ++d) o[d] = v[d] * inv;
     }
   }
   fence_before();

@@ -748,9 +748,78 @@ def make_perturb():
     np.savez_compressed(OUT / "golden_perturb.npz", **out)
 
 
+def make_sa_chains():
+    """simulated_annealing (baselines.py:146-206) for 8 seeds per case, so the device's
+    multi-chain annealing can be checked chain by chain: a 40-node multi-branch CNN on
+    4 devices (placement), a random DAG annealing placement + schedule priorities with
+    2 moves per step and a fixed initial temperature, and a fusion case."""
+    from graphopt.baselines import SAConfig, simulated_annealing
+    from graphopt.costmodel import uniform_topology
+    out = {}
+    rng = np.random.default_rng(31)
+    cases = [("mbc", gen_workload(WorkloadSpec("multi-branch-cnn", 5, 1, 64, seed=0)),
+              uniform_topology(4), ["placement"], dict(iterations=800, cooling_rate=0.995)),
+             ("rand", C.random_graph(rng, 30, p_edge=0.25), rand_topology(rng, 3),
+              ["schedule_priority", "placement"],
+              dict(iterations=500, cooling_rate=0.99, moves_per_step=2,
+                   initial_temperature=2e-4)),
+             ("fuse", C.random_graph(rng, 14, p_edge=0.3, fusible_only=True),
+              rand_topology(rng, 2), ["fusion_priority", "placement"],
+              dict(iterations=150, cooling_rate=0.99))]
+    for name, g, top, tasks, kw in cases:
+        p = name + "/"
+        graph_arrays(g, p, out)
+        topo_arrays(top, p, out)
+        out[p + "tasks"] = np.array(tasks)
+        out[p + "sa"] = np.array(json.dumps(kw))
+        for seed in range(8):
+            res, t = simulated_annealing(g, top, tasks, SAConfig(seed=seed, **kw))
+            out[p + f"s{seed}/time"] = np.float64(t)
+            for tk in tasks:
+                out[p + f"s{seed}/{tk}"] = res[tk].actions
+    np.savez_compressed(OUT / "golden_sa_chains.npz", **out)
+
+
+def make_cfg2():
+    """The UNMODIFIED reference at BASELINE cfg2 (multi-branch-cnn, 13,000 nodes, 4
+    devices, default networks; its tape holds ~15 GB for the heads): iterate_decisions
+    with 2 iterations, then the DES.  Stored compactly -- per-row logit sums of both
+    iterations, logits of 512 seeded rows, both iterations' actions, embedding row
+    sums, the value and the step time -- so the oracle (and through it the device
+    path, tests/test_gpu_headline.py) is pinned to the reference at a headline size,
+    not only on the small fixtures."""
+    from graphopt.costmodel import uniform_topology
+    out = {}
+    g = gen_workload(WorkloadSpec("multi-branch-cnn", 1857, 1, 64, seed=0), node_cap=10**6)
+    top = uniform_topology(4)
+    sizes = {"placement": 4}
+    ecfg, pcfg = EmbedConfig(), PolicyConfig()
+    store = init_all_params(ecfg, pcfg, sizes, seed=0)
+    randomize(store)
+    rows = np.sort(np.random.default_rng(5).choice(g.num_nodes, 512, replace=False))
+    feats = node_features(g, None, [4])
+    emb = embed(g, feats, store, ecfg, seed=77)
+    out["node_embed_rowsum"] = emb.node_embed.data.sum(axis=1)
+    out["graph_embed"] = emb.graph_embed.data
+    bundle, traj = iterate_decisions(g, store, ecfg, pcfg, sizes, 2, 77)
+    for it, b in enumerate(traj):
+        lg = b.logits["placement"]
+        out[f"it{it}/logit_rowsum"] = lg.sum(axis=1)
+        out[f"it{it}/logits_rows"] = lg[rows]
+        out[f"it{it}/actions"] = b.actions["placement"]
+        out[f"it{it}/logp"] = b.log_probs["placement"]
+        out[f"it{it}/value"] = np.float64(b.value)
+    res = simulate(singleton_fused(g), ActionAssignment("placement", bundle.actions["placement"], 4),
+                   ActionAssignment.constant("schedule_priority", g.num_nodes, 8), top)
+    out["rows"] = rows
+    out["step_time"] = np.float64(res.step_time)
+    out["seed"] = np.int64(77)
+    np.savez_compressed(OUT / "golden_cfg2.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "forward", "des", "sample", "rollouts", "ppo", "ppo1", "workloads", "grads",
-                             "baselines", "rollouts_joint", "json", "train", "fusion", "trace", "perturb"]
+                             "baselines", "rollouts_joint", "json", "train", "fusion", "trace", "perturb", "sa_chains", "cfg2"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

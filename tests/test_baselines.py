@@ -82,3 +82,24 @@ def test_simulated_annealing_matches_reference():
         assert t == float(z[p + "time"]), (i, tasks)
         for tk in tasks:
             assert np.array_equal(res[tk].actions, z[p + "actions/" + tk]), (i, tk)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["mbc", "rand", "fuse"])
+def test_anneal_chains_each_chain_is_the_reference_chain(case):
+    """anneal_chains runs 8 chains at once (on the device for placement / priorities,
+    device DES per candidate with host fusion passes for fusion priorities); chain k
+    must end exactly where the reference's simulated_annealing with seed k ends
+    (golden_sa_chains.npz): same best time, same best actions."""
+    import json
+
+    from paper_2010_12438_b200.baselines import SAConfig, anneal_chains
+    z = golden("sa_chains")
+    p = case + "/"
+    tasks = [str(t) for t in z[p + "tasks"]]
+    sa = SAConfig(**json.loads(str(z[p + "sa"])))
+    out = anneal_chains(_g(z, p), _topology(z, p), tasks, sa, seeds=range(8))
+    for seed, (res, t) in enumerate(out):
+        assert t == float(z[p + f"s{seed}/time"]), (seed, t)
+        for tk in tasks:
+            assert np.array_equal(res[tk].actions, z[p + f"s{seed}/{tk}"]), (seed, tk)

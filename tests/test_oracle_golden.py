@@ -168,3 +168,34 @@ def test_row_subset_heads_and_per_row_sampler_match_full_oracle():
                               step["logits"]["placement"], step["logits"]["placement"],
                               g["topo"], np.arange(n), 11, it, 0, 1)
         assert rep["flips"] == 0 and rep["logp_max_abs_err"] == 0.0, rep
+
+
+def test_oracle_matches_unmodified_reference_at_cfg2():
+    """The float64 oracle (tape-free, layer-major trunk, row-chunked heads: 'ref-lean',
+    SURVEY §8(d) D4) against the UNMODIFIED reference at BASELINE cfg2 (13,000 nodes,
+    golden_cfg2.npz): both iterations' logits to 1e-9, every action identical, the DES
+    step time bit-exact.  The device's headline parity tests check against this oracle."""
+    from synthetic.workloads import WorkloadSpec, gen_workload
+    z = golden("cfg2")
+    g = gen_workload(WorkloadSpec("multi-branch-cnn", 1857, 1, 64, seed=0), node_cap=10**6)
+    ogr = og.make(g.num_nodes, g.op, g.flops, g.out_bytes, g.src, g.dst, g.ebytes)
+    ecfg, pcfg = of.EmbedCfg(), of.PolicyCfg()
+    P = op.randomize_zero_init(op.init_all_params(ecfg, pcfg, {"placement": 4}, 0))
+    seed = int(z["seed"])
+    feats = og.node_features(ogr, None, [4])
+    ne, ge = of.embed(ogr, feats, P, ecfg, seed=seed)
+    assert np.allclose(ne.sum(axis=1), z["node_embed_rowsum"], rtol=1e-10, atol=1e-10)
+    assert np.allclose(ge, z["graph_embed"], rtol=1e-11, atol=1e-12)
+    traj = of.iterate_decisions(ogr, P, ecfg, pcfg, {"placement": 4}, 2, seed)
+    rows = z["rows"]
+    for it, step in enumerate(traj):
+        lg = step["logits"]["placement"]
+        assert np.allclose(lg[rows], z[f"it{it}/logits_rows"], rtol=1e-9, atol=1e-11), it
+        assert np.allclose(lg.sum(axis=1), z[f"it{it}/logit_rowsum"], rtol=1e-9, atol=1e-10)
+        assert np.array_equal(step["actions"]["placement"], z[f"it{it}/actions"]), it
+        assert np.allclose(step["log_probs"]["placement"], z[f"it{it}/logp"], rtol=1e-9,
+                           atol=1e-11)
+        assert abs(step["value"] - float(z[f"it{it}/value"])) < 1e-9
+    res = od.simulate(ogr, od.singleton(ogr), traj[-1]["actions"]["placement"],
+                      np.zeros(ogr["n"]), od.uniform_topology(4))
+    assert res["step_time"] == float(z["step_time"])
