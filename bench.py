@@ -16,6 +16,7 @@ results read back every step.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -23,6 +24,7 @@ import subprocess
 import sys
 import tempfile
 import time
+import types
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -58,6 +60,9 @@ def parse():
                     help="placements per step (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--mode", default="R", choices=["R", "S"],
+                    help="R: reference semantics, own forwards per placement (headline); "
+                         "S: one shared forward per step, K placements sampled from it")
     return ap.parse_args()
 
 
@@ -373,13 +378,44 @@ def workload_config(args, w):
             f"{x.num_nodes}" for x in w["graphs"]) + "-node dilated stacks (graph drawn "
             "per rollout)")
     tdesc = "+".join(w["sizes"]) if len(w["sizes"]) > 1 else f"{w['d']}-device placement"
+    mode = getattr(args, "mode", "R")
+    mdesc = ("mode R (own neighbour sample + 2 forwards per placement)" if mode == "R" else
+             "mode S (one shared forward per step, iterations=1, every placement sampled "
+             "from its logits with its own stream)")
     return {"workload": f"{args.workload}: {gdesc}, {tdesc}, "
                         f"{args.placements or w['k']} placements/step sharded over ranks, "
-                        "mode R (own neighbour sample + 2 forwards per placement)",
+                        + mdesc,
+            "mode": mode,
             "nodes": w["graph"].num_nodes, "devices": w["d"], "tasks": list(w["sizes"]),
-            "placements_per_step": args.placements or w["k"], "iterations": 2,
+            "placements_per_step": args.placements or w["k"],
+            "iterations": 2 if mode == "R" else 1,
             "weights": "init_all_params(seed=0) + zero-init tensors refilled U(+-1/sqrt(fan_in))",
             "l2": "inputs larger than L2 (per-step activations >> 126 MB); no explicit flush"}
+
+
+def des_events_per_placement(batch, graphs):
+    """Mean DES events per placement of a rollout batch (simulator.py:353-406): one
+    compute per group (singleton groups: every node) plus one transfer per edge whose
+    endpoints sit on different devices."""
+    import torch
+    edges = [(torch.as_tensor(g.src, device="cuda", dtype=torch.int64),
+              torch.as_tensor(g.dst, device="cuda", dtype=torch.int64)) for g in graphs]
+    tot, cnt = 0.0, 0
+    if hasattr(batch, "placements"):  # mode S: [K, n] placements of the single graph
+        src, dst = edges[0]
+        pl = batch.placements.long()
+        return float(graphs[0].num_nodes + (pl[:, src] != pl[:, dst]).sum(1).double().mean())
+    for w in batch._waves:
+        acts = w.iters[-1]["actions"][0]
+        for j, k in enumerate(w.idx):
+            gi = int(batch.graph_index[k])
+            n = graphs[gi].num_nodes
+            src, dst = edges[gi]
+            lo = int(w.row_off[j])
+            pl = acts[lo:lo + n].long()
+            tot += n + float((pl[src] != pl[dst]).sum())
+            cnt += 1
+    return tot / max(1, cnt)
 
 
 def main():
@@ -412,13 +448,41 @@ def main():
     hyper = PPOHyper(rollouts=K)
     ctx = context()
 
-    def step(s, store):
-        """One step: this rank's shard of the K placements (global rollout ids
+    def step_r(s, store):
+        """Mode R step: this rank's shard of the K placements (global rollout ids
         [rank*K/world, (rank+1)*K/world) of the step's outer stream)."""
         batch = collect_rollouts(store, graphs, top, sizes, bl, K, 1000 + s, hyper, w["ecfg"],
                                  w["pcfg"], FusionConfig(), base_assignments=base,
                                  keep_logits=False, shard=(rank, world))
         return batch
+
+    pcfg_s = dataclasses.replace(w["pcfg"], iterations=1)
+
+    def step_s(s, store):
+        """Mode S step: ONE forward of the graph per step (iterations
+        = 1, embed seed = the step's first rollout seed), this rank's K/world placements
+        sampled from its logits with their own numpy streams (shared-logits sampler),
+        one batched DES launch with the reward fused in."""
+        from paper_2010_12438_b200.engine import forward_batch, pcg_words, sample_batch
+        from paper_2010_12438_b200.simulator import simulate_many, singleton_fused
+        from paper_2010_12438_b200.training import outer_draws, shard_bounds
+        _gi, seeds = outer_draws(1000 + s, K, 1)
+        lo, hi = shard_bounds(K, rank, world)
+        h = ctx.graph(g)
+        out = forward_batch(store, w["ecfg"], pcfg_s, sizes, [h], [int(seeds[0])])
+        words = [pcg_words(np.random.default_rng(int(x))) for x in seeds[lo:hi]]
+        acts, _logp = sample_batch(w["ecfg"], pcfg_s, sizes, [h] * (hi - lo), words,
+                                   out.logits_packed, 1.0, shared_logits=True)
+        pl = acts[0].view(hi - lo, g.num_nodes)
+        res = simulate_many(singleton_fused(g), pl, base[0]["schedule_priority"].actions, top,
+                            baseline=bl[0])
+        return types.SimpleNamespace(rewards=res.reward, step_times=res.step_time,
+                                     valid=res.valid, values=out.value.expand(hi - lo),
+                                     placements=pl)
+
+    if args.mode == "S" and (len(graphs) > 1 or len(sizes) > 1):
+        raise SystemExit("mode S is defined for single-graph placement workloads")
+    step = step_s if args.mode == "S" else step_r
 
     store = w["store"]
     params_on_device(store, w["ecfg"], w["pcfg"], sizes)  # resident before timing
@@ -444,7 +508,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     stats = {}
     for cls, name in ((0, "heads_attention"), (1, "trunk_attention"), (2, "segment_max"),
-                      (4, "des")):
+                      (4, "des"), (5, "sampler")):
         import ctypes as C
         cnt, tms, work = C.c_int64(), C.c_double(), C.c_double()
         _lib.call("go_ctx_kernel_stats", ctx.handle, cls, C.byref(cnt), C.byref(tms),
@@ -489,7 +553,8 @@ def main():
     mufu = mufu_peak()
     ncu = ncu_traffic()
     cnt, hms, hflops = stats["heads_attention"]
-    n_fwd = K * args.steps * 2 // max(1, world)  # forwards this rank ran in the timed region
+    # forwards this rank ran in the timed region
+    n_fwd = (K * 2 // max(1, world) if args.mode == "R" else 1) * args.steps
     fwd_per_launch = n_fwd / cnt if cnt else 0.0
     roof = None
     if cnt:
@@ -522,6 +587,27 @@ def main():
                                 if "segment_max_bytes_per_forward_per_layer" in ncu else None),
                     "launches": cnt2, "avg_launch_ms": sms / cnt2,
                     "algorithmic_bytes_per_launch": sbytes / cnt2, "share_of_step": sms / ms}
+    # sampler: HBM-bound streaming pass (logits in, action + log-prob out per row and task)
+    cnt3, sams, sambytes = stats["sampler"]
+    roof_sampler = None
+    if cnt3:
+        ach = sambytes / (sams / 1000.0) / 1e9
+        roof_sampler = {"bound": "hbm", "kernel": "categorical sampler (sample_rows)",
+                        "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "bytes_per_row_and_task": "4a (fp32 logits) + 4 (int32 action) + "
+                                                  "8 (float64 log-prob)",
+                        "launches": cnt3, "avg_launch_ms": sams / cnt3,
+                        "share_of_step": sams / ms}
+    # DES: latency-bound event chains; events = group computes + cross-device transfers
+    cnt4, dms, _dw = stats["des"]
+    des_line = None
+    if cnt4:
+        ev = des_events_per_placement(b, graphs)
+        des_line = {"bound": "latency (one dependent event chain per placement, all "
+                             "placements resident)",
+                    "events_per_placement": ev, "placements_per_launch": K // max(1, world),
+                    "events_per_s": ev * K * args.steps / max(1, world) / (dms / 1000.0),
+                    "launches": cnt4, "avg_launch_ms": dms / cnt4, "share_of_step": dms / ms}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -529,7 +615,8 @@ def main():
         "config": workload_config(args, w),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "roofline": roof, "roofline_aggregation": roof_agg,
+        "roofline": roof, "roofline_aggregation": roof_agg, "roofline_sampler": roof_sampler,
+        "des": des_line,
         "kernel_ms": {k: v[1] / max(1, args.steps) for k, v in stats.items()},
         "gpu_launches": int(launches), "clocks": clk,
     }

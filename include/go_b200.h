@@ -182,12 +182,14 @@ int go_neighbor_arrays(go_ctx_t ctx, go_graph_t g, int64_t seed, int32_t k,
  * state_lo, inc_hi, inc_lo) of each forward's numpy PCG64 generator *before* this
  * call; row r of task t consumes draw t*n_f + r (policy.py:235, 299-306: rng.random
  * per task in canonical order).  The caller advances its generators by T*n_f draws.
- * logits dev [T][rows, a_t] float32 or float64 (logits_f64 flag).  actions_out dev
+ * logits dev [T][rows, a_t] float32 or float64 (logits_flags bit 0); with bit 1 set
+ * every forward reads the SAME logits block, [T][rows of forward 0, a_t] (mode S: many
+ * placements sampled from one forward).  actions_out dev
  * int32 [T][rows]: node-indexed within each forward's span (row order when graphs is
  * NULL); logp_out dev float64 [T][rows], topo-row indexed. */
 int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards,
               const go_graph_t* graphs, const int64_t* row_counts,
-              const uint64_t* pcg_states, const void* logits, int32_t logits_f64,
+              const uint64_t* pcg_states, const void* logits, int32_t logits_flags,
               double temperature, int32_t* actions_out, double* logp_out, void* stream);
 
 /* PPO loss and parameter gradient of one minibatch (replaces training.py:146-227:

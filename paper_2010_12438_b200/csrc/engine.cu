@@ -971,7 +971,7 @@ int go_neighbor_arrays(go_ctx_t ctx, go_graph_t g, int64_t seed, int32_t k, int6
 
 int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards, const go_graph_t* graphs,
               const int64_t* row_counts, const uint64_t* pcg_states, const void* logits,
-              int32_t logits_f64, double temperature, int32_t* actions_out, double* logp_out,
+              int32_t logits_flags, double temperature, int32_t* actions_out, double* logp_out,
               void* stream) {
   return guarded([&] {
     CUDA_CHECK(cudaSetDevice(ctx->device));
@@ -994,12 +994,25 @@ int go_sample(go_ctx_t ctx, const go_config_t* cfg, int32_t num_forwards, const 
     row_node_fill(m.d_views, m.d_row_off, row_fwd, m.R, row_node, st);
     int64_t col = 0;
     const int T = cfg->num_tasks;
+    const int logits_f64 = logits_flags & 1;
+    const bool shared = (logits_flags & 2) != 0;  // all forwards read forward 0's block
+    const int64_t lrows = shared ? m.row_off[1] - m.row_off[0] : m.R;
+    GO_CHECK(!shared || [&] {
+      for (int f = 1; f < m.F; ++f)
+        if (m.row_off[f + 1] - m.row_off[f] != lrows) return false;
+      return true;
+    }(), "shared logits need forwards of equal row count");
+    double bytes = 0;  // logits in, int32 action + float64 log-prob out, per row and task
+    for (int t = 0; t < T; ++t)
+      bytes += (double)m.R * ((logits_f64 ? 8.0 : 4.0) * cfg->task_sizes[t] + 12.0);
+    KTimer kt(ctx, K_SAMPLE, st, bytes);
     for (int t = 0; t < T; ++t) {
       int a = cfg->task_sizes[t];
       const char* lp = reinterpret_cast<const char*>(logits) + col * (logits_f64 ? 8 : 4);
       sample_rows(lp, logits_f64, a, a, m.R, m.d_row_off, row_fwd, row_node, dstate, t,
-                  temperature, actions_out + (int64_t)t * m.R, logp_out + (int64_t)t * m.R, st);
-      col += m.R * a;
+                  temperature, actions_out + (int64_t)t * m.R, logp_out + (int64_t)t * m.R, st,
+                  shared);
+      col += lrows * a;
     }
   });
 }

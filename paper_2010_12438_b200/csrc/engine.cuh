@@ -289,7 +289,7 @@ void tc_gemm_ln(const float* A1, int64_t lda1, int K1, const float* A2, int64_t 
 void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t R,
                  const int64_t* row_off_dev, const int32_t* row_fwd, const int32_t* order_of_row,
                  const uint64_t* pcg_dev, int64_t task, double temperature,
-                 int32_t* actions, double* logp, cudaStream_t st);
+                 int32_t* actions, double* logp, cudaStream_t st, bool shared = false);
 
 // ---- kernels: des.cu
 // device simulated annealing, C chains (des.cu anneal_kernel); cur / best: dev

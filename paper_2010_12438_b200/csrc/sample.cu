@@ -36,15 +36,17 @@ __global__ void sample_kernel(const void* __restrict__ logits, int f64, int64_t 
                               const int32_t* __restrict__ row_node,
                               const uint64_t* __restrict__ pcg, int64_t task,
                               double temperature, int32_t* __restrict__ actions,
-                              double* __restrict__ logp_out) {
+                              double* __restrict__ logp_out, bool shared) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   int f = row_fwd[r];
   int64_t base = row_off[f];
   int64_t lr = r - base, nf = row_off[f + 1] - base;
   double z[SMAX];
+  const int64_t lrow = shared ? lr : r;  // shared: every forward reads forward 0's rows
   for (int j = 0; j < a; ++j)
-    z[j] = f64 ? ((const double*)logits)[r * ldl + j] : (double)((const float*)logits)[r * ldl + j];
+    z[j] = f64 ? ((const double*)logits)[lrow * ldl + j]
+               : (double)((const float*)logits)[lrow * ldl + j];
   int act = 0;
   double lp = 0.0;
   if (temperature == 0.0) {
@@ -91,13 +93,13 @@ __global__ void sample_kernel(const void* __restrict__ logits, int f64, int64_t 
 void sample_rows(const void* logits, int logits_f64, int64_t ldl, int a, int64_t R,
                  const int64_t* row_off_dev, const int32_t* row_fwd, const int32_t* row_node,
                  const uint64_t* pcg_dev, int64_t task, double temperature,
-                 int32_t* actions, double* logp, cudaStream_t st) {
+                 int32_t* actions, double* logp, cudaStream_t st, bool shared) {
   if (R <= 0) return;
   if (a < 1 || a > SMAX) GO_THROW(GO_ERR_UNSUPPORTED, "action space %d outside [1, %d]", a, SMAX);
   sample_kernel<<<(unsigned)cdiv(R, 128), 128, 0, st>>>(logits, logits_f64, ldl, a, R,
                                                         row_off_dev, row_fwd, row_node,
                                                         pcg_dev, task, temperature,
-                                                        actions, logp);
+                                                        actions, logp, shared);
   LAUNCH_CHECK();
 }
 

@@ -41,6 +41,10 @@ class DeviceArray:
     def shape(self):
         return tuple(self.dev.shape)
 
+    def __array__(self, dtype=None, copy=None):
+        """numpy conversion (np.asarray(x), the reference's Tensor(x)) reads the host copy."""
+        return self.data if dtype is None else self.data.astype(dtype)
+
 
 @dataclass
 class ForwardOut:
@@ -165,10 +169,11 @@ def advance(gen, n: int):
 
 
 def sample_batch(embed_cfg, cfg, task_sizes, handles, states, logits_packed, temperature,
-                 logits_f64=False, row_counts=None):
+                 logits_f64=False, row_counts=None, shared_logits=False):
     """-> (actions int32 [T, R], logp f64 [T, R]).  states: [F][4] PCG64 words
     (pcg_words) before this call.  Actions are node-indexed per forward span (row
-    order for graph-less batches)."""
+    order for graph-less batches).  shared_logits: every forward samples from the same
+    logits block (one forward's rows; mode S)."""
     T = torch()
     ctx = context()
     dev = T.device("cuda", ctx.device)
@@ -187,7 +192,8 @@ def sample_batch(embed_cfg, cfg, task_sizes, handles, states, logits_packed, tem
         carr = np.asarray(counts, np.int64)
         gptr, cptr = None, carr.ctypes.data
     _lib.call("go_sample", ctx.handle, C.byref(cfg_c), F, gptr, cptr, words.ctypes.data,
-              _lib.ptr(logits_packed), 1 if logits_f64 else 0, float(temperature),
+              _lib.ptr(logits_packed), (1 if logits_f64 else 0) | (2 if shared_logits else 0),
+              float(temperature),
               _lib.ptr(actions), _lib.ptr(logp), stream_ptr())
     return actions, logp
 

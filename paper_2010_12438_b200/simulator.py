@@ -102,6 +102,14 @@ class FusedGraph:
         return None if not self.install().acyclic else True
 
 
+def as_fused(fg) -> FusedGraph:
+    """This package's FusedGraph, or the reference's (duck-typed: .graph, .group_map)
+    re-expressed as one, so a graphopt.simulator.FusedGraph passes straight through."""
+    if isinstance(fg, FusedGraph):
+        return fg
+    return FusedGraph(fg.graph, fg.group_map)
+
+
 def singleton_fused(graph) -> FusedGraph:
     g = as_graph(graph)
     return FusedGraph(g, np.arange(g.num_nodes))
@@ -135,7 +143,7 @@ def simulate_many(fg: FusedGraph, placements, priorities, topology, policy="prio
     [n]; returns engine.SimBatch of device tensors."""
     T = torch()
     dev = T.device("cuda", context().device)
-    h = fg.install()
+    h = as_fused(fg).install()
     top = as_topology(topology)
     pl = T.as_tensor(placements).to(device=dev, dtype=T.int32)
     if pl.dim() == 1:
@@ -157,6 +165,7 @@ def simulate(fg: FusedGraph, placement: ActionAssignment, priorities: ActionAssi
     if policy not in ("fifo", "priority"):
         raise ValueError(f"unknown policy {policy!r}")
     top = as_topology(topology)
+    fg = as_fused(fg)
     _check_inputs(fg.graph.num_nodes, top.num_devices, placement, priorities)
     if record_trace:
         return _simulate_traced(fg, placement, priorities, top, policy)
@@ -173,6 +182,7 @@ def _simulate_traced(fg, placement, priorities, top, policy) -> SimResult:
     from .engine import simulate_trace
     T = torch()
     dev = T.device("cuda", context().device)
+    fg = as_fused(fg)
     h = fg.install()
     g = fg.graph
     pl = T.as_tensor(placement.actions).to(device=dev, dtype=T.int32)

@@ -259,3 +259,33 @@ def test_simulate_record_trace_matches_reference():
         assert [e.group_id for e in tr] == list(z[p + "group"]), c
         total += len(tr)
     assert total > 1000
+
+
+def test_shared_logits_sampler_is_per_placement_sample_actions():
+    """Mode S sampling (go_sample with shared logits): K placements
+    drawn from ONE forward's logits, each with its own numpy stream, equal K separate
+    sample_actions calls (policy.py:220-237) on those logits, bit for bit."""
+    from paper_2010_12438_b200 import EmbedConfig, PolicyConfig, init_all_params, randomize_zero_init
+    from paper_2010_12438_b200.engine import forward_batch, pcg_words, sample_batch
+    from paper_2010_12438_b200.policy import sample_actions
+    from paper_2010_12438_b200.runtime import context
+    from synthetic.workloads import WorkloadSpec, gen_workload
+    g = gen_workload(WorkloadSpec("attention-stack", 20, 1, 64, seed=0))
+    sizes = {"placement": 8}
+    ecfg, pcfg = EmbedConfig(), PolicyConfig(iterations=1)
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
+    h = context().graph(g)
+    out = forward_batch(store, ecfg, pcfg, sizes, [h], [11])
+    seeds = [3, 1 << 40, 17, 99, 5]
+    acts, logp = sample_batch(ecfg, pcfg, sizes, [h] * len(seeds),
+                              [pcg_words(np.random.default_rng(s)) for s in seeds],
+                              out.logits_packed, 1.0, shared_logits=True)
+    lg = out.logits[0].double().cpu().numpy()
+    order = np.asarray(g.topo_order())
+    n = g.num_nodes
+    for k, s in enumerate(seeds):
+        a_ref, lp_ref = sample_actions(lg, 1.0, np.random.default_rng(s))
+        node = np.zeros(n, np.int64)
+        node[order] = a_ref
+        assert np.array_equal(acts[0, k * n:(k + 1) * n].cpu().numpy(), node), k
+        assert np.array_equal(logp[0, k * n:(k + 1) * n].cpu().numpy(), lp_ref), k
