@@ -21,6 +21,9 @@ void dgemm_nt(const float* dY, int64_t ldd, const float* W, int64_t ldw, float* 
 void transpose(const float* W, int64_t ldw, int rows, int cols, float* out, cudaStream_t st);
 void wgrad(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
            const float* dY, int64_t ldd, int64_t M, int N, float* dW, float* db, cudaStream_t st);
+void wgrad_tc(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
+              const float* dY, int64_t ldd, int64_t M, int N, float* dW, float* db,
+              cudaStream_t st);
 void ln_backward(const float* u, int64_t ldu, const float* g, const float* dout, int64_t ldd,
                  float* dx, int64_t ldx, bool accumulate, int64_t M, int D, float* dg, float* db,
                  cudaStream_t st);

@@ -168,6 +168,15 @@ __global__ void __launch_bounds__(256) wgrad_kernel(const float* __restrict__ A1
 void wgrad(const float* A1, int64_t lda1, int K1, const float* A2, int64_t lda2, int K2,
            const float* dY, int64_t ldd, int64_t M, int N, float* dW, float* db,
            cudaStream_t st) {
+  // tcgen05 split-tf32 GEMM (tc_wgrad.cu); GO_TRAIN_GEMM=simt keeps the fp32 SIMT kernel
+  static const bool simt = [] {
+    const char* e = getenv("GO_TRAIN_GEMM");
+    return e && !strcmp(e, "simt");
+  }();
+  if (!simt) {
+    wgrad_tc(A1, lda1, K1, A2, lda2, K2, dY, ldd, M, N, dW, db, st);
+    return;
+  }
   if (M <= 0 || N <= 0 || (K1 + K2) <= 0) return;
   int64_t chunks = std::min<int64_t>(cdiv(M, 256), 4 * num_sms());
   int64_t rpc = round_up(cdiv(M, chunks), 16);
