@@ -164,7 +164,7 @@ def mufu_peak():
 
 def ncu_traffic():
     try:
-        return json.loads((ROOT / "profiles" / "r1_ncu_summary.json").read_text())["traffic"]
+        return json.loads((ROOT / "profiles" / "r2_ncu_summary.json").read_text())["traffic"]
     except Exception:
         return {}
 
@@ -569,7 +569,7 @@ def main():
                             if "heads_attention_bytes_per_forward" in ncu else None),
                 "traffic_note": "dram read+write per launch (one launch = one wave of "
                                 f"{fwd_per_launch:.1f} forwards) = per-forward bytes of the ncu "
-                                "--set full capture (profiles/r1_ncu_summary.json) x forwards per launch",
+                                "--set full capture (profiles/r2_ncu_summary.json) x forwards per launch",
                 "launches": cnt, "avg_launch_ms": hms / cnt,
                 "algorithmic_flops_per_launch": hflops / cnt,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if peaks
