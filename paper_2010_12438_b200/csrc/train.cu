@@ -101,6 +101,27 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   build_q_tiles(row_off, 0, false, hq);
   build_kv_tiles(row_off, cfg.segment_len, true, tk);
   build_kv_tiles(row_off, 0, false, hk);
+  // tcgen05 tape head attention (tc_tape.cu): 384-query work items and 64-row tiles
+  std::vector<TcWork> tcw;
+  std::vector<int64_t> trow0;
+  std::vector<int32_t> tn;
+  tc_build_tables(row_off, tcw, trow0, tn);
+  std::vector<TcWork> qw;   // (forward, 256 queries) items of the tcgen05 dq kernel
+  for (size_t i = 0; i < tcw.size(); ++i)
+    if (tcw[i].q0 == 0)
+      for (int32_t q0 = 0; q0 < tcw[i].n; q0 += 256) {
+        TcWork x = tcw[i];
+        x.q0 = q0;
+        qw.push_back(x);
+      }
+  std::vector<TcWork> kvw;  // (forward, 128 keys) items of the tcgen05 dk / dv kernel
+  for (size_t i = 0; i < tcw.size(); ++i)
+    if (tcw[i].q0 == 0)
+      for (int32_t k0 = 0; k0 < tcw[i].n; k0 += 128) {
+        TcWork x = tcw[i];
+        x.q0 = k0;
+        kvw.push_back(x);
+      }
   std::vector<char> extra;
   auto put = [&](const void* p, size_t n) {
     size_t o = round_up((int64_t)extra.size(), 256);
@@ -113,6 +134,11 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   size_t o_hq = put(hq.data(), hq.size() * sizeof(AttnTile));
   size_t o_tk = put(tk.data(), tk.size() * sizeof(KvTile));
   size_t o_hk = put(hk.data(), hk.size() * sizeof(KvTile));
+  size_t o_tcw = put(tcw.data(), tcw.size() * sizeof(TcWork));
+  size_t o_tr0 = put(trow0.data(), trow0.size() * sizeof(int64_t));
+  size_t o_tn = put(tn.data(), tn.size() * sizeof(int32_t));
+  size_t o_kvw = put(kvw.data(), kvw.size() * sizeof(TcWork));
+  size_t o_qw = put(qw.data(), qw.size() * sizeof(TcWork));
   const void* exd = nullptr;
   BatchMeta m = make_meta(ctx, cfg, bb, true, false, false, st, extra.data(), extra.size(), &exd);
   const char* ex = reinterpret_cast<const char*>(exd);
@@ -121,6 +147,12 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   const AttnTile* d_hq = reinterpret_cast<const AttnTile*>(ex + o_hq);
   const KvTile* d_tk = reinterpret_cast<const KvTile*>(ex + o_tk);
   const KvTile* d_hk = reinterpret_cast<const KvTile*>(ex + o_hk);
+  const TcWork* d_tcw = reinterpret_cast<const TcWork*>(ex + o_tcw);
+  const int64_t* d_tr0 = reinterpret_cast<const int64_t*>(ex + o_tr0);
+  const int32_t* d_tn = reinterpret_cast<const int32_t*>(ex + o_tn);
+  const int64_t Ttot = (int64_t)trow0.size();
+  const TcWork* d_kvw = reinterpret_cast<const TcWork*>(ex + o_kvw);
+  const TcWork* d_qw = reinterpret_cast<const TcWork*>(ex + o_qw);
   const int64_t R = m.R;
 
   // ---- workspace
@@ -133,7 +165,8 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
                  (size_t)R * T * 64 + (8u << 20) + attention_backward_mma_scratch(R, H) +
                  /* backward dX scratch */ (size_t)R * std::max(dm, gs) * 4 +
                  /* packed tape weights (forward + transposed backward) */ 2 * (size_t)(2 * Lg + 6 * Lt + 8 * T + 4) *
-                     (size_t)tc_gemm_packed_floats(std::max(2 * gs, di), std::max(dm, di)) * 6 + (16u << 20);
+                     (size_t)tc_gemm_packed_floats(std::max(2 * gs, di), std::max(dm, di)) * 6 + (16u << 20) +
+                 tape_attention_tc_scratch(R, F, H);
   Arena2 A{reinterpret_cast<char*>(ctx->ensure(bytes)), 0, ctx->ws_bytes};
   int32_t* row_fwd = A.take<int32_t>(R);
   int32_t* row_node = A.take<int32_t>(R);
@@ -151,6 +184,11 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   const bool attn_split = !(ta_env && !strcmp(ta_env, "mma16"));  // 3-MMA split precision
   int32_t* aflag = A.take<int32_t>(64);
   void* abw = A.take<char>((int64_t)attention_backward_mma_scratch(R, H));
+  // the N x N head attention's tape forward on tcgen05 (split fp16, tc_tape.cu) unless
+  // GO_TRAIN_ATTN selects another variant; falls back to the mma.sync forward when a score
+  // bound exceeds the fp16 limit
+  const bool tape_tc = attn_mma && attn_split && dh <= 15 && !(ta_env && !strcmp(ta_env, "mma"));
+  void* tape_ws = A.take<char>((int64_t)tape_attention_tc_scratch(R, F, H));
   auto attn_fwd = [&](const float* q, const float* k, const float* v, const AttnTile* tiles,
                       int64_t nt, float* out, float* lse) {
     if (attn_mma_fwd) {
@@ -342,7 +380,11 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(Q_W)), W, Pw(S.ta(Q_B)), hqv[t], W, R, W, 0, st);
     fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(K_W)), W, Pw(S.ta(K_B)), hkv[t], W, R, W, 0, st);
     fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(V_W)), W, Pw(S.ta(V_B)), hvv[t], W, R, W, 0, st);
-    attn_fwd(hqv[t], hkv[t], hvv[t], d_hq, (int64_t)hq.size(), hat[t], hls[t]);
+    if (!tape_tc ||
+        !tape_attention_fwd_tc(hqv[t], hkv[t], hvv[t], W, H, dh, R, F, d_tcw,
+                               (int64_t)tcw.size(), d_tr0, d_tn, Ttot, row_fwd, hat[t], W,
+                               hls[t], tape_ws, st))
+      attn_fwd(hqv[t], hkv[t], hvv[t], d_hq, (int64_t)hq.size(), hat[t], hls[t]);
     fgemm(hat[t], W, W, nullptr, 0, 0, Pw(S.ta(O_W)), dm, Pw(S.ta(O_B)), ho[t], dm, R, dm, 0, st);
     fgemm(ho[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, FC_W1)), di, Pw(S.task(t, FC_B1)), hf1[t], di, R,
          di, 1, st);
@@ -418,8 +460,16 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     // o = att Wo + bo
     dgemm(dO, dm, Pw(S.ta(O_W)), dm, dAt, W, R, W, dm, false);
     wgrad(hat[t], W, W, nullptr, 0, 0, dO, dm, R, dm, Gw(S.ta(O_W)), Gw(S.ta(O_B)), st);
-    attn_bwd(hqv[t], hkv[t], hvv[t], hat[t], dAt, hls[t], d_hq, (int64_t)hq.size(), d_hk,
-             (int64_t)hk.size(), Dbuf, dQ, dK, dV, nullptr, nullptr);
+    // dq, dk, dv on tcgen05 (tc_tape.cu) when the operands fit the split-fp16 path,
+    // otherwise on the mma.sync kernels
+    const bool bwd_tc = tape_tc &&
+                        tape_attention_bwd_tc(hqv[t], hkv[t], hvv[t], hat[t], dAt, W, H, dh, R, F,
+                                              hls[t], d_kvw, (int64_t)kvw.size(), d_qw,
+                                              (int64_t)qw.size(), d_tr0, d_tn, Ttot, Dbuf, dQ, dK,
+                                              dV, tape_ws, st);
+    if (!bwd_tc)
+      attn_bwd(hqv[t], hkv[t], hvv[t], hat[t], dAt, hls[t], d_hq, (int64_t)hq.size(), d_hk,
+               (int64_t)hk.size(), Dbuf, dQ, dK, dV, nullptr, nullptr);
     float* dHH = d3;
     dgemm(dQ, W, Pw(S.ta(Q_W)), W, dHH, dm, R, dm, W, false);
     dgemm(dK, W, Pw(S.ta(K_W)), W, dHH, dm, R, dm, W, true);
