@@ -61,7 +61,8 @@ __device__ __forceinline__ uint32_t ld32(const __half* p) {
 
 // max |dO| over the head columns (non-negative floats order like their bit patterns)
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t ld, int64_t M, int W,
-                              unsigned* __restrict__ out) {
+                              unsigned* __restrict__ out, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;  // gated: only when the tcgen05 tape flagged the call
   float m = 0.f;
   const int64_t n = M * W;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -94,7 +95,9 @@ __global__ void pack_kernel(const float* __restrict__ q, const float* __restrict
                             int64_t M, int n_head, int d_head, float qscale,
                             const unsigned* __restrict__ gbits, __half* __restrict__ Qh,
                             __half* __restrict__ Kh, __half* __restrict__ Vh,
-                            __half* __restrict__ Oh, int32_t* __restrict__ flag) {
+                            __half* __restrict__ Oh, int32_t* __restrict__ flag,
+                            const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   constexpr int RW = SPLIT ? 32 : 16;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (head, row)
   if (i >= M * n_head) return;
@@ -226,7 +229,8 @@ __global__ void __launch_bounds__(128) dq_kernel(
     const __half* __restrict__ Oh, int64_t M, const float* __restrict__ lse,
     const float* __restrict__ Dv, int n_head, int d_head, const AttnTile* __restrict__ tiles,
     float* __restrict__ dq, int64_t ld, float scale, const unsigned* __restrict__ gbits,
-    int32_t* __restrict__ flag) {
+    int32_t* __restrict__ flag, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
   __shared__ __align__(16) __half Ks2[2][TS * RS2];
   __shared__ __align__(16) __half Vs2[2][TS * RS2];
@@ -336,7 +340,8 @@ __global__ void __launch_bounds__(128, 4) dkv_kernel(
     const float* __restrict__ Dv, int n_head, int d_head, const KvTile* __restrict__ tiles,
     float* __restrict__ dk_a, float* __restrict__ dv_a, float* __restrict__ dk_b,
     float* __restrict__ dv_b, int64_t ld, float kscale, const unsigned* __restrict__ gbits,
-    int32_t* __restrict__ flag) {
+    int32_t* __restrict__ flag, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
   __shared__ __align__(16) __half Qs2[2][TS * RS2];
   __shared__ __align__(16) __half Os2[2][TS * RS2];
@@ -476,7 +481,9 @@ template <bool SPLIT>
 __global__ void __launch_bounds__(128) fwd_kernel(
     const __half* __restrict__ Qh, const __half* __restrict__ Kh, const __half* __restrict__ Vh,
     int64_t M, int n_head, int d_head, const AttnTile* __restrict__ tiles,
-    float* __restrict__ out, int64_t ldo, float* __restrict__ lse) {
+    float* __restrict__ out, int64_t ldo, float* __restrict__ lse,
+    const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   constexpr int RW = SPLIT ? 32 : 16, RS2 = row_stride<SPLIT>();
   __shared__ __align__(16) __half Ks2[2][TS * RS2];
   __shared__ __align__(16) __half Vs2[2][TS * RS2];
@@ -613,7 +620,7 @@ static void launch_bwd(const float* q, const float* k, const float* v, const flo
                        int64_t ld, const float* lse, int n_head, int d_head,
                        const AttnTile* qtiles, int64_t nq, const KvTile* ktiles, int64_t nk,
                        const float* Dbuf, int64_t M, float* dq, float* dk_a, float* dv_a,
-                       float* dk_b, float* dv_b, char* base, int32_t* flag, cudaStream_t st) {
+                       float* dk_b, float* dv_b, char* base, int32_t* flag, cudaStream_t st, const int32_t* gate) {
   constexpr int RW = SPLIT ? 32 : 16;
   const size_t rows = (size_t)M * n_head * RW;
   __half* Qh = reinterpret_cast<__half*>(base);
@@ -626,21 +633,21 @@ static void launch_bwd(const float* q, const float* k, const float* v, const flo
   CUDA_CHECK(cudaMemsetAsync(gbits, 0, 3 * sizeof(unsigned), st));
   const int64_t W = (int64_t)n_head * d_head;
   ab::absmax_kernel<<<(unsigned)std::min<int64_t>(cdiv(M * W, 256), 148 * 8), 256, 0, st>>>(
-      dO, ld, M, (int)W, gbits);
+      dO, ld, M, (int)W, gbits, gate);
   LAUNCH_CHECK();
   ab::pack_kernel<SPLIT><<<(unsigned)cdiv(M * n_head, 128), 128, 0, st>>>(
-      q, k, v, dO, ld, M, n_head, d_head, qscale, gbits, Qh, Kh, Vh, Oh, flag);
+      q, k, v, dO, ld, M, n_head, d_head, qscale, gbits, Qh, Kh, Vh, Oh, flag, gate);
   LAUNCH_CHECK();
   if (nq > 0) {
     ab::dq_kernel<SPLIT><<<dim3((unsigned)nq, (unsigned)n_head), 128, 0, st>>>(
-        Qh, Kh, Vh, Oh, M, lse, Dbuf, n_head, d_head, qtiles, dq, ld, scale, gbits, flag);
+        Qh, Kh, Vh, Oh, M, lse, Dbuf, n_head, d_head, qtiles, dq, ld, scale, gbits, flag, gate);
     LAUNCH_CHECK();
   }
   if (nk > 0) {
     // dk = scale * sum dS q and the packed q carries log2(e) * scale: multiply by 1/log2(e)
     ab::dkv_kernel<SPLIT><<<dim3((unsigned)nk, (unsigned)n_head), 128, 0, st>>>(
         Qh, Kh, Vh, Oh, M, lse, Dbuf, n_head, d_head, ktiles, dk_a, dv_a, dk_b, dv_b, ld,
-        (float)(1.0 / 1.4426950408889634), gbits, flag);
+        (float)(1.0 / 1.4426950408889634), gbits, flag, gate);
     LAUNCH_CHECK();
   }
 }
@@ -648,7 +655,7 @@ static void launch_bwd(const float* q, const float* k, const float* v, const flo
 void attention_forward_mma(const float* q, const float* k, const float* v, int64_t ld,
                                 int n_head, int d_head, const AttnTile* tiles, int64_t nt,
                                 int64_t M, float* out, int64_t ldo, float* lse, void* scratch,
-                                int32_t* flag, cudaStream_t st) {
+                                int32_t* flag, cudaStream_t st, const int32_t* gate) {
   if (nt <= 0 || M <= 0) return;
   GO_CHECK(d_head >= 1 && d_head <= 15, "attention_forward_mma needs d_head <= 15");
   const size_t rows = (size_t)M * n_head * 32;
@@ -660,10 +667,10 @@ void attention_forward_mma(const float* q, const float* k, const float* v, int64
   CUDA_CHECK(cudaMemsetAsync(gbits, 0, 3 * sizeof(unsigned), st));
   CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
   ab::pack_kernel<true><<<(unsigned)cdiv(M * n_head, 128), 128, 0, st>>>(
-      q, k, v, nullptr, ld, M, n_head, d_head, qscale, gbits, Qh, Kh, Vh, nullptr, flag);
+      q, k, v, nullptr, ld, M, n_head, d_head, qscale, gbits, Qh, Kh, Vh, nullptr, flag, gate);
   LAUNCH_CHECK();
   ab::fwd_kernel<true><<<dim3((unsigned)nt, (unsigned)n_head), 128, 0, st>>>(
-      Qh, Kh, Vh, M, n_head, d_head, tiles, out, ldo, lse);
+      Qh, Kh, Vh, M, n_head, d_head, tiles, out, ldo, lse, gate);
   LAUNCH_CHECK();
 }
 
@@ -672,7 +679,7 @@ void attention_backward_mma(const float* q, const float* k, const float* v, cons
                             int d_head, const AttnTile* qtiles, int64_t nq, const KvTile* ktiles,
                             int64_t nk, float* Dbuf, int64_t M, float* dq, float* dk_a,
                             float* dv_a, float* dk_b, float* dv_b, void* scratch,
-                            int32_t* flag, cudaStream_t st) {
+                            int32_t* flag, cudaStream_t st, const int32_t* gate) {
   if (M <= 0) return;
   GO_CHECK(d_head >= 1 && d_head <= 16, "attention_backward_mma needs d_head <= 16");
   CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
@@ -680,10 +687,10 @@ void attention_backward_mma(const float* q, const float* k, const float* v, cons
   char* base = reinterpret_cast<char*>(scratch);
   if (bwd_split())
     launch_bwd<true>(q, k, v, dO, ld, lse, n_head, d_head, qtiles, nq, ktiles, nk, Dbuf, M, dq,
-                     dk_a, dv_a, dk_b, dv_b, base, flag, st);
+                     dk_a, dv_a, dk_b, dv_b, base, flag, st, gate);
   else
     launch_bwd<false>(q, k, v, dO, ld, lse, n_head, d_head, qtiles, nq, ktiles, nk, Dbuf, M, dq,
-                      dk_a, dv_a, dk_b, dv_b, base, flag, st);
+                      dk_a, dv_a, dk_b, dv_b, base, flag, st, gate);
   // fp32 SIMT re-run, a no-op unless the fp16 range check fired
   attention_backward_simt(q, k, v, dO, ld, lse, n_head, d_head, qtiles, nq, ktiles, nk, Dbuf, dq,
                           dk_a, dv_a, dk_b, dv_b, flag, st);

@@ -691,15 +691,12 @@ __global__ void pack_b16_kernel(const float* __restrict__ W0, const float* __res
 }  // namespace tg
 
 int tc_gemm_bn(int N) {
-  // GO_GEMM_BN256=0 caps the block width at 144 (deeper smem ring, more A re-reads)
-  const char* e = getenv("GO_GEMM_BN256");
-  const bool allow256 = !(e && e[0] == '0');
   if (N <= 16) return 16;
   if (N <= 32) return 32;
   if (N <= 48) return 48;
   if (N <= 64) return 64;
   if (N <= 128) return 128;
-  if (N <= 144 || !allow256) return N <= 144 ? 144 : 128;
+  if (N <= 144) return 144;
   return 256;
 }
 
@@ -801,13 +798,6 @@ static bool w_resident_ok() {
   return !(e && e[0] == '0');
 }
 
-// GO_GEMM_MH=2: two 128-row accumulators per tile sharing each W chunk (half the weight
-// traffic from L2, but only a 2-stage ring: measured 13.7-13.8 ms vs 12.4 ms per 8 cfg4
-// forwards for the default single accumulator; tf32 path only)
-static bool two_halves() {
-  const char* e = getenv("GO_GEMM_MH");
-  return e && e[0] == '2';
-}
 // GO_GEMM_F16=0 keeps the tf32 operands
 static bool use_f16() {
   const char* e = getenv("GO_GEMM_F16");
@@ -822,7 +812,6 @@ void launch_all(const float* A1, int64_t lda1, const float* A2, int64_t lda2, tg
   GO_CHECK(a.M < ((int64_t)1 << 31), "too many rows for one GEMM launch");
   const CUtensorMap m1 = a_map(A1, a.M, a.K1, lda1);
   const CUtensorMap m2 = A2 ? a_map(A2, a.M, a.K2, lda2) : m1;
-  constexpr bool can2 = BN <= 128;
   if (W.gate) {  // tf32 re-run of a fused kernel's layer, gated on its range flag
     a.gate = W.gate;
     a.Bpk = W.w32;
@@ -844,8 +833,7 @@ void launch_all(const float* A1, int64_t lda1, const float* A2, int64_t lda2, tg
     a.gate = W.ovf;
   }
   a.Bpk = W.w32;
-  if (can2 && !f16 && two_halves()) launch<BN, can2 ? 2 : 1, LN, ACT, false>(m1, m2, a, nblk, st);
-  else launch<BN, 1, LN, ACT, false>(m1, m2, a, nblk, st);
+  launch<BN, 1, LN, ACT, false>(m1, m2, a, nblk, st);
 }
 
 template <int BN>

@@ -516,7 +516,8 @@ __global__ void __launch_bounds__(KV_THREADS, 1)
                     int64_t Ttot, const TcWork* __restrict__ works,
                     const float* __restrict__ lsd_t, const unsigned* __restrict__ bits,
                     int d_head, float* __restrict__ dk, float* __restrict__ dv, int64_t ld,
-                    float kscale) {
+                    float kscale, const int32_t* __restrict__ flag) {
+  if (*flag) return;  // an operand left the fp16 range: the gated mma.sync path runs
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   KvSmem& sm = *reinterpret_cast<KvSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -747,7 +748,8 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
                    int64_t Ttot, const TcWork* __restrict__ works, int64_t R,
                    const float* __restrict__ lse_h, const float* __restrict__ d_h,
                    const unsigned* __restrict__ bits, int d_head, float* __restrict__ dq,
-                   int64_t ld, float scale) {
+                   int64_t ld, float scale, const int32_t* __restrict__ flag) {
+  if (*flag) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   DqSmem& sm = *reinterpret_cast<DqSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -935,16 +937,15 @@ size_t tape_attention_tc_scratch(int64_t R, int F, int n_head) {
          (size_t)F * n_head * 4 + 8192;
 }
 
-// The tape forward of the full N x N head attention on tcgen05.  Returns false (and leaves
-// the output untouched) when some score bound exceeds the fp16 limit or an operand left
-// the fp16 range; the caller then runs the mma.sync forward.
-bool tape_attention_fwd_tc(const float* q, const float* k, const float* v, int64_t ld,
+// The tape forward of the full N x N head attention on tcgen05.  Returns the device flag:
+// non-zero when some score bound exceeds the fp16 limit or an operand left the fp16 range
+// (the forward kernel then writes nothing and the caller's gated mma.sync forward runs).
+const int32_t* tape_attention_fwd_tc(const float* q, const float* k, const float* v, int64_t ld,
                            int n_head, int d_head, int64_t R, int F, const TcWork* works_dev,
                            int64_t num_works, const int64_t* tile_row0_dev,
                            const int32_t* tile_n_dev, int64_t Ttot, const int32_t* row_fwd,
                            float* out, int64_t ldo, float* lse, void* scratch,
                            cudaStream_t st) {
-  if (num_works <= 0) return true;
   GO_CHECK(d_head >= 1 && d_head <= 15, "tape_attention_fwd_tc needs d_head <= 15");
   static bool attr = false;
   const size_t smem = sizeof(tt::FwdSmem) + 1024;
@@ -980,31 +981,29 @@ bool tape_attention_fwd_tc(const float* q, const float* k, const float* v, int64
                                                 tile_n_dev, Ttot, 2, c15, qh, ql, nullptr,
                                                 nullptr, nullptr, flag);
   LAUNCH_CHECK();
-  int32_t hflag = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_CHECK(cudaStreamSynchronize(st));
-  if (hflag) return false;
+
   dim3 grid((unsigned)num_works, (unsigned)n_head);
-  tt::tape_fwd_kernel<<<grid, tt::NUM_THREADS, smem, st>>>(qh, ql, kh, kl, vh, vl, Ttot, works_dev,
-                                                          bound, n_head, out, ldo, d_head, lse,
-                                                          flag);
-  LAUNCH_CHECK();
-  return true;
+  if (num_works > 0) {
+    tt::tape_fwd_kernel<<<grid, tt::NUM_THREADS, smem, st>>>(qh, ql, kh, kl, vh, vl, Ttot,
+                                                            works_dev, bound, n_head, out, ldo,
+                                                            d_head, lse, flag);
+    LAUNCH_CHECK();
+  }
+  return flag;
 }
 
 
 // dk, dv of the full N x N head attention on tcgen05 (tape_dkv_kernel).  kv_works: one
 // entry per (forward, 128 keys) (TcWork with q0 = first local key).  Computes D = dO.O into
 // Dbuf first.  Returns false when an operand left the fp16 range (nothing written then).
-bool tape_attention_bwd_tc(const float* q, const float* k, const float* v, const float* O,
+const int32_t* tape_attention_bwd_tc(const float* q, const float* k, const float* v, const float* O,
                            const float* dO, int64_t ld, int n_head, int d_head, int64_t R,
                            int F, const float* lse, const TcWork* kv_works_dev,
                            int64_t num_kv_works, const TcWork* q_works_dev,
                            int64_t num_q_works, const int64_t* tile_row0_dev,
                            const int32_t* tile_n_dev, int64_t Ttot, float* Dbuf, float* dq,
                            float* dk, float* dv, void* scratch, cudaStream_t st) {
-  if (num_kv_works <= 0) return true;
-  GO_CHECK(d_head >= 1 && d_head <= 16, "tape_attention_dkv_tc needs d_head <= 16");
+  GO_CHECK(d_head >= 1 && d_head <= 16, "tape_attention_bwd_tc needs d_head <= 16");
   static bool attr = false;
   const size_t smem = sizeof(tt::KvSmem) + 1024;
   const size_t smem_q = sizeof(tt::DqSmem) + 1024;
@@ -1054,23 +1053,24 @@ bool tape_attention_bwd_tc(const float* q, const float* k, const float* v, const
   pack(v, ld, 1.f, vrh, vrl, nullptr, nullptr);
   pack(q, ld, qscale, qrh, qrl, qth, qtl);
   pack(dOs, W, 1.f, orh, orl, oth, otl);
-  int32_t hflag = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_CHECK(cudaStreamSynchronize(st));
-  if (hflag) return false;
+
   dim3 grid((unsigned)num_kv_works, (unsigned)n_head);
-  tt::tape_dkv_kernel<<<grid, tt::KV_THREADS, smem, st>>>(
-      krh, krl, vrh, vrl, qrh, qrl, qth, qtl, orh, orl, oth, otl, Ttot, kv_works_dev, lsd, bits,
-      d_head, dk, dv, ld, (float)(1.0 / 1.4426950408889634));
-  LAUNCH_CHECK();
+  if (num_kv_works > 0) {
+    tt::tape_dkv_kernel<<<grid, tt::KV_THREADS, smem, st>>>(
+        krh, krl, vrh, vrl, qrh, qrl, qth, qtl, orh, orl, oth, otl, Ttot, kv_works_dev, lsd,
+        bits, d_head, dk, dv, ld, (float)(1.0 / 1.4426950408889634), flag);
+    LAUNCH_CHECK();
+  }
   // dq: K^T tiles into the Q^T slots (stream-ordered after the dk / dv kernel read them)
   pack(k, ld, 1.f, nullptr, nullptr, qth, qtl);
   dim3 gq((unsigned)num_q_works, (unsigned)n_head);
-  tt::tape_dq_kernel<<<gq, tt::DQ_THREADS, smem_q, st>>>(
-      qrh, qrl, orh, orl, krh, krl, vrh, vrl, qth, qtl, Ttot, q_works_dev, R, lse_h, d_h, bits,
-      d_head, dq, ld, (float)(1.0 / std::sqrt((double)d_head)));
-  LAUNCH_CHECK();
-  return true;
+  if (num_q_works > 0) {
+    tt::tape_dq_kernel<<<gq, tt::DQ_THREADS, smem_q, st>>>(
+        qrh, qrl, orh, orl, krh, krl, vrh, vrl, qth, qtl, Ttot, q_works_dev, R, lse_h, d_h,
+        bits, d_head, dq, ld, (float)(1.0 / std::sqrt((double)d_head)), flag);
+    LAUNCH_CHECK();
+  }
+  return flag;
 }
 
 }  // namespace go

@@ -190,10 +190,11 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   const bool tape_tc = attn_mma && attn_split && dh <= 15 && !(ta_env && !strcmp(ta_env, "mma"));
   void* tape_ws = A.take<char>((int64_t)tape_attention_tc_scratch(R, F, H));
   auto attn_fwd = [&](const float* q, const float* k, const float* v, const AttnTile* tiles,
-                      int64_t nt, float* out, float* lse) {
+                      int64_t nt, float* out, float* lse, const int32_t* gate = nullptr) {
     if (attn_mma_fwd) {
       if (attn_split && dh <= 15)
-        attention_forward_mma(q, k, v, W, H, dh, tiles, nt, R, out, W, lse, abw, aflag, st);
+        attention_forward_mma(q, k, v, W, H, dh, tiles, nt, R, out, W, lse, abw, aflag, st,
+                              gate);
       else
         trunk_attention_mma(q, k, v, W, H, dh, tiles, nt, out, W, aflag, st, lse, attn_split);
       attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse, aflag);
@@ -262,10 +263,10 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   auto attn_bwd = [&](const float* q, const float* k, const float* v, const float* O,
                       const float* dO_, const float* lse, const AttnTile* qt, int64_t nq,
                       const KvTile* kt, int64_t nk, float* Db, float* dq_, float* dk_a,
-                      float* dv_a, float* dk_b, float* dv_b) {
+                      float* dv_a, float* dk_b, float* dv_b, const int32_t* gate = nullptr) {
     if (attn_mma)
       attention_backward_mma(q, k, v, O, dO_, W, lse, H, dh, qt, nq, kt, nk, Db, R, dq_, dk_a,
-                             dv_a, dk_b, dv_b, abw, aflag, st);
+                             dv_a, dk_b, dv_b, abw, aflag, st, gate);
     else
       attention_backward(q, k, v, O, dO_, W, lse, H, dh, qt, nq, kt, nk, Db, R, dq_, dk_a, dv_a,
                          dk_b, dv_b, st);
@@ -380,11 +381,14 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(Q_W)), W, Pw(S.ta(Q_B)), hqv[t], W, R, W, 0, st);
     fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(K_W)), W, Pw(S.ta(K_B)), hkv[t], W, R, W, 0, st);
     fgemm(hh[t], dm, dm, nullptr, 0, 0, Pw(S.ta(V_W)), W, Pw(S.ta(V_B)), hvv[t], W, R, W, 0, st);
-    if (!tape_tc ||
-        !tape_attention_fwd_tc(hqv[t], hkv[t], hvv[t], W, H, dh, R, F, d_tcw,
-                               (int64_t)tcw.size(), d_tr0, d_tn, Ttot, row_fwd, hat[t], W,
-                               hls[t], tape_ws, st))
-      attn_fwd(hqv[t], hkv[t], hvv[t], d_hq, (int64_t)hq.size(), hat[t], hls[t]);
+    // tcgen05 first; the mma.sync kernels are gated on its flag (they run only if the
+    // split-fp16 tcgen05 path could not take the call) -- no host synchronisation
+    const int32_t* fgate =
+        tape_tc ? tape_attention_fwd_tc(hqv[t], hkv[t], hvv[t], W, H, dh, R, F, d_tcw,
+                                        (int64_t)tcw.size(), d_tr0, d_tn, Ttot, row_fwd, hat[t],
+                                        W, hls[t], tape_ws, st)
+                : nullptr;
+    attn_fwd(hqv[t], hkv[t], hvv[t], d_hq, (int64_t)hq.size(), hat[t], hls[t], fgate);
     fgemm(hat[t], W, W, nullptr, 0, 0, Pw(S.ta(O_W)), dm, Pw(S.ta(O_B)), ho[t], dm, R, dm, 0, st);
     fgemm(ho[t], dm, dm, nullptr, 0, 0, Pw(S.task(t, FC_W1)), di, Pw(S.task(t, FC_B1)), hf1[t], di, R,
          di, 1, st);
@@ -462,14 +466,14 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
     wgrad(hat[t], W, W, nullptr, 0, 0, dO, dm, R, dm, Gw(S.ta(O_W)), Gw(S.ta(O_B)), st);
     // dq, dk, dv on tcgen05 (tc_tape.cu) when the operands fit the split-fp16 path,
     // otherwise on the mma.sync kernels
-    const bool bwd_tc = tape_tc &&
-                        tape_attention_bwd_tc(hqv[t], hkv[t], hvv[t], hat[t], dAt, W, H, dh, R, F,
-                                              hls[t], d_kvw, (int64_t)kvw.size(), d_qw,
-                                              (int64_t)qw.size(), d_tr0, d_tn, Ttot, Dbuf, dQ, dK,
-                                              dV, tape_ws, st);
-    if (!bwd_tc)
-      attn_bwd(hqv[t], hkv[t], hvv[t], hat[t], dAt, hls[t], d_hq, (int64_t)hq.size(), d_hk,
-               (int64_t)hk.size(), Dbuf, dQ, dK, dV, nullptr, nullptr);
+    const int32_t* bgate =
+        tape_tc ? tape_attention_bwd_tc(hqv[t], hkv[t], hvv[t], hat[t], dAt, W, H, dh, R, F,
+                                        hls[t], d_kvw, (int64_t)kvw.size(), d_qw,
+                                        (int64_t)qw.size(), d_tr0, d_tn, Ttot, Dbuf, dQ, dK, dV,
+                                        tape_ws, st)
+                : nullptr;
+    attn_bwd(hqv[t], hkv[t], hvv[t], hat[t], dAt, hls[t], d_hq, (int64_t)hq.size(), d_hk,
+             (int64_t)hk.size(), Dbuf, dQ, dK, dV, nullptr, nullptr, bgate);
     float* dHH = d3;
     dgemm(dQ, W, Pw(S.ta(Q_W)), W, dHH, dm, R, dm, W, false);
     dgemm(dK, W, Pw(S.ta(K_W)), W, dHH, dm, R, dm, W, true);

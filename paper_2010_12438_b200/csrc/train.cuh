@@ -56,21 +56,23 @@ void attention_backward_simt(const float* q, const float* k, const float* v, con
 void attention_forward_mma(const float* q, const float* k, const float* v, int64_t ld,
                            int n_head, int d_head, const AttnTile* tiles, int64_t nt, int64_t M,
                            float* out, int64_t ldo, float* lse, void* scratch, int32_t* flag,
-                           cudaStream_t st);
+                           cudaStream_t st, const int32_t* gate = nullptr);
 // tensor-core (mma.sync fp16) backward, d_head <= 16, with the gated SIMT re-run
 // (csrc/attn_bwd_mma.cu); scratch >= attention_backward_mma_scratch(M, n_head) bytes
 size_t attention_backward_mma_scratch(int64_t M, int n_head);
-// PPO tape head attention on tcgen05 (tc_tape.cu): forward with log2-sum-exp; false when
-// the fp16 split path cannot take the call (bound or range), nothing written then
+// PPO tape head attention on tcgen05 (tc_tape.cu): forward with log2-sum-exp.  No host
+// synchronisation: returns a device flag that is non-zero when the fp16 split path could not
+// take the call (bound or range; the tcgen05 kernels then write nothing) -- pass it as the
+// `gate` of the mma.sync path, whose kernels run only then.
 size_t tape_attention_tc_scratch(int64_t R, int F, int n_head);
-bool tape_attention_fwd_tc(const float* q, const float* k, const float* v, int64_t ld,
+const int32_t* tape_attention_fwd_tc(const float* q, const float* k, const float* v, int64_t ld,
                            int n_head, int d_head, int64_t R, int F, const TcWork* works_dev,
                            int64_t num_works, const int64_t* tile_row0_dev,
                            const int32_t* tile_n_dev, int64_t Ttot, const int32_t* row_fwd,
                            float* out, int64_t ldo, float* lse, void* scratch,
                            cudaStream_t st);
-// backward (dq, dk, dv; D into Dbuf); false when an operand left the fp16 range
-bool tape_attention_bwd_tc(const float* q, const float* k, const float* v, const float* O,
+// backward (dq, dk, dv; D into Dbuf); device flag as for the forward
+const int32_t* tape_attention_bwd_tc(const float* q, const float* k, const float* v, const float* O,
                            const float* dO, int64_t ld, int n_head, int d_head, int64_t R,
                            int F, const float* lse, const TcWork* kv_works_dev,
                            int64_t num_kv_works, const TcWork* q_works_dev,
@@ -82,7 +84,7 @@ void attention_backward_mma(const float* q, const float* k, const float* v, cons
                             int d_head, const AttnTile* qtiles, int64_t nq, const KvTile* ktiles,
                             int64_t nk, float* Dbuf, int64_t M, float* dq, float* dk_a,
                             float* dv_a, float* dk_b, float* dv_b, void* scratch,
-                            int32_t* flag, cudaStream_t st);
+                            int32_t* flag, cudaStream_t st, const int32_t* gate = nullptr);
 void ppo_loss(const float* logits, int a, int64_t R, const int32_t* actions,
               const int32_t* row_node, const double* old_logp, const int32_t* row_fwd,
               const int64_t* row_off, const double* fparams, double eps, double c_ent, int T,

@@ -2,7 +2,7 @@
 """Micro-benchmarks on one GPU (development aid, not the headline bench):
   des      : batched DES throughput on the cfg4 graph, per launch mode
   forward  : one wave of cfg4 forwards, per-kernel-class CUDA-event times
-  poly     : forward with GO_POLY = 0..4 (exp2 split between MUFU and FMA)
+  attn     : forward with the fp16 / tf32 head-attention kernels (GO_ATTN)
 Usage: python scripts/micro.py des|forward|poly [K]"""
 import ctypes as C
 import os
@@ -93,13 +93,6 @@ if __name__ == "__main__":
         des(n or 512)
     elif what == "attn":
         forward(n or 8, env=[("GO_ATTN", "f16"), ("GO_ATTN", "tf32"), ("GO_ATTN", "f16")])
-    elif what == "mh":
-        forward(n or 8, env=[("GO_GEMM_MH", "2"), ("GO_GEMM_MH", "1"), ("GO_GEMM_MH", "2"),
-                             ("GO_GEMM_BN256", "0")])
-    elif what == "bn":
-        forward(n or 8, env=[("GO_GEMM_BN256", "1"), ("GO_GEMM_BN256", "0"), ("GO_GEMM_BN256", "1")])
-    elif what == "poly":
-        forward(n or 8, env=[("GO_POLY", str(k)) for k in (0, 5, 1, 0)])
     elif what == "tc":
         forward(n or 8, modes=("tc",))
     else:

@@ -131,3 +131,53 @@ def test_superpositioned_batch_cfg3_through_collect_rollouts():
         rep["rollouts"].append(r)
     assert len(seen) >= 3
     _report("cfg3_batch", rep)
+
+
+def test_joint_tasks_at_13k_nodes():
+    """cfg5's joint placement + scheduling + fusion heads (three chained task heads, each a
+    full N x N attention; policy.py:187-217) on the 13,000-node cfg2 graph, both
+    iterations, every row and task against the float64 oracle: logits 1e-4 normwise, every
+    action flip explained; then the joint assignment through the fusion pass and the
+    priority DES (evaluate_assignments, simulator.py:472-487) bit-exact against the
+    oracle's apply_fusion + simulate."""
+    from oracle import forward as of
+    from paper_2010_12438_b200 import EmbedConfig, PolicyConfig, init_all_params, randomize_zero_init
+    from paper_2010_12438_b200.costmodel import uniform_topology
+    from paper_2010_12438_b200.policy import iterate_decisions
+    from paper_2010_12438_b200.simulator import ActionAssignment, evaluate_assignments
+    g = _graph(("multi-branch-cnn", 1857, 1, 64, 0))
+    sizes = {"placement": 4, "schedule_priority": 8, "fusion_priority": 8}
+    ecfg, pcfg = EmbedConfig(), PolicyConfig()
+    store = randomize_zero_init(init_all_params(ecfg, pcfg, sizes, 0))
+    P = H.oracle_params(store)
+    ogr = H.oracle_graph(g)
+    seed = 4242
+    bundle, traj = iterate_decisions(g, store, ecfg, pcfg, sizes, 2, seed)
+    order = np.asarray(g.topo_order())
+    tasks = of.ordered_tasks(sizes)
+    rep = {"iterations": []}
+    prev = None
+    for it, b in enumerate(traj):
+        lg_ref, _ = H.oracle_logits(ogr, P, sizes, prev, seed)
+        r = {}
+        for t_i, (t, _a) in enumerate(tasks):
+            e = H.errors(b.logits[t], lg_ref[t])
+            acts = H.check_actions(b.actions[t], b.log_probs[t], lg_ref[t], b.logits[t], order,
+                                   np.arange(g.num_nodes), seed, it, t_i, len(tasks))
+            r[t] = {"logits": e, "actions": acts}
+            assert e["normwise"] < H.NORM_BAR, (it, t, e)
+            assert not acts["unexplained"], (it, t, acts)
+        rep["iterations"].append(r)
+        prev = b.actions
+    top = uniform_topology(4)
+    asg = {t: ActionAssignment(t, bundle.actions[t], a) for t, a in sizes.items()}
+    res = evaluate_assignments(g, top, asg)
+    roots = H.od.apply_fusion(ogr, bundle.actions["fusion_priority"], max_group=8)
+    fg = H.od.Fused(ogr, roots)
+    want = H.od.simulate(ogr, fg, bundle.actions["placement"], bundle.actions["schedule_priority"],
+                         H.od.uniform_topology(4))
+    rep["des"] = {"got": res.step_time, "want": want["step_time"],
+                  "groups": int(max(fg.group_map) + 1)}
+    assert res.step_time == want["step_time"] and res.valid == want["valid"], rep["des"]
+    assert res.per_device_busy == list(want["busy"]) and res.peak_mem == list(want["peak"])
+    _report("cfg2_joint", rep)
