@@ -174,16 +174,33 @@ __device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
       : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
   return *reinterpret_cast<const float2*>(&r);
 }
+// packed fp32 pair arithmetic (FADD2 / FMUL2: one issue slot for two lanes' worth)
+__device__ __forceinline__ float2 sub_f32x2(float2 a, float2 b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+  return *reinterpret_cast<const float2*>(&r);
+}
+__device__ __forceinline__ float2 mul_f32x2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+  return *reinterpret_cast<const float2*>(&r);
+}
+// a pair of fp32 values -> fp16x2 hi and lo words (x = hi + lo), the residual in FADD2
+__device__ __forceinline__ void split2(float2 x, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x.x, x.y);
+  const float2 r = sub_f32x2(x, __half22float2(h));
+  const __half2 l = __floats2half2_rn(r.x, r.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 // 16 fp32 values -> 8 packed fp16x2 hi words and 8 lo words (x = hi + lo)
 __device__ __forceinline__ void split16(const float* v, uint32_t* hi, uint32_t* lo) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-    const float2 f = __half22float2(h);
-    const __half2 l = __floats2half2_rn(v[2 * i] - f.x, v[2 * i + 1] - f.y);
-    hi[i] = *reinterpret_cast<const uint32_t*>(&h);
-    lo[i] = *reinterpret_cast<const uint32_t*>(&l);
-  }
+  for (int i = 0; i < 8; ++i) split2(make_float2(v[2 * i], v[2 * i + 1]), hi[i], lo[i]);
 }
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -460,7 +477,9 @@ __global__ void tile_lsd_kernel(const float* __restrict__ lse, const float* __re
   const int64_t row = tile_row0[t] + local;
   const bool ok = local < n;
   float* o = lsd + ht * 2 * KT;
-  o[j] = ok ? lse[row * n_head + head] : 0.f;
+  // lse - 15: 2^(s - lse + 15) = 2^15 P comes straight from the MUFU; padded queries get
+  // +inf so their P is exactly 0 without a per-element mask
+  o[j] = ok ? lse[row * n_head + head] - 15.f : __int_as_float(0x7f800000);
   o[KT + j] = ok ? D[row * n_head + head] * grad_scale_t(bits) : 0.f;
 }
 
@@ -659,20 +678,20 @@ __global__ void __launch_bounds__(KV_THREADS, 1)
       const uint32_t sc = tbase + lo + C_SG + (c & 1) * 128;
       PTX_LD16(sc + col, rs);
       PTX_LD16(sc + 64 + col, rg);
-      const float* ls = sm.lsd[s] + col;
-      const float* dd = sm.lsd[s] + KT + col;
-      float p[16], ds[16];
-      const int q0 = c * KT + col;
+      const float2* ls = reinterpret_cast<const float2*>(sm.lsd[s] + col);
+      const float2* dd = reinterpret_cast<const float2*>(sm.lsd[s] + KT + col);
+      const float2 cds = make_float2(dsc / PSCALE, dsc / PSCALE);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const bool ok = q0 + i < w.n;
-        const float pr = ok ? ex2f(__uint_as_float(rs[i]) - ls[i]) : 0.f;
-        ds[i] = pr * (__uint_as_float(rg[i]) - dd[i]) * dsc;
-        p[i] = pr * PSCALE;
+      for (int i = 0; i < 8; ++i) {
+        const float2 x = sub_f32x2(make_float2(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])),
+                                   ls[i]);
+        const float2 p2 = make_float2(ex2f(x.x), ex2f(x.y));  // 2^15 P
+        const float2 g = sub_f32x2(make_float2(__uint_as_float(rg[2 * i]), __uint_as_float(rg[2 * i + 1])),
+                                   dd[i]);
+        split2(p2, ph[i], pl[i]);
+        split2(mul_f32x2(mul_f32x2(p2, g), cds), dh8[i], dl8[i]);
       }
-      split16(p, ph, pl);
-      split16(ds, dh8, dl8);
       if (c > 0) {  // the previous chunk's products have read P^T / dS^T
         mbar_wait_sleep(&sm.pv_done, (c - 1) & 1);
         fence_after();
@@ -855,6 +874,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
     const bool valid = lr < w.n;
     const float l = valid ? lse_h[(int64_t)head * R + w.row0 + lr] : 0.f;
     const float D = valid ? d_h[(int64_t)head * R + w.row0 + lr] : 0.f;
+    const float2 l2 = make_float2(l, l), D2 = make_float2(D, D), dsc2 = make_float2(dsc, dsc);
     float4* acc = &sm.acc[t][0][row];
 #pragma unroll
     for (int c4 = 0; c4 < 4; ++c4) acc[c4 * QT] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -877,20 +897,25 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
       fence_after();
       if (j > 0 && j % DRAIN == 0) drain();  // dq of chunks [j - DRAIN, j) complete
       const int k0 = j * KT;
+      const bool full = valid && k0 + KT <= w.n;  // no padded key in this chunk
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t rs[16], rg[16], dh8[8], dl8[8];
         PTX_LD16(cb + 16 * c, rs);
         PTX_LD16(cb + 64 + 16 * c, rg);
-        float ds[16];
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const bool ok = valid && k0 + 16 * c + i < w.n;
-          const float p = ok ? ex2f(__uint_as_float(rs[i]) - l) : 0.f;
-          ds[i] = p * (__uint_as_float(rg[i]) - D) * dsc;
+        for (int i = 0; i < 8; ++i) {
+          const float2 x = sub_f32x2(make_float2(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), l2);
+          float2 p2 = make_float2(ex2f(x.x), ex2f(x.y));
+          if (!full) {
+            const int kk = k0 + 16 * c + 2 * i;
+            p2.x = valid && kk < w.n ? p2.x : 0.f;
+            p2.y = valid && kk + 1 < w.n ? p2.y : 0.f;
+          }
+          const float2 g = sub_f32x2(make_float2(__uint_as_float(rg[2 * i]), __uint_as_float(rg[2 * i + 1])), D2);
+          split2(mul_f32x2(mul_f32x2(p2, g), dsc2), dh8[i], dl8[i]);
         }
-        split16(ds, dh8, dl8);
         PTX_ST8(cb + 128 + 8 * c, dh8);
         PTX_ST8(cb + 160 + 8 * c, dl8);
       }
