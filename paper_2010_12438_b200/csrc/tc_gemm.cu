@@ -72,6 +72,14 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// one lane of a converged warp (the MMA issuer)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}"
+               : "=r"(p));
+  return p != 0;
+}
+
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -206,7 +214,7 @@ struct Cfg {
   static constexpr size_t SMEM = (size_t)NS * STAGE + W_RES + EPI_BYTES + 1536 + ALIGN_PAD;
 };
 
-constexpr int G_THREADS = 288;  // warps 0-3 split A, 4-7 epilogue, 8 = TMA producer + MMA
+constexpr int G_THREADS = 320;  // warps 0-3 split A, 4-7 epilogue, 8 MMA issue, 9 loads
 
 template <int ACT>
 __device__ __forceinline__ float activate(float x) {
@@ -281,11 +289,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 8) {
-    // ------------------------------------------------ TMA producer + MMA issuer
+  const int total = my_tiles * nch;
+  if (warp == 9) {
+    // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      constexpr uint32_t ID = H ? idesc_f16(BM, BN) : idesc_tf32(BM, BN);
-      const int total = my_tiles * nch;
       auto load = [&](int g) {
         const int s = g % NS;
         const int t = blockIdx.x + (g / nch) * gridDim.x;
@@ -313,68 +320,73 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                      2 * CF::B_BYTES, w_full);
         }
       }
-      for (int g = 0; g < NS && g < total; ++g) load(g);
-      if constexpr (WRCH > 0) {
-        if (my_tiles > 0) mbar_wait(w_full, 0);
+      for (int g = 0; g < total; ++g) {
+        if (g >= NS) mbar_wait(&done[g % NS], ((g / NS) - 1) & 1);  // stage consumed
+        load(g);
       }
-      int g = 0;
-      for (int tl = 0; tl < my_tiles; ++tl) {
-        const int ab = tl & 1;
-        if (tl >= 2) mbar_wait(&acc_empty[ab], ((tl >> 1) - 1) & 1);
+    }
+    __syncwarp();
+  } else if (warp == 8) {
+    // ------------------------------------------------ MMA issue (converged, one elected lane)
+    constexpr uint32_t ID = H ? idesc_f16(BM, BN) : idesc_tf32(BM, BN);
+    if constexpr (WRCH > 0) {
+      if (my_tiles > 0) mbar_wait(w_full, 0);
+    }
+    int g = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int ab = tl & 1;
+      if (tl >= 2) mbar_wait(&acc_empty[ab], ((tl >> 1) - 1) & 1);
+      fence_after();
+      const uint32_t tacc = tbase + ab * CF::ACOLS;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int s = g % NS;
+        const uint32_t ph = (g / NS) & 1;
+        mbar_wait(&full[s], ph);
+        mbar_wait(&a_full[s], ph);
         fence_after();
-        const uint32_t tacc = tbase + ab * CF::ACOLS;
-        for (int c = 0; c < nch; ++c, ++g) {
-          const int s = g % NS;
-          const uint32_t ph = (g / NS) & 1;
-          mbar_wait(&full[s], ph);
-          mbar_wait(&a_full[s], ph);
-          fence_after();
-          const uint32_t bh = WRCH ? smem_u32(w_res + (size_t)c * 2 * CF::B_BYTES) : smem_u32(B_hi(s));
+        if (elect_one()) {
+          const uint32_t bh =
+              WRCH ? smem_u32(w_res + (size_t)c * 2 * CF::B_BYTES) : smem_u32(B_hi(s));
           const uint32_t bl = bh + CF::B_BYTES;
           if constexpr (H) {
             // fp16 hi at +0, lo at +8 KB; 8-half K chunks 2 KB apart (A) / BN*16 B (B)
-            const uint32_t a16 = smem_u32(A_hi(s, 0));
+            const uint64_t da = sdesc(smem_u32(A_hi(s, 0)), 2048, 128);
+            const uint64_t dbh0 = sdesc(bh, BN * 16, 128), dbl0 = sdesc(bl, BN * 16, 128);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint64_t dah = sdesc(a16 + kk * 4096, 2048, 128);
-              const uint64_t dal = sdesc(a16 + 8192 + kk * 4096, 2048, 128);
-              const uint64_t dbh = sdesc(bh + kk * 2 * BN * 16, BN * 16, 128);
-              const uint64_t dbl = sdesc(bl + kk * 2 * BN * 16, BN * 16, 128);
+              // K steps add (bytes >> 4) to the descriptors' start-address field
+              const uint64_t dah = da + kk * 256, dal = da + 512 + kk * 256;
+              const uint64_t dbh = dbh0 + kk * 2 * BN, dbl = dbl0 + kk * 2 * BN;
               umma_ss_f16(tacc, dah, dbh, ID, (c > 0 || kk > 0));
               umma_ss_f16(tacc, dah, dbl, ID, 1);
               umma_ss_f16(tacc, dal, dbh, ID, 1);
             }
           } else {
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
-            const uint64_t dbl = sdesc(bl + k * 32 * BN, 16 * BN, 128);
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint64_t dbh = sdesc(bh + k * 32 * BN, 16 * BN, 128);
+              const uint64_t dbl = sdesc(bl + k * 32 * BN, 16 * BN, 128);
 #pragma unroll
-            for (int h = 0; h < MH; ++h) {
-              const uint64_t dah = sdesc_sw128(smem_u32(A_hi(s, h)) + k * 32);
-              const uint64_t dal = sdesc_sw128(smem_u32(A_lo(s, h)) + k * 32);
-              const uint32_t th = tacc + h * CF::TCOLS;
-              umma_ss(th, dah, dbh, ID, (c > 0 || k > 0));
-              umma_ss(th, dah, dbl, ID, 1);
-              umma_ss(th, dal, dbh, ID, 1);
+              for (int h = 0; h < MH; ++h) {
+                const uint64_t dah = sdesc_sw128(smem_u32(A_hi(s, h)) + k * 32);
+                const uint64_t dal = sdesc_sw128(smem_u32(A_lo(s, h)) + k * 32);
+                const uint32_t th = tacc + h * CF::TCOLS;
+                umma_ss(th, dah, dbh, ID, (c > 0 || k > 0));
+                umma_ss(th, dah, dbl, ID, 1);
+                umma_ss(th, dal, dbh, ID, 1);
+              }
             }
           }
-          }
           umma_commit(&done[s]);
-          if (g >= 1 && (g - 1) + NS < total) {
-            mbar_wait(&done[(g - 1) % NS], ((g - 1) / NS) & 1);
-            load(g - 1 + NS);
-          }
+          if (c == nch - 1) umma_commit(&acc_full[ab]);
         }
-        umma_commit(&acc_full[ab]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else if (warp < 4) {
     // ------------------------------------------------ A split: hi in place, lo in the twin
     // (elementwise, so the lo tile inherits the TMA's swizzled layout)
     const int lt = threadIdx.x;  // 0..127
-    const int total = my_tiles * nch;
     for (int g = 0; g < total; ++g) {
       const int s = g % NS;
       mbar_wait(&full[s], (g / NS) & 1);
@@ -929,7 +941,7 @@ void tc_ffn(const float* X, int64_t ldx, const void* W1_16, const void* W2_16, c
   const CUtensorMap mx = a_map(X, M, 128, ldx);
   const int ntiles = (int)cdiv(M, tg::BM);
   const int grid = std::min(ntiles, num_sms());
-  tg::ffn_kernel<<<grid, tg::G_THREADS, tg::FF_SMEM, st>>>(mx, a, ntiles);
+  tg::ffn_kernel<<<grid, tg::FF_THREADS, tg::FF_SMEM, st>>>(mx, a, ntiles);
   LAUNCH_CHECK();
 }
 

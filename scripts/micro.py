@@ -3,7 +3,7 @@
   des      : batched DES throughput on the cfg4 graph, per launch mode
   forward  : one wave of cfg4 forwards, per-kernel-class CUDA-event times
   attn     : forward with the fp16 / tf32 head-attention kernels (GO_ATTN)
-Usage: python scripts/micro.py des|forward|poly [K]"""
+Usage: python scripts/micro.py des|forward|poly [K] [des modes, e.g. warp]"""
 import ctypes as C
 import os
 import sys
@@ -21,7 +21,7 @@ def cfg4():
     return gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
 
 
-def des(K):
+def des(K, modes=("lane", "warp")):
     from paper_2010_12438_b200.costmodel import uniform_topology
     from paper_2010_12438_b200.simulator import simulate_many, singleton_fused
     g = cfg4()
@@ -31,7 +31,7 @@ def des(K):
     fg = singleton_fused(g)
     top = uniform_topology(8)
     ref = None
-    for mode, smem in (("lane", "-"), ("warp", "-")):
+    for mode in modes:
         os.environ["GO_DES_MODE"] = mode
         simulate_many(fg, pl[:32], pr, top)
         torch.cuda.synchronize()
@@ -90,7 +90,7 @@ if __name__ == "__main__":
     what = sys.argv[1]
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     if what == "des":
-        des(n or 512)
+        des(n or 512, tuple(sys.argv[3].split(",")) if len(sys.argv) > 3 else ("lane", "warp"))
     elif what == "attn":
         forward(n or 8, env=[("GO_ATTN", "f16"), ("GO_ATTN", "tf32"), ("GO_ATTN", "f16")])
     elif what == "tc":
