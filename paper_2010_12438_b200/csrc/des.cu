@@ -47,23 +47,46 @@ struct LinkEnt {
   int32_t grp;
 };
 
+// Per-placement dynamic state of one group: pending in-edges, remaining consumers (<< 5)
+// with the group's device in the low 5 bits, -priority (0 for FIFO) and the topo index --
+// everything mark_ready / deliver / the memory sweep need, in one 16-B load.
+struct DesNodeState {
+  int32_t pend;
+  int32_t remdev;
+  int32_t npri;
+  int32_t topo;
+};
+
 struct DesCaps {
   int64_t cq;  // ready-heap capacity per device
   int64_t cl;  // FIFO capacity per link
   int64_t cm;  // exact-mode memory list capacity per device
-  // pending + remaining-consumer counts, ready heaps, link FIFOs, memory lists, then the
-  // per-group device table (int8, filled by the whole warp before the event loop)
-  __host__ __device__ int64_t gdev_offset(int G, int d) const {
-    int64_t b = 2 * (int64_t)G * 4;
-    b = round_up(b, 16) + (int64_t)d * cq * sizeof(HeapEnt);
+  // group states, ready heaps, link FIFOs, memory lists
+  __host__ __device__ int64_t heap_offset(int G) const { return round_up((int64_t)G * 16, 16); }
+  int64_t per_placement_bytes(int G, int d) const {
+    int64_t b = heap_offset(G) + (int64_t)d * cq * sizeof(HeapEnt);
     b += (int64_t)d * d * cl * sizeof(LinkEnt);
     b += 2 * (int64_t)d * cm * sizeof(double);
-    return round_up(b, 16);
-  }
-  int64_t per_placement_bytes(int G, int d) const {
-    return round_up(gdev_offset(G, d) + G, 256);
+    return round_up(b, 256);
   }
 };
+
+// group states for one placement (simulator.py:320-330 initial pending counts / devices /
+// priorities); lane `l0` of `nl` cooperating threads
+__device__ __forceinline__ void des_init_states(const DesView& V, const int32_t* __restrict__ pl,
+                                                const int32_t* __restrict__ pr, int policy,
+                                                DesNodeState* st, int l0, int nl) {
+  for (int g = l0; g < V.G; g += nl) {
+    const DesGroupRec& r = V.grec[g];
+    const int rep = r.rep;
+    DesNodeState x;
+    x.pend = r.pending0;
+    x.remdev = (r.nsucc << 5) | pl[rep];
+    x.npri = policy == 0 ? -pr[rep] : 0;
+    x.topo = r.topo;
+    st[g] = x;
+  }
+}
 
 enum { ST_OK = 0, ST_OVERFLOW = 1, ST_DEADLOCK = 2, ST_MEMLIST = 3 };
 
@@ -109,15 +132,15 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
                        const double* __restrict__ mbw, const double* __restrict__ cap,
                        const double* __restrict__ lbw, int policy, DesCaps caps, char* base,
                        DesState<MAXD>& S, DesTraceLog tr, double& step, int8_t& viol_out,
-                       const int8_t* __restrict__ gdev_tab = nullptr) {
+                       bool states_ready = false, const double* __restrict__ ctab = nullptr) {
   const int G = V.G;
-  int32_t* pending = reinterpret_cast<int32_t*>(base);
-  int32_t* rem = pending + G;
-  HeapEnt* heaps = reinterpret_cast<HeapEnt*>(base + round_up(2 * (int64_t)G * 4, 16));
+  DesNodeState* gst = reinterpret_cast<DesNodeState*>(base);
+  HeapEnt* heaps = reinterpret_cast<HeapEnt*>(base + caps.heap_offset(G));
   LinkEnt* lq = reinterpret_cast<LinkEnt*>(heaps + (int64_t)d * caps.cq);
   double* mlist = reinterpret_cast<double*>(lq + (int64_t)d * d * caps.cl);
-  // group -> device: the precomputed int8 table (one dependent load instead of two)
-  auto gdev = [&](int g) { return gdev_tab ? (int)gdev_tab[g] : pl[V.grp_rep[g]]; };
+  // the caller's warp may have filled the states already (des_kernel)
+  if (!states_ready) des_init_states(V, pl, pr, policy, gst, 0, 1);
+  auto gdev = [&](int g) { return gst[g].remdev & 31; };
   int64_t n_trace = 0;  // events logged (the single-placement trace launch only)
   auto log_event = [&](double t0, double t1, int kind, int a, int b, int g) {
     if (tr.rec && n_trace < tr.cap) tr.rec[n_trace] = DesTraceRec{t0, t1, kind, a, b, g};
@@ -210,20 +233,23 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
     }
     return top;
   };
-  auto mark_ready = [&](int g, double t) {
-    HeapEnt e;
-    e.rt = t;
-    e.topo = V.topo_index[g];
-    e.grp = g;
-    e.npri = policy == 0 ? -pr[V.grp_rep[g]] : 0;
-    e.pad = 0;
-    heap_push(gdev(g), e);
-  };
   auto deliver = [&](int g, double t) {
-    if (--pending[g] == 0) mark_ready(g, t);
+    DesNodeState x = gst[g];
+    gst[g].pend = --x.pend;
+    if (x.pend == 0) {
+      HeapEnt e;
+      e.rt = t;
+      e.topo = x.topo;
+      e.grp = g;
+      e.npri = x.npri;
+      e.pad = 0;
+      heap_push(x.remdev & 31, e);
+    }
   };
   const bool exact_int = V.mem_int_exact != 0;
+  uint32_t mdirty = 0;  // devices with allocs / frees queued in the current time group
   auto mem_add = [&](int dev, double b, bool alloc) {
+    mdirty |= 1u << dev;
     if (exact_int) {
       if (alloc) acc_a[dev] = __dadd_rn(acc_a[dev], b);
       else acc_f[dev] = __dadd_rn(acc_f[dev], b);
@@ -246,7 +272,8 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
     lst[p] = b;
   };
   auto mem_flush = [&]() {
-    for (int dev = 0; dev < d; ++dev) {
+    for (uint32_t m = mdirty; m; m &= m - 1) {  // ascending device order
+      const int dev = __ffs(m) - 1;
       if (na[dev] == 0 && nf[dev] == 0) continue;
       if (exact_int) {
         double c = __dadd_rn(cur[dev], acc_a[dev]);
@@ -264,14 +291,21 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
       }
       na[dev] = nf[dev] = 0;
     }
+    mdirty = 0;
   };
 
-  for (int g = 0; g < G; ++g) {
-    pending[g] = V.pending0[g];
-    rem[g] = V.nsucc[g];
+  // groups without external in-edges (host-built list, index order) start ready
+  for (int i = 0; i < V.num_src && status == ST_OK; ++i) {
+    const int g = V.src_grp[i];
+    const DesNodeState x = gst[g];
+    HeapEnt e;
+    e.rt = 0.0;
+    e.topo = x.topo;
+    e.grp = g;
+    e.npri = x.npri;
+    e.pad = 0;
+    heap_push(x.remdev & 31, e);
   }
-  for (int g = 0; g < G && status == ST_OK; ++g)
-    if (pending[g] == 0) mark_ready(g, 0.0);
 
   auto schedule = [&](double t) {
     for (int w = 0; w < (L + 63) / 64; ++w) {
@@ -283,7 +317,8 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
         if (link_t[s] != DINF) continue;
         LinkEnt* q = lq + (int64_t)s * caps.cl;
         LinkEnt e = q[lq_h[s]];
-        lq_h[s] = (lq_h[s] + 1) % (int32_t)caps.cl;
+        const int32_t nh = lq_h[s] + 1;  // ring wrap without an integer division
+        lq_h[s] = nh == (int32_t)caps.cl ? 0 : nh;
         if (--lq_n[s] == 0) lmask[w] &= ~(1ull << b);
         double dt = __ddiv_rn(V.out_bytes[e.edge], lbw[s]);
         link_t[s] = __dadd_rn(t, dt);
@@ -299,7 +334,13 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
       if (dev_t[dev] != DINF) continue;
       HeapEnt e = heap_pop(dev);
       int g = e.grp;
-      double dt = fmax(__ddiv_rn(V.cost_flops[g], peakf[dev]), __ddiv_rn(V.cost_bytes[g], mbw[dev]));
+      double dt;
+      if (ctab) {
+        dt = ctab[(int64_t)g * d + dev];  // des_ctab_kernel: the same two divisions
+      } else {
+        const double2 fb = *reinterpret_cast<const double2*>(&V.grec[g].cost_flops);
+        dt = fmax(__ddiv_rn(fb.x, peakf[dev]), __ddiv_rn(fb.y, mbw[dev]));
+      }
       // Python max(a, b) returns a unless b > a; fmax agrees for non-NaN inputs
       busy[dev] = __dadd_rn(busy[dev], dt);
       dev_t[dev] = __dadd_rn(t, dt);
@@ -312,26 +353,67 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
   int done = 0;
   double step_t = 0.0;
   double mem_time = -1.0;
+  constexpr int LW = (MAXD * MAXD + 63) / 64;
   while (status == ST_OK) {
-    double now = DINF;
-    for (int i = 0; i < d; ++i) now = fmin(now, dev_t[i]);
-    for (int w = 0; w < (L + 63) / 64; ++w)
-      for (uint64_t mm = amask[w]; mm; mm &= mm - 1)
-        now = fmin(now, link_t[w * 64 + __ffsll((long long)mm) - 1]);
+    // next event time, with the devices / links that finish exactly then (one pass; the
+    // reference pops every event of the minimum time in (time, kind, slot) order)
+    double dnow = DINF;
+    uint32_t dset = 0;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      if (i < d) {
+        const double t = dev_t[i];
+        if (t < dnow) {
+          dnow = t;
+          dset = 1u << i;
+        } else if (t == dnow) {
+          dset |= 1u << i;
+        }
+      }
+    }
+    double lnow = DINF;
+    uint64_t lset[LW];
+#pragma unroll
+    for (int w = 0; w < LW; ++w) {
+      lset[w] = 0;
+      if (w * 64 < L) {
+        for (uint64_t mm = amask[w]; mm; mm &= mm - 1) {
+          const int b = __ffsll((long long)mm) - 1;
+          const double t = link_t[w * 64 + b];
+          if (t < lnow) {
+#pragma unroll
+            for (int w2 = 0; w2 < LW; ++w2) lset[w2] = 0;
+            lnow = t;
+            lset[w] = 1ull << b;
+          } else if (t == lnow) {
+            lset[w] |= 1ull << b;
+          }
+        }
+      }
+    }
+    const double now = fmin(dnow, lnow);
     if (now == DINF) break;
+    if (dnow != now) dset = 0;
+    if (lnow != now) {
+#pragma unroll
+      for (int w = 0; w < LW; ++w) lset[w] = 0;
+    }
     if (now != mem_time) {
       mem_flush();
       mem_time = now;
     }
     // computes (kind 0) in device order
-    for (int dev = 0; dev < d; ++dev) {
-      if (dev_t[dev] != now) continue;
+    for (uint32_t m = dset; m; m &= m - 1) {
+      const int dev = __ffs(m) - 1;
       int g = dev_g[dev];
       dev_t[dev] = DINF;
       dev_g[dev] = -1;
       ++done;
       step_t = now;
-      for (int64_t e = V.out_off[g]; e < V.out_off[g + 1]; ++e) {
+      const DesGroupRec& rg = V.grec[g];
+      const int4 oc = *reinterpret_cast<const int4*>(&rg.out_off);  // out_off/cnt, pred_off/cnt
+      const double b = rg.resident;
+      for (int64_t e = oc.x; e < (int64_t)oc.x + oc.y; ++e) {
         int gd = V.out_grp[e];
         int dd = gdev(gd);
         if (dd == dev) {
@@ -343,25 +425,31 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
             break;
           }
           LinkEnt* q = lq + (int64_t)s * caps.cl;
-          q[(lq_h[s] + lq_n[s]) % (int32_t)caps.cl] = LinkEnt{(int32_t)e, gd};
+          int32_t qi = lq_h[s] + lq_n[s];
+          if (qi >= (int32_t)caps.cl) qi -= (int32_t)caps.cl;
+          q[qi] = LinkEnt{(int32_t)e, gd};
           ++lq_n[s];
           lmask[s >> 6] |= 1ull << (s & 63);
         }
       }
-      double b = V.resident[g];
       if (b != 0.0) mem_add(dev, b, true);
-      for (int64_t j = V.pred_off[g]; j < V.pred_off[g + 1]; ++j) {
+      for (int64_t j = oc.z; j < (int64_t)oc.z + oc.w; ++j) {
         int p = V.pred_grp[j];
-        if (--rem[p] == 0 && V.resident[p] != 0.0) mem_add(gdev(p), V.resident[p], false);
+        const int rd = gst[p].remdev - 32;
+        gst[p].remdev = rd;
+        if (rd < 32) {
+          const double rp = V.grec[p].resident;
+          if (rp != 0.0) mem_add(rd & 31, rp, false);
+        }
       }
-      if (V.nsucc[g] == 0 && b != 0.0) mem_add(dev, b, false);
+      if (oc.y == 0 && b != 0.0) mem_add(dev, b, false);  // no successors: nsucc == 0
     }
     // transfers (kind 1) in (src, dst) order
-    for (int w = 0; w < (L + 63) / 64; ++w) {
-      for (uint64_t mm = amask[w]; mm; mm &= mm - 1) {
+#pragma unroll
+    for (int w = 0; w < LW; ++w) {
+      for (uint64_t mm = lset[w]; mm; mm &= mm - 1) {
         const int b = __ffsll((long long)mm) - 1;
         const int s = w * 64 + b;
-        if (link_t[s] != now) continue;
         int g = link_g[s];
         link_t[s] = DINF;
         link_g[s] = -1;
@@ -390,6 +478,17 @@ __device__ int des_run(const DesView& V, const int32_t* __restrict__ pl,
   return status;
 }
 
+// compute time of every group on every device, max(flops / peak, bytes / bw)
+// (simulator.py kernel_time), once per launch instead of two float64 divisions per event
+__global__ void des_ctab_kernel(DesView V, int d, const double* __restrict__ peakf,
+                                const double* __restrict__ mbw, double* __restrict__ ctab) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)V.G * d) return;
+  const int g = (int)(i / d), dev = (int)(i % d);
+  ctab[i] = fmax(__ddiv_rn(V.grec[g].cost_flops, peakf[dev]),
+                 __ddiv_rn(V.grec[g].cost_bytes, mbw[dev]));
+}
+
 template <int MAXD, bool SH>
 __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
                            int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
@@ -401,17 +500,17 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
                            int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
                            double* __restrict__ o_peak, double* __restrict__ o_reward,
                            int32_t* __restrict__ o_status, int lanes_per_placement,
-                           DesTraceLog tr) {
+                           DesTraceLog tr, const double* __restrict__ ctab) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int tid = gtid / lanes_per_placement;
   if (tid >= K) return;
   const int kk = which ? which[tid] : tid;
   const int32_t* pl = placement + (int64_t)kk * pstride;
   char* base = scratch + (int64_t)tid * scratch_stride;
-  int8_t* gdev_tab = nullptr;
-  if (lanes_per_placement == 32) {  // warp mode: the whole warp fills the group devices
-    gdev_tab = reinterpret_cast<int8_t*>(base + caps.gdev_offset(V.G, d));
-    for (int g = gtid % 32; g < V.G; g += 32) gdev_tab[g] = (int8_t)pl[V.grp_rep[g]];
+  const int32_t* pr = prio + (int64_t)kk * prio_stride;
+  const bool warp_init = lanes_per_placement == 32;
+  if (warp_init) {  // warp mode: the whole warp fills the group states
+    des_init_states(V, pl, pr, policy, reinterpret_cast<DesNodeState*>(base), gtid % 32, 32);
     __syncwarp();
   }
   if (gtid % lanes_per_placement) return;
@@ -420,8 +519,8 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
   auto& S = pick_state<SH>(sh_state, lo_state);
   double step;
   int8_t viol;
-  const int status = des_run<MAXD>(V, pl, prio + (int64_t)kk * prio_stride, d, peakf, mbw, cap,
-                                   lbw, policy, caps, base, S, tr, step, viol, gdev_tab);
+  const int status = des_run<MAXD>(V, pl, pr, d, peakf, mbw, cap, lbw, policy, caps, base, S, tr,
+                                   step, viol, warp_init, ctab);
   o_status[tid] = status;
   if (status != ST_OK) return;
   o_step[kk] = step;
@@ -456,12 +555,14 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
   const int G = v.G;
   auto run = [&](int count, const int32_t* which, DesCaps c) {
     int64_t stride = c.per_placement_bytes(G, d);
-    int64_t head = round_up((int64_t)topo.size() * 8, 256) + round_up((int64_t)count * 4, 256) +
-                   round_up((int64_t)K * 4, 256);
+    const int64_t h_ctab = round_up((int64_t)topo.size() * 8, 256) +
+                           round_up((int64_t)count * 4, 256) + round_up((int64_t)K * 4, 256);
+    const int64_t head = h_ctab + round_up((int64_t)G * d * 8, 256);
     char* ws = reinterpret_cast<char*>(ctx->ensure_des(head + stride * count));
     double* dtopo = reinterpret_cast<double*>(ws);
     int32_t* dstatus = reinterpret_cast<int32_t*>(ws + round_up((int64_t)topo.size() * 8, 256));
     int32_t* dwhich = dstatus + round_up(count, 64);
+    double* dctab = reinterpret_cast<double*>(ws + h_ctab);
     CUDA_CHECK(cudaMemcpyAsync(dtopo, topo.data(), topo.size() * 8, cudaMemcpyHostToDevice, st));
     if (which)
       CUDA_CHECK(cudaMemcpyAsync(dwhich, which, (size_t)count * 4, cudaMemcpyHostToDevice, st));
@@ -476,11 +577,14 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
                                                             : des_kernel<DES_MAXD, true>)
                     : (d <= 4 ? des_kernel<4, false> : d <= 8 ? des_kernel<8, false>
                                                              : des_kernel<DES_MAXD, false>);
+    const int64_t nct = (int64_t)G * d;
+    des_ctab_kernel<<<(unsigned)cdiv(nct, 256), 256, 0, st>>>(v, d, dtopo, dtopo + d, dctab);
+    LAUNCH_CHECK();
     kern<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
         v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
         dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
         step_time, valid, violation, busy, peak_mem, reward, dstatus, lanes,
-        DesTraceLog{trace, trace_cap, trace_count});
+        DesTraceLog{trace, trace_cap, trace_count}, dctab);
     LAUNCH_CHECK();
     std::vector<int32_t> hstat(count);
     CUDA_CHECK(cudaMemcpyAsync(hstat.data(), dstatus, (size_t)count * 4, cudaMemcpyDeviceToHost,

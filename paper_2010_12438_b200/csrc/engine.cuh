@@ -15,8 +15,23 @@ struct GraphView {
   const int64_t* samp_off; // [n+1] prefix of min(deg, k) for the configured k
 };
 
+// One group's static DES fields packed in a 64-B record, so the event loop reaches all
+// it needs about a group with one L2 round trip (the separate arrays below cost one
+// dependent load each).  Offsets fit int32 (checked when the view is built).
+struct __align__(64) DesGroupRec {
+  double cost_flops, cost_bytes, resident;
+  int32_t topo, rep;            // topo_index, grp_rep
+  int32_t out_off, out_cnt;     // external out edges [out_off, out_off + out_cnt)
+  int32_t pred_off, pred_cnt;   // distinct predecessor groups
+  int32_t pending0, nsucc;
+  int32_t pad[2];
+};
+
 // Device DES tables of the current (fused) grouping: simulator.py:86-172.
 struct DesView {
+  const DesGroupRec* grec;     // [G] packed per-group record (the event loop reads these)
+  const int32_t* src_grp;      // groups without external in-edges, ascending
+  int32_t num_src;
   int32_t n, G;
   const int32_t* grp_rep;      // [G] lowest member node id
   const int32_t* pending0;     // [G] #external in-edges

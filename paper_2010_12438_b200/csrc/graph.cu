@@ -475,9 +475,33 @@ void go_graph::set_fusion(const std::vector<int64_t>& label) {
       coff.push_back((int64_t)cgrp.size());
     }
   }
+  GO_CHECK(num_out < ((int64_t)1 << 31) && pred_off[G] < ((int64_t)1 << 31),
+           "DES edge tables exceed 2^31 entries");
+  std::vector<DesGroupRec> grec(G);
+  for (int i = 0; i < G; ++i) {
+    DesGroupRec& r = grec[i];
+    r = DesGroupRec{};
+    r.cost_flops = cf[i];
+    r.cost_bytes = cb[i];
+    r.resident = res[i];
+    r.topo = tindex[i];
+    r.rep = rep[i];
+    r.out_off = (int32_t)out_off[i];
+    r.out_cnt = (int32_t)(out_off[i + 1] - out_off[i]);
+    r.pred_off = (int32_t)pred_off[i];
+    r.pred_cnt = (int32_t)(pred_off[i + 1] - pred_off[i]);
+    r.pending0 = pend[i];
+    r.nsucc = nsucc[i];
+  }
   DesView v{};
   v.n = n;
   v.G = G;
+  v.grec = upload(grec, &des_allocs);
+  std::vector<int32_t> srcs;
+  for (int i = 0; i < G; ++i)
+    if (pend[i] == 0) srcs.push_back(i);
+  v.src_grp = upload(srcs, &des_allocs);
+  v.num_src = (int32_t)srcs.size();
   v.grp_rep = upload(rep, &des_allocs);
   v.pending0 = upload(pend, &des_allocs);
   v.out_off = upload(out_off, &des_allocs);

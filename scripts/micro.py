@@ -34,6 +34,7 @@ def des(K, modes=("lane", "warp")):
     for mode in modes:
         os.environ["GO_DES_MODE"] = mode
         simulate_many(fg, pl[:32], pr, top)
+        simulate_many(fg, pl, pr, top)  # workspace sized for K
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = simulate_many(fg, pl, pr, top)
