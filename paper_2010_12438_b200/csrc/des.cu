@@ -77,13 +77,12 @@ __device__ __forceinline__ void des_init_states(const DesView& V, const int32_t*
                                                 const int32_t* __restrict__ pr, int policy,
                                                 DesNodeState* st, int l0, int nl) {
   for (int g = l0; g < V.G; g += nl) {
-    const DesGroupRec& r = V.grec[g];
-    const int rep = r.rep;
+    const int4 r = *reinterpret_cast<const int4*>(&V.grec[g].topo);  // topo, rep, pend0, nsucc
     DesNodeState x;
-    x.pend = r.pending0;
-    x.remdev = (r.nsucc << 5) | pl[rep];
-    x.npri = policy == 0 ? -pr[rep] : 0;
-    x.topo = r.topo;
+    x.pend = r.z;
+    x.remdev = (r.w << 5) | pl[r.y];
+    x.npri = policy == 0 ? -pr[r.y] : 0;
+    x.topo = r.x;
     st[g] = x;
   }
 }

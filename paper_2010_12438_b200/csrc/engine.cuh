@@ -1,5 +1,6 @@
 // Internal structures of libgo_b200: context, graph handle, kernel launchers.
 #pragma once
+#include <cstddef>
 #include <vector>
 
 #include "common.cuh"
@@ -19,13 +20,16 @@ struct GraphView {
 // it needs about a group with one L2 round trip (the separate arrays below cost one
 // dependent load each).  Offsets fit int32 (checked when the view is built).
 struct __align__(64) DesGroupRec {
-  double cost_flops, cost_bytes, resident;
-  int32_t topo, rep;            // topo_index, grp_rep
+  double cost_flops, cost_bytes;
+  int32_t topo, rep, pending0, nsucc;  // one 16-B load for the per-placement state fill
   int32_t out_off, out_cnt;     // external out edges [out_off, out_off + out_cnt)
-  int32_t pred_off, pred_cnt;   // distinct predecessor groups
-  int32_t pending0, nsucc;
+  int32_t pred_off, pred_cnt;   // distinct predecessor groups (16-B aligned: one load)
+  double resident;
   int32_t pad[2];
 };
+static_assert(sizeof(DesGroupRec) == 64 && offsetof(DesGroupRec, topo) % 16 == 0 &&
+                  offsetof(DesGroupRec, out_off) % 16 == 0,
+              "DesGroupRec vector loads need 16-B aligned fields");
 
 // Device DES tables of the current (fused) grouping: simulator.py:86-172.
 struct DesView {
