@@ -109,11 +109,6 @@ struct DesState {
   uint64_t lmask[(M * M + 63) / 64];
   uint64_t amask[(M * M + 63) / 64];  // links with a transfer in flight
 };
-template <bool SH, class A, class B>
-__device__ __forceinline__ auto& pick_state(A& sh, B& lo) {
-  if constexpr (SH) return sh;
-  else return lo;
-}
 
 // One placement's simulation: the reference's event loop (simulator.py:320-441) run by
 // one thread.  S (the per-placement device / link state) lives in shared memory when
@@ -488,7 +483,10 @@ __global__ void des_ctab_kernel(DesView V, int d, const double* __restrict__ pea
                  __ddiv_rn(V.grec[g].cost_bytes, mbw[dev]));
 }
 
-template <int MAXD, bool SH>
+// One placement per 32-thread block (measured 4.2x faster than one placement per lane on
+// the cfg4 graph): the warp fills the group states, lane 0 runs the event loop with the
+// device / link state in shared memory.
+template <int MAXD>
 __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placement,
                            int64_t pstride, const int32_t* __restrict__ prio, int64_t prio_stride,
                            int d, const double* __restrict__ peakf, const double* __restrict__ mbw,
@@ -498,28 +496,22 @@ __global__ void des_kernel(DesView V, int K, const int32_t* __restrict__ placeme
                            double* __restrict__ o_step, uint8_t* __restrict__ o_valid,
                            int8_t* __restrict__ o_viol, double* __restrict__ o_busy,
                            double* __restrict__ o_peak, double* __restrict__ o_reward,
-                           int32_t* __restrict__ o_status, int lanes_per_placement,
-                           DesTraceLog tr, const double* __restrict__ ctab) {
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int tid = gtid / lanes_per_placement;
+                           int32_t* __restrict__ o_status, DesTraceLog tr,
+                           const double* __restrict__ ctab) {
+  const int tid = blockIdx.x;
   if (tid >= K) return;
   const int kk = which ? which[tid] : tid;
   const int32_t* pl = placement + (int64_t)kk * pstride;
   char* base = scratch + (int64_t)tid * scratch_stride;
   const int32_t* pr = prio + (int64_t)kk * prio_stride;
-  const bool warp_init = lanes_per_placement == 32;
-  if (warp_init) {  // warp mode: the whole warp fills the group states
-    des_init_states(V, pl, pr, policy, reinterpret_cast<DesNodeState*>(base), gtid % 32, 32);
-    __syncwarp();
-  }
-  if (gtid % lanes_per_placement) return;
-  __shared__ DesState<SH ? MAXD : 1> sh_state;
-  DesState<SH ? 1 : MAXD> lo_state;
-  auto& S = pick_state<SH>(sh_state, lo_state);
+  des_init_states(V, pl, pr, policy, reinterpret_cast<DesNodeState*>(base), threadIdx.x, 32);
+  __syncwarp();
+  if (threadIdx.x) return;
+  __shared__ DesState<MAXD> S;
   double step;
   int8_t viol;
   const int status = des_run<MAXD>(V, pl, pr, d, peakf, mbw, cap, lbw, policy, caps, base, S, tr,
-                                   step, viol, warp_init, ctab);
+                                   step, viol, true, ctab);
   o_status[tid] = status;
   if (status != ST_OK) return;
   o_step[kk] = step;
@@ -565,24 +557,14 @@ int simulate_batch(const DesView& v, int K, const int32_t* placement, int64_t ps
     CUDA_CHECK(cudaMemcpyAsync(dtopo, topo.data(), topo.size() * 8, cudaMemcpyHostToDevice, st));
     if (which)
       CUDA_CHECK(cudaMemcpyAsync(dwhich, which, (size_t)count * 4, cudaMemcpyHostToDevice, st));
-    // one placement per warp (default: no intra-warp divergence; measured 4.2x faster
-    // than 32 placements per warp on the cfg4 graph) or one per lane (GO_DES_MODE=lane)
-    const char* mode = getenv("GO_DES_MODE");
-    const int lanes = (mode && !strcmp(mode, "lane")) ? 1 : 32;
-    const int threads = 32;
-    // warp mode: one placement per 32-thread block, its state in shared memory
-    auto kern = lanes == 32
-                    ? (d <= 4 ? des_kernel<4, true> : d <= 8 ? des_kernel<8, true>
-                                                            : des_kernel<DES_MAXD, true>)
-                    : (d <= 4 ? des_kernel<4, false> : d <= 8 ? des_kernel<8, false>
-                                                             : des_kernel<DES_MAXD, false>);
+    auto kern = d <= 4 ? des_kernel<4> : d <= 8 ? des_kernel<8> : des_kernel<DES_MAXD>;
     const int64_t nct = (int64_t)G * d;
     des_ctab_kernel<<<(unsigned)cdiv(nct, 256), 256, 0, st>>>(v, d, dtopo, dtopo + d, dctab);
     LAUNCH_CHECK();
-    kern<<<(unsigned)cdiv((int64_t)count * lanes, threads), threads, 0, st>>>(
+    kern<<<(unsigned)count, 32, 0, st>>>(
         v, count, placement, pstride, prio, prio_stride, d, dtopo, dtopo + d, dtopo + 2 * d,
         dtopo + 3 * d, policy, baseline, c, ws + head, stride, which ? dwhich : nullptr,
-        step_time, valid, violation, busy, peak_mem, reward, dstatus, lanes,
+        step_time, valid, violation, busy, peak_mem, reward, dstatus,
         DesTraceLog{trace, trace_cap, trace_count}, dctab);
     LAUNCH_CHECK();
     std::vector<int32_t> hstat(count);

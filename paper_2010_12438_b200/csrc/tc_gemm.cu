@@ -804,12 +804,6 @@ void launch(const CUtensorMap& m1, const CUtensorMap& m2, const tg::Args& a, int
   LAUNCH_CHECK();
 }
 
-// GO_GEMM_WRES=0 keeps W in the smem ring (streamed from L2 per tile)
-static bool w_resident_ok() {
-  const char* e = getenv("GO_GEMM_WRES");
-  return !(e && e[0] == '0');
-}
-
 // GO_GEMM_F16=0 keeps the tf32 operands
 static bool use_f16() {
   const char* e = getenv("GO_GEMM_F16");
@@ -838,7 +832,7 @@ void launch_all(const float* A1, int64_t lda1, const float* A2, int64_t lda2, tg
     a16.gate = nullptr;
     // resident W when the whole packed W is one N block of <= 4 chunks (K <= 128): the
     // ring keeps >= 8 A stages (larger K would leave fewer A bytes in flight)
-    if (nblk == 1 && a.nch <= 4 && w_resident_ok() && tg::Cfg<BN, 1, true, 4>::NS >= 6)
+    if (nblk == 1 && a.nch <= 4 && tg::Cfg<BN, 1, true, 4>::NS >= 6)
       launch<BN, 1, LN, ACT, true, 4>(m1, m2, a16, nblk, st);
     else
       launch<BN, 1, LN, ACT, true>(m1, m2, a16, nblk, st);

@@ -175,28 +175,24 @@ void run_ppo_grad(go_ctx* ctx, const go_config_t& cfg, const float* P, const int
   int32_t* segoff = A.take<int32_t>(R + 1);
   // attention on mma.sync tensor cores (split-fp16 operands, three MMAs per product:
   // fp32-class results) with a gated fp32 SIMT re-run on range overflow;
-  // GO_TRAIN_ATTN=simt keeps the fp32 SIMT kernels only, =mma16 one fp16 MMA per product
-  // (faster, ~1e-3 relative gradients); GO_TRAIN_FWD=simt the SIMT tape forward only
+  // GO_TRAIN_ATTN=simt keeps the fp32 SIMT kernels only (the tests' comparison path)
   const char* ta_env = getenv("GO_TRAIN_ATTN");
   const bool attn_mma = trunk_mma_supported(dh) && !(ta_env && !strcmp(ta_env, "simt"));
-  const char* tf_env = getenv("GO_TRAIN_FWD");
-  const bool attn_mma_fwd = attn_mma && !(tf_env && !strcmp(tf_env, "simt"));
-  const bool attn_split = !(ta_env && !strcmp(ta_env, "mma16"));  // 3-MMA split precision
   int32_t* aflag = A.take<int32_t>(64);
   void* abw = A.take<char>((int64_t)attention_backward_mma_scratch(R, H));
   // the N x N head attention's tape forward on tcgen05 (split fp16, tc_tape.cu) unless
   // GO_TRAIN_ATTN selects another variant; falls back to the mma.sync forward when a score
   // bound exceeds the fp16 limit
-  const bool tape_tc = attn_mma && attn_split && dh <= 15 && !(ta_env && !strcmp(ta_env, "mma"));
+  const bool tape_tc = attn_mma && dh <= 15 && !(ta_env && !strcmp(ta_env, "mma"));
   void* tape_ws = A.take<char>((int64_t)tape_attention_tc_scratch(R, F, H));
   auto attn_fwd = [&](const float* q, const float* k, const float* v, const AttnTile* tiles,
                       int64_t nt, float* out, float* lse, const int32_t* gate = nullptr) {
-    if (attn_mma_fwd) {
-      if (attn_split && dh <= 15)
+    if (attn_mma) {
+      if (dh <= 15)
         attention_forward_mma(q, k, v, W, H, dh, tiles, nt, R, out, W, lse, abw, aflag, st,
                               gate);
       else
-        trunk_attention_mma(q, k, v, W, H, dh, tiles, nt, out, W, aflag, st, lse, attn_split);
+        trunk_attention_mma(q, k, v, W, H, dh, tiles, nt, out, W, aflag, st, lse, true);
       attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse, aflag);
     } else {
       attention(q, k, v, W, H, dh, tiles, nt, out, W, st, lse);

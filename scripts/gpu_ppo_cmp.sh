@@ -1,5 +1,5 @@
 # PPO tests + per-sample cfg4 PPO timing under the training-attention modes
-# usage: MODES="default GO_TRAIN_FWD=simt GO_TRAIN_ATTN=simt" bash scripts/gpu_ppo_cmp.sh
+# usage: MODES="default GO_TRAIN_ATTN=mma GO_TRAIN_ATTN=simt" bash scripts/gpu_ppo_cmp.sh
 cd $GRAFT_REPO_ROOT
 for mode in ${MODES:-default}; do
   e=""; [ "$mode" != default ] && e="$mode"

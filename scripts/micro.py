@@ -1,9 +1,9 @@
 #!/usr/bin/env python
 """Micro-benchmarks on one GPU (development aid, not the headline bench):
-  des      : batched DES throughput on the cfg4 graph, per launch mode
+  des      : batched DES throughput on the cfg4 graph (random placements)
   forward  : one wave of cfg4 forwards, per-kernel-class CUDA-event times
   attn     : forward with the fp16 / tf32 head-attention kernels (GO_ATTN)
-Usage: python scripts/micro.py des|forward|poly [K] [des modes, e.g. warp]"""
+Usage: python scripts/micro.py des|forward|poly [K]"""
 import ctypes as C
 import os
 import sys
@@ -21,7 +21,7 @@ def cfg4():
     return gen_workload(WorkloadSpec("attention-stack", 8000, 1, 64, seed=0), node_cap=10**6)
 
 
-def des(K, modes=("lane", "warp")):
+def des(K):
     from paper_2010_12438_b200.costmodel import uniform_topology
     from paper_2010_12438_b200.simulator import simulate_many, singleton_fused
     g = cfg4()
@@ -30,21 +30,15 @@ def des(K, modes=("lane", "warp")):
     pr = torch.zeros(g.num_nodes, dtype=torch.int32, device="cuda")
     fg = singleton_fused(g)
     top = uniform_topology(8)
-    ref = None
-    for mode in modes:
-        os.environ["GO_DES_MODE"] = mode
-        simulate_many(fg, pl[:32], pr, top)
-        simulate_many(fg, pl, pr, top)  # workspace sized for K
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = simulate_many(fg, pl, pr, top)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        st = r.step_time.cpu().numpy()
-        same = "" if ref is None else f" identical={bool((st == ref).all())}"
-        ref = st if ref is None else ref
-        print(f"DES mode={mode} K={K}: {dt*1e3:.1f} ms  ({K/dt:.1f} placements/s)  "
-              f"step[0]={float(r.step_time[0]):.6g}{same}", flush=True)
+    simulate_many(fg, pl[:32], pr, top)
+    simulate_many(fg, pl, pr, top)  # workspace sized for K
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = simulate_many(fg, pl, pr, top)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"DES K={K}: {dt*1e3:.1f} ms  ({K/dt:.1f} placements/s)  "
+          f"step[0]={float(r.step_time[0]):.6g}", flush=True)
 
 
 def forward(F, modes=("tc", "simt"), env=None):
@@ -91,7 +85,7 @@ if __name__ == "__main__":
     what = sys.argv[1]
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     if what == "des":
-        des(n or 512, tuple(sys.argv[3].split(",")) if len(sys.argv) > 3 else ("lane", "warp"))
+        des(n or 512)
     elif what == "attn":
         forward(n or 8, env=[("GO_ATTN", "f16"), ("GO_ATTN", "tf32"), ("GO_ATTN", "f16")])
     elif what == "tc":
