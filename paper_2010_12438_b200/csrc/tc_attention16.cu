@@ -19,7 +19,7 @@
 // Accumulation.  The tensor core's fp32 accumulate does not round the low bits of
 // small addends to nearest; summed over the 1,250 key tiles of an 80k-node graph (where
 // the random-init rows are nearly parallel and every addend has the same sign pattern)
-// that drift reached 1.4e-4 of the logits.  So O accumulates in TMEM over only DRAIN = 8
+// that drift reached 1.4e-4 of the logits.  So O accumulates in TMEM over only DRAIN = 16
 // key tiles; at each group boundary the softmax thread, which owns its row, reads the
 // 16 O columns and adds them into a float sum in shared memory (IEEE round-to-nearest,
 // ~80 additions at 80k keys, two columns per packed FADD2), and the MMA thread restarts

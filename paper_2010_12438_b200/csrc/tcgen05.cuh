@@ -117,11 +117,6 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 // {lo, hi} -> fp16x2, round to nearest
 __device__ __forceinline__ uint32_t pack_f16x2_rn(float lo, float hi) {
   uint32_t r;
@@ -130,30 +125,12 @@ __device__ __forceinline__ uint32_t pack_f16x2_rn(float lo, float hi) {
 }
 // 2^x0, 2^x1 as packed fp16x2 on the FMA/ALU pipes instead of the MUFU (FA4-style
 // exponential emulation), for x in [-14, 15.5] (the fixed-offset softmax range of
-// tc_attention16.cu).  Range reduction in fp32 (x = j + f, j = rint(x), |f| <= 1/2,
-// exact), 2^f by a degree-3 polynomial in fp16x2 Horner form (max rel. error 1.5e-4
-// with fp16 coefficients, below the fp16 output rounding of 4.9e-4), then 2^j added
-// into the fp16 exponent fields of the packed word.  13 instructions per pair.
-__device__ __forceinline__ uint32_t exp2_poly_f16x2(float x0, float x1) {
-  // t = 1.5*2^23 + 15 + rint(x): the low 16 bits of t's encoding hold j + 15 in [1, 31]
-  constexpr float MAGIC = 12582912.f + 15.f;
-  const float t0 = x0 + MAGIC, t1 = x1 + MAGIC;
-  const float f0 = x0 - (t0 - MAGIC), f1 = x1 - (t1 - MAGIC);
-  const uint32_t fh = pack_f16x2_rn(f0, f1);
-  uint32_t jb;  // (j0 + 15) | (j1 + 15) << 16
-  asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(jb) : "r"(__float_as_uint(t0)), "r"(__float_as_uint(t1)));
-  uint32_t p;
-  // fp16x2 constants: c3 = 0.05517578, c2 = 0.24255371, c1 = 0.69335938, c0 = 1
-  asm("{\n.reg .b32 a;\n"
-      "fma.rn.f16x2 a, %1, %2, %3;\n"
-      "fma.rn.f16x2 a, a, %1, %4;\n"
-      "fma.rn.f16x2 %0, a, %1, %5;\n}\n"
-      : "=r"(p)
-      : "r"(fh), "r"(0x2B102B10u), "r"(0x33C333C3u), "r"(0x398C398Cu), "r"(0x3C003C00u));
-  // exponent fields: + (j + 15) << 10, - 15 << 10 (no field crosses: both stay in [0, 2^15))
-  return p + (jb << 10) - 0x3C003C00u;
-}
-// Cheaper variant (9 instructions per pair): x is rounded to fp16 first and the range
+// tc_attention16.cu): 2^f by a degree-3 polynomial in fp16x2 Horner form (max rel. error
+// 1.5e-4 with fp16 coefficients, below the fp16 output rounding of 4.9e-4), then 2^j
+// added into the fp16 exponent fields of the packed word.  (Round 1 measured a variant
+// with the range reduction in fp32, 13 instructions per pair, and a degree-2
+// polynomial, 2.0e-3 error: both slower or less accurate end to end.)
+// 9 instructions per pair: x is rounded to fp16 first and the range
 // reduction runs in fp16x2 (t = x + 1536 rounds to an integer since ulp(1536) = 1).
 // The fp16 rounding of x costs up to 2^-8 absolute in x (0.27% relative in 2^x for
 // |x| >= 8), on top of the polynomial and output rounding.
@@ -172,21 +149,6 @@ __device__ __forceinline__ uint32_t exp2_poly_f16x2_lp(float x0, float x1) {
         "r"(0x3C003C00u));
   // fp16 encodings of t hold 0x6600 + j per half; (t - 0x66006600) is the packed signed j
   // (borrows between the halves cancel in the shifted sum, both results stay positive)
-  return p + ((t - 0x66006600u) << 10);
-}
-// Degree-2 variant of exp2_poly_f16x2_lp (8 instructions per pair, max rel. error
-// 2.0e-3 from the polynomial): an experiment on the accuracy / throughput trade-off.
-__device__ __forceinline__ uint32_t exp2_poly_f16x2_lp2(float x0, float x1) {
-  const uint32_t xh = pack_f16x2_rn(x0, x1);
-  uint32_t t, p;
-  asm("{\n.reg .b32 u, f;\n"
-      "add.rn.f16x2 %0, %2, %3;\n"
-      "sub.rn.f16x2 u, %0, %3;\n"
-      "sub.rn.f16x2 f, %2, u;\n"
-      "fma.rn.f16x2 u, f, %4, %5;\n"
-      "fma.rn.f16x2 %1, u, f, %6;\n}\n"
-      : "=r"(t), "=r"(p)
-      : "r"(xh), "r"(0x66006600u), "r"(0x33AD33ADu), "r"(0x39A039A0u), "r"(0x3C003C00u));
   return p + ((t - 0x66006600u) << 10);
 }
 __device__ __forceinline__ float tf32_rn(float x) {
