@@ -243,11 +243,10 @@ def _forward_env(var, val, store, ecfg, pcfg, sizes, graphs, seeds):
 
 @pytest.mark.parametrize("seg", [64, 32, 16, 48, 100])
 def test_trunk_tc_matches_simt(seg):
-    """The opt-in tcgen05 segmented trunk attention (GO_TRUNK=tc: 128-row tiles over
-    128/S segments, per-row key windows, all heads per CTA, fp16 operands) agrees with
-    the default SIMT banded kernel on a ragged batch whose forwards end mid-segment
-    and mid-tile; segment_len 48 and 100 give key windows wider than the 192-key TMEM
-    budget, so those batches take the SIMT kernel."""
+    """The default trunk attention (split-fp16 mma.sync, trunk_mma.cu; the round-1 opt-in
+    tcgen05 trunk behind GO_TRUNK=tc was removed, so "tc" selects the default) agrees with
+    the fp32 SIMT banded kernel on a ragged batch whose forwards end mid-segment and
+    mid-tile, for segment lengths below, at and above the 64-query tile."""
     from paper_2010_12438_b200 import EmbedConfig, PolicyConfig
     from synthetic.workloads import WorkloadSpec, gen_workload
     sizes = {"placement": 8}
@@ -258,7 +257,6 @@ def test_trunk_tc_matches_simt(seg):
     seeds = [3, 4, 5]
     h_tc, lg_tc = _forward_env("GO_TRUNK", "tc", store, ecfg, pcfg, sizes, graphs, seeds)
     h_s, lg_s = _forward_env("GO_TRUNK", "simt", store, ecfg, pcfg, sizes, graphs, seeds)
-    # single-pass fp16 (tf32-equivalent) Q.K^T and P.V: ~4e-5 normwise
     assert rel_err(h_tc, h_s) < 1e-4
     assert rel_err(lg_tc, lg_s) < 1e-4
 
