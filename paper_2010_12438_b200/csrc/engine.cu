@@ -591,8 +591,6 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
     CUDA_CHECK(cudaMemcpyAsync(bb + 2 * W, bv, W * 4, cudaMemcpyDeviceToDevice, st));
     return bb;
   };
-  double gemm_flops = 0;
-  auto gf = [&](int K, int N) { gemm_flops += 2.0 * R * K * N; };
 
   if (do_e) {
     GO_CHECK(node_embed && graph_embed, "embed outputs required");
@@ -847,8 +845,6 @@ static void run_forward_tc(go_ctx* ctx, const go_config_t& cfg, const float* P,
       value_head(meanb, F, dm, W_(S.value_w()), W_(S.value_b()), value, st);
     }
   }
-  (void)gf;
-  (void)gemm_flops;
 }
 
 extern "C" {

@@ -419,24 +419,22 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           *reinterpret_cast<uint4*>(a16 + off) = *reinterpret_cast<const uint4*>(hi);
           *reinterpret_cast<uint4*>(a16 + 4096 + off) = *reinterpret_cast<const uint4*>(lo);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&a_full[s]);
-        continue;
-      }
+      } else {
 #pragma unroll
-      for (int hh = 0; hh < MH; ++hh) {
-        float4* hp = reinterpret_cast<float4*>(A_hi(s, hh));
-        float4* lp = reinterpret_cast<float4*>(A_lo(s, hh));
-        float4 x[8];
+        for (int hh = 0; hh < MH; ++hh) {
+          float4* hp = reinterpret_cast<float4*>(A_hi(s, hh));
+          float4* lp = reinterpret_cast<float4*>(A_lo(s, hh));
+          float4 x[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = hp[i * 128 + lt];
+          for (int i = 0; i < 8; ++i) x[i] = hp[i * 128 + lt];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
-          const float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
-                                       tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
-          hp[i * 128 + lt] = h;
-          lp[i * 128 + lt] = l;
+          for (int i = 0; i < 8; ++i) {
+            const float4 h = make_float4(tf32rn(x[i].x), tf32rn(x[i].y), tf32rn(x[i].z), tf32rn(x[i].w));
+            const float4 l = make_float4(tf32rn(x[i].x - h.x), tf32rn(x[i].y - h.y),
+                                         tf32rn(x[i].z - h.z), tf32rn(x[i].w - h.w));
+            hp[i * 128 + lt] = h;
+            lp[i * 128 + lt] = l;
+          }
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
