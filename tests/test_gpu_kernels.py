@@ -359,6 +359,39 @@ def test_fused_ffn_matches_unfused_and_reruns_out_of_range():
     assert rel_err(lg_f, lg_u) < 1e-4
 
 
+@pytest.mark.parametrize("diag", [1e12, 7.5e9])
+def test_des_uniform_links_match_oracle(diag):
+    """With one bandwidth on every link the DES takes its transfer times from a per-edge
+    table built once per launch (des_etab_kernel); the diagonal (never used: a group's
+    local consumers need no transfer) may differ without leaving that path.  Step times
+    and busy times agree bit-for-bit with the oracle DES."""
+    from oracle import des as od
+    from oracle import graph as og
+    from paper_2010_12438_b200.costmodel import Topology
+    from paper_2010_12438_b200.simulator import ActionAssignment, simulate, singleton_fused
+    from synthetic.workloads import WorkloadSpec, gen_workload
+    d = 8
+    rng = np.random.default_rng(7)
+    g = gen_workload(WorkloadSpec("multi-branch-cnn", 30, 1, 64, seed=4), node_cap=10**6)
+    ogr = og.make(g.num_nodes, g.op, g.flops, g.out_bytes, g.src, g.dst, g.ebytes)
+    peak = rng.choice([1e11, 5e11, 1e12], d)
+    bw = rng.choice([5e10, 1e11], d)
+    cap = np.full(d, 1e12)
+    lb = np.full((d, d), 3.3e9)
+    np.fill_diagonal(lb, diag)
+    top = Topology(peak, bw, cap, lb)
+    otop = od.Topology(list(peak), list(bw), list(cap), [[float(x) for x in row] for row in lb])
+    fg = singleton_fused(g)
+    for policy in ("priority", "fifo"):
+        pl = rng.integers(0, d, g.num_nodes)
+        pr = rng.integers(0, 8, g.num_nodes)
+        res = simulate(fg, ActionAssignment("placement", pl, d),
+                       ActionAssignment("schedule_priority", pr, 8), top, policy=policy)
+        want = od.simulate(ogr, od.singleton(ogr), pl, pr, otop, policy=policy)
+        assert res.step_time == want["step_time"], policy
+        assert res.per_device_busy == list(want["busy"]), policy
+
+
 @pytest.mark.parametrize("d", [3, 6, 12, 16])
 def test_des_device_bounds_match_oracle(d):
     """The DES kernel is instantiated for 4 / 8 / 16 devices with its per-placement state in
