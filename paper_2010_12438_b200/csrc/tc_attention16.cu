@@ -367,13 +367,20 @@ __global__ void repack_kv16_kernel(const float* __restrict__ k, const float* __r
       *reinterpret_cast<uint4*>(kt + dh * (KT * 8) + g * 64 + e * 8) =
           *reinterpret_cast<const uint4*>(kr);
   }
+  // max |k| per (forward, head): one atomic per group of lanes sharing the address (a warp
+  // spans two tiles), not one per 8-key group -- the per-group atomics serialised on the
+  // 3 addresses of each forward
+  const unsigned kaddr = (unsigned)(fwd * n_head + head);
+  const unsigned kval = (live && dh == 0 && local0 < n) ? __float_as_uint(sqrtf(nkmax)) : 0u;
+  const unsigned grp = __match_any_sync(0xffffffffu, kaddr);
+  const unsigned kred = __reduce_max_sync(grp, kval);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1) && kred != 0u) atomicMax(&kmax[kaddr], kred);
   if (!live) return;
   // V^T: element (key, d) at (key>>3)*128 + (d>>3)*64 + (d&7)*8 + (key&7)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     *reinterpret_cast<uint4*>(vt + g * 128 + dh * 64 + i * 8) =
         *reinterpret_cast<const uint4*>(vv[i]);
-  if (dh == 0 && local0 < n) atomicMax(&kmax[fwd * n_head + head], __float_as_uint(sqrtf(nkmax)));
   if (big) atomicOr(flag, 2);
 }
 
