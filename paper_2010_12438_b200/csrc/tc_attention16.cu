@@ -305,82 +305,118 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 // K and V^T tiles in fp16: K[:,15] = V[:,15] = 1 on valid keys, zero rows past the end;
 // max |k| (of the rounded values) per (forward, head); flags |k|, |v| out of fp16 range.
-// One thread per (head, tile, 8-key group, 8-wide d half): the group is one column of
-// core matrices in both layouts, so every store is a 16-B vector (one per key for K, one
-// per d for V^T); the two d halves of a key sit in adjacent lanes and combine |k|^2.
-__global__ void repack_kv16_kernel(const float* __restrict__ k, const float* __restrict__ v,
-                                   int64_t ld, int n_head, int d_head,
-                                   const int64_t* __restrict__ tile_fwd_row0,
-                                   const int32_t* __restrict__ tile_n, int64_t Ttot,
-                                   __half* __restrict__ kb, __half* __restrict__ vb,
-                                   unsigned* __restrict__ kmax, int32_t* __restrict__ flag) {
-  constexpr int G = KT / 8;  // 8-key groups per tile
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)n_head * Ttot * G * 2;
-  const bool live = idx < total;
-  const int64_t id = live ? idx : total - 1;
-  const int dh = (int)(id & 1);  // d in [8 dh, 8 dh + 8)
-  const int64_t gi = id >> 1;
-  const int head = (int)(gi / (Ttot * G));
-  const int64_t rem = gi % (Ttot * G);
-  const int64_t tile = rem / G;
-  const int g = (int)(rem % G);
+// One CTA per 64-key tile for every head: warps read whole K|V row slices (lanes along
+// the columns: coalesced), the tile is assembled in shared memory and written back as
+// 16-B vectors in both UMMA layouts, and one atomic per head carries the tile's max |k|
+// (grid.y covers the heads four at a time).
+// (Round 1's thread-per-(8 keys, 8 dims) mapping read 32-B pieces of 128 rows per warp
+// instruction: ~1 TB/s.)
+constexpr int RP_THREADS = 128;
+constexpr int RP_MAXH = 4;
+__global__ void __launch_bounds__(RP_THREADS)
+    repack_kv16_kernel(const float* __restrict__ k, const float* __restrict__ v, int64_t ld,
+                       int n_head, int d_head, const int64_t* __restrict__ tile_fwd_row0,
+                       const int32_t* __restrict__ tile_n, int64_t Ttot,
+                       __half* __restrict__ kb, __half* __restrict__ vb,
+                       unsigned* __restrict__ kmax, int32_t* __restrict__ flag) {
+  __shared__ __align__(16) __half Ks[RP_MAXH][KT][16];
+  __shared__ __align__(16) __half Vs[RP_MAXH][KT][16];
+  __shared__ unsigned hmax[RP_MAXH];
+  const int64_t tile = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = tile_n[3 * tile], fwd = tile_n[3 * tile + 2];
-  const int local0 = tile_n[3 * tile + 1] * KT + g * 8;
-  const int64_t grow0 = tile_fwd_row0[tile] + local0;
-  __half* kt = kb + ((int64_t)head * Ttot + tile) * (KT * 16);
-  __half* vt = vb + ((int64_t)head * Ttot + tile) * (KT * 16);
-  __align__(16) __half vv[8][8];  // [d - 8 dh][key]
-  float nkmax = 0.f;
+  const int lt0 = tile_n[3 * tile + 1] * KT;  // first row of the tile within its forward
+  const int64_t grow0 = tile_fwd_row0[tile] + lt0;
+  const int h0 = blockIdx.y * RP_MAXH;                 // heads [h0, h0 + hc) in this CTA
+  const int hc = min(RP_MAXH, n_head - h0);
+  const int W = hc * d_head;
+  if (tid < RP_MAXH) hmax[tid] = 0u;
   bool big = false;
+  // ---- rows: warp per key, lane per column c of [K (W columns) | V (W columns)]
+  {
+    int cd[4], ch[4];
+    bool cv[4], cisv[4];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const bool valid = local0 + e < n;
-    __align__(16) __half kr[8];
-    float nk = 0.f;
+    for (int j = 0; j < 4; ++j) {  // 2W <= 128 columns
+      const int c = lane + 32 * j;
+      cv[j] = c < 2 * W;
+      cisv[j] = c >= W;
+      const int cc = cisv[j] ? c - W : c;
+      ch[j] = cc / d_head;
+      cd[j] = cc - ch[j] * d_head;
+    }
+    // all of this warp's loads first (16 rows x 4 columns per lane in flight), then the
+    // fp16 conversion and the shared-memory stores
+    constexpr int RPW = KT / (RP_THREADS / 32);  // rows per warp
+    float xs[RPW][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int d = dh * 8 + i;
-      float kv = 0.f, vx = 0.f;
-      if (valid) {
-        if (d < d_head) {
-          const int64_t o = (grow0 + e) * ld + head * d_head + d;
-          kv = k[o];
-          vx = v[o];
-          big |= !(fabsf(kv) <= RANGE_LIMIT) || !(fabsf(vx) <= RANGE_LIMIT);
-        } else if (d == 15) {
-          kv = 1.f;
-          vx = 1.f;
+    for (int r = 0; r < RPW; ++r) {
+      const int key = warp + r * (RP_THREADS / 32);
+      const bool valid = lt0 + key < n;
+      const int64_t ro = (grow0 + key) * ld;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x = 0.f;
+        if (valid && cv[j]) {
+          const int64_t o = ro + (int64_t)(h0 + ch[j]) * d_head + cd[j];
+          x = cisv[j] ? v[o] : k[o];
         }
-      }
-      kr[i] = __float2half_rn(kv);
-      vv[i][e] = __float2half_rn(vx);
-      if (d < d_head) {
-        const float kk = __half2float(kr[i]);
-        nk = fmaf(kk, kk, nk);
+        xs[r][j] = x;
       }
     }
-    nk += __shfl_xor_sync(0xffffffffu, nk, 1);
-    nkmax = fmaxf(nkmax, nk);
-    // K: element (key, d) at (d>>3)*(KT*8) + (key>>3)*64 + (key&7)*8 + (d&7)
-    if (live)
-      *reinterpret_cast<uint4*>(kt + dh * (KT * 8) + g * 64 + e * 8) =
-          *reinterpret_cast<const uint4*>(kr);
-  }
-  // max |k| per (forward, head): one atomic per group of lanes sharing the address (a warp
-  // spans two tiles), not one per 8-key group -- the per-group atomics serialised on the
-  // 3 addresses of each forward
-  const unsigned kaddr = (unsigned)(fwd * n_head + head);
-  const unsigned kval = (live && dh == 0 && local0 < n) ? __float_as_uint(sqrtf(nkmax)) : 0u;
-  const unsigned grp = __match_any_sync(0xffffffffu, kaddr);
-  const unsigned kred = __reduce_max_sync(grp, kval);
-  if ((threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1) && kred != 0u) atomicMax(&kmax[kaddr], kred);
-  if (!live) return;
-  // V^T: element (key, d) at (key>>3)*128 + (d>>3)*64 + (d&7)*8 + (key&7)
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    *reinterpret_cast<uint4*>(vt + g * 128 + dh * 64 + i * 8) =
-        *reinterpret_cast<const uint4*>(vv[i]);
+    for (int r = 0; r < RPW; ++r) {
+      const int key = warp + r * (RP_THREADS / 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!cv[j]) continue;
+        big |= !(fabsf(xs[r][j]) <= RANGE_LIMIT);
+        (cisv[j] ? Vs : Ks)[ch[j]][key][cd[j]] = __float2half_rn(xs[r][j]);
+      }
+    }
+  }
+  // ---- padding dims: d_head..14 zero, 15 = 1 on valid keys (offset / row-sum column)
+  for (int i = tid; i < hc * KT; i += RP_THREADS) {
+    const int h = i / KT, key = i - h * KT;
+    for (int d = d_head; d < 16; ++d) {
+      const __half x = __float2half_rn((d == 15 && lt0 + key < n) ? 1.f : 0.f);
+      Ks[h][key][d] = x;
+      Vs[h][key][d] = x;
+    }
+  }
+  __syncthreads();
+  // ---- K row form: element (key, d) at (d>>3)*(KT*8) + key*8 + (d&7); max |k| per head
+  for (int i = tid; i < hc * KT * 2; i += RP_THREADS) {
+    const int dh = i & 1, hk = i >> 1, h = hk / KT, key = hk - h * KT;
+    const uint4 w = *reinterpret_cast<const uint4*>(&Ks[h][key][8 * dh]);
+    __half* kt = kb + ((int64_t)(h0 + h) * Ttot + tile) * (KT * 16);
+    *reinterpret_cast<uint4*>(kt + dh * (KT * 8) + key * 8) = w;
+    if (dh == 0 && lt0 + key < n) {
+      // |k|^2 as the two 8-dim halves summed separately, then added (the round-1 order)
+      float n0 = 0.f, n1 = 0.f;
+      for (int d = 0; d < d_head && d < 8; ++d) {
+        const float kk = __half2float(Ks[h][key][d]);
+        n0 = fmaf(kk, kk, n0);
+      }
+      for (int d = 8; d < d_head; ++d) {
+        const float kk = __half2float(Ks[h][key][d]);
+        n1 = fmaf(kk, kk, n1);
+      }
+      atomicMax(&hmax[h], __float_as_uint(sqrtf(n0 + n1)));
+    }
+  }
+  // ---- V^T: element (key, d) at (key>>3)*128 + (d>>3)*64 + (d&7)*8 + (key&7)
+  for (int i = tid; i < hc * (KT / 8) * 16; i += RP_THREADS) {
+    const int d = i & 15, hg = i >> 4, h = hg / (KT / 8), g = hg - h * (KT / 8);
+    __align__(16) __half col[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) col[e] = Vs[h][8 * g + e][d];
+    __half* vt = vb + ((int64_t)(h0 + h) * Ttot + tile) * (KT * 16);
+    *reinterpret_cast<uint4*>(vt + g * 128 + (d >> 3) * 64 + (d & 7) * 8) =
+        *reinterpret_cast<const uint4*>(col);
+  }
+  __syncthreads();
+  if (tid < hc && lt0 < n) atomicMax(&kmax[fwd * n_head + h0 + tid], hmax[tid]);
   if (big) atomicOr(flag, 2);
 }
 
@@ -434,8 +470,9 @@ void attention_f16_tc(const float* q, const float* k, const float* v, int64_t ld
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t total = (int64_t)n_head * Ttot * (t16::KT / 8) * 2;
-  t16::repack_kv16_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(
+  GO_CHECK(d_head <= 15, "repack_kv16 needs d_head <= 15");
+  const dim3 rgrid((unsigned)Ttot, (unsigned)cdiv(n_head, t16::RP_MAXH));
+  t16::repack_kv16_kernel<<<rgrid, t16::RP_THREADS, 0, st>>>(
       k, v, ld, n_head, d_head, tile_row0_dev, tile_n_dev, Ttot, static_cast<__half*>(kb),
       static_cast<__half*>(vb), kmax, flag);
   LAUNCH_CHECK();
