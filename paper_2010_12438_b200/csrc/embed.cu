@@ -76,6 +76,9 @@ void neighbor_sample(const GraphView* views_dev, const int64_t* row_off_dev,
 // One warp per feature row: the row's metadata (forward, op, the 4 static features, the
 // previous actions) is loaded once per warp and each lane produces 4 output columns as
 // a float4 (D % 4 == 0, D <= 128 * k handled by the column loop); W rows are L1-resident.
+// Four rows per warp (8 lanes per row, each lane a column quad every 8): the row's chain
+// of dependent metadata loads (forward -> view -> static features / op / node -> previous
+// actions) is shared by 4x more output, which is what bounded the warp-per-row form.
 __global__ void features_inproj_kernel(const GraphView* __restrict__ views,
                                        const int64_t* __restrict__ row_off,
                                        const int32_t* __restrict__ row_fwd, int64_t R,
@@ -83,8 +86,8 @@ __global__ void features_inproj_kernel(const GraphView* __restrict__ views,
                                        int tc0, int tc1, int tc2,
                                        const float* __restrict__ W, const float* __restrict__ b,
                                        int D, float* __restrict__ h, int64_t ldh) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, q = lane & 7;
+  const int64_t r = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + (lane >> 3);
   if (r >= R) return;
   const int f = row_fwd[r];
   const GraphView& G = views[f];
@@ -102,7 +105,7 @@ __global__ void features_inproj_kernel(const GraphView* __restrict__ views,
   const float4* W4 = reinterpret_cast<const float4*>(W);
   const float4* b4 = reinterpret_cast<const float4*>(b);
   float4* h4 = reinterpret_cast<float4*>(h + r * ldh);
-  for (int c = lane; c < D4; c += 32) {
+  for (int c = q; c < D4; c += 8) {
     float4 acc = W4[(int64_t)op * D4 + c];
     const float4 w12 = W4[(int64_t)12 * D4 + c], w13 = W4[(int64_t)13 * D4 + c];
     const float4 w14 = W4[(int64_t)14 * D4 + c], w15 = W4[(int64_t)15 * D4 + c];
@@ -170,7 +173,7 @@ void features_inproj(const GraphView* views_dev, const int64_t* row_off_dev,
     LAUNCH_CHECK();
     return;
   }
-  features_inproj_kernel<<<(unsigned)cdiv(R, 8), 256, 0, st>>>(
+  features_inproj_kernel<<<(unsigned)cdiv(R, 32), 256, 0, st>>>(
       views_dev, row_off_dev, row_fwd, R, prev_actions, num_tasks, task_col[0], task_col[1],
       task_col[2], in_w, in_b, D, h, ldh);
   LAUNCH_CHECK();
