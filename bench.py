@@ -612,6 +612,15 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        # what "fp32" means per stage (activations and accumulators are fp32 everywhere)
+        "precision": {
+            "head_attention": "fp16 Q/K/P/V tensor-core operands (kind::f16), fp32 TMEM "
+                              "accumulation drained into IEEE fp32 sums every 1,024 keys; "
+                              "tf32 / online-softmax re-runs per work item out of fp16 range",
+            "trunk_attention": "2-term fp16 splits (3 mma.sync per product), fp32 accumulate",
+            "dense_layers": "3-pass fp16 hi/lo splits (kind::f16), fp32 accumulate",
+            "aggregation": "fp32", "sampler_and_simulator": "float64 (bit-exact)",
+        },
         "config": workload_config(args, w),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
