@@ -290,7 +290,7 @@ class DeviceParams:
     network) and compares the packed blob with the one last uploaded; the device copy
     is reused only when the bytes are identical.  So in-place edits
     (`store[name].data[:] = x`, which the reference's own tests do between calls,
-    tests/test_policy.py:212), reassignments, foreign stores without a version and
+    reference pkg/tests/test_policy.py:212), reassignments, foreign stores without a version and
     a new store that happens to reuse a freed store's id() can never be served stale
     weights."""
 
